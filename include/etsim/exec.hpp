@@ -1,0 +1,71 @@
+// GPU execution API (new in this framework; no reference counterpart beyond
+// the simulate() entry points it implements, ref simulate.hpp:23-36).
+//
+// An Executor owns one et_runtime (include/et_runtime.h): it flattens every
+// sampled schedule of a lowered kernel into device arrays once, binds a tile
+// operation to every call, and then runs one persistent-kernel launch per
+// step at any covered binding without re-lowering or recompiling.
+#pragma once
+
+#include <memory>
+
+#include "et_runtime.h"
+#include "etsim/simulate.hpp"
+
+namespace etsim {
+
+struct ExecConfig {
+    int device = 0;
+    int num_workers = 0;        // 0: the kernel's num_sms
+    bool record_trace = true;   // per-slot %globaltimer records
+    bool enable_prefetch = true;
+    Int watchdog_ns = 2'000'000'000;
+    Int tick_ns = 0;            // synthetic task body: ns per duration unit
+    Int seed = 0;               // duration-model seed for synthetic bodies
+    Int step_limit = 0;         // > 0: SimError::StepLimit after this many tasks
+};
+
+struct StepStats {
+    int sample_index = -1;
+    Int tasks_executed = 0;
+    Int noop_tasks = 0;
+    Int pushes = 0;
+    Int pops = 0;
+    double kernel_ms = 0;
+};
+
+class Executor {
+public:
+    Executor(const StaticMegakernel& k, const ExecConfig& cfg);
+    ~Executor();
+    Executor(const Executor&) = delete;
+    Executor& operator=(const Executor&) = delete;
+
+    // One op per call (index = call index); calls left unbound run the
+    // synthetic body.
+    void bind_ops(const std::vector<et_op>& ops);
+    void set_runtime_tensor(const std::string& name, const std::vector<Int>& values);
+    void set_realization(const RoutingRealization& r);
+    std::vector<Int> runtime_tensor(const std::string& name, size_t n) const;
+
+    StepStats run(const ShapeBinding& binding);                     // synchronous, throws on failure
+    void launch(const ShapeBinding& binding, void* stream = nullptr);  // enqueue only
+    StepStats sync();
+
+    Trace trace() const;                    // last step, reference Trace form (measured ns)
+    std::vector<Int> final_counters() const;
+    const StaticMegakernel& kernel() const;
+    int num_workers() const;
+    double upload_ms() const;
+
+private:
+    struct Impl;
+    std::unique_ptr<Impl> impl_;
+};
+
+// Throws etsim::Error / SimError according to an et_status code.
+void raise_status(int code, const std::string& what);
+
+bool gpu_available();
+
+}  // namespace etsim

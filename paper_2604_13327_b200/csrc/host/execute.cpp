@@ -1,0 +1,440 @@
+// Host side of GPU execution: flattening of lowered kernels into the C-ABI
+// program arrays, the Executor, and the reference-named simulate() entry
+// points (ref simulate.hpp:23-36), which here run on the device.
+#include <chrono>
+#include <cstring>
+
+#include "etsim/exec.hpp"
+#include "etsim/json_io.hpp"
+
+namespace etsim {
+
+void raise_status(int code, const std::string& what) {
+    switch (code) {
+        case ET_OK: return;
+        case ET_ERR_DEADLOCK: throw SimError(SimError::Kind::Deadlock, "deadlock: " + what, {what});
+        case ET_ERR_UNDERFLOW: throw SimError(SimError::Kind::CounterUnderflow, "counter underflow: " + what);
+        case ET_ERR_STEP_LIMIT: throw SimError(SimError::Kind::StepLimit, "step limit exceeded: " + what);
+        case ET_ERR_NO_DEVICE: throw Error("no CUDA device: the executor has no CPU fallback");
+        default: throw Error(what);
+    }
+}
+
+bool gpu_available() {
+    int n = 0;
+    return et_device_count(&n) == ET_OK && n > 0;
+}
+
+namespace {
+
+ExprPtr product_expr(const std::vector<ExprPtr>& dims) {
+    ExprPtr p = SymExpr::constant(1);
+    for (const auto& d : dims) p = p * d;
+    return p;
+}
+
+std::vector<int64_t> binding_vector(const GraphFunction& g, const ShapeBinding& b) {
+    std::vector<int64_t> v;
+    for (const auto& s : g.symbols) {
+        auto it = b.find(s);
+        if (it == b.end()) throw Error("binding " + binding_to_string(b) + " does not bind symbol '" + s + "'");
+        v.push_back(it->second);
+    }
+    return v;
+}
+
+struct HostSample {
+    std::vector<int64_t> binding;
+    std::vector<int32_t> call_extents, queue_off, slot_task, slot_call, slot_flat, slot_duration, wait_off, waits,
+        notify_off, notifies, initial_counts;
+    std::vector<int32_t> slot_queue;  // for trace reconstruction
+    int num_queues = 0, has_dma = 0;
+};
+
+}  // namespace
+
+struct Executor::Impl {
+    StaticMegakernel k;
+    ExecConfig cfg;
+    et_runtime* rt = nullptr;
+    std::vector<HostSample> hs;
+    std::vector<std::string> rt_names;
+    int workers = 0;
+    double upload_ms = 0;
+    ShapeBinding last_binding;
+    int last_sample = -1;
+
+    ~Impl() {
+        if (rt) et_destroy(rt);
+    }
+    void check(int code, const char* what) const {
+        if (code != ET_OK) raise_status(code, std::string(what) + ": " + et_last_error(rt));
+    }
+};
+
+Executor::Executor(const StaticMegakernel& k, const ExecConfig& cfg) : impl_(new Impl) {
+    Impl& I = *impl_;
+    I.k = k;
+    I.cfg = cfg;
+    I.workers = cfg.num_workers > 0 ? cfg.num_workers : k.num_sms;
+    if (I.workers != k.num_sms)
+        throw Error("kernel was compiled for " + std::to_string(k.num_sms) + " SMs, run asked for " +
+                    std::to_string(I.workers));
+    if (k.samples.empty()) throw Error("kernel has no sampled schedules");
+    const auto t0 = std::chrono::steady_clock::now();
+    const GraphFunction& g = k.graph;
+
+    // ---- graph description --------------------------------------------------
+    std::vector<int32_t> call_rank, call_ef, grid_off, code_op, rt_len_off;
+    std::vector<int64_t> code_arg, rt_cap;
+    auto append = [&](const ExprPtr& e) {
+        const ExprCode c = compile_expr(e, g.symbols);
+        for (const auto& ins : c.code) {
+            code_op.push_back(static_cast<int32_t>(ins.op));
+            code_arg.push_back(ins.arg);
+        }
+    };
+    for (const auto& c : g.calls) {
+        const auto& grid = g.call_grid(c);
+        if (grid.size() > 4) throw Error("grid rank above 4 is not supported on the device");
+        call_rank.push_back(static_cast<int32_t>(grid.size()));
+        call_ef.push_back(c.extent_from.empty() ? -1 : g.runtime_index(c.extent_from));
+        for (size_t d = 0; d < 4; ++d) {
+            grid_off.push_back(static_cast<int32_t>(code_op.size()));
+            if (d < grid.size()) append(grid[d]);
+        }
+    }
+    grid_off.push_back(static_cast<int32_t>(code_op.size()));
+    for (const auto& r : g.runtime_tensors) {
+        I.rt_names.push_back(r.name);
+        rt_len_off.push_back(static_cast<int32_t>(code_op.size()));
+        append(product_expr(r.shape));
+        Int cap = 1;
+        for (const auto& s : k.samples) cap = std::max(cap, eval_expr(product_expr(r.shape), s.binding));
+        rt_cap.push_back(cap);
+    }
+    rt_len_off.push_back(static_cast<int32_t>(code_op.size()));
+
+    // ---- samples ---------------------------------------------------------------
+    for (const auto& s : k.samples) {
+        HostSample h;
+        h.binding = binding_vector(g, s.binding);
+        h.num_queues = static_cast<int>(s.sm_queues.size());
+        h.has_dma = s.dma_queue.empty() ? 0 : 1;
+        std::vector<std::vector<Int>> ext(g.calls.size());
+        for (size_t ci = 0; ci < g.calls.size(); ++ci) {
+            const auto& grid = g.call_grid(g.calls[ci]);
+            for (size_t d = 0; d < 4; ++d) {
+                const Int e = d < grid.size() ? eval_expr(grid[d], s.binding) : 1;
+                if (e > INT32_MAX) throw Error("grid extent exceeds int32");
+                if (d < grid.size()) ext[ci].push_back(e);
+                h.call_extents.push_back(static_cast<int32_t>(e));
+            }
+        }
+        auto add_queue = [&](const std::vector<QueueTask>& q, int qi) {
+            for (const auto& t : q) {
+                h.slot_task.push_back(t.id);
+                h.slot_call.push_back(t.call);
+                h.slot_flat.push_back(static_cast<int32_t>(t.flat));
+                h.slot_queue.push_back(qi);
+                h.wait_off.push_back(static_cast<int32_t>(h.waits.size()));
+                h.waits.insert(h.waits.end(), t.waits.begin(), t.waits.end());
+                h.notify_off.push_back(static_cast<int32_t>(h.notifies.size()));
+                h.notifies.insert(h.notifies.end(), t.notifies.begin(), t.notifies.end());
+                if (cfg.tick_ns > 0) {
+                    const DeviceFunctionDecl* fn = g.find_fn(g.calls[static_cast<size_t>(t.call)].fn);
+                    Int dur = 1;
+                    if (fn && !fn->duration.empty())
+                        dur = eval_duration(g.duration_models.at(fn->duration), cfg.seed, t.call, t.coord,
+                                            ext[static_cast<size_t>(t.call)], nullptr);
+                    h.slot_duration.push_back(static_cast<int32_t>(dur));
+                }
+            }
+        };
+        h.queue_off.push_back(0);
+        for (size_t q = 0; q < s.sm_queues.size(); ++q) {
+            add_queue(s.sm_queues[q], static_cast<int>(q));
+            h.queue_off.push_back(static_cast<int32_t>(h.slot_task.size()));
+        }
+        if (h.has_dma) {
+            add_queue(s.dma_queue, h.num_queues);
+            h.queue_off.push_back(static_cast<int32_t>(h.slot_task.size()));
+        }
+        h.wait_off.push_back(static_cast<int32_t>(h.waits.size()));
+        h.notify_off.push_back(static_cast<int32_t>(h.notifies.size()));
+        for (Int c : s.initial_counts) h.initial_counts.push_back(static_cast<int32_t>(c));
+        I.hs.push_back(std::move(h));
+    }
+
+    // ---- runtime ---------------------------------------------------------------
+    et_config ec{};
+    ec.device = cfg.device;
+    ec.num_workers = I.workers;
+    ec.record_trace = cfg.record_trace ? 1 : 0;
+    ec.enable_prefetch = cfg.enable_prefetch ? 1 : 0;
+    ec.watchdog_ns = cfg.watchdog_ns;
+    ec.tick_ns = cfg.tick_ns;
+    ec.step_limit = cfg.step_limit;
+    const int rc = et_create(&ec, &I.rt);
+    if (rc != ET_OK) raise_status(rc, "cannot create the GPU runtime");
+
+    et_graph_desc gd{};
+    gd.num_symbols = static_cast<int32_t>(g.symbols.size());
+    gd.num_calls = static_cast<int32_t>(g.calls.size());
+    gd.call_rank = call_rank.data();
+    gd.call_extent_from = call_ef.data();
+    gd.grid_code_off = grid_off.data();
+    gd.code_op = code_op.data();
+    gd.code_arg = code_arg.data();
+    gd.code_len = static_cast<int32_t>(code_op.size());
+    gd.num_runtime_tensors = static_cast<int32_t>(rt_cap.size());
+    gd.runtime_capacity = rt_cap.data();
+    gd.runtime_len_off = rt_len_off.data();
+    I.check(et_upload_graph(I.rt, &gd), "upload graph");
+
+    std::vector<et_sample_desc> sd(I.hs.size());
+    for (size_t i = 0; i < I.hs.size(); ++i) {
+        const HostSample& h = I.hs[i];
+        et_sample_desc& d = sd[i];
+        d.binding = h.binding.data();
+        d.call_extents = h.call_extents.data();
+        d.num_queues = h.num_queues;
+        d.has_dma = h.has_dma;
+        d.queue_off = h.queue_off.data();
+        d.num_slots = static_cast<int32_t>(h.slot_task.size());
+        d.slot_task = h.slot_task.data();
+        d.slot_call = h.slot_call.data();
+        d.slot_flat = h.slot_flat.data();
+        d.slot_duration = h.slot_duration.empty() ? nullptr : h.slot_duration.data();
+        d.wait_off = h.wait_off.data();
+        d.waits = h.waits.data();
+        d.notify_off = h.notify_off.data();
+        d.notifies = h.notifies.data();
+        d.num_counters = static_cast<int32_t>(h.initial_counts.size());
+        d.initial_counts = h.initial_counts.data();
+        d.counter_dd = nullptr;
+    }
+    I.check(et_upload_static(I.rt, sd.data(), static_cast<int32_t>(sd.size())), "upload program");
+    std::vector<et_op> none(g.calls.size());
+    std::memset(none.data(), 0, none.size() * sizeof(et_op));
+    I.check(et_bind_ops(I.rt, none.data(), static_cast<int32_t>(none.size())), "bind ops");
+    I.upload_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+Executor::~Executor() = default;
+
+void Executor::bind_ops(const std::vector<et_op>& ops) {
+    Impl& I = *impl_;
+    std::vector<et_op> full(I.k.graph.calls.size());
+    std::memset(full.data(), 0, full.size() * sizeof(et_op));
+    for (size_t i = 0; i < ops.size() && i < full.size(); ++i) full[i] = ops[i];
+    I.check(et_bind_ops(I.rt, full.data(), static_cast<int32_t>(full.size())), "bind ops");
+}
+
+void Executor::set_runtime_tensor(const std::string& name, const std::vector<Int>& values) {
+    Impl& I = *impl_;
+    const int idx = I.k.graph.runtime_index(name);
+    if (idx < 0) throw Error("undeclared runtime tensor '" + name + "'");
+    std::vector<int32_t> v(values.begin(), values.end());
+    I.check(et_set_runtime_tensor(I.rt, idx, v.data(), static_cast<int64_t>(v.size())), "runtime tensor");
+}
+
+void Executor::set_realization(const RoutingRealization& r) {
+    for (const auto& kv : r.tensors) set_runtime_tensor(kv.first, kv.second);
+}
+
+std::vector<Int> Executor::runtime_tensor(const std::string& name, size_t n) const {
+    const Impl& I = *impl_;
+    const int idx = I.k.graph.runtime_index(name);
+    if (idx < 0) throw Error("undeclared runtime tensor '" + name + "'");
+    std::vector<int32_t> v(n);
+    I.check(et_get_runtime_tensor(I.rt, idx, v.data(), static_cast<int64_t>(n)), "runtime tensor");
+    return std::vector<Int>(v.begin(), v.end());
+}
+
+void Executor::launch(const ShapeBinding& b, void* stream) {
+    Impl& I = *impl_;
+    const auto v = binding_vector(I.k.graph, b);
+    I.check(et_step(I.rt, v.data(), static_cast<int32_t>(v.size()), stream, 0, nullptr), "launch");
+    I.last_binding = b;
+}
+
+namespace {
+StepStats to_stats(const et_step_info& si) {
+    StepStats s;
+    s.sample_index = si.sample_index;
+    s.tasks_executed = si.tasks_executed;
+    s.noop_tasks = si.noop_tasks;
+    s.pushes = si.pushes;
+    s.pops = si.pops;
+    s.kernel_ms = si.kernel_ms;
+    return s;
+}
+}  // namespace
+
+StepStats Executor::sync() {
+    Impl& I = *impl_;
+    et_step_info si{};
+    const int rc = et_sync(I.rt, &si);
+    I.last_sample = si.sample_index;
+    if (rc != ET_OK) {
+        std::string where = et_last_error(I.rt);
+        if (rc == ET_ERR_DEADLOCK && si.sample_index >= 0 && si.slot >= 0) {
+            const HostSample& h = I.hs[static_cast<size_t>(si.sample_index)];
+            const int call = h.slot_call[static_cast<size_t>(si.slot)];
+            where = "SM" + std::to_string(si.worker) + " blocked in " + I.k.graph.calls[static_cast<size_t>(call)].fn +
+                    " task " + std::to_string(h.slot_task[static_cast<size_t>(si.slot)]) + " waiting on counter " +
+                    std::to_string(si.counter) + " (value " + std::to_string(si.value) + ")";
+        }
+        raise_status(rc, where);
+    }
+    return to_stats(si);
+}
+
+StepStats Executor::run(const ShapeBinding& b) {
+    Impl& I = *impl_;
+    const auto v = binding_vector(I.k.graph, b);
+    et_step_info si{};
+    const int rc = et_step(I.rt, v.data(), static_cast<int32_t>(v.size()), nullptr, 1, &si);
+    I.last_binding = b;
+    I.last_sample = si.sample_index;
+    if (rc != ET_OK) {
+        std::string where = et_last_error(I.rt);
+        if (rc == ET_ERR_DEADLOCK && si.sample_index >= 0 && si.slot >= 0) {
+            const HostSample& h = I.hs[static_cast<size_t>(si.sample_index)];
+            const int call = h.slot_call[static_cast<size_t>(si.slot)];
+            where = (si.worker == h.num_queues ? std::string("DMA") : "SM" + std::to_string(si.worker)) +
+                    " blocked in " + I.k.graph.calls[static_cast<size_t>(call)].fn + " task " +
+                    std::to_string(h.slot_task[static_cast<size_t>(si.slot)]) + " waiting on counter " +
+                    std::to_string(si.counter) + " (value " + std::to_string(si.value) + ")";
+        }
+        raise_status(rc, where);
+    }
+    return to_stats(si);
+}
+
+std::vector<Int> Executor::final_counters() const {
+    const Impl& I = *impl_;
+    if (I.last_sample < 0) throw Error("no step has run");
+    const HostSample& h = I.hs[static_cast<size_t>(I.last_sample)];
+    std::vector<int64_t> v(h.initial_counts.size());
+    I.check(et_read_counters(I.rt, v.data(), static_cast<int64_t>(v.size())), "read counters");
+    return std::vector<Int>(v.begin(), v.end());
+}
+
+Trace Executor::trace() const {
+    const Impl& I = *impl_;
+    if (I.last_sample < 0) throw Error("no step has run");
+    const HostSample& h = I.hs[static_cast<size_t>(I.last_sample)];
+    std::vector<et_trace_rec> recs(h.slot_task.size());
+    int64_t n = static_cast<int64_t>(recs.size());
+    I.check(et_read_trace(I.rt, recs.data(), &n), "read trace");
+    Trace t;
+    t.mode = "static";
+    t.num_sms = h.num_queues;
+    t.has_dma = h.has_dma != 0;
+    t.seed = I.cfg.seed;
+    t.binding = I.last_binding;
+    t.measured = true;
+    t.empty_polls.assign(static_cast<size_t>(t.num_resources()), 0);
+    int64_t base = INT64_MAX;
+    for (const auto& r : recs) base = std::min<int64_t>(base, r.t_begin);
+    if (recs.empty()) base = 0;
+    const GraphFunction& g = I.k.graph;
+    Int last = 0;
+    t.tasks.reserve(recs.size());
+    for (size_t s = 0; s < recs.size(); ++s) {
+        const et_trace_rec& r = recs[s];
+        TaskRecord tr;
+        tr.task_id = h.slot_task[s];
+        tr.call = h.slot_call[s];
+        const auto& grid = g.call_grid(g.calls[static_cast<size_t>(tr.call)]);
+        std::vector<Int> ext;
+        for (size_t d = 0; d < grid.size(); ++d) ext.push_back(h.call_extents[static_cast<size_t>(tr.call) * 4 + d]);
+        tr.coord = unflatten_coord(h.slot_flat[s], ext);
+        tr.resource = h.slot_queue[s];
+        tr.noop = (r.flags & 1) != 0;
+        const Int tb = r.t_begin - base, tw = r.t_wait_end - base, te = r.t_exec_end - base, tn = r.t_notify_end - base;
+        const int nw = h.wait_off[s + 1] - h.wait_off[s];
+        const int nn = h.notify_off[s + 1] - h.notify_off[s];
+        for (int i = 0; i < nw; ++i) tr.waits.push_back(i == 0 ? Interval{tb, tw} : Interval{tw, tw});
+        tr.exec = tr.noop ? Interval{tw, tw} : Interval{tw, te};
+        for (int i = 0; i < nn; ++i) tr.notifies.push_back(i == 0 ? Interval{te, tn} : Interval{tn, tn});
+        last = std::max({last, tr.exec.end, nn ? tn : tr.exec.end, nw ? tw : Int(0)});
+        t.tasks.push_back(std::move(tr));
+    }
+    t.makespan = last;
+    t.final_counters = final_counters();
+    return t;
+}
+
+const StaticMegakernel& Executor::kernel() const { return impl_->k; }
+int Executor::num_workers() const { return impl_->workers; }
+double Executor::upload_ms() const { return impl_->upload_ms; }
+
+// ---------------------------------------------------------------------------
+// Reference-named entry points.
+
+namespace {
+ExecConfig from_sim(const SimConfig& cfg, Int total_slots) {
+    ExecConfig e;
+    e.num_workers = cfg.num_sms;
+    e.seed = cfg.seed;
+    e.enable_prefetch = cfg.enable_prefetch;
+    // The reference counts simulator events; here the bound is on executed
+    // tasks and only enforced when it can trigger.
+    e.step_limit = cfg.step_limit < total_slots ? std::max<Int>(cfg.step_limit, 1) : 0;
+    return e;
+}
+}  // namespace
+
+Trace simulate(const StaticMegakernel& k, const ShapeBinding& binding, const RoutingRealization* realization,
+               const SimConfig& cfg) {
+    if (cfg.num_sms != k.num_sms)
+        throw Error("kernel was compiled for " + std::to_string(k.num_sms) + " SMs, run asked for " +
+                    std::to_string(cfg.num_sms));
+    (void)select_queues(k, binding);  // same validation and errors as the reference
+    Int slots = 0;
+    for (const auto& s : k.samples) slots = std::max(slots, s.num_tasks());
+    Executor ex(k, from_sim(cfg, slots));
+    if (realization) ex.set_realization(*realization);
+    ex.run(binding);
+    return ex.trace();
+}
+
+Trace simulate(const DynamicMegakernel& k, const ShapeBinding& binding, const RoutingRealization* realization,
+               const SimConfig& cfg) {
+    (void)k;
+    (void)binding;
+    (void)realization;
+    (void)cfg;
+    throw Error("dynamic scheduler is not available in this build");
+}
+
+Trace simulate_barrier_baseline(const GraphFunction& g0, const ShapeBinding& binding,
+                                const RoutingRealization* realization, const SimConfig& cfg) {
+    const auto diags = validate_graph(g0);
+    if (!diags.empty()) throw Error("invalid graph: " + diags.front());
+    GraphFunction g = worst_case_rewrite(g0);
+    // one stage per call: a one-element barrier event between consecutive calls
+    for (size_t ci = 0; ci + 1 < g.calls.size(); ++ci) {
+        EventTensorDecl e;
+        e.name = "__stage" + std::to_string(ci);
+        e.shape = {SymExpr::constant(1)};
+        g.event_tensors.push_back(e);
+        EdgeSpec out;
+        out.event = e.name;
+        out.map = {SymExpr::constant(0)};
+        g.calls[ci].out_edges.push_back(out);
+        g.calls[ci + 1].in_edges.push_back(out);
+    }
+    StaticMegakernel k = lower_static(g, {binding}, cfg.num_sms);
+    SimConfig c = cfg;
+    c.num_sms = k.num_sms;
+    Trace t = simulate(k, binding, realization, c);
+    t.mode = "barrier";
+    t.final_counters.clear();
+    return t;
+}
+
+}  // namespace etsim

@@ -1,0 +1,471 @@
+// C-ABI runtime (include/et_runtime.h): device memory for programs, counters,
+// runtime tensors, status and traces; sample selection; one cooperative
+// launch of the persistent megakernel per step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../kernels/megakernel.cuh"
+#include "et_runtime.h"
+
+namespace {
+
+template <typename T>
+struct DevArray {
+    T* ptr = nullptr;
+    size_t n = 0;
+    DevArray() = default;
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    DevArray(DevArray&& o) noexcept : ptr(o.ptr), n(o.n) { o.ptr = nullptr, o.n = 0; }
+    DevArray& operator=(DevArray&& o) noexcept {
+        if (this != &o) {
+            release();
+            ptr = o.ptr, n = o.n;
+            o.ptr = nullptr, o.n = 0;
+        }
+        return *this;
+    }
+    ~DevArray() { release(); }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count) {
+        release();
+        n = count;
+        if (count == 0) return cudaSuccess;
+        return cudaMalloc(&ptr, count * sizeof(T));
+    }
+    cudaError_t upload(const T* host, size_t count) {
+        cudaError_t e = alloc(count);
+        if (e != cudaSuccess || count == 0) return e;
+        if (!host) return cudaMemset(ptr, 0, count * sizeof(T));
+        return cudaMemcpy(ptr, host, count * sizeof(T), cudaMemcpyHostToDevice);
+    }
+};
+
+struct Sample {
+    std::vector<int64_t> binding;
+    std::vector<int32_t> call_extents;
+    int num_queues = 0, has_dma = 0, num_slots = 0, num_counters = 0;
+    std::vector<int32_t> initial_counts;  // host copy for counter readback
+    DevArray<int32_t> d_call_extents, d_queue_off, d_slot_call, d_slot_flat, d_slot_duration, d_wait_off, d_waits,
+        d_notify_off, d_notifies, d_initial;
+};
+
+int64_t eval_host(const std::vector<int32_t>& op, const std::vector<int64_t>& arg, int b, int e,
+                  const int64_t* binding, bool* ok) {
+    int64_t st[32];
+    int sp = 0;
+    for (int i = b; i < e; ++i) {
+        if (op[i] == 0 || op[i] == 1) {
+            if (sp >= 32) {
+                *ok = false;
+                return 0;
+            }
+            st[sp++] = op[i] == 0 ? arg[i] : binding[arg[i]];
+            if (st[sp - 1] < 0) *ok = false;
+            continue;
+        }
+        if (sp < 2) {
+            *ok = false;
+            return 0;
+        }
+        const int64_t y = st[--sp], x = st[sp - 1];
+        int64_t r = 0;
+        switch (op[i]) {
+            case 2: r = x + y; break;
+            case 3: r = x * y; break;
+            case 4: if (y == 0) { *ok = false; return 0; } r = x / y; break;
+            case 5: if (y == 0) { *ok = false; return 0; } r = x % y; break;
+            case 6: r = std::min(x, y); break;
+            default: r = std::max(x, y); break;
+        }
+        if (r < 0) *ok = false;
+        st[sp - 1] = r;
+    }
+    return sp ? st[0] : 0;
+}
+
+}  // namespace
+
+struct et_runtime {
+    et_config cfg{};
+    std::string err;
+    cudaStream_t stream = nullptr;
+    int sm_count = 0;
+
+    // graph
+    int num_symbols = 0, num_calls = 0;
+    std::vector<int32_t> call_rank, call_extent_from, grid_code_off, code_op, rt_len_off;
+    std::vector<int64_t> code_arg, rt_capacity;
+    DevArray<int32_t> d_call_rank, d_call_extent_from, d_grid_code_off, d_code_op;
+    DevArray<int64_t> d_code_arg;
+    std::vector<DevArray<int32_t>> d_rt;
+    DevArray<int*> d_rt_table;
+
+    std::vector<Sample> samples;
+    DevArray<et_op> d_ops;
+    int ops_bound = 0;
+
+    DevArray<uint32_t> d_cnt;  // [2][cap]
+    int cnt_capacity = 0;
+    DevArray<etk::DevStatus> d_status;  // [2]
+    DevArray<et_trace_rec> d_trace;
+    int parity = 0;
+    int last_sample = -1;
+    bool launched = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    int fail(int code, const std::string& m) {
+        err = m;
+        return code;
+    }
+    int cuda_fail(cudaError_t e, const char* what) {
+        err = std::string(what) + ": " + cudaGetErrorString(e);
+        return ET_ERR_CUDA;
+    }
+};
+
+#define ET_CUDA(call, what)                                   \
+    do {                                                      \
+        cudaError_t e__ = (call);                             \
+        if (e__ != cudaSuccess) return rt->cuda_fail(e__, what); \
+    } while (0)
+
+extern "C" {
+
+int et_abi_version(void) { return ET_ABI_VERSION; }
+
+int et_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    if (count) *count = n;
+    return n > 0 ? ET_OK : ET_ERR_NO_DEVICE;
+}
+
+int et_create(const et_config* cfg, et_runtime** out) {
+    if (!cfg || !out) return ET_ERR_INVALID;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return ET_ERR_NO_DEVICE;
+    if (cfg->device < 0 || cfg->device >= n) return ET_ERR_INVALID;
+    et_runtime* rt = new et_runtime();
+    rt->cfg = *cfg;
+    if (rt->cfg.watchdog_ns <= 0) rt->cfg.watchdog_ns = 2'000'000'000LL;
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&rt->sm_count, cudaDevAttrMultiProcessorCount, cfg->device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&rt->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&rt->ev1);
+    if (e == cudaSuccess) e = rt->d_status.alloc(2);
+    if (e == cudaSuccess) e = cudaMemset(rt->d_status.ptr, 0, 2 * sizeof(etk::DevStatus));
+    if (e != cudaSuccess) {
+        delete rt;
+        return ET_ERR_CUDA;
+    }
+    if (rt->cfg.num_workers <= 0) rt->cfg.num_workers = rt->sm_count;
+    *out = rt;
+    return ET_OK;
+}
+
+int et_destroy(et_runtime* rt) {
+    if (!rt) return ET_OK;
+    cudaSetDevice(rt->cfg.device);
+    if (rt->stream) cudaStreamSynchronize(rt->stream);
+    if (rt->ev0) cudaEventDestroy(rt->ev0);
+    if (rt->ev1) cudaEventDestroy(rt->ev1);
+    if (rt->stream) cudaStreamDestroy(rt->stream);
+    delete rt;
+    return ET_OK;
+}
+
+const char* et_last_error(const et_runtime* rt) { return rt ? rt->err.c_str() : "null runtime"; }
+
+int et_upload_graph(et_runtime* rt, const et_graph_desc* g) {
+    if (!rt || !g) return ET_ERR_INVALID;
+    if (g->num_symbols > etk::kMaxSymbols) return rt->fail(ET_ERR_INVALID, "too many symbols for the device binding");
+    if (g->num_runtime_tensors > etk::kMaxRuntime) return rt->fail(ET_ERR_INVALID, "too many runtime tensors");
+    cudaSetDevice(rt->cfg.device);
+    rt->num_symbols = g->num_symbols;
+    rt->num_calls = g->num_calls;
+    rt->call_rank.assign(g->call_rank, g->call_rank + g->num_calls);
+    rt->call_extent_from.assign(g->call_extent_from, g->call_extent_from + g->num_calls);
+    rt->grid_code_off.assign(g->grid_code_off, g->grid_code_off + g->num_calls * 4 + 1);
+    rt->code_op.assign(g->code_op, g->code_op + g->code_len);
+    rt->code_arg.assign(g->code_arg, g->code_arg + g->code_len);
+    for (int c = 0; c < g->num_calls; ++c)
+        if (rt->call_rank[c] > etk::kMaxRank) return rt->fail(ET_ERR_INVALID, "grid rank above 4 is not supported");
+    ET_CUDA(rt->d_call_rank.upload(rt->call_rank.data(), rt->call_rank.size()), "upload graph");
+    ET_CUDA(rt->d_call_extent_from.upload(rt->call_extent_from.data(), rt->call_extent_from.size()), "upload graph");
+    ET_CUDA(rt->d_grid_code_off.upload(rt->grid_code_off.data(), rt->grid_code_off.size()), "upload graph");
+    ET_CUDA(rt->d_code_op.upload(rt->code_op.data(), std::max<size_t>(1, rt->code_op.size())), "upload graph");
+    ET_CUDA(rt->d_code_arg.upload(rt->code_arg.data(), std::max<size_t>(1, rt->code_arg.size())), "upload graph");
+    rt->rt_capacity.assign(g->runtime_capacity, g->runtime_capacity + g->num_runtime_tensors);
+    rt->rt_len_off.assign(g->runtime_len_off, g->runtime_len_off + g->num_runtime_tensors + 1);
+    rt->d_rt.clear();
+    rt->d_rt.resize(static_cast<size_t>(g->num_runtime_tensors));
+    std::vector<int*> table(static_cast<size_t>(std::max(1, g->num_runtime_tensors)), nullptr);
+    for (int i = 0; i < g->num_runtime_tensors; ++i) {
+        ET_CUDA(rt->d_rt[static_cast<size_t>(i)].upload(nullptr, static_cast<size_t>(std::max<int64_t>(1, rt->rt_capacity[i]))),
+                "runtime tensors");
+        table[static_cast<size_t>(i)] = rt->d_rt[static_cast<size_t>(i)].ptr;
+    }
+    ET_CUDA(rt->d_rt_table.upload(table.data(), table.size()), "runtime tensors");
+    rt->samples.clear();
+    rt->last_sample = -1;
+    return ET_OK;
+}
+
+int et_upload_static(et_runtime* rt, const et_sample_desc* s, int32_t num_samples) {
+    if (!rt || (!s && num_samples > 0)) return ET_ERR_INVALID;
+    cudaSetDevice(rt->cfg.device);
+    cudaStreamSynchronize(rt->stream);
+    rt->samples.clear();
+    rt->samples.resize(static_cast<size_t>(num_samples));
+    int max_counters = 1, max_slots = 1;
+    for (int i = 0; i < num_samples; ++i) {
+        const et_sample_desc& d = s[i];
+        Sample& S = rt->samples[static_cast<size_t>(i)];
+        if (d.num_queues != rt->cfg.num_workers)
+            return rt->fail(ET_ERR_INVALID, "kernel was compiled for " + std::to_string(d.num_queues) +
+                                                " SMs, run asked for " + std::to_string(rt->cfg.num_workers));
+        if (d.num_queues > rt->sm_count)
+            return rt->fail(ET_ERR_INVALID, "program needs " + std::to_string(d.num_queues) +
+                                                " co-resident workers; the device has " + std::to_string(rt->sm_count) +
+                                                " SMs");
+        S.binding.assign(d.binding, d.binding + rt->num_symbols);
+        S.call_extents.assign(d.call_extents, d.call_extents + rt->num_calls * 4);
+        S.num_queues = d.num_queues;
+        S.has_dma = d.has_dma;
+        S.num_slots = d.num_slots;
+        S.num_counters = d.num_counters;
+        S.initial_counts.assign(d.initial_counts, d.initial_counts + d.num_counters);
+        const size_t nq = static_cast<size_t>(d.num_queues + d.has_dma + 1);
+        const int nw = d.wait_off[d.num_slots], nn = d.notify_off[d.num_slots];
+        ET_CUDA(S.d_call_extents.upload(d.call_extents, static_cast<size_t>(rt->num_calls * 4)), "upload sample");
+        ET_CUDA(S.d_queue_off.upload(d.queue_off, nq), "upload sample");
+        ET_CUDA(S.d_slot_call.upload(d.slot_call, static_cast<size_t>(std::max(1, d.num_slots))), "upload sample");
+        ET_CUDA(S.d_slot_flat.upload(d.slot_flat, static_cast<size_t>(std::max(1, d.num_slots))), "upload sample");
+        if (d.slot_duration)
+            ET_CUDA(S.d_slot_duration.upload(d.slot_duration, static_cast<size_t>(std::max(1, d.num_slots))), "upload sample");
+        ET_CUDA(S.d_wait_off.upload(d.wait_off, static_cast<size_t>(d.num_slots + 1)), "upload sample");
+        ET_CUDA(S.d_waits.upload(d.waits, static_cast<size_t>(std::max(1, nw))), "upload sample");
+        ET_CUDA(S.d_notify_off.upload(d.notify_off, static_cast<size_t>(d.num_slots + 1)), "upload sample");
+        ET_CUDA(S.d_notifies.upload(d.notifies, static_cast<size_t>(std::max(1, nn))), "upload sample");
+        ET_CUDA(S.d_initial.upload(d.initial_counts, static_cast<size_t>(std::max(1, d.num_counters))), "upload sample");
+        max_counters = std::max(max_counters, d.num_counters);
+        max_slots = std::max(max_slots, d.num_slots);
+    }
+    rt->cnt_capacity = max_counters;
+    ET_CUDA(rt->d_cnt.upload(nullptr, static_cast<size_t>(2 * max_counters)), "counters");
+    ET_CUDA(rt->d_trace.upload(nullptr, static_cast<size_t>(max_slots)), "trace");
+    ET_CUDA(cudaMemset(rt->d_status.ptr, 0, 2 * sizeof(etk::DevStatus)), "status");
+    rt->parity = 0;
+    rt->last_sample = -1;
+    rt->launched = false;
+    return ET_OK;
+}
+
+int et_upload_dynamic(et_runtime* rt, const et_sample_desc*, const et_dynamic_desc*, int32_t) {
+    return rt ? rt->fail(ET_ERR_INVALID, "dynamic scheduler is not available in this build") : ET_ERR_INVALID;
+}
+
+int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
+    if (!rt || (!ops && num_calls > 0)) return ET_ERR_INVALID;
+    if (num_calls != rt->num_calls) return rt->fail(ET_ERR_INVALID, "op table must have one entry per call");
+    cudaSetDevice(rt->cfg.device);
+    cudaStreamSynchronize(rt->stream);
+    ET_CUDA(rt->d_ops.upload(ops, static_cast<size_t>(std::max(1, num_calls))), "bind ops");
+    rt->ops_bound = 1;
+    return ET_OK;
+}
+
+int et_set_runtime_tensor(et_runtime* rt, int32_t index, const int32_t* values, int64_t n) {
+    if (!rt || index < 0 || index >= static_cast<int>(rt->d_rt.size())) return ET_ERR_INVALID;
+    if (n > rt->rt_capacity[static_cast<size_t>(index)])
+        return rt->fail(ET_ERR_INVALID, "runtime tensor larger than its capacity");
+    cudaSetDevice(rt->cfg.device);
+    ET_CUDA(cudaMemcpyAsync(rt->d_rt[static_cast<size_t>(index)].ptr, values, static_cast<size_t>(n) * 4,
+                            cudaMemcpyHostToDevice, rt->stream),
+            "runtime tensor");
+    ET_CUDA(cudaStreamSynchronize(rt->stream), "runtime tensor");
+    return ET_OK;
+}
+
+int et_clear_runtime_tensors(et_runtime* rt) {
+    if (!rt) return ET_ERR_INVALID;
+    cudaSetDevice(rt->cfg.device);
+    for (auto& d : rt->d_rt)
+        if (d.ptr) ET_CUDA(cudaMemsetAsync(d.ptr, 0, d.n * 4, rt->stream), "runtime tensor");
+    return ET_OK;
+}
+
+int et_get_runtime_tensor(et_runtime* rt, int32_t index, int32_t* values, int64_t n) {
+    if (!rt || index < 0 || index >= static_cast<int>(rt->d_rt.size())) return ET_ERR_INVALID;
+    cudaSetDevice(rt->cfg.device);
+    const int64_t m = std::min<int64_t>(n, static_cast<int64_t>(rt->d_rt[static_cast<size_t>(index)].n));
+    ET_CUDA(cudaStreamSynchronize(rt->stream), "runtime tensor");
+    ET_CUDA(cudaMemcpy(values, rt->d_rt[static_cast<size_t>(index)].ptr, static_cast<size_t>(m) * 4, cudaMemcpyDeviceToHost),
+            "runtime tensor");
+    return ET_OK;
+}
+
+static int collect(et_runtime* rt, et_step_info* info) {
+    ET_CUDA(cudaStreamSynchronize(rt->stream), "step");
+    etk::DevStatus st{};
+    const int cur = rt->parity ^ 1;  // parity already advanced past the last launch
+    ET_CUDA(cudaMemcpy(&st, rt->d_status.ptr + cur, sizeof(st), cudaMemcpyDeviceToHost), "status");
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->status = st.code;
+        info->sample_index = rt->last_sample;
+        info->worker = st.worker;
+        info->slot = st.slot;
+        info->counter = st.counter;
+        info->value = st.value;
+        info->tasks_executed = static_cast<int64_t>(st.executed);
+        info->noop_tasks = static_cast<int64_t>(st.noops);
+        info->pushes = static_cast<int64_t>(st.pushes);
+        info->pops = static_cast<int64_t>(st.pops);
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, rt->ev0, rt->ev1) == cudaSuccess) info->kernel_ms = ms;
+    }
+    if (st.code != 0) {
+        // leave the runtime reusable: clear every counter and status block
+        cudaMemset(rt->d_cnt.ptr, 0, rt->d_cnt.n * sizeof(uint32_t));
+        cudaMemset(rt->d_status.ptr, 0, 2 * sizeof(etk::DevStatus));
+        rt->err = st.code == ET_ERR_DEADLOCK    ? "deadlock"
+                  : st.code == ET_ERR_UNDERFLOW ? "counter underflow"
+                                                : "step limit exceeded";
+        return st.code;
+    }
+    return ET_OK;
+}
+
+int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* stream, int32_t synchronous,
+            et_step_info* info) {
+    if (!rt) return ET_ERR_INVALID;
+    if (num_symbols != rt->num_symbols) return rt->fail(ET_ERR_INVALID, "binding has the wrong number of symbols");
+    if (rt->samples.empty()) return rt->fail(ET_ERR_INVALID, "no program uploaded");
+    if (!rt->ops_bound) return rt->fail(ET_ERR_INVALID, "ops not bound");
+    cudaSetDevice(rt->cfg.device);
+    // next-larger covering sample (samples are uploaded in selection order)
+    int pick = -1;
+    for (size_t i = 0; i < rt->samples.size() && pick < 0; ++i) {
+        bool covers = true;
+        for (int k = 0; k < num_symbols; ++k) covers &= rt->samples[i].binding[static_cast<size_t>(k)] >= binding[k];
+        if (covers) pick = static_cast<int>(i);
+    }
+    if (pick < 0) return rt->fail(ET_ERR_INVALID, "binding exceeds every sampled shape");
+    const Sample& S = rt->samples[static_cast<size_t>(pick)];
+    // the actual grids must fit inside the sample's (ref sched_static.cpp:153-156)
+    for (int c = 0; c < rt->num_calls; ++c)
+        for (int d = 0; d < rt->call_rank[static_cast<size_t>(c)]; ++d) {
+            bool ok = true;
+            const int64_t a = eval_host(rt->code_op, rt->code_arg, rt->grid_code_off[static_cast<size_t>(c * 4 + d)],
+                                        rt->grid_code_off[static_cast<size_t>(c * 4 + d + 1)], binding, &ok);
+            if (!ok) return rt->fail(ET_ERR_INVALID, "grid of call " + std::to_string(c) + " is invalid at the binding");
+            if (a > S.call_extents[static_cast<size_t>(c * 4 + d)])
+                return rt->fail(ET_ERR_INVALID, "sampled shape does not cover the actual grid of call " + std::to_string(c));
+        }
+
+    etk::StaticParams p{};
+    p.num_symbols = rt->num_symbols;
+    p.num_calls = rt->num_calls;
+    p.call_rank = rt->d_call_rank.ptr;
+    p.call_extent_from = rt->d_call_extent_from.ptr;
+    p.grid_code_off = rt->d_grid_code_off.ptr;
+    p.code_op = rt->d_code_op.ptr;
+    p.code_arg = reinterpret_cast<const long long*>(rt->d_code_arg.ptr);
+    p.call_extents = S.d_call_extents.ptr;
+    p.num_queues = S.num_queues;
+    p.has_dma = S.has_dma;
+    p.queue_off = S.d_queue_off.ptr;
+    p.num_slots = S.num_slots;
+    p.slot_call = S.d_slot_call.ptr;
+    p.slot_flat = S.d_slot_flat.ptr;
+    p.slot_duration = S.d_slot_duration.ptr;
+    p.wait_off = S.d_wait_off.ptr;
+    p.waits = S.d_waits.ptr;
+    p.notify_off = S.d_notify_off.ptr;
+    p.notifies = S.d_notifies.ptr;
+    p.num_counters = S.num_counters;
+    p.initial_counts = S.d_initial.ptr;
+    p.cnt = rt->d_cnt.ptr + static_cast<size_t>(rt->parity) * static_cast<size_t>(rt->cnt_capacity);
+    p.cnt_other = rt->d_cnt.ptr + static_cast<size_t>(rt->parity ^ 1) * static_cast<size_t>(rt->cnt_capacity);
+    p.cnt_capacity = rt->cnt_capacity;
+    p.rt = rt->d_rt_table.ptr;
+    p.num_rt = static_cast<int>(rt->d_rt.size());
+    for (int i = 0; i < p.num_rt; ++i) {
+        bool ok = true;
+        p.rt_len[i] = eval_host(rt->code_op, rt->code_arg, rt->rt_len_off[static_cast<size_t>(i)],
+                                rt->rt_len_off[static_cast<size_t>(i) + 1], binding, &ok);
+        if (!ok || p.rt_len[i] > rt->rt_capacity[static_cast<size_t>(i)])
+            return rt->fail(ET_ERR_INVALID, "runtime tensor shape invalid at the binding");
+    }
+    p.ops = rt->d_ops.ptr;
+    p.trace = rt->d_trace.ptr;
+    p.record = rt->cfg.record_trace;
+    p.status = rt->d_status.ptr + rt->parity;
+    p.status_other = rt->d_status.ptr + (rt->parity ^ 1);
+    for (int k = 0; k < num_symbols; ++k) p.binding[k] = binding[k];
+    p.watchdog_ns = rt->cfg.watchdog_ns;
+    p.tick_ns = rt->cfg.tick_ns;
+    p.step_limit = rt->cfg.step_limit > 0 ? rt->cfg.step_limit : 0;
+    p.prefetch = rt->cfg.enable_prefetch;
+
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rt->stream;
+    if (synchronous) cudaEventRecord(rt->ev0, st);
+    int e = et_launch_static(p, S.num_queues, st);
+    if (e != 0) return rt->cuda_fail(static_cast<cudaError_t>(e), "launch");
+    if (synchronous) cudaEventRecord(rt->ev1, st);
+    rt->parity ^= 1;
+    rt->last_sample = pick;
+    rt->launched = true;
+    if (!synchronous) return ET_OK;
+    if (st != rt->stream) ET_CUDA(cudaStreamSynchronize(st), "step");
+    return collect(rt, info);
+}
+
+int et_sync(et_runtime* rt, et_step_info* info) {
+    if (!rt) return ET_ERR_INVALID;
+    cudaSetDevice(rt->cfg.device);
+    ET_CUDA(cudaDeviceSynchronize(), "sync");
+    return collect(rt, info);
+}
+
+int et_read_counters(et_runtime* rt, int64_t* out, int64_t n) {
+    if (!rt || rt->last_sample < 0) return ET_ERR_INVALID;
+    cudaSetDevice(rt->cfg.device);
+    const Sample& S = rt->samples[static_cast<size_t>(rt->last_sample)];
+    std::vector<uint32_t> got(static_cast<size_t>(S.num_counters));
+    const int cur = rt->parity ^ 1;
+    ET_CUDA(cudaStreamSynchronize(rt->stream), "counters");
+    if (S.num_counters > 0)
+        ET_CUDA(cudaMemcpy(got.data(), rt->d_cnt.ptr + static_cast<size_t>(cur) * static_cast<size_t>(rt->cnt_capacity),
+                           got.size() * 4, cudaMemcpyDeviceToHost),
+                "counters");
+    for (int64_t i = 0; i < std::min<int64_t>(n, S.num_counters); ++i)
+        out[i] = static_cast<int64_t>(S.initial_counts[static_cast<size_t>(i)]) - static_cast<int64_t>(got[static_cast<size_t>(i)]);
+    return ET_OK;
+}
+
+int et_read_trace(et_runtime* rt, et_trace_rec* out, int64_t* n) {
+    if (!rt || !n || rt->last_sample < 0) return ET_ERR_INVALID;
+    cudaSetDevice(rt->cfg.device);
+    const Sample& S = rt->samples[static_cast<size_t>(rt->last_sample)];
+    const int64_t m = std::min<int64_t>(*n, S.num_slots);
+    ET_CUDA(cudaStreamSynchronize(rt->stream), "trace");
+    if (m > 0) ET_CUDA(cudaMemcpy(out, rt->d_trace.ptr, static_cast<size_t>(m) * sizeof(et_trace_rec), cudaMemcpyDeviceToHost), "trace");
+    *n = S.num_slots;
+    return ET_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,279 @@
+"""Event Tensor graphs for LLM decode and their GPU runtime.
+
+The reference has no transformer template (ref SPEC.md:515); this module
+expresses one decode step of a Llama-style decoder in the reference's own
+graph-spec format (the JSON schema of ref src/json_io.cpp:115-230), lowers it
+with the reference-compatible static scheduler (`lower_static`), binds every
+call to a tile operation of the megakernel and runs it with one persistent
+launch per step.
+
+Graph per layer l (all events are Event Tensors; counts are derived):
+    qkv_l   [T]            waits D_{l-1}[0]      notifies QKV_l[0]
+    attn_l  [kv, ceil(s/CH)] waits QKV_l[0]      notifies A_l[t0]
+    merge_l [kv]           waits A_l[t0], QKV_l[0] notifies M_l[0]
+    oproj_l [T]            waits M_l[0]          notifies O_l[0]
+    gateup_l[T]            waits O_l[0]          notifies G_l[0]
+    down_l  [T]            waits G_l[0]          notifies D_l[0]
+followed by lm_head [T_lm] waiting on D_{L-1}[0].  `s` (cached positions) is
+the graph's symbolic size: one compiled artifact serves every sequence length
+covered by its samples, with out-of-range attention splits masked on device.
+
+Device layout (HBM): weights bf16 row-major [out][in]; the q and k rows of
+Wqkv are stored so that rotary pairs are adjacent (GPT-J style rotation on
+(2j, 2j+1), frequency theta^(-2j/head_dim)), which is Llama's rotate-half
+RoPE up to a fixed permutation of the q/k rows; the residual stream is fp32;
+KV caches are bf16 [kv_heads][capacity][head_dim] per layer.
+"""
+
+import dataclasses
+import json
+import math
+
+import torch
+
+from . import etsim
+from .ops import (
+    EPI_BF16,
+    EPI_F32,
+    EPI_QKV_ROPE,
+    EPI_RESID,
+    EPI_SILU_MUL,
+    OP_ATTN_MERGE,
+    OP_ATTN_SPLIT,
+    OP_EMBED,
+    OP_GEMV,
+    make_op,
+    pack,
+    ptr,
+)
+
+
+@dataclasses.dataclass
+class DecoderConfig:
+    name: str
+    hidden: int
+    layers: int
+    heads: int
+    kv_heads: int
+    head_dim: int
+    intermediate: int
+    vocab: int
+    rope_theta: float = 500000.0
+    eps: float = 1e-5
+    attn_chunk: int = 64
+
+    @property
+    def q_rows(self):
+        return self.heads * self.head_dim
+
+    @property
+    def kv_rows(self):
+        return self.kv_heads * self.head_dim
+
+    def weight_bytes(self):
+        h, i = self.hidden, self.intermediate
+        per_layer = 2 * (h * (self.q_rows + 2 * self.kv_rows) + self.q_rows * h + 3 * h * i + 2 * h)
+        return self.layers * per_layer + 2 * self.vocab * h + 4 * h
+
+    def kv_bytes(self, s, b=1):
+        """Algorithmic KV traffic of one step: read s cached positions, write one."""
+        per_pos = self.layers * 2 * self.kv_rows * 2 * b
+        return per_pos * s + per_pos
+
+    def step_bytes(self, s, b=1):
+        return self.weight_bytes() + self.kv_bytes(s, b)
+
+
+TINY = DecoderConfig("tiny-2L-h256", hidden=256, layers=2, heads=4, kv_heads=2, head_dim=64, intermediate=768,
+                     vocab=1024, rope_theta=10000.0)
+LLAMA3_8B = DecoderConfig("llama3-8b", hidden=4096, layers=32, heads=32, kv_heads=8, head_dim=128,
+                          intermediate=14336, vocab=128256)
+LLAMA3_70B = DecoderConfig("llama3-70b", hidden=8192, layers=80, heads=64, kv_heads=8, head_dim=128,
+                           intermediate=28672, vocab=128256)
+CONFIGS = {c.name: c for c in (TINY, LLAMA3_8B, LLAMA3_70B)}
+
+
+def graph_spec(cfg: DecoderConfig, tasks: int, lm_tasks: int):
+    """Reference-format graph spec of one decode step (symbol `s`)."""
+    CH = cfg.attn_chunk
+    fns, events, calls = [], [], []
+
+    def fn(name, grid):
+        fns.append({"name": name, "grid": grid, "resource": "sm", "duration": "unit"})
+        return name
+
+    def ev(name, shape):
+        events.append({"name": name, "shape": shape})
+        return name
+
+    def call(f, ins=(), outs=()):
+        c = {"fn": f}
+        if ins:
+            c["in"] = [{"event": e, "map": m} for e, m in ins]
+        if outs:
+            c["out"] = [{"event": e, "map": m} for e, m in outs]
+        calls.append(c)
+
+    T, kv = str(tasks), str(cfg.kv_heads)
+    ev("EMB", ["1"])
+    call(fn("embed", ["1"]), outs=[("EMB", ["0"])])
+    prev = "EMB"
+    for l in range(cfg.layers):
+        qkv, a, m, o, g, d = (ev(f"{x}{l}", ["1"]) for x in ("QKV", "A", "M", "O", "G", "D"))
+        events[-5]["shape"] = [kv]  # A_l has one element per kv head
+        call(fn(f"L{l}.qkv", [T]), ins=[(prev, ["0"])], outs=[(qkv, ["0"])])
+        call(fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
+        call(fn(f"L{l}.merge", [kv]), ins=[(a, ["t0"]), (qkv, ["0"])], outs=[(m, ["0"])])
+        call(fn(f"L{l}.oproj", [T]), ins=[(m, ["0"])], outs=[(o, ["0"])])
+        call(fn(f"L{l}.gateup", [T]), ins=[(o, ["0"])], outs=[(g, ["0"])])
+        call(fn(f"L{l}.down", [T]), ins=[(g, ["0"])], outs=[(d, ["0"])])
+        prev = d
+    ev("LM", ["1"])
+    call(fn("lm_head", [str(lm_tasks)]), ins=[(prev, ["0"])], outs=[("LM", ["0"])])
+    return {
+        "symbols": ["s"],
+        "size_symbol": "s",
+        "duration_models": {"unit": {"kind": "constant", "value": 1}},
+        "device_functions": fns,
+        "event_tensors": events,
+        "calls": calls,
+    }
+
+
+def build_graph(cfg, tasks, lm_tasks):
+    return etsim.Graph.from_json(json.dumps(graph_spec(cfg, tasks, lm_tasks)))
+
+
+def rope_inv_freq(cfg):
+    j = torch.arange(0, cfg.head_dim // 2, dtype=torch.float64)
+    return (cfg.rope_theta ** (-2.0 * j / cfg.head_dim)).to(torch.float32)
+
+
+def init_weights(cfg: DecoderConfig, device, seed=0, std=0.02):
+    """Random-init weights of the architecture (bf16, N(0, std)); norms ~ 1 + N(0, 0.01)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def w(*shape):
+        t = torch.empty(*shape, dtype=torch.bfloat16, device=device)
+        t.normal_(0.0, std, generator=g)
+        return t
+
+    def norm():
+        t = torch.empty(cfg.hidden, dtype=torch.float32, device=device)
+        t.normal_(1.0, 0.01, generator=g)
+        return t
+
+    W = {"embed": w(cfg.vocab, cfg.hidden), "final_norm": norm(), "lm_head": w(cfg.vocab, cfg.hidden), "layers": []}
+    for _ in range(cfg.layers):
+        W["layers"].append({
+            "attn_norm": norm(),
+            "wqkv": w(cfg.q_rows + 2 * cfg.kv_rows, cfg.hidden),
+            "wo": w(cfg.hidden, cfg.q_rows),
+            "ffn_norm": norm(),
+            "wgate": w(cfg.intermediate, cfg.hidden),
+            "wup": w(cfg.intermediate, cfg.hidden),
+            "wdown": w(cfg.hidden, cfg.intermediate),
+        })
+    return W
+
+
+class DecodeModel:
+    """One decoder + its lowered megakernel, ready to run decode steps.
+
+    `samples` are the sequence lengths the static program is lowered for; any
+    `s` up to the largest runs on the next-larger sample without re-lowering.
+    """
+
+    def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
+                 seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None):
+        if not etsim.gpu_available():
+            raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
+        self.cfg = cfg
+        self.device = torch.device(device)
+        props = torch.cuda.get_device_properties(self.device)
+        self.num_workers = num_workers or props.multi_processor_count
+        self.tasks = self.num_workers
+        self.lm_tasks = lm_tasks or self.num_workers
+        self.samples = sorted(int(s) for s in samples)
+        self.capacity = capacity or (self.samples[-1] + 1)
+        self.max_splits = max(1, (self.samples[-1] + cfg.attn_chunk - 1) // cfg.attn_chunk)
+
+        import time
+        t0 = time.perf_counter()
+        self.graph = build_graph(cfg, self.tasks, self.lm_tasks)
+        self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
+        self.lower_ms = (time.perf_counter() - t0) * 1e3
+
+        dev = self.device
+        self.W = weights if weights is not None else init_weights(cfg, dev, seed)
+        self.kcache = [torch.zeros(cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
+                       for _ in range(cfg.layers)]
+        self.vcache = [torch.zeros_like(k) for k in self.kcache]
+        self.tokens = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.h_a = torch.zeros(1, cfg.hidden, dtype=torch.float32, device=dev)
+        self.h_b = torch.zeros_like(self.h_a)
+        self.q = torch.zeros(cfg.q_rows, dtype=torch.float32, device=dev)
+        self.attn = torch.zeros(cfg.q_rows, dtype=torch.bfloat16, device=dev)
+        self.act = torch.zeros(cfg.intermediate, dtype=torch.bfloat16, device=dev)
+        self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=dev)
+        self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        self.inv_freq = rope_inv_freq(cfg).to(dev)
+
+        t1 = time.perf_counter()
+        self.executor = etsim.Executor(self.kernel, device=self.device.index or 0, num_workers=self.num_workers,
+                                       record_trace=record_trace, prefetch=prefetch)
+        self.executor.bind_ops(pack(self._ops()))
+        self.upload_ms = (time.perf_counter() - t1) * 1e3
+
+    # ------------------------------------------------------------------
+    def _ops(self):
+        cfg, W = self.cfg, self.W
+        H, dh, CH = cfg.hidden, cfg.head_dim, cfg.attn_chunk
+        ops = [make_op(OP_EMBED, i=[H, -1], p=[ptr(W["embed"]), ptr(self.tokens), ptr(self.h_a)])]
+        s_slot = 0
+        scale = 1.0 / math.sqrt(dh)
+        G = cfg.heads // cfg.kv_heads
+        for l, L in enumerate(W["layers"]):
+            kc, vc = self.kcache[l], self.vcache[l]
+            ops.append(make_op(OP_GEMV, i=[cfg.q_rows + 2 * cfg.kv_rows, H, 1, 1, EPI_QKV_ROPE, -1, s_slot, 2, dh, H,
+                                           cfg.q_rows, cfg.kv_rows, self.capacity],
+                               f=[cfg.eps], p=[ptr(L["wqkv"]), 0, ptr(self.h_a), ptr(L["attn_norm"]), ptr(self.q), 0,
+                                               ptr(kc), ptr(vc), ptr(self.inv_freq)]))
+            attn_i = [dh, G, CH, self.capacity, s_slot, self.max_splits, cfg.kv_heads]
+            ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale],
+                               p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials)]))
+            ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale],
+                               p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn)]))
+            ops.append(make_op(OP_GEMV, i=[H, cfg.q_rows, 1, 0, EPI_RESID, -1, 0, 1],
+                               p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_b), ptr(self.h_a)]))
+            ops.append(make_op(OP_GEMV, i=[cfg.intermediate, H, 2, 1, EPI_SILU_MUL, -1, 0, 1, 0, H],
+                               f=[cfg.eps], p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(self.h_b), ptr(L["ffn_norm"]),
+                                               ptr(self.act)]))
+            ops.append(make_op(OP_GEMV, i=[H, cfg.intermediate, 1, 0, EPI_RESID, -1, 0, 1],
+                               p=[ptr(L["wdown"]), 0, ptr(self.act), 0, ptr(self.h_a), ptr(self.h_b)]))
+        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 1, 0, H], f=[cfg.eps],
+                           p=[ptr(W["lm_head"]), 0, ptr(self.h_a), ptr(W["final_norm"]), ptr(self.logits)]))
+        return ops
+
+    def fill_cache(self, s, seed=1):
+        """Synthetic prefilled KV cache: N(0, 1) bf16 for positions [0, s)."""
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        for k, v in zip(self.kcache, self.vcache):
+            k.zero_()
+            v.zero_()
+            k[:, :s].normal_(0.0, 1.0, generator=g)
+            v[:, :s].normal_(0.0, 1.0, generator=g)
+
+    def set_token(self, token):
+        self.tokens.fill_(int(token))
+
+    def step(self, s):
+        """One synchronous decode step at position s; returns device logits [1, vocab]."""
+        stats = self.executor.run({"s": int(s)})
+        self.last_stats = stats
+        return self.logits
+
+    def launch(self, s, stream=0):
+        self.executor.launch({"s": int(s)}, stream)

@@ -1,0 +1,53 @@
+"""Decode-step numerics: megakernel logits vs the CPU fp32 oracle on the same
+random-init weights (oracle/decoder_oracle.py).  Tolerances (bf16 weights,
+fp32 accumulation):
+  * vs the bf16-emulating oracle: max |err| <= 2e-3 * max|logit| + 2e-3
+  * vs the pure fp32 oracle:      max |err| <= 5e-2 * max|logit| + 5e-2
+and the appended K/V rows must equal the oracle's bf16 rows to 1 bf16 ulp."""
+
+import pytest
+import torch
+
+from oracle.decoder_oracle import decode_step, weights_to_cpu
+from paper_2604_13327_b200.decode import TINY, DecodeModel
+
+pytestmark = pytest.mark.gpu
+
+
+def _errs(got, want):
+    err = (got - want).abs().max().item()
+    scale = want.abs().max().item()
+    return err, scale
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return DecodeModel(TINY, samples=(16, 64), num_workers=16, seed=0, record_trace=True)
+
+
+@pytest.mark.parametrize("s", [16, 10, 40, 0, 64])
+def test_tiny_logits_match_oracle(tiny, s):
+    m = tiny
+    m.fill_cache(s, seed=1)
+    m.set_token(7)
+    cpu_k = [k.cpu() for k in m.kcache]
+    cpu_v = [v.cpu() for v in m.vcache]
+    logits = m.step(s)[0].cpu()
+    Wc = weights_to_cpu(m.W)
+    inv = m.inv_freq.cpu()
+    ref, nk, nv = decode_step(m.cfg, Wc, cpu_k, cpu_v, 7, s, inv, emulate_bf16=True)
+    err, scale = _errs(logits, ref)
+    assert err <= 2e-3 * scale + 2e-3, (s, err, scale)
+    ref32, _, _ = decode_step(m.cfg, Wc, cpu_k, cpu_v, 7, s, inv, emulate_bf16=False)
+    err32, scale32 = _errs(logits, ref32)
+    assert err32 <= 5e-2 * scale32 + 5e-2, (s, err32, scale32)
+    for l in range(m.cfg.layers):
+        dk = m.kcache[l][:, s].float().cpu()
+        dv = m.vcache[l][:, s].float().cpu()
+        assert torch.allclose(dk, nk[l], rtol=1e-2, atol=1e-2)
+        assert torch.allclose(dv, nv[l], rtol=1e-2, atol=1e-2)
+    t = m.executor.trace()
+    mg = m.graph.instantiate({"s": s})
+    assert mg.check(t) == []
+    assert all(c == 0 for c in m.executor.final_counters())
+    assert m.last_stats["tasks_executed"] == mg.num_tasks
