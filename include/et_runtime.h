@@ -83,6 +83,10 @@ typedef struct et_config {
     int64_t watchdog_ns;     /* a wait spinning longer than this reports deadlock   */
     int64_t tick_ns;         /* synthetic body length per duration unit            */
     int64_t step_limit;      /* > 0: abort after this many executed tasks (StepLimit) */
+    int32_t max_batch;       /* largest batch a GEMV tile sees (<= 8)               */
+    int32_t reserved;
+    int64_t l2_prefetch_bytes; /* per worker: weights prefetched into L2 beyond the
+                                  shared-memory ring (< 0: default)                  */
 } et_config;
 
 /* Shape-independent description of the graph (uploaded once). */
@@ -153,13 +157,14 @@ typedef struct et_dynamic_desc {
 /* Per-slot (static) or per-task (dynamic) trace record, nanoseconds of
  * %globaltimer.  flags bit0 = masked no-op. */
 typedef struct et_trace_rec {
-    int64_t t_begin;      /* slot reached / task popped */
-    int64_t t_wait_end;   /* all waits satisfied        */
-    int64_t t_exec_end;   /* body finished              */
-    int64_t t_notify_end; /* all notifies issued        */
+    int64_t t_begin;      /* slot reached / task popped                 */
+    int64_t t_wait_end;   /* all waits satisfied                        */
+    int64_t t_prologue;   /* body prologue done (activations staged), 0 if none */
+    int64_t t_exec_end;   /* body finished                              */
+    int64_t t_notify_end; /* all notifies issued                        */
     int32_t worker;
     int32_t flags;
-    int32_t task;         /* slot index (static) / task id (dynamic) */
+    int32_t task;         /* slot index (static) / task id (dynamic)    */
     int32_t pad;
 } et_trace_rec;
 

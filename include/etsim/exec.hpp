@@ -23,6 +23,8 @@ struct ExecConfig {
     Int tick_ns = 0;            // synthetic task body: ns per duration unit
     Int seed = 0;               // duration-model seed for synthetic bodies
     Int step_limit = 0;         // > 0: SimError::StepLimit after this many tasks
+    int max_batch = 1;          // largest GEMV batch (<= 8 on the mma.sync GEMV path)
+    Int l2_prefetch_bytes = -1; // per worker L2 run-ahead beyond the smem ring (-1: default)
 };
 
 struct StepStats {

@@ -175,6 +175,8 @@ Executor::Executor(const StaticMegakernel& k, const ExecConfig& cfg) : impl_(new
     ec.watchdog_ns = cfg.watchdog_ns;
     ec.tick_ns = cfg.tick_ns;
     ec.step_limit = cfg.step_limit;
+    ec.max_batch = cfg.max_batch;
+    ec.l2_prefetch_bytes = cfg.l2_prefetch_bytes;
     const int rc = et_create(&ec, &I.rt);
     if (rc != ET_OK) raise_status(rc, "cannot create the GPU runtime");
 
@@ -299,8 +301,12 @@ StepStats Executor::run(const ShapeBinding& b) {
     I.last_binding = b;
     I.last_sample = si.sample_index;
     if (rc != ET_OK) {
-        std::string where = et_last_error(I.rt);
-        if (rc == ET_ERR_DEADLOCK && si.sample_index >= 0 && si.slot >= 0) {
+        std::string where = std::string(et_last_error(I.rt)) + " (worker " + std::to_string(si.worker) + ", slot " +
+                            std::to_string(si.slot) + ", counter " + std::to_string(si.counter) + ", value " +
+                            std::to_string(si.value) + ")";
+        if (si.counter == -2) where += ": a consumer ring stage never filled";
+        if (si.counter == -3) where += ": the producer never got a free ring stage";
+        if (rc == ET_ERR_DEADLOCK && si.sample_index >= 0 && si.slot >= 0 && si.counter >= 0) {
             const HostSample& h = I.hs[static_cast<size_t>(si.sample_index)];
             const int call = h.slot_call[static_cast<size_t>(si.slot)];
             where = (si.worker == h.num_queues ? std::string("DMA") : "SM" + std::to_string(si.worker)) +
@@ -359,6 +365,7 @@ Trace Executor::trace() const {
         const int nn = h.notify_off[s + 1] - h.notify_off[s];
         for (int i = 0; i < nw; ++i) tr.waits.push_back(i == 0 ? Interval{tb, tw} : Interval{tw, tw});
         tr.exec = tr.noop ? Interval{tw, tw} : Interval{tw, te};
+        if (r.t_prologue > 0 && !tr.noop) tr.prefetch = Interval{tw, r.t_prologue - base};  // staging of activations
         for (int i = 0; i < nn; ++i) tr.notifies.push_back(i == 0 ? Interval{te, tn} : Interval{tn, tn});
         last = std::max({last, tr.exec.end, nn ? tn : tr.exec.end, nw ? tw : Int(0)});
         t.tasks.push_back(std::move(tr));

@@ -33,6 +33,7 @@ struct SlotInfo {
     int coord[kMaxRank];
     int ext0;  // sample extent of dim 0 (GEMV task count)
     bool masked;
+    bool lazy;
 };
 
 __device__ __forceinline__ long long eval_code(const StaticParams& P, int call, int d) {
@@ -78,18 +79,22 @@ __device__ __forceinline__ SlotInfo slot_info(const StaticParams& P, int s) {
         flat /= sext[d];
     }
     si.masked = false;
-    long long aflat = 0;
-    for (int d = 0; d < si.rank; ++d) {
-        const long long a = eval_code(P, si.call, d);
-        if (si.coord[d] >= a) si.masked = true;
-        aflat = aflat * a + si.coord[d];
-    }
-    const int ef = __ldg(P.call_extent_from + si.call);
-    if (!si.masked && ef >= 0 && P.rt_len[ef] > 0) {
-        const long long live = __ldcg(P.rt[ef] + P.rt_len[ef] - 1);
-        if (aflat >= live) si.masked = true;
-    }
+    for (int d = 0; d < si.rank; ++d)
+        if (si.coord[d] >= eval_code(P, si.call, d)) si.masked = true;
+    si.lazy = __ldg(P.call_extent_from + si.call) >= 0;
     return si;
+}
+
+// extent_from masking (ref simulate.cpp:199-202): tasks whose row-major index
+// in the actual grid is at or beyond the realized count are no-ops.  Only
+// valid once the writer of the indptr tensor has finished (after the waits).
+__device__ bool extent_masked(const StaticParams& P, int call, const int* coord) {
+    const int ef = __ldg(P.call_extent_from + call);
+    if (ef < 0 || P.rt_len[ef] <= 0) return false;
+    const int rank = __ldg(P.call_rank + call);
+    long long aflat = 0;
+    for (int d = 0; d < rank; ++d) aflat = aflat * eval_code(P, call, d) + coord[d];
+    return aflat >= static_cast<long long>(__ldcg(P.rt[ef] + P.rt_len[ef] - 1));
 }
 
 __device__ __forceinline__ void report(DevStatus* st, int code, int worker, int slot, int counter, int value) {
@@ -105,35 +110,34 @@ __device__ __forceinline__ bool aborted(const DevStatus* st) {
     return *reinterpret_cast<const volatile int*>(&st->code) != 0;
 }
 
-// Spin until every wait element of slot s has received its initial count.
-__device__ bool wait_slot(const StaticParams& P, int s, int worker) {
-    const int b = __ldg(P.wait_off + s), e = __ldg(P.wait_off + s + 1);
+// Spin until every wait element in [b, e) has received its initial count.
+// Acquire loads: the producer's data written before its release increment is
+// visible to this thread, and to the rest of the CTA after the barrier that
+// follows (PTX causality order through bar.sync).
+__device__ bool wait_range(const StaticParams& P, int b, int e, int s, int worker) {
     for (int w = b; w < e; ++w) {
         const int el = __ldg(P.waits + w);
         const uint32_t need = static_cast<uint32_t>(__ldg(P.initial_counts + el));
-        uint32_t v = ld_relaxed(P.cnt + el);
-        if (v < need) {
-            const uint64_t t0 = globaltimer();
-            uint32_t it = 0;
-            while ((v = ld_relaxed(P.cnt + el)) < need) {
-                if ((++it & 255u) == 0) {
-                    if (aborted(P.status)) return false;
-                    if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
-                        report(P.status, ET_ERR_DEADLOCK, worker, s, el, static_cast<int>(need - v));
-                        return false;
-                    }
+        uint32_t v = ld_acquire(P.cnt + el);
+        if (v >= need) continue;
+        const uint64_t t0 = globaltimer();
+        uint32_t it = 0;
+        while ((v = ld_acquire(P.cnt + el)) < need) {
+            if ((++it & 255u) == 0) {
+                if (aborted(P.status)) return false;
+                if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                    report(P.status, ET_ERR_DEADLOCK, worker, s, el, static_cast<int>(need - v));
+                    return false;
                 }
             }
         }
     }
-    fence_acq_rel_gpu();
     return true;
 }
 
-__device__ bool notify_slot(const StaticParams& P, int s, int worker) {
-    const int b = __ldg(P.notify_off + s), e = __ldg(P.notify_off + s + 1);
-    if (b == e) return true;
-    fence_acq_rel_gpu();
+// Release increments: the consumer warps' writes precede this thread's
+// release through the barrier the caller executed just before.
+__device__ bool notify_range(const StaticParams& P, int b, int e, int s, int worker) {
     bool ok = true;
     for (int n = b; n < e; ++n) {
         const int el = __ldg(P.notifies + n);
@@ -146,26 +150,107 @@ __device__ bool notify_slot(const StaticParams& P, int s, int worker) {
     return ok;
 }
 
+__device__ __forceinline__ bool wait_slot(const StaticParams& P, int s, int worker) {
+    return wait_range(P, __ldg(P.wait_off + s), __ldg(P.wait_off + s + 1), s, worker);
+}
+__device__ __forceinline__ bool notify_slot(const StaticParams& P, int s, int worker) {
+    return notify_range(P, __ldg(P.notify_off + s), __ldg(P.notify_off + s + 1), s, worker);
+}
+
 // ---------------------------------------------------------------------------
-// Consumer-side ring cursor (identical in every consumer thread).
+// Per-CTA slot table in shared memory, filled once per launch: the task loop
+// then needs no dependent global loads to find a slot's call, coordinates,
+// mask and wait/notify ranges.  Entry = {call | masked<<31 | lazy<<30,
+// c0 | c1<<16, wait_off, notify_off}; a sentinel entry closes the ranges.
+struct SlotTable {
+    const uint4* ent;
+    const int* ext0;
+    bool valid;
+};
+
+struct SlotView {
+    int call;
+    bool masked;
+    bool lazy;  // extent_from call: mask known only after the waits
+    int coord[kMaxRank];
+    int ext0;
+    int wb, we, nb, ne;
+};
+
+__device__ __forceinline__ SlotView view_slot(const StaticParams& P, const SlotTable& T, int s, int qb) {
+    SlotView v;
+    if (T.valid) {
+        const uint4 a = T.ent[s - qb];
+        const uint4 b = T.ent[s - qb + 1];
+        v.call = static_cast<int>(a.x & 0x3fffffffu);
+        v.masked = (a.x >> 31) != 0;
+        v.lazy = ((a.x >> 30) & 1u) != 0;
+        v.coord[0] = static_cast<int>(a.y & 0xffffu);
+        v.coord[1] = static_cast<int>(a.y >> 16);
+        v.coord[2] = v.coord[3] = 0;
+        v.ext0 = T.ext0[v.call];
+        v.wb = static_cast<int>(a.z);
+        v.we = static_cast<int>(b.z);
+        v.nb = static_cast<int>(a.w);
+        v.ne = static_cast<int>(b.w);
+    } else {
+        const SlotInfo si = slot_info(P, s);
+        v.call = si.call;
+        v.masked = si.masked;
+        v.lazy = si.lazy;
+        for (int d = 0; d < kMaxRank; ++d) v.coord[d] = si.coord[d];
+        v.ext0 = si.ext0;
+        v.wb = __ldg(P.wait_off + s);
+        v.we = __ldg(P.wait_off + s + 1);
+        v.nb = __ldg(P.notify_off + s);
+        v.ne = __ldg(P.notify_off + s + 1);
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Ring protocol.  The producer fills stages in chunk-sequence order c = 0, 1,
+// 2, ... (stage c % kStages, parity (c / kStages) & 1).  Chunk c is owned by
+// consumer warp c % kConsumerWarps: the owner (or, for chunks all warps read,
+// the owner after a consumer barrier) releases the stage with one arrive, so
+// the empty barriers count 1.  Every consumer thread tracks the same 64-bit
+// sequence number, so no per-stage state has to be shared.
 struct Ring {
     uint8_t* buf;
     uint64_t* full;
     uint64_t* empty;
-    int stage;
-    uint32_t phase;
+    unsigned long long seq;  // sequence number of the next chunk to consume
+    DevStatus* status;
+    long long watchdog_ns;
+    int worker;
 
-    __device__ __forceinline__ const uint8_t* acquire() {
-        mbar_wait(&full[stage], phase);
-        return buf + stage * kStageBytes;
+    __device__ __forceinline__ static int stage_of(unsigned long long c) { return static_cast<int>(c % kStages); }
+    __device__ __forceinline__ static uint32_t parity_of(unsigned long long c) {
+        return static_cast<uint32_t>((c / kStages) & 1ull);
     }
-    __device__ __forceinline__ void release(int lane) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1u;
+    // Bounded wait: a stage that never fills (protocol bug, aborted producer)
+    // reports a deadlock instead of hanging the device.  Returns nullptr then.
+    __device__ __forceinline__ const uint8_t* wait(unsigned long long c) {
+        const int st = stage_of(c);
+        const uint32_t par = parity_of(c);
+        if (!mbar_try_wait(&full[st], par)) {
+            const uint64_t t0 = globaltimer();
+            uint32_t it = 0;
+            while (!mbar_try_wait(&full[st], par)) {
+                if ((++it & 1023u) == 0) {
+                    if (aborted(status)) return nullptr;
+                    if (globaltimer() - t0 > static_cast<uint64_t>(watchdog_ns)) {
+                        report(status, ET_ERR_DEADLOCK, worker, -1, -2, static_cast<int>(c & 0x7fffffff));
+                        return nullptr;
+                    }
+                }
+            }
         }
+        return buf + st * kStageBytes;
+    }
+    __device__ __forceinline__ void release(unsigned long long c) { mbar_arrive(&empty[stage_of(c)]); }
+    __device__ __forceinline__ static int owner(unsigned long long c) {
+        return static_cast<int>(c % kConsumerWarps);
     }
 };
 
@@ -176,10 +261,10 @@ __device__ __forceinline__ int batch_of(const et_op& op, const StaticParams& P) 
 // ---------------------------------------------------------------------------
 // Tile bodies.  `ctid` in [0, kConsumers); bar id 1 syncs the consumer warps.
 
-__device__ void body_splitk(const StaticParams& P, const et_op& op, const SlotInfo& si, int ctid) {
+__device__ void body_splitk(const StaticParams& P, const et_op& op, const int* coord, int ctid) {
     if (op.kind == ET_OP_SPLITK_PARTIAL) {
         const int L = op.i[0], parts = op.i[1];
-        const int row = si.coord[0], part = si.coord[1];
+        const int row = coord[0], part = coord[1];
         const int* data = reinterpret_cast<const int*>(op.p[0]) + (static_cast<long long>(row) * parts + part) * L;
         int acc = 0;
         for (int i = ctid; i < L; i += kConsumers) acc += __ldcg(data + i);
@@ -194,7 +279,7 @@ __device__ void body_splitk(const StaticParams& P, const et_op& op, const SlotIn
         }
     } else {
         const int parts = op.i[1];
-        const int row = si.coord[0];
+        const int row = coord[0];
         if (ctid == 0) {
             const int* part = reinterpret_cast<const int*>(op.p[1]) + row * parts;
             int t = 0;
@@ -204,9 +289,14 @@ __device__ void body_splitk(const StaticParams& P, const et_op& op, const SlotIn
     }
 }
 
-template <int NB>
-__device__ void body_gemv(const StaticParams& P, const et_op& op, const SlotInfo& si, uint16_t* xs, float* acc,
-                          float* red, Ring& ring, int ctid) {
+// Row-range GEMV y[b][r] = sum_k W[r][k] x[b][k] for rows [r0, r1) of a
+// row-major bf16 weight (K % 256 == 0).  The weight rows stream through the
+// shared-memory ring; each consumer warp owns whole 16 KB chunks and walks
+// them in 512-byte groups (32 lanes x 16 bytes), each group inside one row.
+// Products use FHFMA.BF16 (bf16 x bf16 -> fp32 accumulate), four groups in
+// flight per lane; every row run is warp-reduced once into shared memory.
+__device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
+                              float* red, Ring& ring, int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int N = op.i[0], K = op.i[1], nseg = op.i[2];
     const int nb = batch_of(op, P);
@@ -214,91 +304,131 @@ __device__ void body_gemv(const StaticParams& P, const et_op& op, const SlotInfo
     gemv_rows(op, si.coord[0], si.ext0, &r0, &r1);
     const int R = r1 - r0;
 
-    // ---- prologue: activations into shared memory (bf16), accumulators zeroed
+    // ---- prologue: activations into shared memory (bf16 [nb][K]), accumulators zeroed
     if (op.i[3] == 0) {
         const uint16_t* x = reinterpret_cast<const uint16_t*>(op.p[2]);
         const int nv = nb * K / 8;
         for (int v = ctid; v < nv; v += kConsumers)
             reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x) + v);
     } else {
+        // RMSNorm prologue: one pass over the fp32 residual stream held in
+        // registers (K <= 8192), sum of squares reduced across the CTA
         const float* h = reinterpret_cast<const float*>(op.p[2]);
         const float* gam = reinterpret_cast<const float*>(op.p[3]);
         const int stride = op.i[9];
-        float ss[NB];
-#pragma unroll
-        for (int bi = 0; bi < NB; ++bi) ss[bi] = 0.f;
-        for (int bi = 0; bi < nb; ++bi)
-            for (int k = ctid * 4; k < K; k += kConsumers * 4) {
-                const float4 v = ldcg_f4(h + static_cast<long long>(bi) * stride + k);
-                ss[bi] += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-            }
-#pragma unroll
-        for (int bi = 0; bi < NB; ++bi) {
-            const float t = warp_sum(ss[bi]);
-            if (lane == 0) red[warp * NB + bi] = t;
-        }
-        bar_sync(1, kConsumers);
+        constexpr int kMaxPer = 8;  // float4 per thread: K <= 8192
         for (int bi = 0; bi < nb; ++bi) {
-            float t = 0.f;
-            for (int w = 0; w < kConsumerWarps; ++w) t += red[w * NB + bi];
-            const float scale = rsqrtf(t / static_cast<float>(K) + op.f[0]);
-            for (int k = ctid * 4; k < K; k += kConsumers * 4) {
-                const float4 v = ldcg_f4(h + static_cast<long long>(bi) * stride + k);
-                const float4 g = __ldg(reinterpret_cast<const float4*>(gam + k));
-                uint2 o;
-                o.x = static_cast<uint32_t>(f2bf(v.x * scale * g.x)) | (static_cast<uint32_t>(f2bf(v.y * scale * g.y)) << 16);
-                o.y = static_cast<uint32_t>(f2bf(v.z * scale * g.z)) | (static_cast<uint32_t>(f2bf(v.w * scale * g.w)) << 16);
-                *reinterpret_cast<uint2*>(xs + bi * K + k) = o;
-            }
-        }
-    }
-    for (int i = ctid; i < nseg * R * NB; i += kConsumers) acc[i] = 0.f;
-    bar_sync(1, kConsumers);
-
-    // ---- main loop: consume the streamed weight rows chunk by chunk
-    const int vpr = K / 8;  // 16-byte vectors per row (multiple of 32)
-    float run[NB];
-    int cur = -1;
+            float4 hv[kMaxPer], gv[kMaxPer];
+            float ss = 0.f;
 #pragma unroll
-    for (int bi = 0; bi < NB; ++bi) run[bi] = 0.f;
-    auto flush = [&]() {
-        if (cur < 0) return;
-#pragma unroll
-        for (int bi = 0; bi < NB; ++bi) {
-            if (bi < nb) {
-                const float t = warp_sum(run[bi]);
-                if (lane == 0) atomicAdd(&acc[cur * NB + bi], t);
-            }
-            run[bi] = 0.f;
-        }
-    };
-    constexpr int kVecPerStage = kStageBytes / 16;
-    for (int seg = 0; seg < nseg; ++seg) {
-        const long long total_vec = static_cast<long long>(R) * vpr;
-        const int nch = static_cast<int>((total_vec + kVecPerStage - 1) / kVecPerStage);
-        for (int ch = 0; ch < nch; ++ch) {
-            const uint8_t* buf = ring.acquire();
-            const long long vb = static_cast<long long>(ch) * kVecPerStage;
-            long long ve = vb + kVecPerStage;
-            if (ve > total_vec) ve = total_vec;
-            const int ngroups = static_cast<int>((ve - vb) >> 5);
-            for (int g = warp; g < ngroups; g += kConsumerWarps) {
-                const long long v0 = vb + (static_cast<long long>(g) << 5);
-                const int row = seg * R + static_cast<int>(v0 / vpr);
-                const int kv = static_cast<int>(v0 % vpr) + lane;
-                if (row != cur) {
-                    flush();
-                    cur = row;
+            for (int j = 0; j < kMaxPer; ++j) {
+                const int k = (ctid + j * kConsumers) * 4;
+                if (k < K) {
+                    hv[j] = ldcg_f4(h + static_cast<long long>(bi) * stride + k);
+                    gv[j] = __ldg(reinterpret_cast<const float4*>(gam + k));
                 }
-                const uint4 w = lds128(buf + ((g << 5) + lane) * 16);
-#pragma unroll
-                for (int bi = 0; bi < NB; ++bi)
-                    if (bi < nb) run[bi] += dot8(w, lds128(xs + bi * K + kv * 8));
             }
-            ring.release(lane);
+#pragma unroll
+            for (int j = 0; j < kMaxPer; ++j)
+                if ((ctid + j * kConsumers) * 4 < K)
+                    ss += hv[j].x * hv[j].x + hv[j].y * hv[j].y + hv[j].z * hv[j].z + hv[j].w * hv[j].w;
+            ss = warp_sum(ss);
+            if (lane == 0) red[warp] = ss;
+            bar_sync(1, kConsumers);
+            float t = 0.f;
+#pragma unroll
+            for (int w = 0; w < kConsumerWarps; ++w) t += red[w];
+            const float scale = rsqrtf(t / static_cast<float>(K) + op.f[0]);
+#pragma unroll
+            for (int j = 0; j < kMaxPer; ++j) {
+                const int k = (ctid + j * kConsumers) * 4;
+                if (k < K) {
+                    const float4 g = gv[j];
+                    uint2 o;
+                    o.x = static_cast<uint32_t>(f2bf(hv[j].x * scale * g.x)) |
+                          (static_cast<uint32_t>(f2bf(hv[j].y * scale * g.y)) << 16);
+                    o.y = static_cast<uint32_t>(f2bf(hv[j].z * scale * g.z)) |
+                          (static_cast<uint32_t>(f2bf(hv[j].w * scale * g.w)) << 16);
+                    *reinterpret_cast<uint2*>(xs + bi * K + k) = o;
+                }
+            }
+            if (bi + 1 < nb) bar_sync(1, kConsumers);  // red[] is reused
         }
     }
-    flush();
+    for (int i = ctid; i < nseg * R * nb; i += kConsumers) acc[i] = 0.f;
+    bar_sync(1, kConsumers);
+    const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
+
+    // ---- main loop
+    const int gpr = K / 256;  // 512-byte groups per weight row
+    constexpr int kGroupsPerChunk = kStageBytes / 512;
+    unsigned long long c = ring.seq;
+    for (int seg = 0; seg < nseg; ++seg) {
+        const long long seg_groups = static_cast<long long>(R) * gpr;
+        const int nch = static_cast<int>((seg_groups + kGroupsPerChunk - 1) / kGroupsPerChunk);
+        for (int ch = 0; ch < nch; ++ch, ++c) {
+            if (Ring::owner(c) != warp) continue;
+            const uint8_t* buf = ring.wait(c);
+            if (!buf) continue;  // aborted: the step reports an error
+            const long long g0 = static_cast<long long>(ch) * kGroupsPerChunk;
+            const int ng = static_cast<int>(seg_groups - g0 < kGroupsPerChunk ? seg_groups - g0 : kGroupsPerChunk);
+            int row = seg * R + static_cast<int>(g0 / gpr);
+            int kg = static_cast<int>(g0 % gpr);
+            const uint4* wbase = reinterpret_cast<const uint4*>(buf) + lane;
+            const uint4* xbase = reinterpret_cast<const uint4*>(xs) + lane;
+            const int xrow4 = K / 8;  // uint4 per activation row
+            int j = 0;
+            while (j < ng) {
+                const int len = (gpr - kg < ng - j) ? gpr - kg : ng - j;
+                const uint4* wp = wbase + j * 32;
+                const uint4* xp = xbase + kg * 32;
+                if (nb == 1) {
+                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
+                    int t = 0;
+                    for (; t + 4 <= len; t += 4) {
+                        uint4 w[4], x[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) w[u] = wp[(t + u) * 32];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) x[u] = xp[(t + u) * 32];
+                        dot8_bf16(a0, a1, w[0], x[0]);
+                        dot8_bf16(a2, a3, w[1], x[1]);
+                        dot8_bf16(a4, a5, w[2], x[2]);
+                        dot8_bf16(a6, a7, w[3], x[3]);
+                    }
+                    for (; t < len; ++t) dot8_bf16(a0, a1, wp[t * 32], xp[t * 32]);
+                    const float v = warp_sum(((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7)));
+                    if (lane == 0) atomicAdd(&acc[row], v);
+                } else {
+                    float lo[kMaxBatch], hi[kMaxBatch];
+#pragma unroll
+                    for (int bi = 0; bi < kMaxBatch; ++bi) lo[bi] = hi[bi] = 0.f;
+                    for (int t = 0; t < len; ++t) {
+                        const uint4 w = wp[t * 32];
+#pragma unroll
+                        for (int bi = 0; bi < kMaxBatch; ++bi)
+                            if (bi < nb) dot8_bf16(lo[bi], hi[bi], w, xp[t * 32 + bi * xrow4]);
+                    }
+#pragma unroll
+                    for (int bi = 0; bi < kMaxBatch; ++bi) {
+                        if (bi < nb) {
+                            const float v = warp_sum(lo[bi] + hi[bi]);
+                            if (lane == 0) atomicAdd(&acc[row * nb + bi], v);
+                        }
+                    }
+                }
+                j += len;
+                kg += len;
+                if (kg == gpr) {
+                    kg = 0;
+                    ++row;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) ring.release(c);
+        }
+    }
+    ring.seq = c;
     bar_sync(1, kConsumers);
 
     // ---- epilogue
@@ -312,7 +442,7 @@ __device__ void body_gemv(const StaticParams& P, const et_op& op, const SlotInfo
         uint16_t* vc = reinterpret_cast<uint16_t*>(op.p[7]);
         for (int pr = ctid; pr < R / 2; pr += kConsumers) {
             const int row = r0 + 2 * pr;
-            float a = acc[(2 * pr) * NB], b = acc[(2 * pr + 1) * NB];
+            float a = acc[(2 * pr) * nb], b = acc[(2 * pr + 1) * nb];
             if (row < nq + nkv) {  // q or k: rotate the interleaved pair
                 const int d = row % dh;
                 const float inv = __ldg(invf + d / 2);
@@ -337,7 +467,7 @@ __device__ void body_gemv(const StaticParams& P, const et_op& op, const SlotInfo
     } else {
         for (int idx = ctid; idx < R * nb; idx += kConsumers) {
             const int i = idx / nb, bi = idx % nb;
-            const float v = acc[i * NB + bi];
+            const float v = acc[i * nb + bi];
             const long long o = static_cast<long long>(bi) * N + r0 + i;
             if (epi == EPI_F32) {
                 reinterpret_cast<float*>(op.p[4])[o] = v;
@@ -346,15 +476,16 @@ __device__ void body_gemv(const StaticParams& P, const et_op& op, const SlotInfo
             } else if (epi == EPI_RESID) {
                 reinterpret_cast<float*>(op.p[4])[o] = __ldcg(reinterpret_cast<const float*>(op.p[5]) + o) + v;
             } else if (epi == EPI_SILU_MUL) {
-                const float u = acc[(R + i) * NB + bi];
+                const float u = acc[(R + i) * nb + bi];
                 const float sv = v / (1.f + __expf(-v));
                 reinterpret_cast<uint16_t*>(op.p[4])[o] = f2bf(sv * u);
             }
         }
     }
+    return t_pro;
 }
 
-__device__ void body_attn_split(const StaticParams& P, const et_op& op, const SlotInfo& si, float* scratch, Ring& ring,
+__device__ void body_attn_split(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, Ring& ring,
                                 int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5];
@@ -362,98 +493,148 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     const int g = si.coord[0], c = si.coord[1];
     const long long p0 = static_cast<long long>(c) * CH;
     const int np = static_cast<int>((p0 + CH < s ? p0 + CH : s) - p0);
-    float* qs = scratch;                 // [G][dh]
-    float* sc = scratch + G * dh;        // [G][CH]
+    const int qstride = dh + 4;          // padded rows: heads land on different banks
+    const int nvec = dh / 8;             // 16-byte vectors per K/V row
+    float* qs = scratch;                 // [G][dh+4]
+    float* sc = scratch + G * qstride;   // [G][CH]
     const float* q = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
-    for (int i = ctid; i < G * dh; i += kConsumers) qs[i] = __ldcg(q + i);
+    for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
     bar_sync(1, kConsumers);
     const float scale = op.f[0];
+    const unsigned long long ck = ring.seq, cv = ring.seq + 1;
+    ring.seq += 2;
 
-    // scores: K block [np][dh]
-    {
-        const uint8_t* kb = ring.acquire();
-        const uint16_t* kr = reinterpret_cast<const uint16_t*>(kb);
-        for (int p = warp; p < np; p += kConsumerWarps) {
-            float kv[4];
-            const int nd = dh >> 5;  // dims per lane (head_dim 32..128)
-            for (int j = 0; j < nd; ++j) kv[j] = bf2f(kr[p * dh + j * 32 + lane]);
-            for (int h = 0; h < G; ++h) {
-                const float* qh = qs + h * dh + lane;
-                float d = 0.f;
-                for (int j = 0; j < nd; ++j) d = fmaf(kv[j], qh[j * 32], d);
-                d = warp_sum(d);
-                if (lane == 0) sc[h * CH + p] = d * scale;
-            }
+    // scores: one (position, head) dot product per thread; each position starts
+    // its walk over the row at a different 16-byte vector (bank rotation)
+    const uint8_t* kb = ring.wait(ck);
+    if (!kb) return;
+    for (int t = ctid; t < G * np; t += kConsumers) {
+        const int h = t % G, p = t / G;
+        const uint8_t* kr = kb + p * dh * 2;
+        const float* qh = qs + h * qstride;
+        float a0 = 0.f, a1 = 0.f;
+        for (int v = 0; v < nvec; ++v) {
+            const int vv = (v + p) & (nvec - 1);
+            const uint4 k8 = lds128(kr + vv * 16);
+            const float4 qa = *reinterpret_cast<const float4*>(qh + vv * 8);
+            const float4 qb = *reinterpret_cast<const float4*>(qh + vv * 8 + 4);
+            a0 = fmaf(bf16lo(k8.x), qa.x, a0);
+            a1 = fmaf(bf16hi(k8.x), qa.y, a1);
+            a0 = fmaf(bf16lo(k8.y), qa.z, a0);
+            a1 = fmaf(bf16hi(k8.y), qa.w, a1);
+            a0 = fmaf(bf16lo(k8.z), qb.x, a0);
+            a1 = fmaf(bf16hi(k8.z), qb.y, a1);
+            a0 = fmaf(bf16lo(k8.w), qb.z, a0);
+            a1 = fmaf(bf16hi(k8.w), qb.w, a1);
         }
-        ring.release(lane);
+        sc[h * CH + p] = (a0 + a1) * scale;
     }
     bar_sync(1, kConsumers);
+    if (ctid == Ring::owner(ck) * 32) ring.release(ck);
+
     // softmax statistics per head (warp h), probabilities in place
     float* part = reinterpret_cast<float*>(op.p[3]);
-    if (warp < G) {
+    for (int h = warp; h < G; h += kConsumerWarps) {
         float m = -INFINITY;
-        for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[warp * CH + p]);
+        for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
         m = warp_max(m);
         float l = 0.f;
         for (int p = lane; p < np; p += 32) {
-            const float e = __expf(sc[warp * CH + p] - m);
-            sc[warp * CH + p] = e;
+            const float e = __expf(sc[h * CH + p] - m);
+            sc[h * CH + p] = e;
             l += e;
         }
         l = warp_sum(l);
         if (lane == 0) {
-            float* pr = part + ((static_cast<long long>(g) * G + warp) * maxs + c) * (dh + 2);
+            float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2);
             pr[0] = m;
             pr[1] = l;
         }
     }
     bar_sync(1, kConsumers);
-    {
-        const uint8_t* vb = ring.acquire();
-        const uint16_t* v = reinterpret_cast<const uint16_t*>(vb);
-        for (int idx = ctid; idx < G * dh; idx += kConsumers) {
-            const int h = idx / dh, d = idx % dh;
-            float o = 0.f;
-            for (int p = 0; p < np; ++p) o = fmaf(sc[h * CH + p], bf2f(v[p * dh + d]), o);
-            part[((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2) + 2 + d] = o;
+
+    // o = P V: one (head, dim pair) per thread
+    const uint8_t* vb = ring.wait(cv);
+    if (!vb) return;
+    const uint32_t* v2 = reinterpret_cast<const uint32_t*>(vb);
+    const int half = dh / 2;
+    for (int idx = ctid; idx < G * half; idx += kConsumers) {
+        const int h = idx / half, dp = idx % half;
+        const float* ph = sc + h * CH;
+        float o0 = 0.f, o1 = 0.f;
+#pragma unroll 8
+        for (int p = 0; p < np; ++p) {
+            const uint32_t vv = v2[p * half + dp];
+            const float w = ph[p];
+            o0 = fmaf(w, bf16lo(vv), o0);
+            o1 = fmaf(w, bf16hi(vv), o1);
         }
-        ring.release(lane);
+        float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2) + 2 + 2 * dp;
+        pr[0] = o0;
+        pr[1] = o1;
     }
+    bar_sync(1, kConsumers);
+    if (ctid == Ring::owner(cv) * 32) ring.release(cv);
 }
 
-__device__ void body_attn_merge(const StaticParams& P, const et_op& op, const SlotInfo& si, int ctid) {
+// Merge of the splits of one kv head's q heads with the new token at s:
+//   O = (sum_c e^(m_c-M) o_c + e^(s_new-M) v_new) / (sum_c e^(m_c-M) l_c + e^(s_new-M)).
+// Split statistics are staged in shared memory with independent loads, then
+// every (head, dim) output is one thread's dot product over the splits.
+__device__ void body_attn_merge(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
     const int nspl = static_cast<int>((s + CH - 1) / CH);
     const int g = si.coord[0];
     const float scale = op.f[0];
-    const float* part = reinterpret_cast<const float*>(op.p[3]);
+    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);
     const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + (static_cast<long long>(g) * cap + s) * dh;
     const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + (static_cast<long long>(g) * cap + s) * dh;
-    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]);
+    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) + static_cast<long long>(g) * G * dh;
+    float* ml = scratch;                // [G][nspl][2]
+    float* wts = ml + 2 * G * nspl;     // [G][nspl]
+    float* hs = wts + G * nspl;         // [G]: s_new, then e^(s_new-M)/L
+    for (int idx = ctid; idx < G * nspl; idx += kConsumers) {
+        const float* pr = part + (static_cast<long long>(idx / nspl) * maxs + idx % nspl) * (dh + 2);
+        ml[2 * idx] = __ldcg(pr);
+        ml[2 * idx + 1] = __ldcg(pr + 1);
+    }
     for (int hh = warp; hh < G; hh += kConsumerWarps) {
-        const int h = g * G + hh;
-        const float* q = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(h) * dh;
+        const float* q = reinterpret_cast<const float*>(op.p[0]) + (static_cast<long long>(g) * G + hh) * dh;
         float dot = 0.f;
         for (int d = lane; d < dh; d += 32) dot += __ldcg(q + d) * bf2f(__ldcg(kn + d));
-        const float snew = warp_sum(dot) * scale;
+        dot = warp_sum(dot);
+        if (lane == 0) hs[hh] = dot * scale;
+    }
+    bar_sync(1, kConsumers);
+    for (int hh = warp; hh < G; hh += kConsumerWarps) {
+        const float snew = hs[hh];
         float M = snew;
-        for (int c = 0; c < nspl; ++c) M = fmaxf(M, __ldcg(part + (static_cast<long long>(h) * maxs + c) * (dh + 2)));
-        float L = __expf(snew - M);
-        for (int c = 0; c < nspl; ++c) {
-            const float* pr = part + (static_cast<long long>(h) * maxs + c) * (dh + 2);
-            L += __ldcg(pr + 1) * __expf(__ldcg(pr) - M);
+        for (int c = lane; c < nspl; c += 32) M = fmaxf(M, ml[2 * (hh * nspl + c)]);
+        M = warp_max(M);
+        float L = 0.f;
+        for (int c = lane; c < nspl; c += 32) {
+            const float e = __expf(ml[2 * (hh * nspl + c)] - M);
+            wts[hh * nspl + c] = e;
+            L += e * ml[2 * (hh * nspl + c) + 1];
         }
-        const float wn = __expf(snew - M) / L;
-        for (int d = lane; d < dh; d += 32) {
-            float o = wn * bf2f(__ldcg(vn + d));
-            for (int c = 0; c < nspl; ++c) {
-                const float* pr = part + (static_cast<long long>(h) * maxs + c) * (dh + 2);
-                o += __ldcg(pr + 2 + d) * (__expf(__ldcg(pr) - M) / L);
-            }
-            out[static_cast<long long>(h) * dh + d] = f2bf(o);
-        }
+        const float en = __expf(snew - M);
+        L = warp_sum(L) + en;
+        const float inv = 1.f / L;
+        for (int c = lane; c < nspl; c += 32) wts[hh * nspl + c] *= inv;
+        __syncwarp();
+        if (lane == 0) hs[hh] = en * inv;
+    }
+    bar_sync(1, kConsumers);
+    for (int idx = ctid; idx < G * dh; idx += kConsumers) {
+        const int hh = idx / dh, d = idx % dh;
+        const float* ph = part + static_cast<long long>(hh) * maxs * (dh + 2) + 2 + d;
+        const float* w = wts + hh * nspl;
+        float o = hs[hh] * bf2f(__ldcg(vn + d));
+#pragma unroll 8
+        for (int c = 0; c < nspl; ++c) o = fmaf(w[c], __ldcg(ph + static_cast<long long>(c) * (dh + 2)), o);
+        out[idx] = f2bf(o);
     }
 }
 
@@ -473,25 +654,23 @@ __device__ void body_embed(const StaticParams& P, const et_op& op, int ctid) {
 
 __device__ __forceinline__ bool op_streams(int kind) { return kind == ET_OP_GEMV || kind == ET_OP_ATTN_SPLIT; }
 
-__device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem) {
+__device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     const int ctid = threadIdx.x;
-    const int lane = ctid & 31;
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
     float* acc = reinterpret_cast<float*>(smem + kSmemAcc);
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
     float* red = reinterpret_cast<float*>(smem + kSmemMisc + 64);
     Ring ring{smem + kSmemRing, reinterpret_cast<uint64_t*>(smem + kSmemBar),
-              reinterpret_cast<uint64_t*>(smem + kSmemBar) + kStages, 0, 0u};
+              reinterpret_cast<uint64_t*>(smem + kSmemBar) + kStages, 0ull, P.status, P.watchdog_ns, worker};
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
     unsigned long long executed = 0, noops = 0;
     for (int s = qb; s < qe; ++s) {
-        const SlotInfo si = slot_info(P, s);
-        const et_op& op = P.ops[si.call];
-        const int kind = op.kind;
-        uint64_t t_begin = 0, t_wait = 0, t_exec = 0;
+        uint64_t t_begin = 0, t_wait = 0, t_pro = 0, t_exec = 0;
+        if (ctid == 0) t_begin = globaltimer();
+        SlotView v = view_slot(P, T, s, qb);
+        const et_op& op = P.ops[v.call];
         if (ctid == 0) {
-            t_begin = globaltimer();
-            bool ok = wait_slot(P, s, worker);
+            bool ok = wait_range(P, v.wb, v.we, s, worker);
             if (ok && P.step_limit > 0 &&
                 atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
                 report(P.status, ET_ERR_STEP_LIMIT, worker, s, -1, 0);
@@ -503,11 +682,12 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem) 
         }
         bar_sync(1, kConsumers);
         if (misc[0]) break;
-        if (si.masked) {
+        if (v.lazy && !v.masked) v.masked = extent_masked(P, v.call, v.coord);
+        if (v.masked) {
             ++noops;
         } else {
             ++executed;
-            switch (kind) {
+            switch (op.kind) {
                 case ET_OP_NONE:
                     if (ctid == 0 && P.tick_ns > 0 && P.slot_duration) {
                         const uint64_t until = t_wait + static_cast<uint64_t>(__ldg(P.slot_duration + s)) *
@@ -517,17 +697,16 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem) 
                     }
                     break;
                 case ET_OP_SPLITK_PARTIAL:
-                case ET_OP_SPLITK_FINAL: body_splitk(P, op, si, ctid); break;
-                case ET_OP_GEMV: {
-                    const int nb = batch_of(op, P);
-                    if (nb <= 1) body_gemv<1>(P, op, si, xs, acc, red, ring, ctid);
-                    else if (nb <= 2) body_gemv<2>(P, op, si, xs, acc, red, ring, ctid);
-                    else if (nb <= 4) body_gemv<4>(P, op, si, xs, acc, red, ring, ctid);
-                    else body_gemv<8>(P, op, si, xs, acc, red, ring, ctid);
+                case ET_OP_SPLITK_FINAL: body_splitk(P, op, v.coord, ctid); break;
+                case ET_OP_GEMV:
+                    if (batch_of(op, P) > kMaxBatch) {
+                        if (ctid == 0) report(P.status, ET_ERR_INVALID, worker, s, -1, batch_of(op, P));
+                        break;
+                    }
+                    t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid);
                     break;
-                }
-                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, si, acc, ring, ctid); break;
-                case ET_OP_ATTN_MERGE: body_attn_merge(P, op, si, ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
+                case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 default: break;
             }
@@ -535,63 +714,137 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem) 
         bar_sync(1, kConsumers);
         if (ctid == 0) {
             t_exec = globaltimer();
-            notify_slot(P, s, worker);
+            notify_range(P, v.nb, v.ne, s, worker);
             if (P.record) {
                 et_trace_rec r;
                 r.t_begin = static_cast<int64_t>(t_begin);
                 r.t_wait_end = static_cast<int64_t>(t_wait);
+                r.t_prologue = static_cast<int64_t>(t_pro);
                 r.t_exec_end = static_cast<int64_t>(t_exec);
                 r.t_notify_end = static_cast<int64_t>(globaltimer());
                 r.worker = worker;
-                r.flags = si.masked ? 1 : 0;
+                r.flags = v.masked ? 1 : 0;
                 r.task = s;
                 r.pad = 0;
                 P.trace[s] = r;
             }
         }
     }
-    (void)lane;
     if (ctid == 0) {
         if (P.step_limit <= 0) atomicAdd(&P.status->executed, executed);
         atomicAdd(&P.status->noops, noops);
     }
 }
 
-__device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem) {
+// L2 run-ahead cursor of the producer: walks the same chunk sequence as the
+// shared-memory ring and issues cp.async.bulk.prefetch.L2 for chunks up to
+// `l2_ahead` bytes in front of the ring, so HBM keeps streaming the next tasks'
+// weights through dependency bubbles longer than the ring can cover.
+struct L2Cursor {
+    int slot;
+    int chunk;
+    int nchunks;
+    StreamPlan plan;
+    bool has_plan;
+    bool blocked;  // reached a data-dependent (lazy) slot
+};
+
+__device__ bool l2_step(const StaticParams& P, const SlotTable& T, int qb, int qe, L2Cursor& L, long long* bytes,
+                        bool issue) {
+    while (!L.blocked && L.slot < qe) {
+        if (!L.has_plan) {
+            const SlotView v = view_slot(P, T, L.slot, qb);
+            const et_op& op = P.ops[v.call];
+            if (v.masked || !op_streams(op.kind)) {
+                ++L.slot;
+                continue;
+            }
+            if (v.lazy) {
+                L.blocked = true;
+                return false;
+            }
+            L.plan = make_plan(op, v.coord, v.ext0, P.binding);
+            L.nchunks = L.plan.total_chunks();
+            L.chunk = 0;
+            L.has_plan = true;
+        }
+        if (L.chunk < L.nchunks) {
+            const Chunk ch = L.plan.chunk(L.chunk++);
+            if (issue) bulk_prefetch_l2(ch.src, ch.bytes);
+            *bytes += ch.bytes;
+            return true;
+        }
+        L.has_plan = false;
+        ++L.slot;
+    }
+    return false;
+}
+
+__device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     if ((threadIdx.x & 31) != 0) return;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
     uint64_t* empty = full + kStages;
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
     const uint64_t pol = policy_evict_first();
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
-    int stage = 0;
-    uint32_t phase = 0;
+    unsigned long long cseq = 0;
+    L2Cursor L{qb, 0, 0, StreamPlan{}, false, false};
+    long long l2_bytes = 0, ring_bytes = 0;  // cumulative bytes issued by each cursor
+    const long long ahead = P.prefetch ? P.l2_ahead : 0;
+    auto resume_after = [&](int s) {  // the ring passed lazy slot s: the L2 cursor may continue
+        if (L.blocked && L.slot == s) {
+            L.blocked = false;
+            L.has_plan = false;
+            L.slot = s + 1;
+            l2_bytes = ring_bytes;
+        }
+    };
     for (int s = qb; s < qe; ++s) {
-        const int call = __ldg(P.slot_call + s);
-        const et_op& op = P.ops[call];
+        SlotView v = view_slot(P, T, s, qb);
+        if (v.masked) continue;
+        const et_op& op = P.ops[v.call];
         if (!op_streams(op.kind)) continue;
-        const SlotInfo si = slot_info(P, s);
-        if (si.masked) continue;
-        if (!P.prefetch) {
+        if (!P.prefetch || v.lazy) {
+            // data-dependent extents are known only once the slot's waits pass
             while (misc[1] <= s) {
                 if (aborted(P.status)) return;
             }
+            if (v.lazy && extent_masked(P, v.call, v.coord)) {
+                resume_after(s);
+                continue;
+            }
         }
-        const StreamPlan pl = make_plan(op, si.coord, si.ext0, P.binding);
+        const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding);
         const int n = pl.total_chunks();
-        for (int c = 0; c < n; ++c) {
+        for (int c = 0; c < n; ++c, ++cseq) {
+            const int stage = static_cast<int>(cseq % kStages);
+            const uint32_t phase = static_cast<uint32_t>((cseq / kStages) & 1ull);
             uint32_t spins = 0;
+            uint64_t t0 = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
-                if ((++spins & 1023u) == 0 && aborted(P.status)) return;
+                if (ahead > 0 && l2_bytes - ring_bytes < ahead && l2_step(P, T, qb, qe, L, &l2_bytes, true)) continue;
+                if ((++spins & 1023u) == 0) {
+                    if (aborted(P.status)) return;
+                    if (t0 == 0) t0 = globaltimer();
+                    else if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                        report(P.status, ET_ERR_DEADLOCK, worker, s, -3, c);
+                        return;
+                    }
+                }
             }
             const Chunk ch = pl.chunk(c);
             mbar_arrive_expect_tx(&full[stage], ch.bytes);
             bulk_g2s(smem + kSmemRing + stage * kStageBytes, ch.src, ch.bytes, &full[stage], pol);
-            if (++stage == kStages) {
-                stage = 0;
-                phase ^= 1u;
+            if (ahead > 0) {
+                ring_bytes += ch.bytes;
+                // keep the L2 cursor at or ahead of the ring (skipping, not issuing)
+                while (l2_bytes < ring_bytes && l2_step(P, T, qb, qe, L, &l2_bytes, false)) {
+                }
+                while (l2_bytes - ring_bytes < ahead && l2_step(P, T, qb, qe, L, &l2_bytes, true)) {
+                }
             }
         }
+        if (v.lazy && ahead > 0) resume_after(s);
     }
 }
 
@@ -610,23 +863,25 @@ __device__ void dma_loop(const StaticParams& P) {
             return;
         }
         const uint64_t t_wait = globaltimer();
-        if (!si.masked && P.tick_ns > 0 && P.slot_duration) {
+        const bool masked = si.masked || (si.lazy && extent_masked(P, si.call, si.coord));
+        if (!masked && P.tick_ns > 0 && P.slot_duration) {
             const uint64_t until = t_wait + static_cast<uint64_t>(__ldg(P.slot_duration + s)) * P.tick_ns;
             while (globaltimer() < until) {
             }
         }
         const uint64_t t_exec = globaltimer();
         notify_slot(P, s, q);
-        if (P.step_limit <= 0 && !si.masked) atomicAdd(&P.status->executed, 1ull);
-        if (si.masked) atomicAdd(&P.status->noops, 1ull);
+        if (P.step_limit <= 0 && !masked) atomicAdd(&P.status->executed, 1ull);
+        if (masked) atomicAdd(&P.status->noops, 1ull);
         if (P.record) {
             et_trace_rec r;
             r.t_begin = static_cast<int64_t>(t_begin);
             r.t_wait_end = static_cast<int64_t>(t_wait);
+            r.t_prologue = 0;
             r.t_exec_end = static_cast<int64_t>(t_exec);
             r.t_notify_end = static_cast<int64_t>(globaltimer());
             r.worker = q;
-            r.flags = si.masked ? 1 : 0;
+            r.flags = masked ? 1 : 0;
             r.task = s;
             r.pad = 0;
             P.trace[s] = r;
@@ -646,19 +901,45 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
         uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&full[kStages + i], kConsumerWarps);
+            mbar_init(&full[kStages + i], 1);
         }
         fence_mbar_init();
         volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
         misc[0] = 0;
         misc[1] = 0;
     }
+    // slot table for this CTA's queue
+    SlotTable T;
+    T.ent = reinterpret_cast<const uint4*>(smem + kSmemTable);
+    T.ext0 = reinterpret_cast<const int*>(smem + kSmemExt0);
+    const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
+    T.valid = P.table_ok && (qe - qb) <= kMaxTableSlots && P.num_calls <= kMaxTableCalls;
+    if (T.valid) {
+        uint4* ent = reinterpret_cast<uint4*>(smem + kSmemTable);
+        int* ext0 = reinterpret_cast<int*>(smem + kSmemExt0);
+        for (int c = threadIdx.x; c < P.num_calls; c += blockDim.x) ext0[c] = __ldg(P.call_extents + c * 4);
+        for (int i = threadIdx.x; i <= qe - qb; i += blockDim.x) {
+            const int s = qb + i;
+            uint4 e;
+            if (i < qe - qb) {
+                const SlotInfo si = slot_info(P, s);
+                e.x = static_cast<uint32_t>(si.call) | (si.masked ? 0x80000000u : 0u) | (si.lazy ? 0x40000000u : 0u);
+                e.y = static_cast<uint32_t>(si.coord[0] & 0xffff) |
+                      (static_cast<uint32_t>(si.rank > 1 ? si.coord[1] & 0xffff : 0) << 16);
+            } else {
+                e.x = e.y = 0u;
+            }
+            e.z = static_cast<uint32_t>(__ldg(P.wait_off + s));
+            e.w = static_cast<uint32_t>(__ldg(P.notify_off + s));
+            ent[i] = e;
+        }
+    }
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     if (warp < kConsumerWarps) {
-        consumer_loop(P, worker, smem);
+        consumer_loop(P, worker, smem, T);
     } else if (warp == kProducerWarp) {
-        producer_loop(P, worker, smem);
+        producer_loop(P, worker, smem, T);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
         dma_loop(P);
     }
@@ -668,7 +949,9 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
 
 int et_static_smem_bytes() { return etk::kSmemTotal; }
 
-int et_launch_static(const etk::StaticParams& p, int num_workers, void* stream) {
+// max_batch > 8 needs the tensor-memory (tcgen05) GEMV path, not in this build.
+int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, void* stream) {
+    if (max_batch > etk::kMaxBatch) return static_cast<int>(cudaErrorInvalidValue);
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(etk::et_static_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -688,6 +971,5 @@ int et_launch_static(const etk::StaticParams& p, int num_workers, void* stream) 
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, etk::et_static_kernel, p);
-    return static_cast<int>(e);
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, etk::et_static_kernel, p));
 }

@@ -13,18 +13,27 @@ constexpr int kConsumers = kConsumerWarps * 32;   // compute threads
 constexpr int kProducerWarp = kConsumerWarps;     // TMA issuer
 constexpr int kDmaWarp = kConsumerWarps + 1;      // DMA-queue executor (worker 0 only)
 constexpr int kThreads = (kConsumerWarps + 2) * 32;
-constexpr int kStages = 10;
-constexpr int kStageBytes = 16384;
-constexpr int kXBytes = 48 * 1024;
-constexpr int kAccFloats = 4096;
+// One ring stage per consumer warp: stage c % kStages is always consumed by
+// warp c % kConsumerWarps, in order, so an mbarrier parity can never alias a
+// phase two steps ahead (chunks may land out of order).
+constexpr int kStages = kConsumerWarps;
+constexpr int kStageBytes = 20480;
+constexpr int kXBytes = 28 * 1024;
+constexpr int kAccFloats = 2048;
 constexpr int kMaxSymbols = 8;
 constexpr int kMaxRuntime = 16;
 constexpr int kMaxRank = 4;
+constexpr int kMaxBatch = 8;   // GEMV batch rows carried in the mma M dimension
+
+constexpr int kMaxTableSlots = 512;   // per-CTA slot table in shared memory
+constexpr int kMaxTableCalls = 1024;  // per-call sample extent of dim 0
 
 constexpr int kSmemRing = 0;
 constexpr int kSmemX = kSmemRing + kStages * kStageBytes;
 constexpr int kSmemAcc = kSmemX + kXBytes;
-constexpr int kSmemBar = kSmemAcc + kAccFloats * 4;
+constexpr int kSmemTable = kSmemAcc + kAccFloats * 4;
+constexpr int kSmemExt0 = kSmemTable + (kMaxTableSlots + 1) * 16;
+constexpr int kSmemBar = kSmemExt0 + kMaxTableCalls * 4;
 constexpr int kSmemMisc = kSmemBar + 2 * kStages * 8;
 constexpr int kSmemTotal = kSmemMisc + 512;
 
@@ -83,10 +92,12 @@ struct StaticParams {
     long long tick_ns;
     long long step_limit;  // 0 = unlimited
     int prefetch;
+    int table_ok;  // every coordinate fits 16 bits (slot tables usable)
+    long long l2_ahead;  // bytes the producer prefetches into L2 beyond the ring
 };
 
 }  // namespace etk
 
 // Host-side launcher (megakernel.cu).
-int et_launch_static(const etk::StaticParams& p, int num_workers, void* stream);
+int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, void* stream);
 int et_static_smem_bytes();

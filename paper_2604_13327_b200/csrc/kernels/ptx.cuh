@@ -121,6 +121,43 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
     return v;
 }
 
+__device__ __forceinline__ uint4 lds128a(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+// acc + <w, x> over 8 bf16 pairs, as two interleaved FMA chains
+__device__ __forceinline__ float dot8_acc(uint4 w, uint4 x, float acc) {
+    float a = acc, b = 0.f;
+    a = fmaf(__uint_as_float(w.x << 16), __uint_as_float(x.x << 16), a);
+    b = fmaf(__uint_as_float(w.x & 0xffff0000u), __uint_as_float(x.x & 0xffff0000u), b);
+    a = fmaf(__uint_as_float(w.y << 16), __uint_as_float(x.y << 16), a);
+    b = fmaf(__uint_as_float(w.y & 0xffff0000u), __uint_as_float(x.y & 0xffff0000u), b);
+    a = fmaf(__uint_as_float(w.z << 16), __uint_as_float(x.z << 16), a);
+    b = fmaf(__uint_as_float(w.z & 0xffff0000u), __uint_as_float(x.z & 0xffff0000u), b);
+    a = fmaf(__uint_as_float(w.w << 16), __uint_as_float(x.w << 16), a);
+    b = fmaf(__uint_as_float(w.w & 0xffff0000u), __uint_as_float(x.w & 0xffff0000u), b);
+    return a + b;
+}
+
+// acc_lo += lo(w)*lo(x); acc_hi += hi(w)*hi(x) with bf16 inputs and fp32
+// accumulation: sm_100's mixed-precision fma (SASS FHFMA.BF16 with half
+// selects), so no bf16->fp32 conversion instructions are needed.
+__device__ __forceinline__ void fma2_bf16(float& lo, float& hi, uint32_t w, uint32_t x) {
+    asm("{\n\t.reg .b16 wl, wh, xl, xh;\n\tmov.b32 {wl, wh}, %2;\n\tmov.b32 {xl, xh}, %3;\n\t"
+        "fma.rn.f32.bf16 %0, wl, xl, %0;\n\tfma.rn.f32.bf16 %1, wh, xh, %1;\n\t}"
+        : "+f"(lo), "+f"(hi)
+        : "r"(w), "r"(x));
+}
+
+__device__ __forceinline__ void dot8_bf16(float& lo, float& hi, const uint4& w, const uint4& x) {
+    fma2_bf16(lo, hi, w.x, x.x);
+    fma2_bf16(lo, hi, w.y, x.y);
+    fma2_bf16(lo, hi, w.z, x.z);
+    fma2_bf16(lo, hi, w.w, x.w);
+}
+
 __device__ __forceinline__ uint4 ldg_nc_na(const void* p) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

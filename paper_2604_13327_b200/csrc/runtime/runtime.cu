@@ -54,6 +54,7 @@ struct Sample {
     std::vector<int32_t> call_extents;
     int num_queues = 0, has_dma = 0, num_slots = 0, num_counters = 0;
     std::vector<int32_t> initial_counts;  // host copy for counter readback
+    int table_ok = 1;                     // all grid extents < 65536 (16-bit slot-table coordinates)
     DevArray<int32_t> d_call_extents, d_queue_off, d_slot_call, d_slot_flat, d_slot_duration, d_wait_off, d_waits,
         d_notify_off, d_notifies, d_initial;
 };
@@ -247,6 +248,9 @@ int et_upload_static(et_runtime* rt, const et_sample_desc* s, int32_t num_sample
         S.num_slots = d.num_slots;
         S.num_counters = d.num_counters;
         S.initial_counts.assign(d.initial_counts, d.initial_counts + d.num_counters);
+        for (int c = 0; c < rt->num_calls; ++c)
+            for (int k = 0; k < 4; ++k)
+                if (S.call_extents[static_cast<size_t>(c * 4 + k)] >= 65536) S.table_ok = 0;
         const size_t nq = static_cast<size_t>(d.num_queues + d.has_dma + 1);
         const int nw = d.wait_off[d.num_slots], nn = d.notify_off[d.num_slots];
         ET_CUDA(S.d_call_extents.upload(d.call_extents, static_cast<size_t>(rt->num_calls * 4)), "upload sample");
@@ -420,10 +424,12 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     p.tick_ns = rt->cfg.tick_ns;
     p.step_limit = rt->cfg.step_limit > 0 ? rt->cfg.step_limit : 0;
     p.prefetch = rt->cfg.enable_prefetch;
+    p.table_ok = S.table_ok;
+    p.l2_ahead = rt->cfg.l2_prefetch_bytes < 0 ? 0 : rt->cfg.l2_prefetch_bytes;
 
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rt->stream;
     if (synchronous) cudaEventRecord(rt->ev0, st);
-    int e = et_launch_static(p, S.num_queues, st);
+    int e = et_launch_static(p, S.num_queues, rt->cfg.max_batch, st);
     if (e != 0) return rt->cuda_fail(static_cast<cudaError_t>(e), "launch");
     if (synchronous) cudaEventRecord(rt->ev1, st);
     rt->parity ^= 1;

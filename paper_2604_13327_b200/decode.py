@@ -149,6 +149,31 @@ def rope_inv_freq(cfg):
     return (cfg.rope_theta ** (-2.0 * j / cfg.head_dim)).to(torch.float32)
 
 
+def frag8(w):
+    """Device layout of a GEMV weight [N][K] (N % 8 == 0, K % 32 == 0): row blocks of 8,
+    then 32-wide k groups, then the 32 mma lanes (lane = 4*row + q) holding the B
+    registers of two k16 steps (see body_gemv in csrc/kernels/megakernel.cu)."""
+    N, K = w.shape
+    assert N % 8 == 0 and K % 32 == 0, (N, K)
+    return (w.reshape(N // 8, 8, K // 32, 2, 2, 4, 2).permute(0, 2, 1, 5, 3, 4, 6).contiguous().reshape(N, K))
+
+
+GEMV_WEIGHTS = ("wqkv", "wo", "wgate", "wup", "wdown")
+
+
+def device_layout(W, keep_logical=False):
+    """Copy of the weight dict with every GEMV matrix in frag8 order."""
+    D = {"embed": W["embed"], "final_norm": W["final_norm"], "lm_head": frag8(W["lm_head"]), "layers": []}
+    for L in W["layers"]:
+        D["layers"].append({k: (frag8(v) if k in GEMV_WEIGHTS else v) for k, v in L.items()})
+        if not keep_logical:
+            for k in GEMV_WEIGHTS:
+                L[k] = None
+    if not keep_logical:
+        W["lm_head"] = None
+    return D
+
+
 def init_weights(cfg: DecoderConfig, device, seed=0, std=0.02):
     """Random-init weights of the architecture (bf16, N(0, std)); norms ~ 1 + N(0, 0.01)."""
     g = torch.Generator(device=device)
@@ -186,7 +211,8 @@ class DecodeModel:
     """
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
-                 seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None):
+                 seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
+                 l2_prefetch=-1):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -206,7 +232,9 @@ class DecodeModel:
         self.lower_ms = (time.perf_counter() - t0) * 1e3
 
         dev = self.device
-        self.W = weights if weights is not None else init_weights(cfg, dev, seed)
+        W = weights if weights is not None else init_weights(cfg, dev, seed)
+        self.W = W                                             # what the megakernel reads (row-major bf16)
+        self.W_logical = W                                     # same tensors; the CPU oracle reads these
         self.kcache = [torch.zeros(cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
                        for _ in range(cfg.layers)]
         self.vcache = [torch.zeros_like(k) for k in self.kcache]
@@ -222,7 +250,7 @@ class DecodeModel:
 
         t1 = time.perf_counter()
         self.executor = etsim.Executor(self.kernel, device=self.device.index or 0, num_workers=self.num_workers,
-                                       record_trace=record_trace, prefetch=prefetch)
+                                       record_trace=record_trace, prefetch=prefetch, l2_prefetch=l2_prefetch)
         self.executor.bind_ops(pack(self._ops()))
         self.upload_ms = (time.perf_counter() - t1) * 1e3
 
@@ -236,7 +264,7 @@ class DecodeModel:
         G = cfg.heads // cfg.kv_heads
         for l, L in enumerate(W["layers"]):
             kc, vc = self.kcache[l], self.vcache[l]
-            ops.append(make_op(OP_GEMV, i=[cfg.q_rows + 2 * cfg.kv_rows, H, 1, 1, EPI_QKV_ROPE, -1, s_slot, 2, dh, H,
+            ops.append(make_op(OP_GEMV, i=[cfg.q_rows + 2 * cfg.kv_rows, H, 1, 1, EPI_QKV_ROPE, -1, s_slot, 8, dh, H,
                                            cfg.q_rows, cfg.kv_rows, self.capacity],
                                f=[cfg.eps], p=[ptr(L["wqkv"]), 0, ptr(self.h_a), ptr(L["attn_norm"]), ptr(self.q), 0,
                                                ptr(kc), ptr(vc), ptr(self.inv_freq)]))
@@ -245,14 +273,14 @@ class DecodeModel:
                                p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials)]))
             ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale],
                                p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn)]))
-            ops.append(make_op(OP_GEMV, i=[H, cfg.q_rows, 1, 0, EPI_RESID, -1, 0, 1],
+            ops.append(make_op(OP_GEMV, i=[H, cfg.q_rows, 1, 0, EPI_RESID, -1, 0, 8],
                                p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_b), ptr(self.h_a)]))
-            ops.append(make_op(OP_GEMV, i=[cfg.intermediate, H, 2, 1, EPI_SILU_MUL, -1, 0, 1, 0, H],
+            ops.append(make_op(OP_GEMV, i=[cfg.intermediate, H, 2, 1, EPI_SILU_MUL, -1, 0, 8, 0, H],
                                f=[cfg.eps], p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(self.h_b), ptr(L["ffn_norm"]),
                                                ptr(self.act)]))
-            ops.append(make_op(OP_GEMV, i=[H, cfg.intermediate, 1, 0, EPI_RESID, -1, 0, 1],
+            ops.append(make_op(OP_GEMV, i=[H, cfg.intermediate, 1, 0, EPI_RESID, -1, 0, 8],
                                p=[ptr(L["wdown"]), 0, ptr(self.act), 0, ptr(self.h_a), ptr(self.h_b)]))
-        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 1, 0, H], f=[cfg.eps],
+        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 8, 0, H], f=[cfg.eps],
                            p=[ptr(W["lm_head"]), 0, ptr(self.h_a), ptr(W["final_norm"]), ptr(self.logits)]))
         return ops
 

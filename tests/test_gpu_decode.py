@@ -22,7 +22,7 @@ def _errs(got, want):
 
 @pytest.fixture(scope="module")
 def tiny():
-    return DecodeModel(TINY, samples=(16, 64), num_workers=16, seed=0, record_trace=True)
+    return DecodeModel(TINY, samples=(16, 64), num_workers=16, seed=0, record_trace=True, keep_logical=True)
 
 
 @pytest.mark.parametrize("s", [16, 10, 40, 0, 64])
@@ -33,7 +33,7 @@ def test_tiny_logits_match_oracle(tiny, s):
     cpu_k = [k.cpu() for k in m.kcache]
     cpu_v = [v.cpu() for v in m.vcache]
     logits = m.step(s)[0].cpu()
-    Wc = weights_to_cpu(m.W)
+    Wc = weights_to_cpu(m.W_logical)
     inv = m.inv_freq.cpu()
     ref, nk, nv = decode_step(m.cfg, Wc, cpu_k, cpu_v, 7, s, inv, emulate_bf16=True)
     err, scale = _errs(logits, ref)
