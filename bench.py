@@ -69,7 +69,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
@@ -109,22 +109,28 @@ def cpu_reference_step_us(cfg, seq, budget_s=12.0):
 
     detail = {}
     sim_us = None
+    # The reference module registers pybind types with the same names as this
+    # framework's module, so it runs in its own interpreter.
+    code = (
+        "import json, sys, time\n"
+        f"sys.path.insert(0, {os.path.join(ROOT, 'oracle', '_ref')!r})\n"
+        "import etsim\n"
+        "g = etsim.Graph.from_json(sys.stdin.read())\n"
+        f"k = etsim.lower_static(g, [{{'s': {seq}}}], num_sms=148)\n"
+        "t0 = time.perf_counter(); n = 0\n"
+        f"while time.perf_counter() - t0 < {budget_s * 0.3} or n < 2:\n"
+        f"    etsim.simulate(k, {{'s': {seq}}}); n += 1\n"
+        "print(json.dumps({'us': (time.perf_counter() - t0) / n * 1e6, 'runs': n}))\n"
+    )
     try:
-        sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
-        import etsim as ref  # the unmodified reference module
-
-        g = ref.Graph.from_json(build_graph(cfg, 148, 148).to_json())
-        k = ref.lower_static(g, [{"s": seq}], num_sms=148)
-        t0 = time.perf_counter()
-        n = 0
-        while time.perf_counter() - t0 < budget_s * 0.3 or n < 2:
-            ref.simulate(k, {"s": seq})
-            n += 1
-        sim_us = (time.perf_counter() - t0) / n * 1e6
+        out = subprocess.run([sys.executable, "-c", code], input=build_graph(cfg, 148, 148).to_json(),
+                             capture_output=True, text=True, timeout=budget_s * 3 + 60)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        sim_us = r["us"]
         detail["reference_simulate_us"] = sim_us
-        detail["reference_runs"] = n
+        detail["reference_runs"] = r["runs"]
     except Exception as exc:  # reference build absent on this host
-        detail["reference_error"] = str(exc)[:200]
+        detail["reference_error"] = (str(exc) + " " + (out.stderr[-200:] if "out" in dir() else ""))[:300]
     # numerics: one layer + lm_head in fp32 on CPU
     torch.manual_seed(0)
     H, I, V = cfg.hidden, cfg.intermediate, cfg.vocab
@@ -326,7 +332,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3-8b")

@@ -211,10 +211,10 @@ __device__ __forceinline__ SlotView view_slot(const StaticParams& P, const SlotT
 // ---------------------------------------------------------------------------
 // Ring protocol.  The producer fills stages in chunk-sequence order c = 0, 1,
 // 2, ... (stage c % kStages, parity (c / kStages) & 1).  Chunk c is owned by
-// consumer warp c % kConsumerWarps: the owner (or, for chunks all warps read,
-// the owner after a consumer barrier) releases the stage with one arrive, so
-// the empty barriers count 1.  Every consumer thread tracks the same 64-bit
-// sequence number, so no per-stage state has to be shared.
+// consumer warp c % kConsumerWarps (== its stage): the owner waits for it and
+// releases the stage with one arrive, so each warp has its own stage in flight
+// while it computes on another (see kStages).  Every consumer thread tracks the
+// same 64-bit sequence number.
 struct Ring {
     uint8_t* buf;
     uint64_t* full;
@@ -228,6 +228,7 @@ struct Ring {
     __device__ __forceinline__ static uint32_t parity_of(unsigned long long c) {
         return static_cast<uint32_t>((c / kStages) & 1ull);
     }
+    __device__ __forceinline__ static int owner(unsigned long long c) { return static_cast<int>(c % kConsumerWarps); }
     // Bounded wait: a stage that never fills (protocol bug, aborted producer)
     // reports a deadlock instead of hanging the device.  Returns nullptr then.
     __device__ __forceinline__ const uint8_t* wait(unsigned long long c) {
@@ -249,9 +250,6 @@ struct Ring {
         return buf + st * kStageBytes;
     }
     __device__ __forceinline__ void release(unsigned long long c) { mbar_arrive(&empty[stage_of(c)]); }
-    __device__ __forceinline__ static int owner(unsigned long long c) {
-        return static_cast<int>(c % kConsumerWarps);
-    }
 };
 
 __device__ __forceinline__ int batch_of(const et_op& op, const StaticParams& P) {
@@ -359,9 +357,15 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     bar_sync(1, kConsumers);
     const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
 
-    // ---- main loop
+    // ---- main loop: each consumer warp owns whole chunks (chunk c -> warp
+    // c % 8) and walks them in 512-byte groups (32 lanes x 16 bytes, inside one
+    // weight row), four groups in flight per lane (loads first, eight FHFMA
+    // chains).  A per-warp running sum is reduced into shared memory whenever
+    // the row changes and at the end of each owned chunk.
     const int gpr = K / 256;  // 512-byte groups per weight row
     constexpr int kGroupsPerChunk = kStageBytes / 512;
+    const uint4* xlane = reinterpret_cast<const uint4*>(xs) + lane;
+    const int xrow4 = K / 8;  // uint4 per activation row
     unsigned long long c = ring.seq;
     for (int seg = 0; seg < nseg; ++seg) {
         const long long seg_groups = static_cast<long long>(R) * gpr;
@@ -374,30 +378,28 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
             const int ng = static_cast<int>(seg_groups - g0 < kGroupsPerChunk ? seg_groups - g0 : kGroupsPerChunk);
             int row = seg * R + static_cast<int>(g0 / gpr);
             int kg = static_cast<int>(g0 % gpr);
-            const uint4* wbase = reinterpret_cast<const uint4*>(buf) + lane;
-            const uint4* xbase = reinterpret_cast<const uint4*>(xs) + lane;
-            const int xrow4 = K / 8;  // uint4 per activation row
+            const uint4* wl = reinterpret_cast<const uint4*>(buf) + lane;
             int j = 0;
             while (j < ng) {
                 const int len = (gpr - kg < ng - j) ? gpr - kg : ng - j;
-                const uint4* wp = wbase + j * 32;
-                const uint4* xp = xbase + kg * 32;
+                const uint4* wp = wl + j * 32;
+                const uint4* xp = xlane + kg * 32;
                 if (nb == 1) {
-                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f;
+                    float a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] = 0.f;
                     int t = 0;
                     for (; t + 4 <= len; t += 4) {
-                        uint4 w[4], x[4];
+                        uint4 w[4], xv[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) w[u] = wp[(t + u) * 32];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) x[u] = xp[(t + u) * 32];
-                        dot8_bf16(a0, a1, w[0], x[0]);
-                        dot8_bf16(a2, a3, w[1], x[1]);
-                        dot8_bf16(a4, a5, w[2], x[2]);
-                        dot8_bf16(a6, a7, w[3], x[3]);
+                        for (int u = 0; u < 4; ++u) xv[u] = xp[(t + u) * 32];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) dot8_bf16(a[2 * u], a[2 * u + 1], w[u], xv[u]);
                     }
-                    for (; t < len; ++t) dot8_bf16(a0, a1, wp[t * 32], xp[t * 32]);
-                    const float v = warp_sum(((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7)));
+                    for (; t < len; ++t) dot8_bf16(a[0], a[1], wp[t * 32], xp[t * 32]);
+                    const float v = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
                     if (lane == 0) atomicAdd(&acc[row], v);
                 } else {
                     float lo[kMaxBatch], hi[kMaxBatch];
@@ -669,8 +671,16 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         if (ctid == 0) t_begin = globaltimer();
         SlotView v = view_slot(P, T, s, qb);
         const et_op& op = P.ops[v.call];
+        // operands that do not depend on the Event Tensors (RMSNorm gamma) are
+        // pulled into L1 while thread 0 spins on the dependency
+        if (op.kind == ET_OP_GEMV && op.i[3] == 1 && !v.masked) {
+            const char* gam = reinterpret_cast<const char*>(op.p[3]);
+            for (int off = ctid * 128; off < op.i[1] * 4; off += kConsumers * 128) prefetch_l1(gam + off);
+        }
         if (ctid == 0) {
+            misc[2] = 1;  // consumers blocked on an Event Tensor: HBM idles, the producer may fill L2
             bool ok = wait_range(P, v.wb, v.we, s, worker);
+            misc[2] = 0;
             if (ok && P.step_limit > 0 &&
                 atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
                 report(P.status, ET_ERR_STEP_LIMIT, worker, s, -1, 0);
@@ -822,7 +832,11 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             uint32_t spins = 0;
             uint64_t t0 = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
-                if (ahead > 0 && l2_bytes - ring_bytes < ahead && l2_step(P, T, qb, qe, L, &l2_bytes, true)) continue;
+                // L2 run-ahead only while the consumers wait on a dependency (a bubble):
+                // during streaming it would compete with the current stage's loads
+                if (ahead > 0 && misc[2] && l2_bytes - ring_bytes < ahead &&
+                    l2_step(P, T, qb, qe, L, &l2_bytes, true))
+                    continue;
                 if ((++spins & 1023u) == 0) {
                     if (aborted(P.status)) return;
                     if (t0 == 0) t0 = globaltimer();
@@ -839,8 +853,6 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 ring_bytes += ch.bytes;
                 // keep the L2 cursor at or ahead of the ring (skipping, not issuing)
                 while (l2_bytes < ring_bytes && l2_step(P, T, qb, qe, L, &l2_bytes, false)) {
-                }
-                while (l2_bytes - ring_bytes < ahead && l2_step(P, T, qb, qe, L, &l2_bytes, true)) {
                 }
             }
         }
@@ -907,6 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
         volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
         misc[0] = 0;
         misc[1] = 0;
+        misc[2] = 0;
     }
     // slot table for this CTA's queue
     SlotTable T;

@@ -13,9 +13,12 @@ constexpr int kConsumers = kConsumerWarps * 32;   // compute threads
 constexpr int kProducerWarp = kConsumerWarps;     // TMA issuer
 constexpr int kDmaWarp = kConsumerWarps + 1;      // DMA-queue executor (worker 0 only)
 constexpr int kThreads = (kConsumerWarps + 2) * 32;
-// One ring stage per consumer warp: stage c % kStages is always consumed by
-// warp c % kConsumerWarps, in order, so an mbarrier parity can never alias a
-// phase two steps ahead (chunks may land out of order).
+// Chunk c lives in stage c % kStages and is consumed by warp c % kConsumerWarps.
+// With kStages == kConsumerWarps every stage has exactly one consumer warp that
+// takes its chunks in order, so an mbarrier parity can never alias a phase two
+// steps ahead even though TMA copies may complete out of order.  Chunks that
+// every warp must read (attention K/V blocks) are released by their owner after
+// a consumer barrier.
 constexpr int kStages = kConsumerWarps;
 constexpr int kStageBytes = 20480;
 constexpr int kXBytes = 28 * 1024;
