@@ -32,6 +32,7 @@ import math
 import torch
 
 from . import etsim
+from .graphs import graph_spec  # noqa: F401  (re-exported)
 from .ops import (
     EPI_BF16,
     EPI_F32,
@@ -91,53 +92,6 @@ LLAMA3_8B = DecoderConfig("llama3-8b", hidden=4096, layers=32, heads=32, kv_head
 LLAMA3_70B = DecoderConfig("llama3-70b", hidden=8192, layers=80, heads=64, kv_heads=8, head_dim=128,
                            intermediate=28672, vocab=128256)
 CONFIGS = {c.name: c for c in (TINY, LLAMA3_8B, LLAMA3_70B)}
-
-
-def graph_spec(cfg: DecoderConfig, tasks: int, lm_tasks: int):
-    """Reference-format graph spec of one decode step (symbol `s`)."""
-    CH = cfg.attn_chunk
-    fns, events, calls = [], [], []
-
-    def fn(name, grid):
-        fns.append({"name": name, "grid": grid, "resource": "sm", "duration": "unit"})
-        return name
-
-    def ev(name, shape):
-        events.append({"name": name, "shape": shape})
-        return name
-
-    def call(f, ins=(), outs=()):
-        c = {"fn": f}
-        if ins:
-            c["in"] = [{"event": e, "map": m} for e, m in ins]
-        if outs:
-            c["out"] = [{"event": e, "map": m} for e, m in outs]
-        calls.append(c)
-
-    T, kv = str(tasks), str(cfg.kv_heads)
-    ev("EMB", ["1"])
-    call(fn("embed", ["1"]), outs=[("EMB", ["0"])])
-    prev = "EMB"
-    for l in range(cfg.layers):
-        qkv, a, m, o, g, d = (ev(f"{x}{l}", ["1"]) for x in ("QKV", "A", "M", "O", "G", "D"))
-        events[-5]["shape"] = [kv]  # A_l has one element per kv head
-        call(fn(f"L{l}.qkv", [T]), ins=[(prev, ["0"])], outs=[(qkv, ["0"])])
-        call(fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
-        call(fn(f"L{l}.merge", [kv]), ins=[(a, ["t0"]), (qkv, ["0"])], outs=[(m, ["0"])])
-        call(fn(f"L{l}.oproj", [T]), ins=[(m, ["0"])], outs=[(o, ["0"])])
-        call(fn(f"L{l}.gateup", [T]), ins=[(o, ["0"])], outs=[(g, ["0"])])
-        call(fn(f"L{l}.down", [T]), ins=[(g, ["0"])], outs=[(d, ["0"])])
-        prev = d
-    ev("LM", ["1"])
-    call(fn("lm_head", [str(lm_tasks)]), ins=[(prev, ["0"])], outs=[("LM", ["0"])])
-    return {
-        "symbols": ["s"],
-        "size_symbol": "s",
-        "duration_models": {"unit": {"kind": "constant", "value": 1}},
-        "device_functions": fns,
-        "event_tensors": events,
-        "calls": calls,
-    }
 
 
 def build_graph(cfg, tasks, lm_tasks):
