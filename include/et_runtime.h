@@ -127,36 +127,52 @@ typedef struct et_sample_desc {
     const int32_t* counter_dd;       /* [num_counters] runtime counts tensor or -1 (dynamic) */
 } et_sample_desc;
 
-/* Dynamic-scheduler additions for one sample (ref sched_dynamic.hpp, the
- * consumer tables of simulate.cpp:347-353 built per sample, plus the
- * data-dependent edge descriptors resolved on the device). */
+/* Dynamic-scheduler program for one sample (ref sched_dynamic.hpp and the
+ * engine state of ref simulate.cpp:303-354), flattened.  Tasks are the sample
+ * grids' tasks in program order (id = call_first_task[call] + flat).  Static
+ * map edges are resolved on the host; data-dependent edges are resolved on the
+ * device from runtime tensors written by their writer task:
+ *   routed notify  (ref materialize.cpp:288-304): element = base + routing[flat]
+ *   range trigger  (ref materialize.cpp:252-273): task f of the call waits on
+ *                  base + g where indptr[g] <= f < indptr[g+1]; tasks at or past
+ *                  indptr[last] do not exist (extent_from)
+ * Data-dependent elements get their initial count from their counts tensor and
+ * become visible when the writer call's tasks have all finished (ref
+ * simulate.cpp:326-345, 632-649). */
 typedef struct et_dynamic_desc {
     int32_t num_tasks;
-    const int32_t* task_call;            /* [num_tasks]                           */
-    const int32_t* task_flat;
-    const int32_t* task_duration;        /* may be NULL                           */
-    const int32_t* task_wait_off;        /* [num_tasks+1] static-map waits        */
+    const int32_t* task_call;           /* [num_tasks]                               */
+    const int32_t* task_flat;           /* row-major index in the call's sample grid */
+    const int32_t* task_duration;       /* synthetic duration units, may be NULL     */
+    const int32_t* task_wait_off;       /* [num_tasks+1] static-map waits            */
     const int32_t* task_waits;
-    const uint8_t* task_wait_armed;      /* aligned with task_waits               */
-    const int32_t* task_notify_off;      /* [num_tasks+1] static-map notifies     */
+    const uint8_t* task_wait_armed;     /* aligned with task_waits                   */
+    const int32_t* task_notify_off;     /* [num_tasks+1] static-map notifies         */
     const int32_t* task_notifies;
-    const int32_t* consumer_off;         /* [num_counters+1] static-map consumers */
+    const int32_t* task_rem_init;       /* waits that must fire before the push      */
+    const int32_t* consumer_off;        /* [num_counters+1] static-map consumers     */
     const int32_t* consumers;
-    /* per call data-dependent edges: routed notify (routing tensor, event base)
-     * and range trigger (indptr tensor, event base, armed); -1 when absent. */
-    const int32_t* call_first_task;      /* [num_calls]                           */
-    const int32_t* call_routed_rt;
-    const int32_t* call_routed_base;
-    const int32_t* call_range_rt;
+    const int32_t* call_first_task;     /* [num_calls]                               */
+    const int32_t* call_routed_rt;      /* routing tensor of a routed notify, or -1  */
+    const int32_t* call_routed_base;    /* event element base of that notify         */
+    const int32_t* call_range_rt;       /* indptr tensor of a range trigger, or -1   */
     const int32_t* call_range_base;
     const uint8_t* call_range_armed;
-    const int32_t* call_writes_dd;       /* call whose completion reveals dd counters, else -1 */
+    int32_t num_dd;                     /* data-dependent event tensors              */
+    const int32_t* dd_base;             /* [num_dd] first element                    */
+    const int32_t* dd_count;            /* [num_dd] elements                         */
+    const int32_t* dd_counts_rt;        /* [num_dd] runtime tensor holding counts    */
+    const int32_t* dd_writer_call;      /* [num_dd] call whose completion reveals it */
+    const int32_t* el_dd;               /* [num_counters] dd tensor index or -1      */
+    int32_t num_ready;                  /* tasks ready at launch (seeded in id order)*/
+    const int32_t* ready;
     int32_t early_push;
 } et_dynamic_desc;
 
 /* Per-slot (static) or per-task (dynamic) trace record, nanoseconds of
  * %globaltimer.  flags bit0 = masked no-op. */
 typedef struct et_trace_rec {
+    int64_t t_push;       /* dynamic: task entered the ready queue (0: seeded) */
     int64_t t_begin;      /* slot reached / task popped                 */
     int64_t t_wait_end;   /* all waits satisfied                        */
     int64_t t_prologue;   /* body prologue done (activations staged), 0 if none */
@@ -182,7 +198,7 @@ typedef struct et_step_info {
     int64_t pushes;
     int64_t pops;
     float kernel_ms;      /* CUDA-event time of the step's launch (when synchronous) */
-    float pad;
+    int32_t step_id;      /* stamped into the trace records' pad field             */
 } et_step_info;
 
 typedef struct et_runtime et_runtime;

@@ -39,6 +39,10 @@ struct StepStats {
 class Executor {
 public:
     Executor(const StaticMegakernel& k, const ExecConfig& cfg);
+    // Dynamic scheduler: one device program per sampled binding (any covered
+    // binding runs on the next-larger sample with masked no-ops); data-dependent
+    // routing is resolved on the device.
+    Executor(const DynamicMegakernel& k, const std::vector<ShapeBinding>& samples, const ExecConfig& cfg);
     ~Executor();
     Executor(const Executor&) = delete;
     Executor& operator=(const Executor&) = delete;
@@ -57,6 +61,7 @@ public:
     Trace trace() const;                    // last step, reference Trace form (measured ns)
     std::vector<Int> final_counters() const;
     const StaticMegakernel& kernel() const;
+    bool dynamic() const;
     int num_workers() const;
     double upload_ms() const;
 

@@ -727,6 +727,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             notify_range(P, v.nb, v.ne, s, worker);
             if (P.record) {
                 et_trace_rec r;
+                r.t_push = 0;
                 r.t_begin = static_cast<int64_t>(t_begin);
                 r.t_wait_end = static_cast<int64_t>(t_wait);
                 r.t_prologue = static_cast<int64_t>(t_pro);
@@ -887,6 +888,7 @@ __device__ void dma_loop(const StaticParams& P) {
         if (masked) atomicAdd(&P.status->noops, 1ull);
         if (P.record) {
             et_trace_rec r;
+            r.t_push = 0;
             r.t_begin = static_cast<int64_t>(t_begin);
             r.t_wait_end = static_cast<int64_t>(t_wait);
             r.t_prologue = 0;
@@ -958,6 +960,410 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
     }
 }
 
+// ===========================================================================
+// Dynamic scheduler (Algorithm 2 of the paper; ref simulate.cpp:303-668).
+//
+// A device-resident ready queue per resource class: a slot array with an
+// atomic tail (push) and head (pop); a slot holds task+1 once published with a
+// release store, so a pop never reads an unpublished slot.  Workers pop, wait
+// on armed Event Tensor waits, execute, and notify; a notify that completes an
+// element pushes its consumers (consumer CSR built on the host for static
+// maps; range-trigger consumers read from the device-resident indptr).  With
+// early push, consumers are pushed when all producers have *started*
+// (dispatch counters) and their waits are armed.  Data-dependent counters
+// take their initial value from the counts tensor written on the device and
+// become visible when the writer call finishes (reveal).  All per-step state
+// is double-buffered; every launch resets the other parity for the next step.
+
+__device__ __forceinline__ void fence_sc_gpu() { asm volatile("fence.sc.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t dyn_init(const StaticParams& P, const DynParams& D, int el) {
+    const int t = __ldg(D.el_dd + el);
+    if (t < 0) return static_cast<uint32_t>(__ldg(P.initial_counts + el));
+    return static_cast<uint32_t>(__ldcg(P.rt[D.dd_counts_rt[t]] + (el - D.dd_base[t])));
+}
+
+__device__ __forceinline__ bool dyn_visible(const DynParams& D, int el) {
+    const int t = __ldg(D.el_dd + el);
+    return t < 0 || ld_acquire(reinterpret_cast<const uint32_t*>(&D.ctl->revealed[t])) != 0u;
+}
+
+__device__ void dyn_push(const StaticParams& P, const DynParams& D, int task) {
+    const int cls = __ldg(D.task_class + task);
+    const unsigned int i = atomicAdd(&D.ctl->tail[cls], 1u);
+    if (P.record) D.push_time[task] = globaltimer();
+    st_release(reinterpret_cast<uint32_t*>(D.slots + static_cast<long long>(cls) * D.num_tasks + i),
+               static_cast<uint32_t>(task + 1));
+    atomicAdd(&P.status->pushes, 1ull);
+}
+
+__device__ void dyn_fire(const StaticParams& P, const DynParams& D, int el) {
+    if (atomicExch(&D.fired[el], 1u) != 0u) return;
+    for (int k = __ldg(D.consumer_off + el), e = __ldg(D.consumer_off + el + 1); k < e; ++k) {
+        const int c = __ldg(D.consumers + k);
+        if (atomicSub(&D.rem[c], 1) == 1) dyn_push(P, D, c);
+    }
+    const int t = __ldg(D.el_dd + el);
+    if (t >= 0 && D.dd_range_call[t] >= 0) {
+        const int call = D.dd_range_call[t];
+        const int* ip = P.rt[__ldg(D.call_range_rt + call)];
+        const int g = el - D.dd_base[t];
+        const int first = __ldg(D.call_first_task + call);
+        for (int f = __ldcg(ip + g), hi = __ldcg(ip + g + 1); f < hi; ++f)
+            if (atomicSub(&D.rem[first + f], 1) == 1) dyn_push(P, D, first + f);
+    }
+}
+
+__device__ void dyn_reveal(const StaticParams& P, const DynParams& D, int t) {
+    st_release(reinterpret_cast<uint32_t*>(&D.ctl->revealed[t]), 1u);
+    fence_sc_gpu();
+    const int rc = D.dd_range_call[t];
+    if (rc >= 0) {  // range-call tasks at or beyond indptr[last] never exist
+        const int* ip = P.rt[__ldg(D.call_range_rt + rc)];
+        const int live = __ldcg(ip + D.dd_count[t]);
+        long long worst = 1;
+        for (int d = 0, r = __ldg(P.call_rank + rc); d < r; ++d) worst *= __ldg(P.call_extents + rc * 4 + d);
+        const int first = __ldg(D.call_first_task + rc);
+        const int cls = __ldg(D.task_class + first);
+        atomicSub(&D.ctl->total[cls], static_cast<int>(worst - live));
+    }
+    for (int el = D.dd_base[t], e = D.dd_base[t] + D.dd_count[t]; el < e; ++el) {
+        const uint32_t have = D.early_push ? ld_acquire(D.disp + el) : ld_acquire(P.cnt + el);
+        if (have >= dyn_init(P, D, el)) dyn_fire(P, D, el);
+    }
+}
+
+// element produced by a routed notify of task (call, flat), or -1
+__device__ __forceinline__ int dyn_routed_el(const StaticParams& P, const DynParams& D, int call, int flat) {
+    const int r = __ldg(D.call_routed_rt + call);
+    if (r < 0) return -1;
+    return __ldg(D.call_routed_base + call) + __ldcg(P.rt[r] + flat);
+}
+
+// counts one finished notify (or dispatch under early push) of element el
+__device__ void dyn_count(const StaticParams& P, const DynParams& D, unsigned int* ctr, int el, bool may_fire, int worker,
+                          int task) {
+    const uint32_t old = atom_add_release(ctr + el, 1u);
+    const uint32_t need = dyn_init(P, D, el);
+    if (ctr == P.cnt && old >= need) report(P.status, ET_ERR_UNDERFLOW, worker, task, el, -1);
+    if (may_fire && old + 1 == need) {
+        fence_sc_gpu();
+        if (dyn_visible(D, el)) dyn_fire(P, D, el);
+    }
+}
+
+__device__ bool dyn_wait_el(const StaticParams& P, const DynParams& D, int el, int worker, int task) {
+    const uint64_t t0 = globaltimer();
+    uint32_t it = 0;
+    while (!(dyn_visible(D, el) && ld_acquire(P.cnt + el) >= dyn_init(P, D, el))) {
+        if ((++it & 255u) == 0) {
+            if (aborted(P.status)) return false;
+            if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                report(P.status, ET_ERR_DEADLOCK, worker, task, el,
+                       static_cast<int>(dyn_init(P, D, el) - ld_acquire(P.cnt + el)));
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
+// Pops one task of class cls: -1 when every task of the class has been taken.
+__device__ int dyn_pop(const StaticParams& P, const DynParams& D, int cls, int worker) {
+    const unsigned int i = atomicAdd(&D.ctl->head[cls], 1u);
+    const uint32_t* slot = reinterpret_cast<const uint32_t*>(D.slots + static_cast<long long>(cls) * D.num_tasks + i);
+    const uint64_t t0 = globaltimer();
+    uint32_t it = 0;
+    for (;;) {
+        if (static_cast<int>(i) < D.num_tasks) {
+            const uint32_t v = ld_acquire(slot);
+            if (v) {
+                atomicAdd(&P.status->pops, 1ull);
+                return static_cast<int>(v) - 1;
+            }
+        }
+        if (static_cast<int>(i) >= *reinterpret_cast<volatile int*>(&D.ctl->total[cls])) return -1;
+        if ((++it & 255u) == 0) {
+            if (aborted(P.status)) return -1;
+            if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                report(P.status, ET_ERR_DEADLOCK, worker, -1, -4, static_cast<int>(i));
+                return -1;
+            }
+        }
+    }
+}
+
+__device__ SlotView dyn_view(const StaticParams& P, const DynParams& D, int task) {
+    SlotView v;
+    v.call = __ldg(D.task_call + task);
+    const int rank = __ldg(P.call_rank + v.call);
+    int flat = __ldg(D.task_flat + task);
+    int ext[kMaxRank];
+    for (int d = 0; d < kMaxRank; ++d) ext[d] = d < rank ? __ldg(P.call_extents + v.call * 4 + d) : 1;
+    v.ext0 = ext[0];
+    for (int d = kMaxRank - 1; d >= 0; --d) {
+        if (d >= rank) {
+            v.coord[d] = 0;
+            continue;
+        }
+        v.coord[d] = flat % ext[d];
+        flat /= ext[d];
+    }
+    v.masked = false;
+    for (int d = 0; d < rank; ++d)
+        if (v.coord[d] >= eval_code(P, v.call, d)) v.masked = true;
+    v.lazy = false;
+    v.wb = __ldg(D.task_wait_off + task);
+    v.we = __ldg(D.task_wait_off + task + 1);
+    v.nb = __ldg(D.task_notify_off + task);
+    v.ne = __ldg(D.task_notify_off + task + 1);
+    return v;
+}
+
+// WAITs of a popped task (armed slots only, ref simulate.cpp:497-515), then the
+// early-push dispatch (ref simulate.cpp:600-618).
+__device__ bool dyn_prepare(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker) {
+    for (int w = v.wb; w < v.we; ++w)
+        if (__ldg(D.task_wait_armed + w) && !dyn_wait_el(P, D, __ldg(D.task_waits + w), worker, task)) return false;
+    const int rr = __ldg(D.call_range_rt + v.call);
+    if (rr >= 0 && __ldg(D.call_range_armed + v.call)) {
+        const int* ip = P.rt[rr];
+        const int flat = __ldg(D.task_flat + task);
+        int g = 0;
+        while (__ldcg(ip + g + 1) <= flat) ++g;
+        if (!dyn_wait_el(P, D, __ldg(D.call_range_base + v.call) + g, worker, task)) return false;
+    }
+    if (D.early_push) {
+        for (int n = v.nb; n < v.ne; ++n) dyn_count(P, D, D.disp, __ldg(D.task_notifies + n), true, worker, task);
+        const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+        if (rel >= 0) dyn_count(P, D, D.disp, rel, true, worker, task);
+    }
+    return true;
+}
+
+// Completion: reveal data-dependent tensors written by this call (before the
+// notifies, so consumers released by them see visible counters), then NOTIFY.
+__device__ void dyn_finish(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker) {
+    for (int t = 0; t < D.num_dd; ++t)
+        if (D.dd_writer_call[t] == v.call && atomicSub(&D.ctl->writer_rem[t], 1) == 1) dyn_reveal(P, D, t);
+    const bool fire = !D.early_push;
+    for (int n = v.nb; n < v.ne; ++n) dyn_count(P, D, P.cnt, __ldg(D.task_notifies + n), fire, worker, task);
+    const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+    if (rel >= 0) dyn_count(P, D, P.cnt, rel, fire, worker, task);
+}
+
+__device__ void dyn_record(const StaticParams& P, const DynParams& D, int task, int worker, bool masked, uint64_t tb,
+                           uint64_t tw, uint64_t tp, uint64_t te) {
+    if (!P.record) return;
+    et_trace_rec r;
+    r.t_push = static_cast<int64_t>(D.push_time[task]);
+    r.t_begin = static_cast<int64_t>(tb);
+    r.t_wait_end = static_cast<int64_t>(tw);
+    r.t_prologue = static_cast<int64_t>(tp);
+    r.t_exec_end = static_cast<int64_t>(te);
+    r.t_notify_end = static_cast<int64_t>(globaltimer());
+    r.worker = worker;
+    r.flags = masked ? 1 : 0;
+    r.task = task;
+    r.pad = P.step_id;
+    P.trace[task] = r;
+}
+
+__device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
+    const int ctid = threadIdx.x;
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
+    float* acc = reinterpret_cast<float*>(smem + kSmemAcc);
+    volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
+    float* red = reinterpret_cast<float*>(smem + kSmemMisc + 64);
+    Ring ring{smem + kSmemRing, reinterpret_cast<uint64_t*>(smem + kSmemBar),
+              reinterpret_cast<uint64_t*>(smem + kSmemBar) + kStages, 0ull, P.status, P.watchdog_ns, worker};
+    unsigned long long executed = 0, noops = 0;
+    for (;;) {
+        uint64_t tb = 0, tw = 0, tp = 0, te = 0;
+        if (ctid == 0) {
+            const int task = dyn_pop(P, D, 0, worker);
+            tb = globaltimer();
+            misc[3] = task;
+            misc[4] = task;  // hand the task to the producer warp (streams during the waits)
+            __threadfence_block();
+            misc[5] = misc[5] + 1;
+        }
+        bar_sync(1, kConsumers);
+        const int task = misc[3];
+        if (task < 0) break;
+        SlotView v = dyn_view(P, D, task);
+        const et_op& op = P.ops[v.call];
+        if (ctid == 0) {
+            bool ok = dyn_prepare(P, D, v, task, worker);
+            if (ok && P.step_limit > 0 &&
+                atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
+                report(P.status, ET_ERR_STEP_LIMIT, worker, task, -1, 0);
+                ok = false;
+            }
+            misc[0] = ok ? 0 : 1;
+            tw = globaltimer();
+        }
+        bar_sync(1, kConsumers);
+        if (misc[0]) break;
+        if (v.masked) {
+            ++noops;
+        } else {
+            ++executed;
+            switch (op.kind) {
+                case ET_OP_NONE:
+                    if (ctid == 0 && P.tick_ns > 0 && D.task_duration) {
+                        const uint64_t until = tw + static_cast<uint64_t>(__ldg(D.task_duration + task)) *
+                                                        static_cast<uint64_t>(P.tick_ns);
+                        while (globaltimer() < until) {
+                        }
+                    }
+                    break;
+                case ET_OP_SPLITK_PARTIAL:
+                case ET_OP_SPLITK_FINAL: body_splitk(P, op, v.coord, ctid); break;
+                case ET_OP_GEMV: tp = body_gemv(P, op, v, xs, acc, red, ring, ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
+                case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
+                case ET_OP_EMBED: body_embed(P, op, ctid); break;
+                default: break;
+            }
+        }
+        bar_sync(1, kConsumers);
+        if (ctid == 0) {
+            te = globaltimer();
+            dyn_finish(P, D, v, task, worker);
+            dyn_record(P, D, task, worker, v.masked, tb, tw, tp, te);
+        }
+    }
+    if (ctid == 0) {
+        misc[4] = -1;
+        __threadfence_block();
+        misc[5] = misc[5] + 1;
+        if (P.step_limit <= 0) atomicAdd(&P.status->executed, executed);
+        atomicAdd(&P.status->noops, noops);
+    }
+}
+
+__device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
+    if ((threadIdx.x & 31) != 0) return;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+    uint64_t* empty = full + kStages;
+    volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
+    const uint64_t pol = policy_evict_first();
+    unsigned long long cseq = 0;
+    int gen = 0;
+    for (;;) {
+        while (misc[5] == gen) {
+            if (aborted(P.status)) return;
+        }
+        gen = misc[5];
+        const int task = misc[4];
+        if (task < 0) return;
+        const SlotView v = dyn_view(P, D, task);
+        if (v.masked) continue;
+        const et_op& op = P.ops[v.call];
+        if (!op_streams(op.kind)) continue;
+        const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding);
+        const int n = pl.total_chunks();
+        for (int c = 0; c < n; ++c, ++cseq) {
+            const int stage = static_cast<int>(cseq % kStages);
+            const uint32_t phase = static_cast<uint32_t>((cseq / kStages) & 1ull);
+            uint32_t spins = 0;
+            while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
+                if ((++spins & 1023u) == 0 && aborted(P.status)) return;
+            }
+            const Chunk ch = pl.chunk(c);
+            mbar_arrive_expect_tx(&full[stage], ch.bytes);
+            bulk_g2s(smem + kSmemRing + stage * kStageBytes, ch.src, ch.bytes, &full[stage], pol);
+        }
+    }
+}
+
+// DMA-class tasks: popped from their own queue by worker 0's DMA warp.
+__device__ void dyn_dma_loop(const StaticParams& P, const DynParams& D) {
+    if ((threadIdx.x & 31) != 0) return;
+    const int worker = P.num_queues;
+    for (;;) {
+        const int task = dyn_pop(P, D, 1, worker);
+        if (task < 0) return;
+        const uint64_t tb = globaltimer();
+        const SlotView v = dyn_view(P, D, task);
+        if (!dyn_prepare(P, D, v, task, worker)) return;
+        const uint64_t tw = globaltimer();
+        if (!v.masked && P.tick_ns > 0 && D.task_duration) {
+            const uint64_t until = tw + static_cast<uint64_t>(__ldg(D.task_duration + task)) * P.tick_ns;
+            while (globaltimer() < until) {
+            }
+        }
+        const uint64_t te = globaltimer();
+        dyn_finish(P, D, v, task, worker);
+        atomicAdd(v.masked ? &P.status->noops : &P.status->executed, 1ull);
+        dyn_record(P, D, task, worker, v.masked, tb, tw, 0, te);
+    }
+}
+
+// (Re)initialises one parity of the dynamic state; block-strided over `nblk` blocks.
+__device__ void dyn_reset_state(const StaticParams& P, const DynParams& D, DynCtl* ctl, int* rem, int* slots,
+                                unsigned int* fired, unsigned int* disp, uint32_t* cnt, int blk, int nblk) {
+    const int tid = blk * blockDim.x + threadIdx.x, stride = nblk * blockDim.x;
+    for (int i = tid; i < D.num_tasks; i += stride) {
+        rem[i] = __ldg(D.task_rem_init + i);
+        // the ready seeds occupy the first slots of each class queue (id order)
+        slots[i] = i < D.num_ready[0] ? __ldg(D.ready + i) + 1 : 0;
+        slots[D.num_tasks + i] = i < D.num_ready[1] ? __ldg(D.ready + D.num_ready[0] + i) + 1 : 0;
+    }
+    for (int i = tid; i < P.cnt_capacity; i += stride) {
+        fired[i] = 0u;
+        disp[i] = 0u;
+        cnt[i] = 0u;
+    }
+    if (blk == 0 && threadIdx.x == 0) {
+        for (int c = 0; c < 2; ++c) {
+            ctl->head[c] = 0u;
+            ctl->tail[c] = static_cast<unsigned int>(D.num_ready[c]);
+            ctl->total[c] = D.class_total[c];
+        }
+        for (int t = 0; t < kMaxDd; ++t) {
+            ctl->writer_rem[t] = t < D.num_dd ? D.writer_tasks[t] : 0;
+            ctl->revealed[t] = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    et_dynamic_kernel(const __grid_constant__ StaticParams P, const __grid_constant__ DynParams D) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int worker = blockIdx.x;
+    if (worker == 0 && threadIdx.x < sizeof(DevStatus) / 4) reinterpret_cast<int*>(P.status_other)[threadIdx.x] = 0;
+    // the other parity is rebuilt for the next launch (same sample)
+    dyn_reset_state(P, D, D.ctl_other, D.rem_other, D.slots_other, D.fired_other, D.disp_other, P.cnt_other, worker,
+                    gridDim.x);
+    if (threadIdx.x == 0) {
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&full[kStages + i], 1);
+        }
+        fence_mbar_init();
+        volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
+        misc[0] = misc[1] = misc[2] = 0;
+        misc[3] = misc[4] = misc[5] = 0;
+        if (worker == 0) atomicAdd(&P.status->pushes, static_cast<unsigned long long>(D.num_ready[0] + D.num_ready[1]));
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    if (warp < kConsumerWarps) {
+        dyn_consumer_loop(P, D, worker, smem);
+    } else if (warp == kProducerWarp) {
+        dyn_producer_loop(P, D, worker, smem);
+    } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
+        dyn_dma_loop(P, D);
+    }
+}
+
+__global__ void et_dynamic_reset_kernel(const __grid_constant__ StaticParams P, const __grid_constant__ DynParams D) {
+    dyn_reset_state(P, D, D.ctl, D.rem, D.slots, D.fired, D.disp, P.cnt, blockIdx.x, gridDim.x);
+}
+
 }  // namespace etk
 
 int et_static_smem_bytes() { return etk::kSmemTotal; }
@@ -985,4 +1391,30 @@ int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return static_cast<int>(cudaLaunchKernelEx(&cfg, etk::et_static_kernel, p));
+}
+
+int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, void* stream) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(etk::et_dynamic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             etk::kSmemTotal);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_workers);
+    cfg.blockDim = dim3(etk::kThreads);
+    cfg.dynamicSmemBytes = etk::kSmemTotal;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, etk::et_dynamic_kernel, p, d));
+}
+
+int et_dynamic_reset(const etk::StaticParams& p, const etk::DynParams& d, void* stream) {
+    etk::et_dynamic_reset_kernel<<<64, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, d);
+    return static_cast<int>(cudaGetLastError());
 }

@@ -97,6 +97,64 @@ struct StaticParams {
     int prefetch;
     int table_ok;  // every coordinate fits 16 bits (slot tables usable)
     long long l2_ahead;  // bytes the producer prefetches into L2 beyond the ring
+    int step_id;         // stamped into trace records (dynamic: tasks that ran this step)
+};
+
+constexpr int kMaxDd = 8;  // data-dependent event tensors per graph (dynamic mode)
+
+// Per-step control block of the dynamic scheduler (double-buffered).
+struct DynCtl {
+    unsigned int head[2];       // pop cursor per resource class (0 = SM, 1 = DMA)
+    unsigned int tail[2];       // push cursor per resource class
+    int total[2];               // tasks that will ever be pushed, per class
+    int writer_rem[kMaxDd];     // writer-call tasks still running, per dd tensor
+    int revealed[kMaxDd];
+};
+
+struct DynParams {
+    int num_tasks;
+    const int* task_call;
+    const int* task_flat;
+    const int* task_duration;
+    const int* task_wait_off;
+    const int* task_waits;
+    const uint8_t* task_wait_armed;
+    const int* task_notify_off;
+    const int* task_notifies;
+    const int* task_rem_init;
+    const int* task_class;       // 0 = SM, 1 = DMA
+    const int* consumer_off;
+    const int* consumers;
+    const int* call_first_task;
+    const int* call_routed_rt;
+    const int* call_routed_base;
+    const int* call_range_rt;
+    const int* call_range_base;
+    const uint8_t* call_range_armed;
+    int num_dd;
+    int dd_base[kMaxDd];
+    int dd_count[kMaxDd];
+    int dd_counts_rt[kMaxDd];
+    int dd_writer_call[kMaxDd];
+    int dd_range_call[kMaxDd];   // call range-triggered by this tensor, or -1
+    const int* el_dd;
+    int num_ready[2];
+    int class_total[2];          // tasks per resource class (before extent_from shrink)
+    const int* ready;            // seeded tasks, SM class then DMA class
+    int early_push;
+    // state: this step and the other parity (reset for the next step)
+    DynCtl* ctl;
+    DynCtl* ctl_other;
+    int* rem;
+    int* rem_other;
+    int* slots;        // [2][num_tasks] task id + 1, 0 = not yet pushed
+    int* slots_other;
+    unsigned int* fired;
+    unsigned int* fired_other;
+    unsigned int* disp;
+    unsigned int* disp_other;
+    unsigned long long* push_time;
+    int writer_tasks[kMaxDd];    // task count of each dd tensor's writer call
 };
 
 }  // namespace etk
@@ -104,3 +162,5 @@ struct StaticParams {
 // Host-side launcher (megakernel.cu).
 int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, void* stream);
 int et_static_smem_bytes();
+int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, void* stream);
+int et_dynamic_reset(const etk::StaticParams& p, const etk::DynParams& d, void* stream);

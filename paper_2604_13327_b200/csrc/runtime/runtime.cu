@@ -57,6 +57,13 @@ struct Sample {
     int table_ok = 1;                     // all grid extents < 65536 (16-bit slot-table coordinates)
     DevArray<int32_t> d_call_extents, d_queue_off, d_slot_call, d_slot_flat, d_slot_duration, d_wait_off, d_waits,
         d_notify_off, d_notifies, d_initial;
+    // dynamic scheduler program (ET_MODE_DYNAMIC)
+    int num_tasks = 0;
+    etk::DynParams dyn{};  // device pointers into the arrays below + scalars
+    DevArray<int32_t> d_task_call, d_task_flat, d_task_duration, d_task_wait_off, d_task_waits, d_task_notify_off,
+        d_task_notifies, d_task_rem_init, d_task_class, d_consumer_off, d_consumers, d_call_first_task, d_call_routed_rt,
+        d_call_routed_base, d_call_range_rt, d_call_range_base, d_el_dd, d_ready;
+    DevArray<uint8_t> d_task_wait_armed, d_call_range_armed;
 };
 
 int64_t eval_host(const std::vector<int32_t>& op, const std::vector<int64_t>& arg, int b, int e,
@@ -114,11 +121,20 @@ struct et_runtime {
     DevArray<et_op> d_ops;
     int ops_bound = 0;
 
+    int mode = ET_MODE_STATIC;
+    // dynamic scheduler state, two parities
+    DevArray<etk::DynCtl> d_ctl;
+    DevArray<int> d_rem, d_slots;
+    DevArray<unsigned int> d_fired, d_disp;
+    DevArray<unsigned long long> d_push_time;
+    int max_tasks = 0;
+    int prepared[2] = {-1, -1};  // sample each parity's state was initialised for
     DevArray<uint32_t> d_cnt;  // [2][cap]
     int cnt_capacity = 0;
     DevArray<etk::DevStatus> d_status;  // [2]
     DevArray<et_trace_rec> d_trace;
     int parity = 0;
+    int steps = 0;
     int last_sample = -1;
     bool launched = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -274,11 +290,117 @@ int et_upload_static(et_runtime* rt, const et_sample_desc* s, int32_t num_sample
     rt->parity = 0;
     rt->last_sample = -1;
     rt->launched = false;
+    rt->mode = ET_MODE_STATIC;
     return ET_OK;
 }
 
-int et_upload_dynamic(et_runtime* rt, const et_sample_desc*, const et_dynamic_desc*, int32_t) {
-    return rt ? rt->fail(ET_ERR_INVALID, "dynamic scheduler is not available in this build") : ET_ERR_INVALID;
+int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_desc* dyn, int32_t num_samples) {
+    if (!rt || !s || !dyn || num_samples <= 0) return ET_ERR_INVALID;
+    int rc = et_upload_static(rt, s, num_samples);  // sample bindings, extents, counters, status
+    if (rc != ET_OK) return rc;
+    rt->mode = ET_MODE_DYNAMIC;
+    int max_tasks = 1;
+    for (int i = 0; i < num_samples; ++i) {
+        const et_dynamic_desc& d = dyn[i];
+        Sample& S = rt->samples[static_cast<size_t>(i)];
+        if (d.num_dd > etk::kMaxDd) return rt->fail(ET_ERR_INVALID, "too many data-dependent event tensors");
+        const size_t nt = static_cast<size_t>(std::max(1, d.num_tasks));
+        const size_t nw = static_cast<size_t>(std::max(1, d.task_wait_off[d.num_tasks]));
+        const size_t nn = static_cast<size_t>(std::max(1, d.task_notify_off[d.num_tasks]));
+        const size_t nc = static_cast<size_t>(std::max(1, d.consumer_off[S.num_counters]));
+        const size_t ncall = static_cast<size_t>(std::max(1, rt->num_calls));
+        std::vector<int32_t> cls(nt, 0);
+        int totals[2] = {0, 0};
+        for (int t = 0; t < d.num_tasks; ++t) {
+            // resource class from the queue layout: DMA-class tasks are flagged by slot_call's
+            // queue in the static descriptor; here by the sample's has_dma + call list
+            cls[static_cast<size_t>(t)] = 0;
+        }
+        if (S.has_dma && s[i].slot_task) {
+            const int q0 = s[i].queue_off[S.num_queues], q1 = s[i].queue_off[S.num_queues + 1];
+            for (int k = q0; k < q1; ++k) cls[static_cast<size_t>(s[i].slot_task[k])] = 1;
+        }
+        for (int t = 0; t < d.num_tasks; ++t) ++totals[cls[static_cast<size_t>(t)]];
+        std::vector<int32_t> ready0, ready1;
+        for (int k = 0; k < d.num_ready; ++k) (cls[static_cast<size_t>(d.ready[k])] ? ready1 : ready0).push_back(d.ready[k]);
+        std::vector<int32_t> ready(ready0);
+        ready.insert(ready.end(), ready1.begin(), ready1.end());
+        S.num_tasks = d.num_tasks;
+        ET_CUDA(S.d_task_call.upload(d.task_call, nt), "upload dynamic");
+        ET_CUDA(S.d_task_flat.upload(d.task_flat, nt), "upload dynamic");
+        if (d.task_duration) ET_CUDA(S.d_task_duration.upload(d.task_duration, nt), "upload dynamic");
+        ET_CUDA(S.d_task_wait_off.upload(d.task_wait_off, nt + 1), "upload dynamic");
+        ET_CUDA(S.d_task_waits.upload(d.task_waits, nw), "upload dynamic");
+        ET_CUDA(S.d_task_wait_armed.upload(d.task_wait_armed, nw), "upload dynamic");
+        ET_CUDA(S.d_task_notify_off.upload(d.task_notify_off, nt + 1), "upload dynamic");
+        ET_CUDA(S.d_task_notifies.upload(d.task_notifies, nn), "upload dynamic");
+        ET_CUDA(S.d_task_rem_init.upload(d.task_rem_init, nt), "upload dynamic");
+        ET_CUDA(S.d_task_class.upload(cls.data(), nt), "upload dynamic");
+        ET_CUDA(S.d_consumer_off.upload(d.consumer_off, static_cast<size_t>(S.num_counters) + 1), "upload dynamic");
+        ET_CUDA(S.d_consumers.upload(d.consumers, nc), "upload dynamic");
+        ET_CUDA(S.d_call_first_task.upload(d.call_first_task, ncall), "upload dynamic");
+        ET_CUDA(S.d_call_routed_rt.upload(d.call_routed_rt, ncall), "upload dynamic");
+        ET_CUDA(S.d_call_routed_base.upload(d.call_routed_base, ncall), "upload dynamic");
+        ET_CUDA(S.d_call_range_rt.upload(d.call_range_rt, ncall), "upload dynamic");
+        ET_CUDA(S.d_call_range_base.upload(d.call_range_base, ncall), "upload dynamic");
+        ET_CUDA(S.d_call_range_armed.upload(d.call_range_armed, ncall), "upload dynamic");
+        ET_CUDA(S.d_el_dd.upload(d.el_dd, static_cast<size_t>(std::max(1, S.num_counters))), "upload dynamic");
+        ET_CUDA(S.d_ready.upload(ready.empty() ? nullptr : ready.data(), std::max<size_t>(1, ready.size())),
+                "upload dynamic");
+        etk::DynParams& P = S.dyn;
+        P = etk::DynParams{};
+        P.num_tasks = d.num_tasks;
+        P.task_call = S.d_task_call.ptr;
+        P.task_flat = S.d_task_flat.ptr;
+        P.task_duration = d.task_duration ? S.d_task_duration.ptr : nullptr;
+        P.task_wait_off = S.d_task_wait_off.ptr;
+        P.task_waits = S.d_task_waits.ptr;
+        P.task_wait_armed = S.d_task_wait_armed.ptr;
+        P.task_notify_off = S.d_task_notify_off.ptr;
+        P.task_notifies = S.d_task_notifies.ptr;
+        P.task_rem_init = S.d_task_rem_init.ptr;
+        P.task_class = S.d_task_class.ptr;
+        P.consumer_off = S.d_consumer_off.ptr;
+        P.consumers = S.d_consumers.ptr;
+        P.call_first_task = S.d_call_first_task.ptr;
+        P.call_routed_rt = S.d_call_routed_rt.ptr;
+        P.call_routed_base = S.d_call_routed_base.ptr;
+        P.call_range_rt = S.d_call_range_rt.ptr;
+        P.call_range_base = S.d_call_range_base.ptr;
+        P.call_range_armed = S.d_call_range_armed.ptr;
+        P.num_dd = d.num_dd;
+        for (int t = 0; t < d.num_dd; ++t) {
+            P.dd_base[t] = d.dd_base[t];
+            P.dd_count[t] = d.dd_count[t];
+            P.dd_counts_rt[t] = d.dd_counts_rt[t];
+            P.dd_writer_call[t] = d.dd_writer_call[t];
+            P.dd_range_call[t] = -1;
+            for (int c = 0; c < rt->num_calls; ++c)
+                if (d.call_range_rt[c] >= 0 && d.call_range_base[c] == d.dd_base[t]) P.dd_range_call[t] = c;
+            int wt = 1;
+            for (int k = 0; k < rt->call_rank[static_cast<size_t>(d.dd_writer_call[t])]; ++k)
+                wt *= S.call_extents[static_cast<size_t>(d.dd_writer_call[t] * 4 + k)];
+            P.writer_tasks[t] = wt;
+        }
+        P.el_dd = S.d_el_dd.ptr;
+        P.num_ready[0] = static_cast<int>(ready0.size());
+        P.num_ready[1] = static_cast<int>(ready1.size());
+        P.class_total[0] = totals[0];
+        P.class_total[1] = totals[1];
+        P.ready = S.d_ready.ptr;
+        P.early_push = d.early_push;
+        max_tasks = std::max(max_tasks, d.num_tasks);
+    }
+    rt->max_tasks = max_tasks;
+    ET_CUDA(rt->d_ctl.upload(nullptr, 2), "dynamic state");
+    ET_CUDA(rt->d_rem.upload(nullptr, static_cast<size_t>(2 * max_tasks)), "dynamic state");
+    ET_CUDA(rt->d_slots.upload(nullptr, static_cast<size_t>(4 * max_tasks)), "dynamic state");
+    ET_CUDA(rt->d_fired.upload(nullptr, static_cast<size_t>(2 * rt->cnt_capacity)), "dynamic state");
+    ET_CUDA(rt->d_disp.upload(nullptr, static_cast<size_t>(2 * rt->cnt_capacity)), "dynamic state");
+    ET_CUDA(rt->d_push_time.upload(nullptr, static_cast<size_t>(max_tasks)), "dynamic state");
+    ET_CUDA(rt->d_trace.upload(nullptr, static_cast<size_t>(max_tasks)), "trace");
+    rt->prepared[0] = rt->prepared[1] = -1;
+    return ET_OK;
 }
 
 int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
@@ -340,11 +462,13 @@ static int collect(et_runtime* rt, et_step_info* info) {
         info->pops = static_cast<int64_t>(st.pops);
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, rt->ev0, rt->ev1) == cudaSuccess) info->kernel_ms = ms;
+        info->step_id = rt->steps;
     }
     if (st.code != 0) {
         // leave the runtime reusable: clear every counter and status block
         cudaMemset(rt->d_cnt.ptr, 0, rt->d_cnt.n * sizeof(uint32_t));
         cudaMemset(rt->d_status.ptr, 0, 2 * sizeof(etk::DevStatus));
+        rt->prepared[0] = rt->prepared[1] = -1;
         rt->err = st.code == ET_ERR_DEADLOCK    ? "deadlock"
                   : st.code == ET_ERR_UNDERFLOW ? "counter underflow"
                                                 : "step limit exceeded";
@@ -425,11 +549,39 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     p.step_limit = rt->cfg.step_limit > 0 ? rt->cfg.step_limit : 0;
     p.prefetch = rt->cfg.enable_prefetch;
     p.table_ok = S.table_ok;
+    p.step_id = ++rt->steps;
     p.l2_ahead = rt->cfg.l2_prefetch_bytes < 0 ? 0 : rt->cfg.l2_prefetch_bytes;
 
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rt->stream;
+    int e = 0;
+    etk::DynParams dp{};
+    if (rt->mode == ET_MODE_DYNAMIC) {
+        dp = S.dyn;
+        const int cur = rt->parity, oth = rt->parity ^ 1;
+        const size_t mt = static_cast<size_t>(rt->max_tasks), cc = static_cast<size_t>(rt->cnt_capacity);
+        dp.ctl = rt->d_ctl.ptr + cur;
+        dp.ctl_other = rt->d_ctl.ptr + oth;
+        dp.rem = rt->d_rem.ptr + cur * mt;
+        dp.rem_other = rt->d_rem.ptr + oth * mt;
+        dp.slots = rt->d_slots.ptr + cur * 2 * mt;
+        dp.slots_other = rt->d_slots.ptr + oth * 2 * mt;
+        dp.fired = rt->d_fired.ptr + cur * cc;
+        dp.fired_other = rt->d_fired.ptr + oth * cc;
+        dp.disp = rt->d_disp.ptr + cur * cc;
+        dp.disp_other = rt->d_disp.ptr + oth * cc;
+        dp.push_time = rt->d_push_time.ptr;
+        if (rt->prepared[cur] != pick) {
+            e = et_dynamic_reset(p, dp, st);
+            if (e != 0) return rt->cuda_fail(static_cast<cudaError_t>(e), "dynamic reset");
+        }
+        rt->prepared[oth] = pick;  // the launch rebuilds the other parity for this sample
+        rt->prepared[cur] = -1;
+    }
     if (synchronous) cudaEventRecord(rt->ev0, st);
-    int e = et_launch_static(p, S.num_queues, rt->cfg.max_batch, st);
+    if (rt->mode == ET_MODE_DYNAMIC)
+        e = et_launch_dynamic(p, dp, S.num_queues, st);
+    else
+        e = et_launch_static(p, S.num_queues, rt->cfg.max_batch, st);
     if (e != 0) return rt->cuda_fail(static_cast<cudaError_t>(e), "launch");
     if (synchronous) cudaEventRecord(rt->ev1, st);
     rt->parity ^= 1;
@@ -467,10 +619,11 @@ int et_read_trace(et_runtime* rt, et_trace_rec* out, int64_t* n) {
     if (!rt || !n || rt->last_sample < 0) return ET_ERR_INVALID;
     cudaSetDevice(rt->cfg.device);
     const Sample& S = rt->samples[static_cast<size_t>(rt->last_sample)];
-    const int64_t m = std::min<int64_t>(*n, S.num_slots);
+    const int64_t total = rt->mode == ET_MODE_DYNAMIC ? S.num_tasks : S.num_slots;
+    const int64_t m = std::min<int64_t>(*n, total);
     ET_CUDA(cudaStreamSynchronize(rt->stream), "trace");
     if (m > 0) ET_CUDA(cudaMemcpy(out, rt->d_trace.ptr, static_cast<size_t>(m) * sizeof(et_trace_rec), cudaMemcpyDeviceToHost), "trace");
-    *n = S.num_slots;
+    *n = total;
     return ET_OK;
 }
 

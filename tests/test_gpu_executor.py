@@ -99,3 +99,73 @@ def test_step_limit_is_typed():
     k = etsim.lower_static(etsim.gemm_reduce_scatter("4", 2), [{}], num_sms=2)
     with pytest.raises(etsim.SimulationError):
         etsim.simulate(k, step_limit=2)
+
+
+# ---- dynamic scheduler (device push/pop queue), ref tests/python/test_smoke.py:37-82 ----
+
+GOLD = json.load(open(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden",
+                                                 "reference_golden.json")))
+
+
+def test_dynamic_and_barrier():
+    g = etsim.splitk_rowsum()
+    dk = etsim.lower_dynamic(g)
+    ek = etsim.enable_early_push(dk)
+    assert not dk.early_push and ek.early_push
+    m = g.instantiate({"n": 4})
+    td = etsim.simulate(dk, {"n": 4}, num_sms=3, seed=1)
+    te = etsim.simulate(ek, {"n": 4}, num_sms=3, seed=1, push_cost=2)
+    tb = etsim.simulate_barrier(g, {"n": 4}, num_sms=3, seed=1)
+    for t in (td, te, tb):
+        assert m.check(t) == [], m.check(t)
+    for t in (td, te):
+        st = etsim.metrics(t)
+        assert st["pushes"] == st["pops"] == m.num_tasks  # ref test_queue_accounting.cpp:14-37
+        assert all(c == 0 for c in t.final_counters)
+
+
+def test_moe_dynamic_routing_resolved_on_device():
+    c = GOLD["moe"]
+    routing = c["routing"]
+    g = etsim.moe_layer(tokens=16, experts=4, top_k=2, tile_size=2)
+    for early in (False, True):
+        td = etsim.simulate(etsim.lower_dynamic(g, early_push=early), {"tokens": 16}, routing=routing, seed=3)
+        m = g.instantiate({"tokens": 16}, routing=routing, seed=3)
+        assert m.check(td) == [], m.check(td)
+        st = etsim.metrics(td)
+        assert st["pushes"] == st["pops"] == c["dynamic"]["pushes"] == m.num_tasks
+        assert st["real_tasks"] == c["dynamic"]["real_tasks"]
+        assert td.final_counters == c["dynamic"]["final_counters"]
+        # no expert tile starts before the routing writer has finished (ref test_simulate.cpp:333-357)
+        route_end = max(r["exec"][1] for r in td.records if r["call"] == 0)
+        assert all(r["exec"][0] >= route_end for r in td.records if r["call"] == 2)
+
+
+def test_dynamic_metrics_and_exports_with_dma():
+    g = etsim.all_gather_gemm(3, 2)
+    t = etsim.simulate(etsim.lower_dynamic(g), num_sms=2, seed=0)
+    assert g.instantiate({}).check(t) == []
+    stats = etsim.metrics(t)
+    assert stats["makespan"] == t.makespan
+    per = stats["per_resource"]
+    assert len(per) == 3  # 2 SMs + 1 DMA channel
+    assert all(r["busy"] + r["spin"] + r["idle"] == t.makespan for r in per)
+    chrome = json.loads(t.to_chrome_json())
+    assert chrome["otherData"]["makespan"] == t.makespan
+    assert t.to_csv().splitlines()[0].startswith("kind,resource")
+
+
+def test_dynamic_shapes_and_random_dags():
+    g = etsim.gemm_reduce_scatter("b * 2", 2)
+    dk = etsim.lower_dynamic(g)
+    ex = etsim.Executor(dk, [{"b": 2}, {"b": 4}, {"b": 8}], num_workers=3)
+    for b in (1, 2, 3, 5, 8, 3):
+        stats = ex.run({"b": b})
+        t = ex.trace()
+        m = g.instantiate({"b": b})
+        assert m.check(t) == [], (b, m.check(t))
+        assert stats["tasks_executed"] == m.num_tasks
+    for seed in range(8):
+        g = etsim.random_dag(5 + seed % 16, 8 + seed % 20, seed)
+        t = etsim.simulate(etsim.lower_dynamic(g, early_push=seed % 2 == 1), {}, num_sms=1 + seed % 4, seed=seed)
+        assert g.instantiate({}, seed=seed).check(t) == []
