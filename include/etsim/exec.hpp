@@ -59,6 +59,7 @@ public:
     StepStats sync();
 
     Trace trace() const;                    // last step, reference Trace form (measured ns)
+    std::vector<et_trace_rec> raw_trace() const;  // last step, device records in slot / task order
     std::vector<Int> final_counters() const;
     const StaticMegakernel& kernel() const;
     bool dynamic() const;

@@ -791,6 +791,17 @@ Trace Executor::trace() const {
     return t;
 }
 
+std::vector<et_trace_rec> Executor::raw_trace() const {
+    Impl& I = *impl_;
+    if (I.last_sample < 0) throw Error("no step has run");
+    const HostSample& h = I.hs[static_cast<size_t>(I.last_sample)];
+    std::vector<et_trace_rec> recs(I.dyn ? h.slot_call.size() : h.slot_task.size());
+    int64_t n = static_cast<int64_t>(recs.size());
+    I.check(et_read_trace(I.rt, recs.data(), &n), "read trace");
+    recs.resize(static_cast<size_t>(n));
+    return recs;
+}
+
 const StaticMegakernel& Executor::kernel() const { return impl_->k; }
 bool Executor::dynamic() const { return impl_->dyn; }
 int Executor::num_workers() const { return impl_->workers; }

@@ -223,6 +223,10 @@ struct Ring {
     DevStatus* status;
     long long watchdog_ns;
     int worker;
+    unsigned long long stall = 0;  // ns spent waiting for filled stages (ET_DEBUG bit 2)
+    bool dbg = false;
+    unsigned long long busy = 0;   // ns between a stage's arrival and its release (ET_DEBUG bit 8)
+    uint64_t t_ret = 0;
 
     __device__ __forceinline__ static int stage_of(unsigned long long c) { return static_cast<int>(c % kStages); }
     __device__ __forceinline__ static uint32_t parity_of(unsigned long long c) {
@@ -234,6 +238,7 @@ struct Ring {
     __device__ __forceinline__ const uint8_t* wait(unsigned long long c) {
         const int st = stage_of(c);
         const uint32_t par = parity_of(c);
+        const uint64_t t00 = dbg ? globaltimer() : 0;
         if (!mbar_try_wait(&full[st], par)) {
             const uint64_t t0 = globaltimer();
             uint32_t it = 0;
@@ -247,13 +252,27 @@ struct Ring {
                 }
             }
         }
+        if (dbg) {
+            const uint64_t now = globaltimer();
+            stall += now - t00;
+            t_ret = now;
+        }
         return buf + st * kStageBytes;
     }
-    __device__ __forceinline__ void release(unsigned long long c) { mbar_arrive(&empty[stage_of(c)]); }
+    __device__ __forceinline__ void release(unsigned long long c) {
+        if (dbg) busy += globaltimer() - t_ret;
+        mbar_arrive(&empty[stage_of(c)]);
+    }
 };
 
 __device__ __forceinline__ int batch_of(const et_op& op, const StaticParams& P) {
     return op.i[5] >= 0 ? static_cast<int>(P.binding[op.i[5]]) : 1;
+}
+
+// A GEMV task's staged activations and accumulators must fit shared memory.
+__device__ __forceinline__ bool gemv_fits(const et_op& op, const StaticParams& P) {
+    const int nb = batch_of(op, P);
+    return nb <= kMaxBatch && nb * op.i[1] * 2 <= kXBytes;
 }
 
 // ---------------------------------------------------------------------------
@@ -287,20 +306,18 @@ __device__ void body_splitk(const StaticParams& P, const et_op& op, const int* c
     }
 }
 
-// Row-range GEMV y[b][r] = sum_k W[r][k] x[b][k] for rows [r0, r1) of a
-// row-major bf16 weight (K % 256 == 0).  The weight rows stream through the
-// shared-memory ring; each consumer warp owns whole 16 KB chunks and walks
-// them in 512-byte groups (32 lanes x 16 bytes), each group inside one row.
-// Products use FHFMA.BF16 (bf16 x bf16 -> fp32 accumulate), four groups in
-// flight per lane; every row run is warp-reduced once into shared memory.
+// Row-range GEMV y[b][r] = sum_k W[r][k] x[b][k] for rows [r0, r1) (multiples
+// of 16) of a bf16 weight in mma-fragment tile order (K % 32 == 0).  The
+// weight tiles stream through the shared-memory ring; activations are staged
+// once per task in shared memory (with the fused RMSNorm when x is the fp32
+// residual stream); the epilogue applies the op's fused tail.
 __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
                               float* red, Ring& ring, int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int N = op.i[0], K = op.i[1], nseg = op.i[2];
     const int nb = batch_of(op, P);
-    int r0, r1;
-    gemv_rows(op, si.coord[0], si.ext0, &r0, &r1);
-    const int R = r1 - r0;
+    const GemvSpan sp = gemv_span(op, si.coord[0], si.ext0);
+    const int r0 = sp.row0, R = sp.rows;
 
     // ---- prologue: activations into shared memory (bf16 [nb][K]), accumulators zeroed
     if (op.i[3] == 0) {
@@ -357,74 +374,60 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     bar_sync(1, kConsumers);
     const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
 
-    // ---- main loop: each consumer warp owns whole chunks (chunk c -> warp
-    // c % 8) and walks them in 512-byte groups (32 lanes x 16 bytes, inside one
-    // weight row), four groups in flight per lane (loads first, eight FHFMA
-    // chains).  A per-warp running sum is reduced into shared memory whenever
-    // the row changes and at the end of each owned chunk.
-    const int gpr = K / 256;  // 512-byte groups per weight row
-    constexpr int kGroupsPerChunk = kStageBytes / 512;
-    const uint4* xlane = reinterpret_cast<const uint4*>(xs) + lane;
-    const int xrow4 = K / 8;  // uint4 per activation row
+    // ---- main loop (tensor cores).  Weights sit in HBM as m16n8k16 A-fragment
+    // tiles (decode.py `frag16`): tile (t, j) = rows [16t, 16t+16) x k-step j is
+    // 512 B = 32 lanes x 16 B, lane (g = lane/4, q = lane%4) holding its a0..a3.
+    // Inside every 32-wide k block the k order is permuted so that the B
+    // fragment of lane (g, q) for the k-step pair (2p, 2p+1) is the 16
+    // contiguous bytes x[g][32p + 8q, 32p + 8q + 8): one LDS.128 of the
+    // activations per two MMAs, and one LDS.128 of weights per MMA.  Batch rows
+    // are the mma N dimension (nb <= 8).  A task's rows are a contiguous byte
+    // range of the tiled matrix, so the ring streams it exactly like row-major
+    // data; each consumer warp owns whole chunks (chunk c -> warp c % 8) and
+    // adds its 16-row partial sums into shared memory at every row-tile change.
+    const int kst = K / 16;                              // k-steps per row tile (even)
+    constexpr int kTilesPerChunk = kStageBytes / 512;    // 40 (even)
+    const int g = lane >> 2, q = lane & 3;
+    const bool xlane = g < nb;
+    const uint16_t* xrow = xs + (xlane ? g : 0) * K + 8 * q;
     unsigned long long c = ring.seq;
+    const int seg_tiles = static_cast<int>(sp.u1 - sp.u0);
+    const int u0 = static_cast<int>(sp.u0 - static_cast<long long>(r0 / 16) * kst);  // offset in the first tile
     for (int seg = 0; seg < nseg; ++seg) {
-        const long long seg_groups = static_cast<long long>(R) * gpr;
-        const int nch = static_cast<int>((seg_groups + kGroupsPerChunk - 1) / kGroupsPerChunk);
+        const int nch = (seg_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
         for (int ch = 0; ch < nch; ++ch, ++c) {
             if (Ring::owner(c) != warp) continue;
             const uint8_t* buf = ring.wait(c);
             if (!buf) continue;  // aborted: the step reports an error
-            const long long g0 = static_cast<long long>(ch) * kGroupsPerChunk;
-            const int ng = static_cast<int>(seg_groups - g0 < kGroupsPerChunk ? seg_groups - g0 : kGroupsPerChunk);
-            int row = seg * R + static_cast<int>(g0 / gpr);
-            int kg = static_cast<int>(g0 % gpr);
-            const uint4* wl = reinterpret_cast<const uint4*>(buf) + lane;
-            int j = 0;
-            while (j < ng) {
-                const int len = (gpr - kg < ng - j) ? gpr - kg : ng - j;
-                const uint4* wp = wl + j * 32;
-                const uint4* xp = xlane + kg * 32;
-                if (nb == 1) {
-                    float a[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) a[u] = 0.f;
-                    int t = 0;
-                    for (; t + 4 <= len; t += 4) {
-                        uint4 w[4], xv[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) w[u] = wp[(t + u) * 32];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) xv[u] = xp[(t + u) * 32];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) dot8_bf16(a[2 * u], a[2 * u + 1], w[u], xv[u]);
-                    }
-                    for (; t < len; ++t) dot8_bf16(a[0], a[1], wp[t * 32], xp[t * 32]);
-                    const float v = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
-                    if (lane == 0) atomicAdd(&acc[row], v);
-                } else {
-                    float lo[kMaxBatch], hi[kMaxBatch];
-#pragma unroll
-                    for (int bi = 0; bi < kMaxBatch; ++bi) lo[bi] = hi[bi] = 0.f;
-                    for (int t = 0; t < len; ++t) {
-                        const uint4 w = wp[t * 32];
-#pragma unroll
-                        for (int bi = 0; bi < kMaxBatch; ++bi)
-                            if (bi < nb) dot8_bf16(lo[bi], hi[bi], w, xp[t * 32 + bi * xrow4]);
-                    }
-#pragma unroll
-                    for (int bi = 0; bi < kMaxBatch; ++bi) {
-                        if (bi < nb) {
-                            const float v = warp_sum(lo[bi] + hi[bi]);
-                            if (lane == 0) atomicAdd(&acc[row * nb + bi], v);
-                        }
-                    }
+            const int t0 = ch * kTilesPerChunk;
+            const int nt = seg_tiles - t0 < kTilesPerChunk ? seg_tiles - t0 : kTilesPerChunk;
+            int done = 0;
+            while (done < nt) {
+                const int tt = u0 + t0 + done;  // unit index relative to row r0's tile
+                const int rtile = tt / kst, j = tt - rtile * kst;
+                const int len = (kst - j < nt - done) ? kst - j : nt - done;
+                float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint4* ap = reinterpret_cast<const uint4*>(buf + done * 512) + lane;
+                const uint16_t* xp = xrow + j * 16;
+#pragma unroll 4
+                for (int i = 0; i < len; i += 2) {
+                    const uint4 a0 = lds128(ap + i * 32);
+                    const uint4 a1 = lds128(ap + (i + 1) * 32);
+                    const uint4 xv = xlane ? lds128(xp + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+                    mma_bf16_16816(d0, a0, xv.x, xv.y);
+                    mma_bf16_16816(d1, a1, xv.z, xv.w);
                 }
-                j += len;
-                kg += len;
-                if (kg == gpr) {
-                    kg = 0;
-                    ++row;
+                // d[0] = D[g][2q], d[1] = D[g][2q+1], d[2] = D[g+8][2q], d[3] = D[g+8][2q+1]
+                const int row = seg * R + rtile * 16 + g;
+                if (2 * q < nb) {
+                    atomicAdd(&acc[row * nb + 2 * q], d0[0] + d1[0]);
+                    atomicAdd(&acc[(row + 8) * nb + 2 * q], d0[2] + d1[2]);
                 }
+                if (2 * q + 1 < nb) {
+                    atomicAdd(&acc[row * nb + 2 * q + 1], d0[1] + d1[1]);
+                    atomicAdd(&acc[(row + 8) * nb + 2 * q + 1], d0[3] + d1[3]);
+                }
+                done += len;
             }
             __syncwarp();
             if (lane == 0) ring.release(c);
@@ -477,6 +480,8 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
                 reinterpret_cast<uint16_t*>(op.p[4])[o] = f2bf(v);
             } else if (epi == EPI_RESID) {
                 reinterpret_cast<float*>(op.p[4])[o] = __ldcg(reinterpret_cast<const float*>(op.p[5]) + o) + v;
+            } else if (epi == EPI_ADD) {
+                atomicAdd(reinterpret_cast<float*>(op.p[4]) + o, v);
             } else if (epi == EPI_SILU_MUL) {
                 const float u = acc[(R + i) * nb + bi];
                 const float sv = v / (1.f + __expf(-v));
@@ -664,6 +669,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     float* red = reinterpret_cast<float*>(smem + kSmemMisc + 64);
     Ring ring{smem + kSmemRing, reinterpret_cast<uint64_t*>(smem + kSmemBar),
               reinterpret_cast<uint64_t*>(smem + kSmemBar) + kStages, 0ull, P.status, P.watchdog_ns, worker};
+    ring.dbg = (P.debug & 10) != 0 && P.record;
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
     unsigned long long executed = 0, noops = 0;
     for (int s = qb; s < qe; ++s) {
@@ -679,7 +685,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         }
         if (ctid == 0) {
             misc[2] = 1;  // consumers blocked on an Event Tensor: HBM idles, the producer may fill L2
-            bool ok = wait_range(P, v.wb, v.we, s, worker);
+            bool ok = (P.debug & 1) ? true : wait_range(P, v.wb, v.we, s, worker);
             misc[2] = 0;
             if (ok && P.step_limit > 0 &&
                 atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
@@ -709,7 +715,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 case ET_OP_SPLITK_PARTIAL:
                 case ET_OP_SPLITK_FINAL: body_splitk(P, op, v.coord, ctid); break;
                 case ET_OP_GEMV:
-                    if (batch_of(op, P) > kMaxBatch) {
+                    if (!gemv_fits(op, P)) {
                         if (ctid == 0) report(P.status, ET_ERR_INVALID, worker, s, -1, batch_of(op, P));
                         break;
                     }
@@ -736,7 +742,9 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 r.worker = worker;
                 r.flags = v.masked ? 1 : 0;
                 r.task = s;
-                r.pad = 0;
+                r.pad = (P.debug & 8) ? static_cast<int>(ring.busy) : (P.debug & 2) ? static_cast<int>(ring.stall) : 0;
+                ring.stall = 0;
+                ring.busy = 0;
                 P.trace[s] = r;
             }
         }
@@ -747,50 +755,6 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     }
 }
 
-// L2 run-ahead cursor of the producer: walks the same chunk sequence as the
-// shared-memory ring and issues cp.async.bulk.prefetch.L2 for chunks up to
-// `l2_ahead` bytes in front of the ring, so HBM keeps streaming the next tasks'
-// weights through dependency bubbles longer than the ring can cover.
-struct L2Cursor {
-    int slot;
-    int chunk;
-    int nchunks;
-    StreamPlan plan;
-    bool has_plan;
-    bool blocked;  // reached a data-dependent (lazy) slot
-};
-
-__device__ bool l2_step(const StaticParams& P, const SlotTable& T, int qb, int qe, L2Cursor& L, long long* bytes,
-                        bool issue) {
-    while (!L.blocked && L.slot < qe) {
-        if (!L.has_plan) {
-            const SlotView v = view_slot(P, T, L.slot, qb);
-            const et_op& op = P.ops[v.call];
-            if (v.masked || !op_streams(op.kind)) {
-                ++L.slot;
-                continue;
-            }
-            if (v.lazy) {
-                L.blocked = true;
-                return false;
-            }
-            L.plan = make_plan(op, v.coord, v.ext0, P.binding);
-            L.nchunks = L.plan.total_chunks();
-            L.chunk = 0;
-            L.has_plan = true;
-        }
-        if (L.chunk < L.nchunks) {
-            const Chunk ch = L.plan.chunk(L.chunk++);
-            if (issue) bulk_prefetch_l2(ch.src, ch.bytes);
-            *bytes += ch.bytes;
-            return true;
-        }
-        L.has_plan = false;
-        ++L.slot;
-    }
-    return false;
-}
-
 __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     if ((threadIdx.x & 31) != 0) return;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -798,18 +762,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
     const uint64_t pol = policy_evict_first();
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
-    unsigned long long cseq = 0;
-    L2Cursor L{qb, 0, 0, StreamPlan{}, false, false};
-    long long l2_bytes = 0, ring_bytes = 0;  // cumulative bytes issued by each cursor
-    const long long ahead = P.prefetch ? P.l2_ahead : 0;
-    auto resume_after = [&](int s) {  // the ring passed lazy slot s: the L2 cursor may continue
-        if (L.blocked && L.slot == s) {
-            L.blocked = false;
-            L.has_plan = false;
-            L.slot = s + 1;
-            l2_bytes = ring_bytes;
-        }
-    };
+    unsigned long long cseq = 0;  // chunks issued to the ring
     for (int s = qb; s < qe; ++s) {
         SlotView v = view_slot(P, T, s, qb);
         if (v.masked) continue;
@@ -820,10 +773,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             while (misc[1] <= s) {
                 if (aborted(P.status)) return;
             }
-            if (v.lazy && extent_masked(P, v.call, v.coord)) {
-                resume_after(s);
-                continue;
-            }
+            if (v.lazy && extent_masked(P, v.call, v.coord)) continue;
         }
         const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding);
         const int n = pl.total_chunks();
@@ -833,11 +783,6 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             uint32_t spins = 0;
             uint64_t t0 = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
-                // L2 run-ahead only while the consumers wait on a dependency (a bubble):
-                // during streaming it would compete with the current stage's loads
-                if (ahead > 0 && misc[2] && l2_bytes - ring_bytes < ahead &&
-                    l2_step(P, T, qb, qe, L, &l2_bytes, true))
-                    continue;
                 if ((++spins & 1023u) == 0) {
                     if (aborted(P.status)) return;
                     if (t0 == 0) t0 = globaltimer();
@@ -848,16 +793,13 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 }
             }
             const Chunk ch = pl.chunk(c);
-            mbar_arrive_expect_tx(&full[stage], ch.bytes);
-            bulk_g2s(smem + kSmemRing + stage * kStageBytes, ch.src, ch.bytes, &full[stage], pol);
-            if (ahead > 0) {
-                ring_bytes += ch.bytes;
-                // keep the L2 cursor at or ahead of the ring (skipping, not issuing)
-                while (l2_bytes < ring_bytes && l2_step(P, T, qb, qe, L, &l2_bytes, false)) {
-                }
+            if (P.debug & 4) {  // timing experiment: stages "fill" instantly (no HBM traffic)
+                mbar_arrive(&full[stage]);
+            } else {
+                mbar_arrive_expect_tx(&full[stage], ch.bytes);
+                bulk_g2s(smem + kSmemRing + stage * kStageBytes, ch.src, ch.bytes, &full[stage], pol);
             }
         }
-        if (v.lazy && ahead > 0) resume_after(s);
     }
 }
 
@@ -1220,7 +1162,13 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     break;
                 case ET_OP_SPLITK_PARTIAL:
                 case ET_OP_SPLITK_FINAL: body_splitk(P, op, v.coord, ctid); break;
-                case ET_OP_GEMV: tp = body_gemv(P, op, v, xs, acc, red, ring, ctid); break;
+                case ET_OP_GEMV:
+                    if (!gemv_fits(op, P)) {
+                        if (ctid == 0) report(P.status, ET_ERR_INVALID, worker, task, -1, batch_of(op, P));
+                        break;
+                    }
+                    tp = body_gemv(P, op, v, xs, acc, red, ring, ctid);
+                    break;
                 case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;

@@ -98,6 +98,8 @@ struct StaticParams {
     int table_ok;  // every coordinate fits 16 bits (slot tables usable)
     long long l2_ahead;  // bytes the producer prefetches into L2 beyond the ring
     int step_id;         // stamped into trace records (dynamic: tasks that ran this step)
+    int debug;           // ET_DEBUG env bits (timing experiments only): 1 = skip Event Tensor waits,
+                         // 2 = record consumer ring-stall ns of warp 0 in the trace pad field
 };
 
 constexpr int kMaxDd = 8;  // data-dependent event tensors per graph (dynamic mode)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -551,6 +552,10 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     p.table_ok = S.table_ok;
     p.step_id = ++rt->steps;
     p.l2_ahead = rt->cfg.l2_prefetch_bytes < 0 ? 0 : rt->cfg.l2_prefetch_bytes;
+    {
+        const char* dbg = getenv("ET_DEBUG");
+        p.debug = dbg ? atoi(dbg) : 0;
+    }
 
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rt->stream;
     int e = 0;

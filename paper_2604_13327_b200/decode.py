@@ -18,7 +18,8 @@ followed by lm_head [T_lm] waiting on D_{L-1}[0].  `s` (cached positions) is
 the graph's symbolic size: one compiled artifact serves every sequence length
 covered by its samples, with out-of-range attention splits masked on device.
 
-Device layout (HBM): weights bf16 row-major [out][in]; the q and k rows of
+Device layout (HBM): GEMV weights bf16 in mma-fragment tile order (`frag16`,
+row ranges of whole 16-row tiles are contiguous); the q and k rows of
 Wqkv are stored so that rotary pairs are adjacent (GPT-J style rotation on
 (2j, 2j+1), frequency theta^(-2j/head_dim)), which is Llama's rotate-half
 RoPE up to a fixed permutation of the q/k rows; the residual stream is fp32;
@@ -37,6 +38,7 @@ from .ops import (
     EPI_BF16,
     EPI_F32,
     EPI_QKV_ROPE,
+    EPI_ADD,
     EPI_RESID,
     EPI_SILU_MUL,
     OP_ATTN_MERGE,
@@ -61,7 +63,7 @@ class DecoderConfig:
     vocab: int
     rope_theta: float = 500000.0
     eps: float = 1e-5
-    attn_chunk: int = 64
+    attn_chunk: int = 64      # cached positions per attention split task
 
     @property
     def q_rows(self):
@@ -103,28 +105,37 @@ def rope_inv_freq(cfg):
     return (cfg.rope_theta ** (-2.0 * j / cfg.head_dim)).to(torch.float32)
 
 
-def frag8(w):
-    """Device layout of a GEMV weight [N][K] (N % 8 == 0, K % 32 == 0): row blocks of 8,
-    then 32-wide k groups, then the 32 mma lanes (lane = 4*row + q) holding the B
-    registers of two k16 steps (see body_gemv in csrc/kernels/megakernel.cu)."""
+def frag16(w):
+    """Device layout of a GEMV weight [N][K] (N % 16 == 0, K % 32 == 0): m16n8k16
+    A-fragment tiles (see body_gemv in csrc/kernels/megakernel.cu).  Tile (t, j)
+    covers rows [16t, 16t+16) and k-step j; tiles are row-tile major, so a row
+    range of whole tiles is one contiguous byte range.  Inside a tile lane
+    (g, q) = (lane // 4, lane % 4) holds 8 bf16: rows (g, g+8) x k = 32p + 8q + 4e
+    + {0, 1, 2, 3} of the 32-wide block p = j // 2, e = j % 2, ordered
+    (k-pair c, row-half h, d) -- its a0..a3 registers under the k permutation
+    that makes the matching activation fragment 16 contiguous bytes."""
     N, K = w.shape
-    assert N % 8 == 0 and K % 32 == 0, (N, K)
-    return (w.reshape(N // 8, 8, K // 32, 2, 2, 4, 2).permute(0, 2, 1, 5, 3, 4, 6).contiguous().reshape(N, K))
+    assert N % 16 == 0 and K % 32 == 0, (N, K)
+    # (t, h, g, p, q, e, c, d) -> (t, p, e, g, q, c, h, d)
+    return (w.reshape(N // 16, 2, 8, K // 32, 4, 2, 2, 2).permute(0, 3, 5, 2, 4, 6, 1, 7).contiguous()
+            .reshape(N, K))
 
 
 GEMV_WEIGHTS = ("wqkv", "wo", "wgate", "wup", "wdown")
 
 
 def device_layout(W, keep_logical=False):
-    """Copy of the weight dict with every GEMV matrix in frag8 order."""
-    D = {"embed": W["embed"], "final_norm": W["final_norm"], "lm_head": frag8(W["lm_head"]), "layers": []}
+    """Weight dict the megakernel reads: every GEMV matrix in frag16 order.  With
+    keep_logical the row-major originals stay referenced (the CPU oracle reads
+    them); otherwise they are dropped as each layer is converted."""
+    D = {"embed": W["embed"], "final_norm": W["final_norm"], "lm_head": frag16(W["lm_head"]), "layers": []}
+    if not keep_logical:
+        W["lm_head"] = None
     for L in W["layers"]:
-        D["layers"].append({k: (frag8(v) if k in GEMV_WEIGHTS else v) for k, v in L.items()})
+        D["layers"].append({k: (frag16(v) if k in GEMV_WEIGHTS else v) for k, v in L.items()})
         if not keep_logical:
             for k in GEMV_WEIGHTS:
                 L[k] = None
-    if not keep_logical:
-        W["lm_head"] = None
     return D
 
 
@@ -166,7 +177,7 @@ class DecodeModel:
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
-                 l2_prefetch=-1):
+                 l2_prefetch=-1, residual="split"):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -178,6 +189,7 @@ class DecodeModel:
         self.samples = sorted(int(s) for s in samples)
         self.capacity = capacity or (self.samples[-1] + 1)
         self.max_splits = max(1, (self.samples[-1] + cfg.attn_chunk - 1) // cfg.attn_chunk)
+        self.residual = residual
 
         import time
         t0 = time.perf_counter()
@@ -187,18 +199,18 @@ class DecodeModel:
 
         dev = self.device
         W = weights if weights is not None else init_weights(cfg, dev, seed)
-        self.W = W                                             # what the megakernel reads (row-major bf16)
-        self.W_logical = W                                     # same tensors; the CPU oracle reads these
+        self.W_logical = W if keep_logical else None           # row-major bf16; the CPU oracle reads these
+        self.W = device_layout(W, keep_logical=keep_logical or weights is not None)  # what the megakernel reads
         self.kcache = [torch.zeros(cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
                        for _ in range(cfg.layers)]
         self.vcache = [torch.zeros_like(k) for k in self.kcache]
         self.tokens = torch.zeros(1, dtype=torch.int32, device=dev)
         self.h_a = torch.zeros(1, cfg.hidden, dtype=torch.float32, device=dev)
-        self.h_b = torch.zeros_like(self.h_a)
         self.q = torch.zeros(cfg.q_rows, dtype=torch.float32, device=dev)
         self.attn = torch.zeros(cfg.q_rows, dtype=torch.bfloat16, device=dev)
         self.act = torch.zeros(cfg.intermediate, dtype=torch.bfloat16, device=dev)
         self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=dev)
+        self.h_b = torch.zeros_like(self.h_a) if residual == "double" else self.h_a
         self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
 
@@ -218,7 +230,7 @@ class DecodeModel:
         G = cfg.heads // cfg.kv_heads
         for l, L in enumerate(W["layers"]):
             kc, vc = self.kcache[l], self.vcache[l]
-            ops.append(make_op(OP_GEMV, i=[cfg.q_rows + 2 * cfg.kv_rows, H, 1, 1, EPI_QKV_ROPE, -1, s_slot, 8, dh, H,
+            ops.append(make_op(OP_GEMV, i=[cfg.q_rows + 2 * cfg.kv_rows, H, 1, 1, EPI_QKV_ROPE, -1, s_slot, 16, dh, H,
                                            cfg.q_rows, cfg.kv_rows, self.capacity],
                                f=[cfg.eps], p=[ptr(L["wqkv"]), 0, ptr(self.h_a), ptr(L["attn_norm"]), ptr(self.q), 0,
                                                ptr(kc), ptr(vc), ptr(self.inv_freq)]))
@@ -227,14 +239,24 @@ class DecodeModel:
                                p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials)]))
             ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale],
                                p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn)]))
-            ops.append(make_op(OP_GEMV, i=[H, cfg.q_rows, 1, 0, EPI_RESID, -1, 0, 8],
-                               p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_b), ptr(self.h_a)]))
-            ops.append(make_op(OP_GEMV, i=[cfg.intermediate, H, 2, 1, EPI_SILU_MUL, -1, 0, 8, 0, H],
+            if self.residual == "split":
+                # row-parallel products add into the residual stream in place: split-K
+                # spans (every task streams the same bytes), red.global.add epilogue
+                ops.append(make_op(OP_GEMV, i=[H, cfg.q_rows, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],
+                                   p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_a)]))
+            else:  # whole-row tasks, residual ping-pong h_a -> h_b -> h_a
+                ops.append(make_op(OP_GEMV, i=[H, cfg.q_rows, 1, 0, EPI_RESID, -1, 0, 16],
+                                   p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_b), ptr(self.h_a)]))
+            ops.append(make_op(OP_GEMV, i=[cfg.intermediate, H, 2, 1, EPI_SILU_MUL, -1, 0, 16, 0, H],
                                f=[cfg.eps], p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(self.h_b), ptr(L["ffn_norm"]),
                                                ptr(self.act)]))
-            ops.append(make_op(OP_GEMV, i=[H, cfg.intermediate, 1, 0, EPI_RESID, -1, 0, 8],
-                               p=[ptr(L["wdown"]), 0, ptr(self.act), 0, ptr(self.h_a), ptr(self.h_b)]))
-        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 8, 0, H], f=[cfg.eps],
+            if self.residual == "split":
+                ops.append(make_op(OP_GEMV, i=[H, cfg.intermediate, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],
+                                   p=[ptr(L["wdown"]), 0, ptr(self.act), 0, ptr(self.h_a)]))
+            else:
+                ops.append(make_op(OP_GEMV, i=[H, cfg.intermediate, 1, 0, EPI_RESID, -1, 0, 16],
+                                   p=[ptr(L["wdown"]), 0, ptr(self.act), 0, ptr(self.h_a), ptr(self.h_b)]))
+        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
                            p=[ptr(W["lm_head"]), 0, ptr(self.h_a), ptr(W["final_norm"]), ptr(self.logits)]))
         return ops
 

@@ -24,7 +24,7 @@ OP_MOE_COMBINE = 10
 OP_ARGMAX = 11
 OP_EMBED = 12
 
-EPI_F32, EPI_BF16, EPI_RESID, EPI_SILU_MUL, EPI_QKV_ROPE = range(5)
+EPI_F32, EPI_BF16, EPI_RESID, EPI_SILU_MUL, EPI_QKV_ROPE, EPI_ADD = range(6)
 
 
 class EtOp(ctypes.Structure):
