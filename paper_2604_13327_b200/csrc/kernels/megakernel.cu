@@ -306,6 +306,63 @@ __device__ void body_splitk(const StaticParams& P, const et_op& op, const int* c
     }
 }
 
+// ---- GEMV main loop (tensor cores).  Weights sit in HBM as m16n8k16
+// A-fragment tiles (decode.py `frag16`): tile (t, j) = rows [16t, 16t+16) x
+// k-step j is 512 B = 32 lanes x 16 B, lane (g = lane/4, q = lane%4) holding
+// its a0..a3.  Inside every 32-wide k block the k order is permuted so that the
+// B fragment of lane (g, q) for the k-step pair (2p, 2p+1) is the 16 contiguous
+// bytes x[g][32p + 8q, 32p + 8q + 8): one LDS.128 of the activations per two
+// MMAs, and one LDS.128 of weights per MMA.  Batch rows are the mma N dimension
+// (nb <= 8; x is bf16 [nb][K] in shared memory).  A task's span is a
+// contiguous byte range of the tiled matrix (per segment), streamed through the
+// ring; each consumer warp owns whole chunks (chunk c -> warp c % 8) and hands
+// the 16-row x 8-column partial tile to `flush(seg, row_tile, g, q, d[4])` at
+// every row-tile change (d[0] = D[g][2q], d[1] = D[g][2q+1], d[2] = D[g+8][2q],
+// d[3] = D[g+8][2q+1]; row tiles count from the span's first tile).
+template <typename Flush>
+__device__ __forceinline__ void gemv_stream(Ring& ring, int warp, int lane, int nseg, int seg_tiles, int u0, int K,
+                                            int nb, const uint16_t* xs, Flush&& flush) {
+    const int kst = K / 16;                              // k-steps per row tile (even)
+    constexpr int kTilesPerChunk = kStageBytes / 512;    // 40 (even)
+    const int g = lane >> 2, q = lane & 3;
+    const bool xlane = g < nb;
+    const uint16_t* xrow = xs + (xlane ? g : 0) * K + 8 * q;
+    unsigned long long c = ring.seq;
+    for (int seg = 0; seg < nseg; ++seg) {
+        const int nch = (seg_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
+        for (int ch = 0; ch < nch; ++ch, ++c) {
+            if (Ring::owner(c) != warp) continue;
+            const uint8_t* buf = ring.wait(c);
+            if (!buf) continue;  // aborted: the step reports an error
+            const int t0 = ch * kTilesPerChunk;
+            const int nt = seg_tiles - t0 < kTilesPerChunk ? seg_tiles - t0 : kTilesPerChunk;
+            int done = 0;
+            while (done < nt) {
+                const int tt = u0 + t0 + done;  // unit index relative to the span's first tile
+                const int rtile = tt / kst, j = tt - rtile * kst;
+                const int len = (kst - j < nt - done) ? kst - j : nt - done;
+                float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint4* ap = reinterpret_cast<const uint4*>(buf + done * 512) + lane;
+                const uint16_t* xp = xrow + j * 16;
+#pragma unroll 4
+                for (int i = 0; i < len; i += 2) {
+                    const uint4 a0 = lds128(ap + i * 32);
+                    const uint4 a1 = lds128(ap + (i + 1) * 32);
+                    const uint4 xv = xlane ? lds128(xp + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+                    mma_bf16_16816(d0, a0, xv.x, xv.y);
+                    mma_bf16_16816(d1, a1, xv.z, xv.w);
+                }
+                const float d[4] = {d0[0] + d1[0], d0[1] + d1[1], d0[2] + d1[2], d0[3] + d1[3]};
+                flush(seg, rtile, g, q, d);
+                done += len;
+            }
+            __syncwarp();
+            if (lane == 0) ring.release(c);
+        }
+    }
+    ring.seq = c;
+}
+
 // Row-range GEMV y[b][r] = sum_k W[r][k] x[b][k] for rows [r0, r1) (multiples
 // of 16) of a bf16 weight in mma-fragment tile order (K % 32 == 0).  The
 // weight tiles stream through the shared-memory ring; activations are staged
@@ -374,66 +431,19 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     bar_sync(1, kConsumers);
     const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
 
-    // ---- main loop (tensor cores).  Weights sit in HBM as m16n8k16 A-fragment
-    // tiles (decode.py `frag16`): tile (t, j) = rows [16t, 16t+16) x k-step j is
-    // 512 B = 32 lanes x 16 B, lane (g = lane/4, q = lane%4) holding its a0..a3.
-    // Inside every 32-wide k block the k order is permuted so that the B
-    // fragment of lane (g, q) for the k-step pair (2p, 2p+1) is the 16
-    // contiguous bytes x[g][32p + 8q, 32p + 8q + 8): one LDS.128 of the
-    // activations per two MMAs, and one LDS.128 of weights per MMA.  Batch rows
-    // are the mma N dimension (nb <= 8).  A task's rows are a contiguous byte
-    // range of the tiled matrix, so the ring streams it exactly like row-major
-    // data; each consumer warp owns whole chunks (chunk c -> warp c % 8) and
-    // adds its 16-row partial sums into shared memory at every row-tile change.
-    const int kst = K / 16;                              // k-steps per row tile (even)
-    constexpr int kTilesPerChunk = kStageBytes / 512;    // 40 (even)
-    const int g = lane >> 2, q = lane & 3;
-    const bool xlane = g < nb;
-    const uint16_t* xrow = xs + (xlane ? g : 0) * K + 8 * q;
-    unsigned long long c = ring.seq;
-    const int seg_tiles = static_cast<int>(sp.u1 - sp.u0);
-    const int u0 = static_cast<int>(sp.u0 - static_cast<long long>(r0 / 16) * kst);  // offset in the first tile
-    for (int seg = 0; seg < nseg; ++seg) {
-        const int nch = (seg_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
-        for (int ch = 0; ch < nch; ++ch, ++c) {
-            if (Ring::owner(c) != warp) continue;
-            const uint8_t* buf = ring.wait(c);
-            if (!buf) continue;  // aborted: the step reports an error
-            const int t0 = ch * kTilesPerChunk;
-            const int nt = seg_tiles - t0 < kTilesPerChunk ? seg_tiles - t0 : kTilesPerChunk;
-            int done = 0;
-            while (done < nt) {
-                const int tt = u0 + t0 + done;  // unit index relative to row r0's tile
-                const int rtile = tt / kst, j = tt - rtile * kst;
-                const int len = (kst - j < nt - done) ? kst - j : nt - done;
-                float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-                const uint4* ap = reinterpret_cast<const uint4*>(buf + done * 512) + lane;
-                const uint16_t* xp = xrow + j * 16;
-#pragma unroll 4
-                for (int i = 0; i < len; i += 2) {
-                    const uint4 a0 = lds128(ap + i * 32);
-                    const uint4 a1 = lds128(ap + (i + 1) * 32);
-                    const uint4 xv = xlane ? lds128(xp + i * 16) : make_uint4(0u, 0u, 0u, 0u);
-                    mma_bf16_16816(d0, a0, xv.x, xv.y);
-                    mma_bf16_16816(d1, a1, xv.z, xv.w);
-                }
-                // d[0] = D[g][2q], d[1] = D[g][2q+1], d[2] = D[g+8][2q], d[3] = D[g+8][2q+1]
-                const int row = seg * R + rtile * 16 + g;
-                if (2 * q < nb) {
-                    atomicAdd(&acc[row * nb + 2 * q], d0[0] + d1[0]);
-                    atomicAdd(&acc[(row + 8) * nb + 2 * q], d0[2] + d1[2]);
-                }
-                if (2 * q + 1 < nb) {
-                    atomicAdd(&acc[row * nb + 2 * q + 1], d0[1] + d1[1]);
-                    atomicAdd(&acc[(row + 8) * nb + 2 * q + 1], d0[3] + d1[3]);
-                }
-                done += len;
-            }
-            __syncwarp();
-            if (lane == 0) ring.release(c);
-        }
-    }
-    ring.seq = c;
+    gemv_stream(ring, warp, lane, nseg, static_cast<int>(sp.u1 - sp.u0),
+                static_cast<int>(sp.u0 - static_cast<long long>(r0 / 16) * (K / 16)), K, nb, xs,
+                [&](int seg, int rt, int g, int q, const float* d) {
+                    const int row = seg * R + rt * 16 + g;
+                    if (2 * q < nb) {
+                        atomicAdd(&acc[row * nb + 2 * q], d[0]);
+                        atomicAdd(&acc[(row + 8) * nb + 2 * q], d[2]);
+                    }
+                    if (2 * q + 1 < nb) {
+                        atomicAdd(&acc[row * nb + 2 * q + 1], d[1]);
+                        atomicAdd(&acc[(row + 8) * nb + 2 * q + 1], d[3]);
+                    }
+                });
     bar_sync(1, kConsumers);
 
     // ---- epilogue
