@@ -201,10 +201,11 @@ DynProgram build_dynamic(const DynamicMegakernel& dk, const ShapeBinding& b, int
         }
     }
     std::vector<int> dd_of_tensor(g.event_tensors.size(), -1);
+    int num_dd = 0;
     for (size_t ti = 0; ti < g.event_tensors.size(); ++ti) {
         auto& e = gs.event_tensors[ti];
         if (!e.data_dependent) continue;
-        dd_of_tensor[ti] = static_cast<int>(P.dd_base.size());
+        dd_of_tensor[ti] = num_dd++;  // same order as the dd_* arrays filled below
         e.data_dependent = false;
         e.counts_tensor.clear();
         e.writer.clear();

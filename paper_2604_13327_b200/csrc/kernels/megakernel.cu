@@ -390,15 +390,12 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
         const int stride = op.i[9];
         constexpr int kMaxPer = 8;  // float4 per thread: K <= 8192
         for (int bi = 0; bi < nb; ++bi) {
-            float4 hv[kMaxPer], gv[kMaxPer];
+            float4 hv[kMaxPer];
             float ss = 0.f;
 #pragma unroll
             for (int j = 0; j < kMaxPer; ++j) {
                 const int k = (ctid + j * kConsumers) * 4;
-                if (k < K) {
-                    hv[j] = ldcg_f4(h + static_cast<long long>(bi) * stride + k);
-                    gv[j] = __ldg(reinterpret_cast<const float4*>(gam + k));
-                }
+                if (k < K) hv[j] = ldcg_f4(h + static_cast<long long>(bi) * stride + k);
             }
 #pragma unroll
             for (int j = 0; j < kMaxPer; ++j)
@@ -415,7 +412,7 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
             for (int j = 0; j < kMaxPer; ++j) {
                 const int k = (ctid + j * kConsumers) * 4;
                 if (k < K) {
-                    const float4 g = gv[j];
+                    const float4 g = __ldg(reinterpret_cast<const float4*>(gam + k));
                     uint2 o;
                     o.x = static_cast<uint32_t>(f2bf(hv[j].x * scale * g.x)) |
                           (static_cast<uint32_t>(f2bf(hv[j].y * scale * g.y)) << 16);
@@ -502,6 +499,24 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     return t_pro;
 }
 
+// Qwen3-style per-head RMSNorm (weight w[dh]) followed by the pair rotation at
+// position pos, in place on one head vector in shared memory; one warp.
+__device__ __forceinline__ void qk_norm_rope(float* v, int dh, const float* w, float eps, const float* invf,
+                                             long long pos, int lane) {
+    float ss = 0.f;
+    for (int d = lane; d < dh; d += 32) ss += v[d] * v[d];
+    ss = warp_sum(ss);
+    const float sc = rsqrtf(ss / static_cast<float>(dh) + eps);
+    for (int j = lane; j < dh / 2; j += 32) {
+        const float a = v[2 * j] * sc * __ldg(w + 2 * j), b = v[2 * j + 1] * sc * __ldg(w + 2 * j + 1);
+        float sn, cs;
+        sincosf(static_cast<float>(pos) * __ldg(invf + j), &sn, &cs);
+        v[2 * j] = a * cs - b * sn;
+        v[2 * j + 1] = a * sn + b * cs;
+    }
+    __syncwarp();
+}
+
 __device__ void body_attn_split(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, Ring& ring,
                                 int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
@@ -516,6 +531,12 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     float* sc = scratch + G * qstride;   // [G][CH]
     const float* q = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
     for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
+    if (op.flags & 1) {  // q-norm + RoPE applied here (q is the raw projection)
+        bar_sync(1, kConsumers);
+        for (int h = warp; h < G; h += kConsumerWarps)
+            qk_norm_rope(qs + h * qstride, dh, reinterpret_cast<const float*>(op.p[5]), op.f[1],
+                         reinterpret_cast<const float*>(op.p[7]), s, lane);
+    }
     bar_sync(1, kConsumers);
     const float scale = op.f[0];
     const unsigned long long ck = ring.seq, cv = ring.seq + 1;
@@ -617,12 +638,41 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
         ml[2 * idx] = __ldcg(pr);
         ml[2 * idx + 1] = __ldcg(pr + 1);
     }
-    for (int hh = warp; hh < G; hh += kConsumerWarps) {
-        const float* q = reinterpret_cast<const float*>(op.p[0]) + (static_cast<long long>(g) * G + hh) * dh;
-        float dot = 0.f;
-        for (int d = lane; d < dh; d += 32) dot += __ldcg(q + d) * bf2f(__ldcg(kn + d));
-        dot = warp_sum(dot);
-        if (lane == 0) hs[hh] = dot * scale;
+    if (op.flags & 1) {
+        // Qwen3 mode: q, k, v of the new token are raw projections.  q and k get
+        // the per-head RMSNorm + RoPE here; k and v are appended to the cache
+        // (bf16) for later steps and read back below like any cached row.
+        float* qn = hs + G;  // [G][dh] then [dh] for k
+        const float* q = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
+        const float* kr = reinterpret_cast<const float*>(op.p[8]) + static_cast<long long>(g) * dh;
+        const float* vr = kr + static_cast<long long>(op.i[6]) * dh;
+        for (int i = ctid; i < (G + 1) * dh; i += kConsumers) qn[i] = i < G * dh ? __ldcg(q + i) : __ldcg(kr + i - G * dh);
+        bar_sync(1, kConsumers);
+        for (int hh = warp; hh <= G; hh += kConsumerWarps)
+            qk_norm_rope(qn + hh * dh, dh, reinterpret_cast<const float*>(op.p[hh < G ? 5 : 6]), op.f[1],
+                         reinterpret_cast<const float*>(op.p[7]), s, lane);
+        bar_sync(1, kConsumers);
+        uint16_t* kc = const_cast<uint16_t*>(kn);
+        uint16_t* vc = const_cast<uint16_t*>(vn);
+        for (int d = ctid; d < dh; d += kConsumers) {
+            kc[d] = f2bf(qn[G * dh + d]);
+            vc[d] = f2bf(__ldcg(vr + d));
+        }
+        bar_sync(1, kConsumers);
+        for (int hh = warp; hh < G; hh += kConsumerWarps) {
+            float dot = 0.f;
+            for (int d = lane; d < dh; d += 32) dot += qn[hh * dh + d] * bf2f(__ldcg(kn + d));
+            dot = warp_sum(dot);
+            if (lane == 0) hs[hh] = dot * scale;
+        }
+    } else {
+        for (int hh = warp; hh < G; hh += kConsumerWarps) {
+            const float* q = reinterpret_cast<const float*>(op.p[0]) + (static_cast<long long>(g) * G + hh) * dh;
+            float dot = 0.f;
+            for (int d = lane; d < dh; d += 32) dot += __ldcg(q + d) * bf2f(__ldcg(kn + d));
+            dot = warp_sum(dot);
+            if (lane == 0) hs[hh] = dot * scale;
+        }
     }
     bar_sync(1, kConsumers);
     for (int hh = warp; hh < G; hh += kConsumerWarps) {
@@ -655,6 +705,221 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
     }
 }
 
+// ---------------------------------------------------------------------------
+// MoE.  Router: the GEMV above on E/16 tasks (logits, RMSNorm prologue), then
+// the last task to arrive turns the logits into the routing runtime tensors
+// that drive the data-dependent Event Tensors of the layer (ref
+// workloads.cpp:81-150: topk, expert_counts, exp_indptr; plus task_indptr,
+// eoff and elist for the expert call).  Everything is written before this
+// task's NOTIFY (release), and the dynamic scheduler reveals the counts when
+// the whole writer call has finished (ref simulate.cpp:632-649).
+__device__ void body_moe_route(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
+                               float* red, Ring& ring, int ctid, uint64_t* t_pro) {
+    *t_pro = body_gemv(P, op, si, xs, acc, red, ring, ctid);
+    const int warp = ctid >> 5, lane = ctid & 31;
+    const int E = op.i[0], H = op.i[1], K = op.i[6], RS = op.i[12], TS = op.i[13];
+    const int nb = batch_of(op, P);
+    if (si.coord[0] == 0)  // the normalised activations feed the experts
+        for (int v = ctid; v < nb * H / 8; v += kConsumers)
+            reinterpret_cast<uint4*>(op.p[5])[v] = reinterpret_cast<const uint4*>(xs)[v];
+    volatile int* flag = reinterpret_cast<volatile int*>(red + kConsumerWarps);
+    bar_sync(1, kConsumers);
+    if (ctid == 0) {
+        __threadfence();
+        int* arrive = reinterpret_cast<int*>(op.p[7]);
+        const bool last = atomicAdd(arrive, 1) == si.ext0 - 1;
+        if (last) {
+            *reinterpret_cast<volatile int*>(arrive) = 0;
+            __threadfence();
+        }
+        *flag = last ? 1 : 0;
+    }
+    bar_sync(1, kConsumers);
+    if (!*flag) return;
+
+    int* topk = P.rt[op.i[10] & 0xff];
+    int* cnt = P.rt[(op.i[10] >> 8) & 0xff];
+    int* ind = P.rt[(op.i[10] >> 16) & 0xff];
+    int* elist = P.rt[(op.i[10] >> 24) & 0xff];
+    int* eoff = P.rt[op.i[11] & 0xff];
+    int* tind = P.rt[(op.i[11] >> 8) & 0xff];
+    const float* logits = reinterpret_cast<const float*>(op.p[4]);
+    float* wslot = reinterpret_cast<float*>(op.p[6]);
+    int* scnt = reinterpret_cast<int*>(acc);          // [E] counts
+    int* stop = scnt + 256;                           // [nb*K] experts per slot
+    for (int e = ctid; e < E; e += kConsumers) scnt[e] = 0;
+    bar_sync(1, kConsumers);
+    // one warp per token: softmax over E (<= 256), top-K by repeated warp argmax
+    constexpr int kPer = 8;
+    for (int t = warp; t < nb; t += kConsumerWarps) {
+        float lg[kPer];
+        float m = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = lane + 32 * u;
+            lg[u] = e < E ? __ldcg(logits + static_cast<long long>(t) * E + e) : -INFINITY;
+            m = fmaxf(m, lg[u]);
+        }
+        m = warp_max(m);
+        float z = 0.f;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+            if (lane + 32 * u < E) z += __expf(lg[u] - m);
+        z = warp_sum(z);
+        float wsum = 0.f, wsel[8];
+        int esel[8];
+        for (int j = 0; j < K; ++j) {
+            int e;
+            if (op.flags & 1) {  // injected routing (host-written topk)
+                e = __ldcg(topk + t * K + j);
+            } else {  // selection on the raw logits: larger wins, the lower expert index on ties
+                float bv = -INFINITY;
+                int bi = 1 << 30;
+#pragma unroll
+                for (int u = 0; u < kPer; ++u)
+                    if (lane + 32 * u < E && (lg[u] > bv || bi == (1 << 30))) {
+                        bv = lg[u];
+                        bi = lane + 32 * u;
+                    }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (ov > bv || (ov == bv && oi < bi)) {
+                        bv = ov;
+                        bi = oi;
+                    }
+                }
+                e = bi;
+                if ((e & 31) == lane) {  // taken: drop it from the candidates
+#pragma unroll
+                    for (int u = 0; u < kPer; ++u)
+                        if (u == (e >> 5)) lg[u] = -INFINITY;
+                }
+            }
+            esel[j] = e;
+        }
+        // weights: p_e / sum of the selected p (recomputed from the logits, exact)
+        for (int j = 0; j < K; ++j) {
+            wsel[j] = __expf(__ldcg(logits + static_cast<long long>(t) * E + esel[j]) - m) / z;
+            wsum += wsel[j];
+        }
+        if (lane < K) {
+            float wj = 0.f;
+            int ej = 0;
+            for (int j = 0; j < K; ++j)
+                if (j == lane) {
+                    wj = wsel[j];
+                    ej = esel[j];
+                }
+            const int slot = t * K + lane;
+            if (!(op.flags & 1)) topk[slot] = ej;
+            stop[slot] = ej;
+            wslot[slot] = wj / wsum;
+            atomicAdd(&scnt[ej], 1);
+        }
+    }
+    bar_sync(1, kConsumers);
+    if (warp == 0) {  // exclusive scans over E <= 256 experts (8 per lane)
+        int c8[kPer], tiles = 0, toks = 0;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = lane * kPer + u;
+            c8[u] = e < E ? scnt[e] : 0;
+            tiles += (c8[u] + TS - 1) / TS;
+            toks += c8[u];
+        }
+        int it = tiles, io = toks;  // inclusive warp scans
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, it, o), b = __shfl_up_sync(0xffffffffu, io, o);
+            if (lane >= o) {
+                it += a;
+                io += b;
+            }
+        }
+        int tp = it - tiles, op_ = io - toks;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = lane * kPer + u;
+            if (e < E) {
+                cnt[e] = c8[u];
+                ind[e] = tp;
+                tind[e] = tp * RS;
+                eoff[e] = op_;
+                scnt[e] = op_;  // cursor for elist
+            }
+            tp += (c8[u] + TS - 1) / TS;
+            op_ += c8[u];
+        }
+        if (lane == 31) {
+            ind[E] = tp;
+            tind[E] = tp * RS;
+            eoff[E] = op_;
+        }
+    }
+    bar_sync(1, kConsumers);
+    if (ctid == 0)  // slots grouped by expert, stable in slot order
+        for (int sl = 0; sl < nb * K; ++sl) elist[scnt[stop[sl]]++] = sl;
+    __threadfence();
+}
+
+// Routed expert task (see expert_task): gate/up rows of its row split for the
+// tile's tokens, SiLU-mul, then the matching column block of the down
+// projection, added into the residual stream with the routing weight.
+__device__ uint64_t body_moe_expert(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs,
+                                    float* acc, Ring& ring, int ctid) {
+    const int warp = ctid >> 5, lane = ctid & 31;
+    const int I = op.i[0], H = op.i[1], RS = op.i[2], K = op.i[8];
+    const int IR = I / RS;
+    const ExpertTask t = expert_task(op, si.coord[0], P.rt);
+    const int nb = t.ntok;
+    const uint16_t* xn = reinterpret_cast<const uint16_t*>(op.p[3]);
+    for (int v = ctid; v < nb * H / 8; v += kConsumers) {
+        const int j = v / (H / 8), k8 = v - j * (H / 8);
+        reinterpret_cast<uint4*>(xs)[v] =
+            __ldcg(reinterpret_cast<const uint4*>(xn + static_cast<long long>(t.slot[j] / K) * H) + k8);
+    }
+    for (int i = ctid; i < 2 * IR * nb; i += kConsumers) acc[i] = 0.f;
+    bar_sync(1, kConsumers);
+    const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
+    gemv_stream(ring, warp, lane, 2, (IR / 16) * (H / 16), 0, H, nb, xs,
+                [&](int seg, int rt, int g, int q, const float* d) {
+                    const int row = seg * IR + rt * 16 + g;
+                    if (2 * q < nb) {
+                        atomicAdd(&acc[row * nb + 2 * q], d[0]);
+                        atomicAdd(&acc[(row + 8) * nb + 2 * q], d[2]);
+                    }
+                    if (2 * q + 1 < nb) {
+                        atomicAdd(&acc[row * nb + 2 * q + 1], d[1]);
+                        atomicAdd(&acc[(row + 8) * nb + 2 * q + 1], d[3]);
+                    }
+                });
+    bar_sync(1, kConsumers);
+    uint16_t* xa = reinterpret_cast<uint16_t*>(acc + 2 * IR * 8);  // act [nb][IR] bf16
+    for (int idx = ctid; idx < IR * nb; idx += kConsumers) {
+        const int i = idx / nb, j = idx - i * nb;
+        const float gv = acc[i * nb + j], uv = acc[(IR + i) * nb + j];
+        xa[j * IR + i] = f2bf(gv / (1.f + __expf(-gv)) * uv);
+    }
+    bar_sync(1, kConsumers);
+    const float* wslot = reinterpret_cast<const float*>(op.p[4]);
+    float* h = reinterpret_cast<float*>(op.p[5]);
+    gemv_stream(ring, warp, lane, 1, (H / 16) * (IR / 16), 0, IR, nb, xa,
+                [&](int, int rt, int g, int q, const float* d) {
+                    const int row = rt * 16 + g;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int j = 2 * q + c;
+                        if (j < nb) {
+                            const float w = __ldcg(wslot + t.slot[j]);
+                            float* hr = h + static_cast<long long>(t.slot[j] / K) * H;
+                            atomicAdd(hr + row, w * d[c]);
+                            atomicAdd(hr + row + 8, w * d[2 + c]);
+                        }
+                    }
+                });
+    return t_pro;
+}
+
 __device__ void body_embed(const StaticParams& P, const et_op& op, int ctid) {
     const int H = op.i[0];
     const int nb = op.i[1] >= 0 ? static_cast<int>(P.binding[op.i[1]]) : 1;
@@ -669,7 +934,9 @@ __device__ void body_embed(const StaticParams& P, const et_op& op, int ctid) {
 
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ bool op_streams(int kind) { return kind == ET_OP_GEMV || kind == ET_OP_ATTN_SPLIT; }
+__device__ __forceinline__ bool op_streams(int kind) {
+    return kind == ET_OP_GEMV || kind == ET_OP_ATTN_SPLIT || kind == ET_OP_MOE_ROUTE || kind == ET_OP_MOE_EXPERT;
+}
 
 __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     const int ctid = threadIdx.x;
@@ -734,6 +1001,8 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
+                case ET_OP_MOE_ROUTE: body_moe_route(P, op, v, xs, acc, red, ring, ctid, &t_pro); break;
+                case ET_OP_MOE_EXPERT: t_pro = body_moe_expert(P, op, v, xs, acc, ring, ctid); break;
                 default: break;
             }
         }
@@ -785,7 +1054,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             }
             if (v.lazy && extent_masked(P, v.call, v.coord)) continue;
         }
-        const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding);
+        const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
         const int n = pl.total_chunks();
         for (int c = 0; c < n; ++c, ++cseq) {
             const int stage = static_cast<int>(cseq % kStages);
@@ -1182,6 +1451,8 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                 case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
+                case ET_OP_MOE_ROUTE: body_moe_route(P, op, v, xs, acc, red, ring, ctid, &tp); break;
+                case ET_OP_MOE_EXPERT: tp = body_moe_expert(P, op, v, xs, acc, ring, ctid); break;
                 default: break;
             }
         }
@@ -1220,7 +1491,7 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
         if (v.masked) continue;
         const et_op& op = P.ops[v.call];
         if (!op_streams(op.kind)) continue;
-        const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding);
+        const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
         const int n = pl.total_chunks();
         for (int c = 0; c < n; ++c, ++cseq) {
             const int stage = static_cast<int>(cseq % kStages);

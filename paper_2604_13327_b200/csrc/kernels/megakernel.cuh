@@ -21,7 +21,7 @@ constexpr int kThreads = (kConsumerWarps + 2) * 32;
 // a consumer barrier.
 constexpr int kStages = kConsumerWarps;
 constexpr int kStageBytes = 20480;
-constexpr int kXBytes = 28 * 1024;
+constexpr int kXBytes = 32 * 1024;
 constexpr int kAccFloats = 2048;
 constexpr int kMaxSymbols = 8;
 constexpr int kMaxRuntime = 16;
@@ -102,7 +102,7 @@ struct StaticParams {
                          // 2 = record consumer ring-stall ns of warp 0 in the trace pad field
 };
 
-constexpr int kMaxDd = 8;  // data-dependent event tensors per graph (dynamic mode)
+constexpr int kMaxDd = 128;  // data-dependent event tensors per graph (dynamic mode; one per MoE layer)
 
 // Per-step control block of the dynamic scheduler (double-buffered).
 struct DynCtl {

@@ -26,6 +26,28 @@
 // ET_OP_ATTN_MERGE      task (g): merges the splits and the new token at position s
 //   (K/V row s of the cache) for the group's q heads; same i/p as ATTN_SPLIT plus
 //   p4 = out (bf16 [q_heads*head_dim])
+// ATTN flags bit 0 (Qwen3 q/k-norm): q at p0 is the raw projection; SPLIT and MERGE apply
+//   the per-head RMSNorm (p5 = q-norm weight, p6 = k-norm weight, fp32 [head_dim], f1 = eps)
+//   and RoPE (p7 = inverse frequencies) themselves; MERGE also normalises + rotates the raw
+//   new k at p8 + g*head_dim (v at p8 + (kv_heads + g)*head_dim) and appends k/v (bf16) to
+//   the cache at position s before using them.
+// ET_OP_MOE_ROUTE       task t of E/16: router logits rows [16t, 16t+16) (GEMV, RMSNorm prologue,
+//   GEMV fields i0..i9 as ET_OP_GEMV with i3 = 1, i4 = EPI_F32); task 0 also stores the
+//   normalised activations; the last task to arrive computes the routing for every token:
+//   softmax over E, top-k (descending probability, lower expert index wins ties),
+//   renormalised weights -- or, with flags bit 0, the host-injected topk -- then expert
+//   counts, exp_indptr (tiles of TS tokens, ref workloads.cpp:140-144), task_indptr
+//   (x RS), eoff (exclusive prefix of counts) and elist (slots by expert, stable).
+//   i6 = top_k, i10 = rt topk | rt counts << 8 | rt exp_indptr << 16 | rt elist << 24,
+//   i11 = rt eoff | rt task_indptr << 8, i12 = RS, i13 = TS; p0 = router weight (frag16
+//   [E][H]), p2 = h (fp32 [b][H]), p3 = gamma, p4 = logits (fp32 [b][E]), p5 = xn out
+//   (bf16 [b][H]), p6 = slot weights out (fp32 [b*top_k]), p7 = arrival counter (int32)
+// ET_OP_MOE_EXPERT      task flat = tile * RS + r (range-triggered on task_indptr, extent_from):
+//   for the tile's tokens x = xn[token]: act = silu(Wg_e x) * (Wu_e x) on rows [r*IR, r*IR+IR)
+//   (IR = I / RS), then h[token] += w_slot * Wd_e[:, rows] act (red.global.add).
+//   i0 = I, i1 = H, i2 = RS, i3 = TS (<= 8), i4..i7 = rt exp_indptr, counts, elist, eoff,
+//   i8 = top_k, i10 = E; p0/p1 = Wgate/Wup (frag16 [E][I][H]), p2 = Wdown blocks (frag16
+//   [E][RS][H][IR]), p3 = xn (bf16 [b][H]), p4 = slot weights, p5 = h (fp32 [b][H])
 // ET_OP_EMBED           task (0): h[b][:] = float(table[tokens[b]][:]) for every batch row
 //   i0 = hidden, i1 = batch symbol slot (-1: 1); p0 = table (bf16 [vocab][hidden]),
 //   p1 = token ids (int32 [b]), p2 = out (fp32 [b][hidden])
@@ -47,31 +69,63 @@ struct Chunk {
 // chunks of `cbytes` (<= one ring stage).  GEMV streams segment 0 then
 // segment 1; attention interleaves them (K block 0, V block 0, K block 1, ...).
 struct StreamPlan {
-    const uint8_t* base[2];
-    long long bytes[2];
+    static constexpr int kMaxSeg = 3;
+    const uint8_t* base[kMaxSeg];
+    long long bytes[kMaxSeg];
     int nseg;
     int cbytes;
     bool interleave;
-    int n[2];  // chunks per segment (set by finish(); keeps divisions off the per-chunk path)
+    int n[kMaxSeg];  // chunks per segment (set by finish(); keeps divisions off the per-chunk path)
 
     __device__ void finish() {
-        for (int s = 0; s < 2; ++s) n[s] = s < nseg ? static_cast<int>((bytes[s] + cbytes - 1) / cbytes) : 0;
+        for (int s = 0; s < kMaxSeg; ++s) n[s] = s < nseg ? static_cast<int>((bytes[s] + cbytes - 1) / cbytes) : 0;
     }
-    __device__ int total_chunks() const { return n[0] + n[1]; }
+    __device__ int total_chunks() const { return n[0] + n[1] + n[2]; }
     __device__ Chunk chunk(int idx) const {
         int s = 0;
         if (interleave) {
             s = idx & 1;
             idx >>= 1;
-        } else if (idx >= n[0]) {
-            s = 1;
-            idx -= n[0];
+        } else {
+            while (s < kMaxSeg - 1 && idx >= n[s]) idx -= n[s++];
         }
         const long long off = static_cast<long long>(idx) * cbytes;
         const long long rem = bytes[s] - off;
         return Chunk{base[s] + off, static_cast<uint32_t>(rem < cbytes ? rem : cbytes)};
     }
 };
+
+// ---- MoE ------------------------------------------------------------------
+// Expert task (tile, r) of the routed expert call: flat = tile * RS + r.  The
+// tile's expert e is the group of `tile` in exp_indptr (tiles of TS tokens,
+// ref workloads.cpp:140-144); its tokens are the slots elist[eoff[e] + i*TS +
+// j] (slot = token * top_k + k, stable in slot order).  Valid only once the
+// routing writer has finished (after the task's waits).
+struct ExpertTask {
+    int e, tile, r, ntok;
+    int slot[8];
+};
+
+__device__ __forceinline__ ExpertTask expert_task(const et_op& op, int flat, int* const* rt) {
+    const int RS = op.i[2], TS = op.i[3];
+    const int* ind = rt[op.i[4]];
+    const int* cnt = rt[op.i[5]];
+    const int* elist = rt[op.i[6]];
+    const int* eoff = rt[op.i[7]];
+    const int E = op.i[10];
+    ExpertTask t;
+    t.tile = flat / RS;
+    t.r = flat - t.tile * RS;
+    int e = 0;
+    while (e + 1 < E && __ldcg(ind + e + 1) <= t.tile) ++e;
+    t.e = e;
+    const int i = t.tile - __ldcg(ind + e);
+    const int c = __ldcg(cnt + e) - i * TS;
+    t.ntok = c < TS ? c : TS;
+    const int base = __ldcg(eoff + e) + i * TS;
+    for (int j = 0; j < 8; ++j) t.slot[j] = j < t.ntok ? __ldcg(elist + base + j) : 0;
+    return t;
+}
 
 // Work span of GEMV task t of T, in k-step units of the frag16 tile order
 // (unit u = row tile u / kst, k-step u % kst; kst = K / 16).  Without split-K
@@ -110,7 +164,8 @@ __device__ __forceinline__ GemvSpan gemv_span(const et_op& op, int t, int T) {
 }
 
 // Plan for a task of `call` at row-major `flat` with sample coords `coord`.
-__device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coord, int T, const long long* binding) {
+__device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coord, int T, const long long* binding,
+                                                int* const* rt) {
     StreamPlan pl;
     pl.nseg = 0;
     pl.cbytes = kStageBytes;
@@ -122,6 +177,21 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
             pl.base[s] = reinterpret_cast<const uint8_t*>(op.p[s]) + sp.u0 * 512;
             pl.bytes[s] = (sp.u1 - sp.u0) * 512;
         }
+    } else if (op.kind == ET_OP_MOE_ROUTE) {
+        const GemvSpan sp = gemv_span(op, coord[0], T);
+        pl.nseg = 1;
+        pl.base[0] = reinterpret_cast<const uint8_t*>(op.p[0]) + sp.u0 * 512;
+        pl.bytes[0] = (sp.u1 - sp.u0) * 512;
+    } else if (op.kind == ET_OP_MOE_EXPERT) {
+        // gate rows, up rows (rows [r*IR, r*IR+IR) of expert e), then down block (e, r)
+        const ExpertTask t = expert_task(op, coord[0], rt);
+        const long long I = op.i[0], H = op.i[1], RS = op.i[2], IR = I / RS;
+        const long long rows = IR * H * 2;
+        pl.nseg = 3;
+        pl.base[0] = reinterpret_cast<const uint8_t*>(op.p[0]) + (t.e * I + t.r * IR) * H * 2;
+        pl.base[1] = reinterpret_cast<const uint8_t*>(op.p[1]) + (t.e * I + t.r * IR) * H * 2;
+        pl.base[2] = reinterpret_cast<const uint8_t*>(op.p[2]) + (t.e * RS + t.r) * rows;
+        pl.bytes[0] = pl.bytes[1] = pl.bytes[2] = rows;
     } else if (op.kind == ET_OP_ATTN_SPLIT) {
         // K rows then V rows of positions [c*CH, min(s, c*CH+CH)), one chunk each
         const int dh = op.i[0], CH = op.i[2], cap = op.i[3];

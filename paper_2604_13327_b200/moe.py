@@ -1,0 +1,361 @@
+"""Qwen3-MoE-style decode on the Event Tensor megakernel, with routing resolved
+on the GPU.
+
+The reference models an MoE layer as the graph route(1) -> group(tokens*top_k)
+-> expert_mm (ref workloads.cpp:81-114):
+
+- `group` notifies EXP[topk[f]] through a data-dependent notify;
+- `expert_mm` is range-triggered on `exp_indptr` and sizes itself with
+  `extent_from`.
+
+The routing is a seeded RNG (`moe_realization`, ref workloads.cpp:116-150).
+Here the same structure runs inside each decoder layer of one decode step:
+
+    qkv[T] -> attn[kv, ceil(s/CH)] -> merge[kv] -> oproj[T] -> route[E/16]
+      -> group[b*K]      (routed notify EXP_l[topk_l[f]]; EXP_l has data-dependent
+                          counts = cnt_l, written by route_l)
+      -> expert[b*K*RS]  (range trigger on tind_l = exp_indptr_l * RS, extent_from tind_l)
+      -> next layer's qkv
+
+The route tasks run the router GEMV. The last task to arrive computes on the
+device:
+
+- softmax and top-k;
+- expert counts, `exp_indptr` (tiles of TS tokens, the reference's routing
+  algebra);
+- `task_indptr`, the per-expert slot lists and the weights.
+
+These become the runtime tensors the Event Tensors read. No host round trip,
+recompile or relaunch is involved. Routing can also be injected from the host
+(`inject_routing`): route then skips its top-k, as in the reference's
+realization.
+
+Each expert task (tile, r) computes SiLU(gate)*up for rows [r*IR, r*IR+IR) of
+its expert on the tile's tokens. It then adds the matching column block of the
+down projection, times the routing weight, into the fp32 residual stream with
+red.global.add, so no combine stage exists. Attention uses Qwen3's per-head
+q/k RMSNorm before RoPE, applied inside the attention tasks (ATTN flags bit 0).
+"""
+
+import dataclasses
+import json
+import math
+import time
+
+import torch
+
+from . import etsim
+from .decode import frag16, rope_inv_freq
+from .ops import (
+    EPI_ADD,
+    EPI_F32,
+    OP_ATTN_MERGE,
+    OP_ATTN_SPLIT,
+    OP_EMBED,
+    OP_GEMV,
+    OP_MOE_EXPERT,
+    OP_MOE_ROUTE,
+    OP_NONE,
+    make_op,
+    pack,
+    ptr,
+)
+
+
+@dataclasses.dataclass
+class MoEConfig:
+    name: str
+    hidden: int
+    layers: int
+    heads: int
+    kv_heads: int
+    head_dim: int
+    experts: int
+    top_k: int
+    expert_inter: int
+    vocab: int
+    rope_theta: float = 1000000.0
+    eps: float = 1e-6
+    attn_chunk: int = 64
+    row_splits: int = 12       # expert row splits (expert_inter / row_splits % 32 == 0)
+    tile_tokens: int = 8       # tokens per expert tile (<= 8: the mma N dimension)
+
+    @property
+    def q_rows(self):
+        return self.heads * self.head_dim
+
+    @property
+    def kv_rows(self):
+        return self.kv_heads * self.head_dim
+
+    def dense_bytes(self):
+        h = self.hidden
+        per_layer = 2 * (h * (self.q_rows + 2 * self.kv_rows) + self.q_rows * h + self.experts * h + 2 * h
+                         + 2 * self.head_dim)
+        return self.layers * per_layer + 2 * self.vocab * h + 4 * h
+
+    def expert_bytes(self):
+        return 3 * self.expert_inter * self.hidden * 2
+
+    def step_bytes(self, s, active_experts_per_layer, b=1):
+        """Algorithmic bytes: dense weights + touched experts (from the device counts) + KV."""
+        kv = self.layers * 2 * self.kv_rows * 2 * b * (s + 1)
+        return self.dense_bytes() + sum(active_experts_per_layer) * self.expert_bytes() + kv
+
+
+TINY_MOE = MoEConfig("tiny-moe-2L", hidden=256, layers=2, heads=4, kv_heads=2, head_dim=64, experts=16, top_k=4,
+                     expert_inter=64, vocab=1024, row_splits=2, rope_theta=10000.0)
+QWEN3_30B_A3B = MoEConfig("qwen3-30b-a3b", hidden=2048, layers=48, heads=32, kv_heads=4, head_dim=128, experts=128,
+                          top_k=8, expert_inter=768, vocab=151936, row_splits=12)
+MOE_CONFIGS = {c.name: c for c in (TINY_MOE, QWEN3_30B_A3B)}
+
+RT_PER_LAYER = ("topk", "cnt", "ind", "tind", "elist", "eoff")
+
+
+def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1):
+    """Reference-format graph spec (ref json_io.cpp:115-230) of one MoE decode step."""
+    CH = cfg.attn_chunk
+    E, K, RS = cfg.experts, cfg.top_k, cfg.row_splits
+    fns, events, calls, rts = [], [], [], []
+
+    def fn(name, grid):
+        fns.append({"name": name, "grid": grid, "resource": "sm", "duration": "unit"})
+        return name
+
+    def ev(name, shape, **kw):
+        events.append(dict({"name": name, "shape": shape}, **kw))
+        return name
+
+    T, kv = str(tasks), str(cfg.kv_heads)
+    ev("EMB", ["1"])
+    calls.append({"fn": fn("embed", ["1"]), "out": [{"event": "EMB", "map": ["0"]}]})
+    prev = "EMB"
+    for l in range(cfg.layers):
+        rt = {n: f"{n}{l}" for n in RT_PER_LAYER}
+        route = f"L{l}.route"
+        rts += [{"name": rt["topk"], "shape": [str(tokens), str(K)], "role": "routing", "writer": route},
+                {"name": rt["cnt"], "shape": [str(E)], "role": "counts", "writer": route},
+                {"name": rt["ind"], "shape": [str(E + 1)], "role": "indptr", "writer": route},
+                {"name": rt["tind"], "shape": [str(E + 1)], "role": "indptr", "writer": route},
+                {"name": rt["elist"], "shape": [str(tokens * K)], "role": "routing", "writer": route},
+                {"name": rt["eoff"], "shape": [str(E + 1)], "role": "indptr", "writer": route}]
+        qkv, a, m, o, r, x, d = (f"{n}{l}" for n in ("QKV", "A", "M", "O", "R", "EXP", "D"))
+        ev(qkv, ["1"])
+        ev(a, [kv])
+        ev(m, ["1"])
+        ev(o, ["1"])
+        ev(r, ["1"])
+        ev(x, [str(E)], data_dependent=True, counts=rt["cnt"], writer=route)
+        ev(d, ["1"])
+        calls += [
+            {"fn": fn(f"L{l}.qkv", [T]), "in": [{"event": prev, "map": ["0"]}], "out": [{"event": qkv, "map": ["0"]}]},
+            {"fn": fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), "in": [{"event": qkv, "map": ["0"]}],
+             "out": [{"event": a, "map": ["t0"]}]},
+            {"fn": fn(f"L{l}.merge", [kv]), "in": [{"event": a, "map": ["t0"]}, {"event": qkv, "map": ["0"]}],
+             "out": [{"event": m, "map": ["0"]}]},
+            {"fn": fn(f"L{l}.oproj", [T]), "in": [{"event": m, "map": ["0"]}], "out": [{"event": o, "map": ["0"]}]},
+            {"fn": fn(route, [str(E // 16)]), "in": [{"event": o, "map": ["0"]}], "out": [{"event": r, "map": ["0"]}]},
+            {"fn": fn(f"L{l}.group", [str(tokens * K)]), "in": [{"event": r, "map": ["0"]}],
+             "out": [{"event": x, "routed_by": rt["topk"]}]},
+            {"fn": fn(f"L{l}.expert", [str(tokens * K * RS)]), "extent_from": rt["tind"],
+             "in": [{"event": x, "indptr": rt["tind"]}], "out": [{"event": d, "map": ["0"]}]},
+        ]
+        prev = d
+    ev("LM", ["1"])
+    calls.append({"fn": fn("lm_head", [str(lm_tasks)]), "in": [{"event": prev, "map": ["0"]}],
+                  "out": [{"event": "LM", "map": ["0"]}]})
+    return {"symbols": ["s"], "size_symbol": "s", "duration_models": {"unit": {"kind": "constant", "value": 1}},
+            "device_functions": fns, "event_tensors": events, "runtime_tensors": rts, "calls": calls}
+
+
+def init_moe_weights(cfg: MoEConfig, device, seed=0, std=0.02):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def w(*shape, s=std):
+        t = torch.empty(*shape, dtype=torch.bfloat16, device=device)
+        t.normal_(0.0, s, generator=g)
+        return t
+
+    def norm(n):
+        t = torch.empty(n, dtype=torch.float32, device=device)
+        t.normal_(1.0, 0.01, generator=g)
+        return t
+
+    H, I, E = cfg.hidden, cfg.expert_inter, cfg.experts
+    W = {"embed": w(cfg.vocab, H), "final_norm": norm(H), "lm_head": w(cfg.vocab, H), "layers": []}
+    for _ in range(cfg.layers):
+        W["layers"].append({
+            "attn_norm": norm(H), "wqkv": w(cfg.q_rows + 2 * cfg.kv_rows, H), "q_norm": norm(cfg.head_dim),
+            "k_norm": norm(cfg.head_dim), "wo": w(H, cfg.q_rows), "ffn_norm": norm(H),
+            "router": w(E, H, s=0.1),
+            "wgate": w(E, I, H), "wup": w(E, I, H), "wdown": w(E, H, I),
+        })
+    return W
+
+
+def moe_device_layout(cfg, W):
+    """frag16 tiles for every GEMV matrix; expert down projections cut into RS
+    column blocks [E][RS][H][IR], each its own frag16 matrix."""
+    E, H, I, RS = cfg.experts, cfg.hidden, cfg.expert_inter, cfg.row_splits
+    IR = I // RS
+    D = {"embed": W["embed"], "final_norm": W["final_norm"], "lm_head": frag16(W["lm_head"]), "layers": []}
+    for L in W["layers"]:
+        d = dict(L)
+        for k in ("wqkv", "wo", "router"):
+            d[k] = frag16(L[k])
+        d["wgate"] = torch.stack([frag16(L["wgate"][e]) for e in range(E)])
+        d["wup"] = torch.stack([frag16(L["wup"][e]) for e in range(E)])
+        blocks = L["wdown"].reshape(E, H, RS, IR).permute(0, 2, 1, 3)  # [E][RS][H][IR]
+        d["wdown"] = torch.stack([torch.stack([frag16(blocks[e, r].contiguous()) for r in range(RS)])
+                                  for e in range(E)])
+        D["layers"].append(d)
+    return D
+
+
+class MoEDecodeModel:
+    """One MoE decoder + its lowered megakernel (static or dynamic scheduler)."""
+
+    def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
+                 scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False):
+        if not etsim.gpu_available():
+            raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
+        assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
+        self.cfg = cfg
+        self.device = torch.device(device)
+        props = torch.cuda.get_device_properties(self.device)
+        self.num_workers = num_workers or props.multi_processor_count
+        self.tokens = 1
+        self.samples = sorted(int(s) for s in samples)
+        self.capacity = self.samples[-1] + 1
+        self.max_splits = max(1, (self.samples[-1] + cfg.attn_chunk - 1) // cfg.attn_chunk)
+        self.scheduler = scheduler
+        t0 = time.perf_counter()
+        self.spec = moe_graph_spec(cfg, self.num_workers, self.num_workers, self.tokens)
+        self.graph = etsim.Graph.from_json(json.dumps(self.spec))
+        self.rt_index = {r["name"]: i for i, r in enumerate(self.spec["runtime_tensors"])}
+        if scheduler == "dynamic":
+            self.kernel = etsim.lower_dynamic(self.graph, early_push=early_push)
+        else:
+            # static: data-dependent events collapse to worst-case barriers (ref
+            # sched_static.cpp:13-47); extent_from still masks dead expert tiles on device
+            self.kernel = etsim.lower_static(etsim.worst_case_rewrite(self.graph), [{"s": s} for s in self.samples],
+                                             num_sms=self.num_workers)
+        self.lower_ms = (time.perf_counter() - t0) * 1e3
+
+        dev = self.device
+        W = weights if weights is not None else init_moe_weights(cfg, dev, seed)
+        self.W_logical = W if keep_logical else None
+        self.W = moe_device_layout(cfg, W)
+        b, E, K = self.tokens, cfg.experts, cfg.top_k
+        self.kcache = [torch.zeros(cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
+                       for _ in range(cfg.layers)]
+        self.vcache = [torch.zeros_like(k) for k in self.kcache]
+        self.tok = torch.zeros(b, dtype=torch.int32, device=dev)
+        self.h = torch.zeros(b, cfg.hidden, dtype=torch.float32, device=dev)
+        self.qkv = torch.zeros(b, cfg.q_rows + 2 * cfg.kv_rows, dtype=torch.float32, device=dev)
+        self.attn = torch.zeros(b, cfg.q_rows, dtype=torch.bfloat16, device=dev)
+        self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        self.logits_r = torch.zeros(cfg.layers, b, E, dtype=torch.float32, device=dev)   # router logits per layer
+        self.xn = torch.zeros(cfg.layers, b, cfg.hidden, dtype=torch.bfloat16, device=dev)
+        self.wslot = torch.zeros(cfg.layers, b * K, dtype=torch.float32, device=dev)
+        self.arrive = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
+        self.logits = torch.zeros(b, cfg.vocab, dtype=torch.float32, device=dev)
+        self.inv_freq = rope_inv_freq(cfg).to(dev)
+        self.injected = False
+
+        t1 = time.perf_counter()
+        if scheduler == "dynamic":
+            self.executor = etsim.Executor(self.kernel, [{"s": s} for s in self.samples], device=dev.index or 0,
+                                           num_workers=self.num_workers, record_trace=record_trace)
+        else:
+            self.executor = etsim.Executor(self.kernel, device=dev.index or 0, num_workers=self.num_workers,
+                                           record_trace=record_trace)
+        self.bind()
+        self.upload_ms = (time.perf_counter() - t1) * 1e3
+
+    def bind(self):
+        self.executor.bind_ops(pack(self._ops()))
+
+    def _ops(self):
+        cfg, W = self.cfg, self.W
+        H, dh, CH = cfg.hidden, cfg.head_dim, cfg.attn_chunk
+        E, K, RS, TS = cfg.experts, cfg.top_k, cfg.row_splits, cfg.tile_tokens
+        G = cfg.heads // cfg.kv_heads
+        scale = 1.0 / math.sqrt(dh)
+        nq = cfg.q_rows
+        ops = [make_op(OP_EMBED, i=[H, -1], p=[ptr(W["embed"]), ptr(self.tok), ptr(self.h)])]
+        for l, L in enumerate(W["layers"]):
+            ri = {n: self.rt_index[f"{n}{l}"] for n in RT_PER_LAYER}
+            kc, vc = self.kcache[l], self.vcache[l]
+            ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
+                               p=[ptr(L["wqkv"]), 0, ptr(self.h), ptr(L["attn_norm"]), ptr(self.qkv)]))
+            attn_i = [dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads]
+            attn_p = [ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(L["q_norm"]),
+                      ptr(L["k_norm"]), ptr(self.inv_freq), ptr(self.qkv) + 4 * nq]
+            ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
+            ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
+            ops.append(make_op(OP_GEMV, i=[H, nq, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],
+                               p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h)]))
+            rt_a = ri["topk"] | ri["cnt"] << 8 | ri["ind"] << 16 | ri["elist"] << 24
+            rt_b = ri["eoff"] | ri["tind"] << 8
+            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, -1, K, 16, 0, H, rt_a, rt_b, RS, TS],
+                               f=[cfg.eps],
+                               p=[ptr(L["router"]), 0, ptr(self.h), ptr(L["ffn_norm"]), ptr(self.logits_r[l]),
+                                  ptr(self.xn[l]), ptr(self.wslot[l]), ptr(self.arrive[l:l + 1])],
+                               flags=1 if self.injected else 0))
+            ops.append(make_op(OP_NONE))  # group: the routed notify is the Event Tensor edge itself
+            ops.append(make_op(OP_MOE_EXPERT,
+                               i=[cfg.expert_inter, H, RS, TS, ri["ind"], ri["cnt"], ri["elist"], ri["eoff"], K, 0, E],
+                               p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(L["wdown"]), ptr(self.xn[l]), ptr(self.wslot[l]),
+                                  ptr(self.h)]))
+        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
+                           p=[ptr(W["lm_head"]), 0, ptr(self.h), ptr(W["final_norm"]), ptr(self.logits)]))
+        return ops
+
+    # ------------------------------------------------------------------
+    def inject_routing(self, topk_per_layer):
+        """Host-supplied routing (e.g. etsim.moe_realization(...)["topk"] per layer):
+        the route tasks skip their top-k and derive counts/indptr/lists from it."""
+        for l, tk in enumerate(topk_per_layer):
+            self.executor.set_runtime_tensor(f"topk{l}", [int(v) for v in tk])
+        if not self.injected:
+            self.injected = True
+            self.bind()
+
+    def routing(self, l):
+        """Device-written routing tensors of layer l (after a step)."""
+        cfg = self.cfg
+        n = {"topk": self.tokens * cfg.top_k, "cnt": cfg.experts, "ind": cfg.experts + 1, "tind": cfg.experts + 1,
+             "elist": self.tokens * cfg.top_k, "eoff": cfg.experts + 1}
+        return {k: self.executor.runtime_tensor(f"{k}{l}", v) for k, v in n.items()}
+
+    def realization(self):
+        """The device routing of the last step as a reference RoutingRealization dict."""
+        out = {}
+        for l in range(self.cfg.layers):
+            for k, v in self.routing(l).items():
+                out[f"{k}{l}"] = v
+        return out
+
+    def fill_cache(self, s, seed=1):
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        for k, v in zip(self.kcache, self.vcache):
+            k.zero_()
+            v.zero_()
+            k[:, :s].normal_(0.0, 1.0, generator=g)
+            v[:, :s].normal_(0.0, 1.0, generator=g)
+
+    def set_token(self, token):
+        self.tok.fill_(int(token))
+
+    def step(self, s):
+        self.last_stats = self.executor.run({"s": int(s)})
+        return self.logits
+
+    def launch(self, s, stream=0):
+        self.executor.launch({"s": int(s)}, stream)
+
+    def active_experts(self):
+        return [sum(1 for c in self.routing(l)["cnt"] if c > 0) for l in range(self.cfg.layers)]

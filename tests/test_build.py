@@ -1,0 +1,24 @@
+"""The megakernel must stay spill-free: a 10-warp CTA is capped at 168
+registers, and local-memory spills in the persistent task loop cost ~12% of
+decode time (measured this round).  Reads the ptxas report of the in-tree
+build (Makefile: build/cu/megakernel.ptxas.txt)."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPORT = os.path.join(ROOT, "build", "cu", "megakernel.ptxas.txt")
+
+
+@pytest.mark.skipif(not os.path.exists(REPORT), reason="megakernel not built in-tree")
+def test_persistent_kernels_do_not_spill():
+    text = open(REPORT).read()
+    found = {}
+    for m in re.finditer(r"Function properties for (\S+)\n\s+(\d+) bytes stack frame, (\d+) bytes spill stores, "
+                         r"(\d+) bytes spill loads", text):
+        found[m.group(1)] = (int(m.group(3)), int(m.group(4)))
+    kernels = {k: v for k, v in found.items() if "et_static_kernel" in k or "et_dynamic_kernel" in k}
+    assert len(kernels) == 2, found
+    for name, (st, ld) in kernels.items():
+        assert st == 0 and ld == 0, (name, st, ld)

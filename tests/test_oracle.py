@@ -126,3 +126,23 @@ def test_oracle_decode_graphs():
     for s, want in c["simulate"].items():
         acc = O.static_accounting(c["spec"], samples, {"s": int(s)})
         assert acc["noops"] == want["noop_records"]
+
+
+def test_moe_oracle_routing_algebra_matches_reference_realizations():
+    """oracle/moe_oracle.moe_routing_tensors (what the device route task computes)
+    reproduces the reference's counts and tile indptr (ref workloads.cpp:137-144)
+    on every golden realization generated from the reference."""
+    import json
+    import os
+
+    from oracle.moe_oracle import moe_routing_tensors
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))
+    for case in gold["realizations"]:
+        a, out = case["args"], case["out"]
+        got = moe_routing_tensors(out["topk"], a["experts"], a.get("tile_size", 1), 3)
+        assert got["cnt"] == out["expert_counts"], a
+        assert got["ind"] == out["exp_indptr"], a
+        assert got["tind"] == [3 * v for v in out["exp_indptr"]]
+        # elist groups the slots by expert in slot order
+        assert [out["topk"][sl] for sl in got["elist"]] == sorted(out["topk"])
