@@ -737,14 +737,16 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
     bar_sync(1, kConsumers);
     if (!*flag) return;
 
-    int* topk = P.rt[op.i[10] & 0xff];
-    int* cnt = P.rt[(op.i[10] >> 8) & 0xff];
-    int* ind = P.rt[(op.i[10] >> 16) & 0xff];
-    int* elist = P.rt[(op.i[10] >> 24) & 0xff];
-    int* eoff = P.rt[op.i[11] & 0xff];
-    int* tind = P.rt[(op.i[11] >> 8) & 0xff];
+    const int rb = op.i[10];  // the layer's routing tensors: topk, cnt, ind, tind, elist, eoff
+    int* topk = P.rt[rb];
+    int* cnt = P.rt[rb + 1];
+    int* ind = P.rt[rb + 2];
+    int* tind = P.rt[rb + 3];
+    int* elist = P.rt[rb + 4];
+    int* eoff = P.rt[rb + 5];
     const float* logits = reinterpret_cast<const float*>(op.p[4]);
     float* wslot = reinterpret_cast<float*>(op.p[6]);
+    int4* tinfo = reinterpret_cast<int4*>(op.p[8]);   // [tiles] (expert, first slot, tokens)
     int* scnt = reinterpret_cast<int*>(acc);          // [E] counts
     int* stop = scnt + 256;                           // [nb*K] experts per slot
     for (int e = ctid; e < E; e += kConsumers) scnt[e] = 0;
@@ -766,8 +768,6 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
         for (int u = 0; u < kPer; ++u)
             if (lane + 32 * u < E) z += __expf(lg[u] - m);
         z = warp_sum(z);
-        float wsum = 0.f, wsel[8];
-        int esel[8];
         for (int j = 0; j < K; ++j) {
             int e;
             if (op.flags & 1) {  // injected routing (host-written topk)
@@ -796,24 +796,16 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
                         if (u == (e >> 5)) lg[u] = -INFINITY;
                 }
             }
-            esel[j] = e;
+            if (lane == 0) stop[t * K + j] = e;
         }
-        // weights: p_e / sum of the selected p (recomputed from the logits, exact)
-        for (int j = 0; j < K; ++j) {
-            wsel[j] = __expf(__ldcg(logits + static_cast<long long>(t) * E + esel[j]) - m) / z;
-            wsum += wsel[j];
-        }
+        __syncwarp();
+        // weights p_e / sum of the selected p, recomputed from the logits
+        const int ej = lane < K ? stop[t * K + lane] : 0;
+        const float wj = lane < K ? __expf(__ldcg(logits + static_cast<long long>(t) * E + ej) - m) / z : 0.f;
+        const float wsum = warp_sum(wj);
         if (lane < K) {
-            float wj = 0.f;
-            int ej = 0;
-            for (int j = 0; j < K; ++j)
-                if (j == lane) {
-                    wj = wsel[j];
-                    ej = esel[j];
-                }
             const int slot = t * K + lane;
             if (!(op.flags & 1)) topk[slot] = ej;
-            stop[slot] = ej;
             wslot[slot] = wj / wsum;
             atomicAdd(&scnt[ej], 1);
         }
@@ -846,6 +838,8 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
                 tind[e] = tp * RS;
                 eoff[e] = op_;
                 scnt[e] = op_;  // cursor for elist
+                for (int i = 0; i * TS < c8[u]; ++i)  // direct tile table for the expert tasks
+                    tinfo[tp + i] = make_int4(e, op_ + i * TS, c8[u] - i * TS < TS ? c8[u] - i * TS : TS, 0);
             }
             tp += (c8[u] + TS - 1) / TS;
             op_ += c8[u];
@@ -870,13 +864,23 @@ __device__ uint64_t body_moe_expert(const StaticParams& P, const et_op& op, cons
     const int warp = ctid >> 5, lane = ctid & 31;
     const int I = op.i[0], H = op.i[1], RS = op.i[2], K = op.i[8];
     const int IR = I / RS;
-    const ExpertTask t = expert_task(op, si.coord[0], P.rt);
-    const int nb = t.ntok;
+    int* stok = reinterpret_cast<int*>(acc + kAccFloats - 16);     // [8] token of each tile row
+    float* swt = acc + kAccFloats - 8;                             // [8] its routing weight
+    int nb;
+    {
+        const ExpertTask t = expert_task(op, si.coord[0], P.rt);
+        nb = t.ntok;
+        if (ctid < nb) {
+            stok[ctid] = t.slot[ctid] / K;
+            swt[ctid] = __ldcg(reinterpret_cast<const float*>(op.p[4]) + t.slot[ctid]);
+        }
+    }
+    bar_sync(1, kConsumers);
     const uint16_t* xn = reinterpret_cast<const uint16_t*>(op.p[3]);
     for (int v = ctid; v < nb * H / 8; v += kConsumers) {
         const int j = v / (H / 8), k8 = v - j * (H / 8);
         reinterpret_cast<uint4*>(xs)[v] =
-            __ldcg(reinterpret_cast<const uint4*>(xn + static_cast<long long>(t.slot[j] / K) * H) + k8);
+            __ldcg(reinterpret_cast<const uint4*>(xn + static_cast<long long>(stok[j]) * H) + k8);
     }
     for (int i = ctid; i < 2 * IR * nb; i += kConsumers) acc[i] = 0.f;
     bar_sync(1, kConsumers);
@@ -901,7 +905,6 @@ __device__ uint64_t body_moe_expert(const StaticParams& P, const et_op& op, cons
         xa[j * IR + i] = f2bf(gv / (1.f + __expf(-gv)) * uv);
     }
     bar_sync(1, kConsumers);
-    const float* wslot = reinterpret_cast<const float*>(op.p[4]);
     float* h = reinterpret_cast<float*>(op.p[5]);
     gemv_stream(ring, warp, lane, 1, (H / 16) * (IR / 16), 0, IR, nb, xa,
                 [&](int, int rt, int g, int q, const float* d) {
@@ -910,8 +913,8 @@ __device__ uint64_t body_moe_expert(const StaticParams& P, const et_op& op, cons
                     for (int c = 0; c < 2; ++c) {
                         const int j = 2 * q + c;
                         if (j < nb) {
-                            const float w = __ldcg(wslot + t.slot[j]);
-                            float* hr = h + static_cast<long long>(t.slot[j] / K) * H;
+                            const float w = swt[j];
+                            float* hr = h + static_cast<long long>(stok[j]) * H;
                             atomicAdd(hr + row, w * d[c]);
                             atomicAdd(hr + row + 8, w * d[2 + c]);
                         }
@@ -938,6 +941,9 @@ __device__ __forceinline__ bool op_streams(int kind) {
     return kind == ET_OP_GEMV || kind == ET_OP_ATTN_SPLIT || kind == ET_OP_MOE_ROUTE || kind == ET_OP_MOE_EXPERT;
 }
 
+// kMoE: the MoE bodies are compiled into this instantiation.  The dense
+// instantiation keeps them out of the register allocation of the GEMV loop.
+template <bool kMoE>
 __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     const int ctid = threadIdx.x;
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
@@ -1001,8 +1007,12 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
-                case ET_OP_MOE_ROUTE: body_moe_route(P, op, v, xs, acc, red, ring, ctid, &t_pro); break;
-                case ET_OP_MOE_EXPERT: t_pro = body_moe_expert(P, op, v, xs, acc, ring, ctid); break;
+                case ET_OP_MOE_ROUTE:
+                    if constexpr (kMoE) body_moe_route(P, op, v, xs, acc, red, ring, ctid, &t_pro);
+                    break;
+                case ET_OP_MOE_EXPERT:
+                    if constexpr (kMoE) t_pro = body_moe_expert(P, op, v, xs, acc, ring, ctid);
+                    break;
                 default: break;
             }
         }
@@ -1124,6 +1134,7 @@ __device__ void dma_loop(const StaticParams& P) {
     }
 }
 
+template <bool kMoE>
 __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_constant__ StaticParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int worker = blockIdx.x;
@@ -1173,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     if (warp < kConsumerWarps) {
-        consumer_loop(P, worker, smem, T);
+        consumer_loop<kMoE>(P, worker, smem, T);
     } else if (warp == kProducerWarp) {
         producer_loop(P, worker, smem, T);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
@@ -1273,6 +1284,115 @@ __device__ void dyn_count(const StaticParams& P, const DynParams& D, unsigned in
     }
 }
 
+// ---- warp-cooperative completion (the consumer CTAs' warp 0).  A notify that
+// completes an element releases its consumers lane-strided over the warp and
+// pushes the ready ones with one tail reservation per warp (a 148-way fan-out
+// costs ~5 serial atomics instead of ~300).  Lane 0 owns the counter atomics.
+__device__ __forceinline__ void dyn_push_warp(const StaticParams& P, const DynParams& D, int task, bool ready, int lane) {
+    const unsigned any = __ballot_sync(0xffffffffu, ready);
+    if (!any) return;
+    const int cls = ready ? __ldg(D.task_class + task) : 0;
+    for (int c = 0; c < 2; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, ready && cls == c);
+        if (!m) continue;
+        const int leader = __ffs(m) - 1;
+        unsigned int base = 0;
+        if (lane == leader) base = atomicAdd(&D.ctl->tail[c], static_cast<unsigned int>(__popc(m)));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (ready && cls == c) {
+            const unsigned int i = base + __popc(m & ((1u << lane) - 1u));
+            if (P.record) D.push_time[task] = globaltimer();
+            st_release(reinterpret_cast<uint32_t*>(D.slots + static_cast<long long>(c) * D.num_tasks + i),
+                       static_cast<uint32_t>(task + 1));
+        }
+    }
+    if (lane == 0) atomicAdd(&P.status->pushes, static_cast<unsigned long long>(__popc(any)));
+}
+
+__device__ __noinline__ void dyn_fire_warp(const StaticParams& P, const DynParams& D, int el, int lane) {
+    int first = 0;
+    if (lane == 0) first = atomicExch(&D.fired[el], 1u) == 0u;
+    if (!__shfl_sync(0xffffffffu, first, 0)) return;
+    const int cb = __ldg(D.consumer_off + el), ce = __ldg(D.consumer_off + el + 1);
+    for (int k0 = cb; k0 < ce; k0 += 32) {
+        const int k = k0 + lane;
+        const int c = k < ce ? __ldg(D.consumers + k) : -1;
+        const bool ready = c >= 0 && atomicSub(&D.rem[c], 1) == 1;
+        dyn_push_warp(P, D, c, ready, lane);
+    }
+    const int t = __ldg(D.el_dd + el);
+    if (t >= 0 && D.dd_range_call[t] >= 0) {
+        const int call = D.dd_range_call[t];
+        const int* ip = P.rt[__ldg(D.call_range_rt + call)];
+        const int g = el - D.dd_base[t];
+        const int first_task = __ldg(D.call_first_task + call);
+        const int lo = __ldcg(ip + g), hi = __ldcg(ip + g + 1);
+        for (int f0 = lo; f0 < hi; f0 += 32) {
+            const int f = f0 + lane;
+            const bool ready = f < hi && atomicSub(&D.rem[first_task + f], 1) == 1;
+            dyn_push_warp(P, D, first_task + f, ready, lane);
+        }
+    }
+}
+
+__device__ void dyn_reveal_warp(const StaticParams& P, const DynParams& D, int t, int lane) {
+    if (lane == 0) {
+        st_release(reinterpret_cast<uint32_t*>(&D.ctl->revealed[t]), 1u);
+        fence_sc_gpu();
+        const int rc = D.dd_range_call[t];
+        if (rc >= 0) {  // range-call tasks at or beyond indptr[last] never exist
+            const int* ip = P.rt[__ldg(D.call_range_rt + rc)];
+            const int live = __ldcg(ip + D.dd_count[t]);
+            long long worst = 1;
+            for (int d = 0, r = __ldg(P.call_rank + rc); d < r; ++d) worst *= __ldg(P.call_extents + rc * 4 + d);
+            const int first = __ldg(D.call_first_task + rc);
+            const int cls = __ldg(D.task_class + first);
+            atomicSub(&D.ctl->total[cls], static_cast<int>(worst - live));
+        }
+    }
+    __syncwarp();
+    for (int e0 = D.dd_base[t], e1 = D.dd_base[t] + D.dd_count[t]; e0 < e1; e0 += 32) {
+        const int el = e0 + lane;
+        bool f = false;
+        if (el < e1) {
+            const uint32_t need = dyn_init(P, D, el);
+            // an element that releases nothing (no static consumers, empty range) never needs to fire
+            bool releases = __ldg(D.consumer_off + el + 1) > __ldg(D.consumer_off + el);
+            const int rc = D.dd_range_call[t];
+            if (!releases && rc >= 0) {
+                const int* ip = P.rt[__ldg(D.call_range_rt + rc)];
+                const int g = el - D.dd_base[t];
+                releases = __ldcg(ip + g + 1) > __ldcg(ip + g);
+            }
+            if (releases) {
+                const uint32_t have = D.early_push ? ld_acquire(D.disp + el) : ld_acquire(P.cnt + el);
+                f = have >= need;
+            }
+        }
+        unsigned m = __ballot_sync(0xffffffffu, f);
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            dyn_fire_warp(P, D, e0 + b, lane);
+        }
+    }
+}
+
+__device__ void dyn_count_warp(const StaticParams& P, const DynParams& D, unsigned int* ctr, int el, bool may_fire,
+                               int worker, int task, int lane) {
+    int fire = 0;
+    if (lane == 0) {
+        const uint32_t old = atom_add_release(ctr + el, 1u);
+        const uint32_t need = dyn_init(P, D, el);
+        if (ctr == P.cnt && old >= need) report(P.status, ET_ERR_UNDERFLOW, worker, task, el, -1);
+        if (may_fire && old + 1 == need) {
+            fence_sc_gpu();
+            fire = dyn_visible(D, el);
+        }
+    }
+    if (__shfl_sync(0xffffffffu, fire, 0)) dyn_fire_warp(P, D, el, lane);
+}
+
 __device__ bool dyn_wait_el(const StaticParams& P, const DynParams& D, int el, int worker, int task) {
     const uint64_t t0 = globaltimer();
     uint32_t it = 0;
@@ -1343,7 +1463,8 @@ __device__ SlotView dyn_view(const StaticParams& P, const DynParams& D, int task
 
 // WAITs of a popped task (armed slots only, ref simulate.cpp:497-515), then the
 // early-push dispatch (ref simulate.cpp:600-618).
-__device__ bool dyn_prepare(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker) {
+__device__ bool dyn_prepare(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker,
+                            bool dispatch = true) {
     for (int w = v.wb; w < v.we; ++w)
         if (__ldg(D.task_wait_armed + w) && !dyn_wait_el(P, D, __ldg(D.task_waits + w), worker, task)) return false;
     const int rr = __ldg(D.call_range_rt + v.call);
@@ -1354,7 +1475,7 @@ __device__ bool dyn_prepare(const StaticParams& P, const DynParams& D, const Slo
         while (__ldcg(ip + g + 1) <= flat) ++g;
         if (!dyn_wait_el(P, D, __ldg(D.call_range_base + v.call) + g, worker, task)) return false;
     }
-    if (D.early_push) {
+    if (D.early_push && dispatch) {
         for (int n = v.nb; n < v.ne; ++n) dyn_count(P, D, D.disp, __ldg(D.task_notifies + n), true, worker, task);
         const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
         if (rel >= 0) dyn_count(P, D, D.disp, rel, true, worker, task);
@@ -1371,6 +1492,28 @@ __device__ void dyn_finish(const StaticParams& P, const DynParams& D, const Slot
     for (int n = v.nb; n < v.ne; ++n) dyn_count(P, D, P.cnt, __ldg(D.task_notifies + n), fire, worker, task);
     const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
     if (rel >= 0) dyn_count(P, D, P.cnt, rel, fire, worker, task);
+}
+
+// Warp-0 versions used by the consumer CTAs (the DMA warp keeps the scalar ones).
+__device__ void dyn_dispatch_warp(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker,
+                                  int lane) {
+    for (int n = v.nb; n < v.ne; ++n) dyn_count_warp(P, D, D.disp, __ldg(D.task_notifies + n), true, worker, task, lane);
+    const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+    if (rel >= 0) dyn_count_warp(P, D, D.disp, rel, true, worker, task, lane);
+}
+
+__device__ void dyn_finish_warp(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker,
+                                int lane) {
+    for (int t = 0; t < D.num_dd; ++t) {
+        if (D.dd_writer_call[t] != v.call) continue;
+        int last = 0;
+        if (lane == 0) last = atomicSub(&D.ctl->writer_rem[t], 1) == 1;
+        if (__shfl_sync(0xffffffffu, last, 0)) dyn_reveal_warp(P, D, t, lane);
+    }
+    const bool fire = !D.early_push;
+    for (int n = v.nb; n < v.ne; ++n) dyn_count_warp(P, D, P.cnt, __ldg(D.task_notifies + n), fire, worker, task, lane);
+    const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+    if (rel >= 0) dyn_count_warp(P, D, P.cnt, rel, fire, worker, task, lane);
 }
 
 __device__ void dyn_record(const StaticParams& P, const DynParams& D, int task, int worker, bool masked, uint64_t tb,
@@ -1390,6 +1533,7 @@ __device__ void dyn_record(const StaticParams& P, const DynParams& D, int task, 
     P.trace[task] = r;
 }
 
+template <bool kMoE>
 __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
     const int ctid = threadIdx.x;
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
@@ -1414,15 +1558,22 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
         if (task < 0) break;
         SlotView v = dyn_view(P, D, task);
         const et_op& op = P.ops[v.call];
-        if (ctid == 0) {
-            bool ok = dyn_prepare(P, D, v, task, worker);
-            if (ok && P.step_limit > 0 &&
-                atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
-                report(P.status, ET_ERR_STEP_LIMIT, worker, task, -1, 0);
-                ok = false;
+        if (ctid < 32) {
+            int ok = 1;
+            if (ctid == 0) {
+                ok = dyn_prepare(P, D, v, task, worker, false);
+                if (ok && P.step_limit > 0 &&
+                    atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
+                    report(P.status, ET_ERR_STEP_LIMIT, worker, task, -1, 0);
+                    ok = 0;
+                }
             }
-            misc[0] = ok ? 0 : 1;
-            tw = globaltimer();
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (ok && D.early_push) dyn_dispatch_warp(P, D, v, task, worker, ctid);
+            if (ctid == 0) {
+                misc[0] = ok ? 0 : 1;
+                tw = globaltimer();
+            }
         }
         bar_sync(1, kConsumers);
         if (misc[0]) break;
@@ -1451,16 +1602,20 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                 case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
-                case ET_OP_MOE_ROUTE: body_moe_route(P, op, v, xs, acc, red, ring, ctid, &tp); break;
-                case ET_OP_MOE_EXPERT: tp = body_moe_expert(P, op, v, xs, acc, ring, ctid); break;
+                case ET_OP_MOE_ROUTE:
+                    if constexpr (kMoE) body_moe_route(P, op, v, xs, acc, red, ring, ctid, &tp);
+                    break;
+                case ET_OP_MOE_EXPERT:
+                    if constexpr (kMoE) tp = body_moe_expert(P, op, v, xs, acc, ring, ctid);
+                    break;
                 default: break;
             }
         }
         bar_sync(1, kConsumers);
-        if (ctid == 0) {
-            te = globaltimer();
-            dyn_finish(P, D, v, task, worker);
-            dyn_record(P, D, task, worker, v.masked, tb, tw, tp, te);
+        if (ctid < 32) {
+            if (ctid == 0) te = globaltimer();
+            dyn_finish_warp(P, D, v, task, worker, ctid);
+            if (ctid == 0) dyn_record(P, D, task, worker, v.masked, tb, tw, tp, te);
         }
     }
     if (ctid == 0) {
@@ -1558,6 +1713,7 @@ __device__ void dyn_reset_state(const StaticParams& P, const DynParams& D, DynCt
     }
 }
 
+template <bool kMoE>
 __global__ void __launch_bounds__(kThreads, 1)
     et_dynamic_kernel(const __grid_constant__ StaticParams P, const __grid_constant__ DynParams D) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -1581,7 +1737,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     if (warp < kConsumerWarps) {
-        dyn_consumer_loop(P, D, worker, smem);
+        dyn_consumer_loop<kMoE>(P, D, worker, smem);
     } else if (warp == kProducerWarp) {
         dyn_producer_loop(P, D, worker, smem);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
@@ -1597,13 +1753,11 @@ __global__ void et_dynamic_reset_kernel(const __grid_constant__ StaticParams P, 
 
 int et_static_smem_bytes() { return etk::kSmemTotal; }
 
-// max_batch > 8 needs the tensor-memory (tcgen05) GEMV path, not in this build.
-int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, void* stream) {
-    if (max_batch > etk::kMaxBatch) return static_cast<int>(cudaErrorInvalidValue);
-    static bool configured = false;
+namespace {
+template <typename K>
+int launch_persistent(K kernel, bool& configured, int num_workers, void* stream, void** args) {
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(etk::et_static_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             etk::kSmemTotal);
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, etk::kSmemTotal);
         if (e != cudaSuccess) return static_cast<int>(e);
         configured = true;
     }
@@ -1619,28 +1773,24 @@ int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch,
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, etk::et_static_kernel, p));
+    return static_cast<int>(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(kernel), args));
+}
+}  // namespace
+
+// max_batch > 8 needs the tensor-memory (tcgen05) GEMV path, not in this build.
+int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, int moe, void* stream) {
+    if (max_batch > etk::kMaxBatch) return static_cast<int>(cudaErrorInvalidValue);
+    static bool conf[2] = {false, false};
+    void* args[] = {const_cast<etk::StaticParams*>(&p)};
+    return moe ? launch_persistent(etk::et_static_kernel<true>, conf[1], num_workers, stream, args)
+               : launch_persistent(etk::et_static_kernel<false>, conf[0], num_workers, stream, args);
 }
 
-int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, void* stream) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(etk::et_dynamic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             etk::kSmemTotal);
-        if (e != cudaSuccess) return static_cast<int>(e);
-        configured = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(num_workers);
-    cfg.blockDim = dim3(etk::kThreads);
-    cfg.dynamicSmemBytes = etk::kSmemTotal;
-    cfg.stream = static_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, etk::et_dynamic_kernel, p, d));
+int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, int moe, void* stream) {
+    static bool conf[2] = {false, false};
+    void* args[] = {const_cast<etk::StaticParams*>(&p), const_cast<etk::DynParams*>(&d)};
+    return moe ? launch_persistent(etk::et_dynamic_kernel<true>, conf[1], num_workers, stream, args)
+               : launch_persistent(etk::et_dynamic_kernel<false>, conf[0], num_workers, stream, args);
 }
 
 int et_dynamic_reset(const etk::StaticParams& p, const etk::DynParams& d, void* stream) {

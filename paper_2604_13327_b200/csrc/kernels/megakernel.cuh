@@ -24,7 +24,7 @@ constexpr int kStageBytes = 20480;
 constexpr int kXBytes = 32 * 1024;
 constexpr int kAccFloats = 2048;
 constexpr int kMaxSymbols = 8;
-constexpr int kMaxRuntime = 16;
+constexpr int kMaxRuntime = 512;  // runtime tensors per graph (6 per MoE layer)
 constexpr int kMaxRank = 4;
 constexpr int kMaxBatch = 8;   // GEMV batch rows carried in the mma M dimension
 
@@ -83,7 +83,7 @@ struct StaticParams {
     uint32_t* cnt_other;  // the other parity buffer: zeroed for the next step
     int cnt_capacity;
     int* const* rt;       // runtime tensors (device pointers)
-    long long rt_len[kMaxRuntime];
+    int rt_len[kMaxRuntime];  // elements at the binding
     int num_rt;
     const et_op* ops;
     et_trace_rec* trace;
@@ -162,7 +162,8 @@ struct DynParams {
 }  // namespace etk
 
 // Host-side launcher (megakernel.cu).
-int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, void* stream);
+// moe != 0 selects the instantiation that contains the MoE tile bodies
+int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, int moe, void* stream);
 int et_static_smem_bytes();
-int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, void* stream);
+int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, int moe, void* stream);
 int et_dynamic_reset(const etk::StaticParams& p, const etk::DynParams& d, void* stream);

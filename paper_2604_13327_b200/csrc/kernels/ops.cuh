@@ -38,8 +38,8 @@
 //   renormalised weights -- or, with flags bit 0, the host-injected topk -- then expert
 //   counts, exp_indptr (tiles of TS tokens, ref workloads.cpp:140-144), task_indptr
 //   (x RS), eoff (exclusive prefix of counts) and elist (slots by expert, stable).
-//   i6 = top_k, i10 = rt topk | rt counts << 8 | rt exp_indptr << 16 | rt elist << 24,
-//   i11 = rt eoff | rt task_indptr << 8, i12 = RS, i13 = TS; p0 = router weight (frag16
+//   i6 = top_k, i10 = index of the layer's first routing runtime tensor (in order topk,
+//   counts, exp_indptr, task_indptr, elist, eoff), i12 = RS, i13 = TS; p0 = router weight (frag16
 //   [E][H]), p2 = h (fp32 [b][H]), p3 = gamma, p4 = logits (fp32 [b][E]), p5 = xn out
 //   (bf16 [b][H]), p6 = slot weights out (fp32 [b*top_k]), p7 = arrival counter (int32)
 // ET_OP_MOE_EXPERT      task flat = tile * RS + r (range-triggered on task_indptr, extent_from):
@@ -47,7 +47,8 @@
 //   (IR = I / RS), then h[token] += w_slot * Wd_e[:, rows] act (red.global.add).
 //   i0 = I, i1 = H, i2 = RS, i3 = TS (<= 8), i4..i7 = rt exp_indptr, counts, elist, eoff,
 //   i8 = top_k, i10 = E; p0/p1 = Wgate/Wup (frag16 [E][I][H]), p2 = Wdown blocks (frag16
-//   [E][RS][H][IR]), p3 = xn (bf16 [b][H]), p4 = slot weights, p5 = h (fp32 [b][H])
+//   [E][RS][H][IR]), p3 = xn (bf16 [b][H]), p4 = slot weights, p5 = h (fp32 [b][H]),
+//   p6 = tile table (from ET_OP_MOE_ROUTE)
 // ET_OP_EMBED           task (0): h[b][:] = float(table[tokens[b]][:]) for every batch row
 //   i0 = hidden, i1 = batch symbol slot (-1: 1); p0 = table (bf16 [vocab][hidden]),
 //   p1 = token ids (int32 [b]), p2 = out (fp32 [b][hidden])
@@ -107,23 +108,17 @@ struct ExpertTask {
 };
 
 __device__ __forceinline__ ExpertTask expert_task(const et_op& op, int flat, int* const* rt) {
-    const int RS = op.i[2], TS = op.i[3];
-    const int* ind = rt[op.i[4]];
-    const int* cnt = rt[op.i[5]];
+    const int RS = op.i[2];
     const int* elist = rt[op.i[6]];
-    const int* eoff = rt[op.i[7]];
-    const int E = op.i[10];
     ExpertTask t;
     t.tile = flat / RS;
     t.r = flat - t.tile * RS;
-    int e = 0;
-    while (e + 1 < E && __ldcg(ind + e + 1) <= t.tile) ++e;
-    t.e = e;
-    const int i = t.tile - __ldcg(ind + e);
-    const int c = __ldcg(cnt + e) - i * TS;
-    t.ntok = c < TS ? c : TS;
-    const int base = __ldcg(eoff + e) + i * TS;
-    for (int j = 0; j < 8; ++j) t.slot[j] = j < t.ntok ? __ldcg(elist + base + j) : 0;
+    // (expert, first slot, tokens) of the tile, written by the route task
+    const int4 info = __ldcg(reinterpret_cast<const int4*>(op.p[6]) + t.tile);
+    t.e = info.x;
+    t.ntok = info.z;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t.slot[j] = j < t.ntok ? __ldcg(elist + info.y + j) : 0;
     return t;
 }
 

@@ -120,6 +120,7 @@ struct et_runtime {
 
     std::vector<Sample> samples;
     DevArray<et_op> d_ops;
+    int has_moe = 0;  // bound ops include MoE bodies: launch the MoE instantiation
     int ops_bound = 0;
 
     int mode = ET_MODE_STATIC;
@@ -410,6 +411,9 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     cudaSetDevice(rt->cfg.device);
     cudaStreamSynchronize(rt->stream);
     ET_CUDA(rt->d_ops.upload(ops, static_cast<size_t>(std::max(1, num_calls))), "bind ops");
+    rt->has_moe = 0;
+    for (int32_t c = 0; c < num_calls; ++c)
+        if (ops[c].kind == ET_OP_MOE_ROUTE || ops[c].kind == ET_OP_MOE_EXPERT) rt->has_moe = 1;
     rt->ops_bound = 1;
     return ET_OK;
 }
@@ -534,7 +538,7 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     p.num_rt = static_cast<int>(rt->d_rt.size());
     for (int i = 0; i < p.num_rt; ++i) {
         bool ok = true;
-        p.rt_len[i] = eval_host(rt->code_op, rt->code_arg, rt->rt_len_off[static_cast<size_t>(i)],
+        p.rt_len[i] = (int)eval_host(rt->code_op, rt->code_arg, rt->rt_len_off[static_cast<size_t>(i)],
                                 rt->rt_len_off[static_cast<size_t>(i) + 1], binding, &ok);
         if (!ok || p.rt_len[i] > rt->rt_capacity[static_cast<size_t>(i)])
             return rt->fail(ET_ERR_INVALID, "runtime tensor shape invalid at the binding");
@@ -584,9 +588,9 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     }
     if (synchronous) cudaEventRecord(rt->ev0, st);
     if (rt->mode == ET_MODE_DYNAMIC)
-        e = et_launch_dynamic(p, dp, S.num_queues, st);
+        e = et_launch_dynamic(p, dp, S.num_queues, rt->has_moe, st);
     else
-        e = et_launch_static(p, S.num_queues, rt->cfg.max_batch, st);
+        e = et_launch_static(p, S.num_queues, rt->cfg.max_batch, rt->has_moe, st);
     if (e != 0) return rt->cuda_fail(static_cast<cudaError_t>(e), "launch");
     if (synchronous) cudaEventRecord(rt->ev1, st);
     rt->parity ^= 1;

@@ -260,6 +260,7 @@ class MoEDecodeModel:
         self.xn = torch.zeros(cfg.layers, b, cfg.hidden, dtype=torch.bfloat16, device=dev)
         self.wslot = torch.zeros(cfg.layers, b * K, dtype=torch.float32, device=dev)
         self.arrive = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
+        self.tiles = torch.zeros(cfg.layers, b * K, 4, dtype=torch.int32, device=dev)  # expert tile table
         self.logits = torch.zeros(b, cfg.vocab, dtype=torch.float32, device=dev)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
         self.injected = False
@@ -297,18 +298,17 @@ class MoEDecodeModel:
             ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
             ops.append(make_op(OP_GEMV, i=[H, nq, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],
                                p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h)]))
-            rt_a = ri["topk"] | ri["cnt"] << 8 | ri["ind"] << 16 | ri["elist"] << 24
-            rt_b = ri["eoff"] | ri["tind"] << 8
-            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, -1, K, 16, 0, H, rt_a, rt_b, RS, TS],
+            assert [ri[n] for n in RT_PER_LAYER] == list(range(ri["topk"], ri["topk"] + len(RT_PER_LAYER)))
+            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, -1, K, 16, 0, H, ri["topk"], 0, RS, TS],
                                f=[cfg.eps],
                                p=[ptr(L["router"]), 0, ptr(self.h), ptr(L["ffn_norm"]), ptr(self.logits_r[l]),
-                                  ptr(self.xn[l]), ptr(self.wslot[l]), ptr(self.arrive[l:l + 1])],
+                                  ptr(self.xn[l]), ptr(self.wslot[l]), ptr(self.arrive[l:l + 1]), ptr(self.tiles[l])],
                                flags=1 if self.injected else 0))
             ops.append(make_op(OP_NONE))  # group: the routed notify is the Event Tensor edge itself
             ops.append(make_op(OP_MOE_EXPERT,
                                i=[cfg.expert_inter, H, RS, TS, ri["ind"], ri["cnt"], ri["elist"], ri["eoff"], K, 0, E],
                                p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(L["wdown"]), ptr(self.xn[l]), ptr(self.wslot[l]),
-                                  ptr(self.h)]))
+                                  ptr(self.h), ptr(self.tiles[l])]))
         ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
                            p=[ptr(W["lm_head"]), 0, ptr(self.h), ptr(W["final_norm"]), ptr(self.logits)]))
         return ops
