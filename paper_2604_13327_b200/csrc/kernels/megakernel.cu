@@ -499,6 +499,87 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     return t_pro;
 }
 
+// Merge of the splits of kv head g's q heads with the new token at position s
+// (K/V row s of the cache):
+//   O = (sum_c e^(m_c-M) o_c + e^(s_new-M) v_new) / (sum_c e^(m_c-M) l_c + e^(s_new-M)).
+// q (RoPE applied) is in shared memory (qs, row stride qstride).  Every global
+// operand -- split statistics, the new K/V row and this thread's o partials
+// (in registers, up to 16 splits per pass) -- is requested before the first
+// use, so a pass costs one L2 round trip.
+__device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op& op, int g, const float* qs,
+                                                 int qstride, float* scr, int ctid) {
+    constexpr int kPass = 16, kOut = 2;  // splits per pass; outputs per thread (G * dh <= 512)
+    const int warp = ctid >> 5, lane = ctid & 31;
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
+    const long long s = P.binding[op.i[4]];
+    const int nspl = static_cast<int>((s + CH - 1) / CH);
+    const float scale = op.f[0];
+    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);
+    const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + (static_cast<long long>(g) * cap + s) * dh;
+    const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + (static_cast<long long>(g) * cap + s) * dh;
+    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) + static_cast<long long>(g) * G * dh;
+    float* ml = scr;                    // [G][nspl][2]
+    float* wts = ml + 2 * G * nspl;     // [G][nspl]
+    float* hs = wts + G * nspl;         // [G]: weight of the new token
+    float* kns = hs + G;                // [dh]
+    float ov[kOut][kPass];
+    float vv[kOut];
+#pragma unroll
+    for (int j = 0; j < kOut; ++j) {
+        const int idx = ctid + j * kConsumers;
+        const int hh = idx / dh, d = idx - hh * dh;
+        vv[j] = idx < G * dh ? bf2f(__ldcg(vn + d)) : 0.f;
+#pragma unroll
+        for (int c = 0; c < kPass; ++c)
+            ov[j][c] = (idx < G * dh && c < nspl) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d)
+                                                 : 0.f;
+    }
+    for (int i = ctid; i < G * nspl; i += kConsumers) {
+        const float* pr = part + (static_cast<long long>(i / nspl) * maxs + i % nspl) * (dh + 2);
+        ml[2 * i] = __ldcg(pr);
+        ml[2 * i + 1] = __ldcg(pr + 1);
+    }
+    for (int d = ctid; d < dh; d += kConsumers) kns[d] = bf2f(__ldcg(kn + d));
+    bar_sync(1, kConsumers);
+    for (int hh = warp; hh < G; hh += kConsumerWarps) {
+        float dot = 0.f;
+        for (int d = lane; d < dh; d += 32) dot += qs[hh * qstride + d] * kns[d];
+        const float snew = warp_sum(dot) * scale;
+        float M = snew;
+        for (int c = lane; c < nspl; c += 32) M = fmaxf(M, ml[2 * (hh * nspl + c)]);
+        M = warp_max(M);
+        float L = 0.f;
+        for (int c = lane; c < nspl; c += 32) {
+            const float e = __expf(ml[2 * (hh * nspl + c)] - M);
+            wts[hh * nspl + c] = e;
+            L += e * ml[2 * (hh * nspl + c) + 1];
+        }
+        const float en = __expf(snew - M);
+        L = warp_sum(L) + en;
+        const float inv = 1.f / L;
+        for (int c = lane; c < nspl; c += 32) wts[hh * nspl + c] *= inv;
+        __syncwarp();
+        if (lane == 0) hs[hh] = en * inv;
+    }
+    bar_sync(1, kConsumers);
+#pragma unroll
+    for (int j = 0; j < kOut; ++j) {
+        const int idx = ctid + j * kConsumers;
+        if (idx >= G * dh) break;
+        const int hh = idx / dh, d = idx - hh * dh;
+        const float* w = wts + hh * nspl;
+        float o = hs[hh] * vv[j], o2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < kPass; c += 2) {
+            if (c < nspl) o = fmaf(w[c], ov[j][c], o);
+            if (c + 1 < nspl) o2 = fmaf(w[c + 1], ov[j][c + 1], o2);
+        }
+        for (int c = kPass; c < nspl; ++c)  // long contexts: the remaining splits
+            o = fmaf(w[c], __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d), o);
+        out[idx] = f2bf(o + o2);
+    }
+}
+
 // Qwen3-style per-head RMSNorm (weight w[dh]) followed by the pair rotation at
 // position pos, in place on one head vector in shared memory; one warp.
 __device__ __forceinline__ void qk_norm_rope(float* v, int dh, const float* w, float eps, const float* invf,
@@ -524,7 +605,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     const long long s = P.binding[op.i[4]];
     const int g = si.coord[0], c = si.coord[1];
     const long long p0 = static_cast<long long>(c) * CH;
-    const int np = static_cast<int>((p0 + CH < s ? p0 + CH : s) - p0);
+    const int np = p0 < s ? static_cast<int>((p0 + CH < s ? p0 + CH : s) - p0) : 0;
     const int qstride = dh + 4;          // padded rows: heads land on different banks
     const int nvec = dh / 8;             // 16-byte vectors per K/V row
     float* qs = scratch;                 // [G][dh+4]
@@ -539,80 +620,96 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     }
     bar_sync(1, kConsumers);
     const float scale = op.f[0];
-    const unsigned long long ck = ring.seq, cv = ring.seq + 1;
-    ring.seq += 2;
+    if (np > 0) {  // an empty split (s == 0, fused merge) only arrives
+        const unsigned long long ck = ring.seq, cv = ring.seq + 1;
+        ring.seq += 2;
 
-    // scores: one (position, head) dot product per thread; each position starts
-    // its walk over the row at a different 16-byte vector (bank rotation)
-    const uint8_t* kb = ring.wait(ck);
-    if (!kb) return;
-    for (int t = ctid; t < G * np; t += kConsumers) {
-        const int h = t % G, p = t / G;
-        const uint8_t* kr = kb + p * dh * 2;
-        const float* qh = qs + h * qstride;
-        float a0 = 0.f, a1 = 0.f;
-        for (int v = 0; v < nvec; ++v) {
-            const int vv = (v + p) & (nvec - 1);
-            const uint4 k8 = lds128(kr + vv * 16);
-            const float4 qa = *reinterpret_cast<const float4*>(qh + vv * 8);
-            const float4 qb = *reinterpret_cast<const float4*>(qh + vv * 8 + 4);
-            a0 = fmaf(bf16lo(k8.x), qa.x, a0);
-            a1 = fmaf(bf16hi(k8.x), qa.y, a1);
-            a0 = fmaf(bf16lo(k8.y), qa.z, a0);
-            a1 = fmaf(bf16hi(k8.y), qa.w, a1);
-            a0 = fmaf(bf16lo(k8.z), qb.x, a0);
-            a1 = fmaf(bf16hi(k8.z), qb.y, a1);
-            a0 = fmaf(bf16lo(k8.w), qb.z, a0);
-            a1 = fmaf(bf16hi(k8.w), qb.w, a1);
+        // scores: one (position, head) dot product per thread; each position starts
+        // its walk over the row at a different 16-byte vector (bank rotation)
+        const uint8_t* kb = ring.wait(ck);
+        if (!kb) return;
+        for (int t = ctid; t < G * np; t += kConsumers) {
+            const int h = t % G, p = t / G;
+            const uint8_t* kr = kb + p * dh * 2;
+            const float* qh = qs + h * qstride;
+            float a0 = 0.f, a1 = 0.f;
+            for (int v = 0; v < nvec; ++v) {
+                const int vv = (v + p) & (nvec - 1);
+                const uint4 k8 = lds128(kr + vv * 16);
+                const float4 qa = *reinterpret_cast<const float4*>(qh + vv * 8);
+                const float4 qb = *reinterpret_cast<const float4*>(qh + vv * 8 + 4);
+                a0 = fmaf(bf16lo(k8.x), qa.x, a0);
+                a1 = fmaf(bf16hi(k8.x), qa.y, a1);
+                a0 = fmaf(bf16lo(k8.y), qa.z, a0);
+                a1 = fmaf(bf16hi(k8.y), qa.w, a1);
+                a0 = fmaf(bf16lo(k8.z), qb.x, a0);
+                a1 = fmaf(bf16hi(k8.z), qb.y, a1);
+                a0 = fmaf(bf16lo(k8.w), qb.z, a0);
+                a1 = fmaf(bf16hi(k8.w), qb.w, a1);
+            }
+            sc[h * CH + p] = (a0 + a1) * scale;
         }
-        sc[h * CH + p] = (a0 + a1) * scale;
-    }
-    bar_sync(1, kConsumers);
-    if (ctid == Ring::owner(ck) * 32) ring.release(ck);
+        bar_sync(1, kConsumers);
+        if (ctid == Ring::owner(ck) * 32) ring.release(ck);
 
-    // softmax statistics per head (warp h), probabilities in place
-    float* part = reinterpret_cast<float*>(op.p[3]);
-    for (int h = warp; h < G; h += kConsumerWarps) {
-        float m = -INFINITY;
-        for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
-        m = warp_max(m);
-        float l = 0.f;
-        for (int p = lane; p < np; p += 32) {
-            const float e = __expf(sc[h * CH + p] - m);
-            sc[h * CH + p] = e;
-            l += e;
+        // softmax statistics per head (warp h), probabilities in place
+        float* part = reinterpret_cast<float*>(op.p[3]);
+        for (int h = warp; h < G; h += kConsumerWarps) {
+            float m = -INFINITY;
+            for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
+            m = warp_max(m);
+            float l = 0.f;
+            for (int p = lane; p < np; p += 32) {
+                const float e = __expf(sc[h * CH + p] - m);
+                sc[h * CH + p] = e;
+                l += e;
+            }
+            l = warp_sum(l);
+            if (lane == 0) {
+                float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2);
+                pr[0] = m;
+                pr[1] = l;
+            }
         }
-        l = warp_sum(l);
-        if (lane == 0) {
-            float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2);
-            pr[0] = m;
-            pr[1] = l;
-        }
-    }
-    bar_sync(1, kConsumers);
+        bar_sync(1, kConsumers);
 
-    // o = P V: one (head, dim pair) per thread
-    const uint8_t* vb = ring.wait(cv);
-    if (!vb) return;
-    const uint32_t* v2 = reinterpret_cast<const uint32_t*>(vb);
-    const int half = dh / 2;
-    for (int idx = ctid; idx < G * half; idx += kConsumers) {
-        const int h = idx / half, dp = idx % half;
-        const float* ph = sc + h * CH;
-        float o0 = 0.f, o1 = 0.f;
-#pragma unroll 8
-        for (int p = 0; p < np; ++p) {
-            const uint32_t vv = v2[p * half + dp];
-            const float w = ph[p];
-            o0 = fmaf(w, bf16lo(vv), o0);
-            o1 = fmaf(w, bf16hi(vv), o1);
+        // o = P V: one (head, dim pair) per thread
+        const uint8_t* vb = ring.wait(cv);
+        if (!vb) return;
+        const uint32_t* v2 = reinterpret_cast<const uint32_t*>(vb);
+        const int half = dh / 2;
+        for (int idx = ctid; idx < G * half; idx += kConsumers) {
+            const int h = idx / half, dp = idx % half;
+            const float* ph = sc + h * CH;
+            float o0 = 0.f, o1 = 0.f;
+    #pragma unroll 8
+            for (int p = 0; p < np; ++p) {
+                const uint32_t vv = v2[p * half + dp];
+                const float w = ph[p];
+                o0 = fmaf(w, bf16lo(vv), o0);
+                o1 = fmaf(w, bf16hi(vv), o1);
+            }
+            float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2) + 2 + 2 * dp;
+            pr[0] = o0;
+            pr[1] = o1;
         }
-        float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2) + 2 + 2 * dp;
-        pr[0] = o0;
-        pr[1] = o1;
+        bar_sync(1, kConsumers);
+        if (ctid == Ring::owner(cv) * 32) ring.release(cv);
     }
-    bar_sync(1, kConsumers);
-    if (ctid == Ring::owner(cv) * 32) ring.release(cv);
+    if (op.flags & 2) {  // fused merge: the split of group g that arrives last merges it
+        volatile int* flag = reinterpret_cast<volatile int*>(sc + G * CH);
+        if (ctid == 0) {
+            int* arrive = reinterpret_cast<int*>(op.p[5]) + g;
+            const int ntask = s > 0 ? static_cast<int>((s + CH - 1) / CH) : 1;  // grid max(ceil(s/CH), 1)
+            // release: this split's partial (CTA writes ordered by the bar above) before
+            // the arrival; acquire: the other splits' partials after it
+            const bool last = atom_add_acq_rel(arrive, 1) == ntask - 1;
+            if (last) *reinterpret_cast<volatile int*>(arrive) = 0;  // every split of this step arrived
+            *flag = last ? 1 : 0;
+        }
+        bar_sync(1, kConsumers);
+        if (*flag) attn_merge_group(P, op, g, qs, qstride, sc + G * CH + 4, ctid);
+    }
 }
 
 // Merge of the splits of one kv head's q heads with the new token at s:
@@ -1004,7 +1101,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                     }
                     t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid);
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_MOE_ROUTE:
@@ -1599,7 +1696,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     }
                     tp = body_gemv(P, op, v, xs, acc, red, ring, ctid);
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, acc, ring, ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_MOE_ROUTE:

@@ -26,6 +26,9 @@
 // ET_OP_ATTN_MERGE      task (g): merges the splits and the new token at position s
 //   (K/V row s of the cache) for the group's q heads; same i/p as ATTN_SPLIT plus
 //   p4 = out (bf16 [q_heads*head_dim])
+// ATTN_SPLIT flags bit 1 (fused merge): p4 = out, p5 = arrival counters (int32 [kv_heads], zero
+//   between steps; the merger resets them); grid [kv, max(ceil(s/CH), 1)]; the split of
+//   group g that arrives last runs the ATTN_MERGE body for g (no merge stage, one hop less).
 // ATTN flags bit 0 (Qwen3 q/k-norm): q at p0 is the raw projection; SPLIT and MERGE apply
 //   the per-head RMSNorm (p5 = q-norm weight, p6 = k-norm weight, fp32 [head_dim], f1 = eps)
 //   and RoPE (p7 = inverse frequencies) themselves; MERGE also normalises + rotates the raw

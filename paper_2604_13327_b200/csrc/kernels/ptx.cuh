@@ -79,6 +79,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// Acquire-release fetch-add at gpu scope: orders this thread's (and, through a
+// preceding bar.sync, the CTA's) prior writes before the add, and later reads
+// after it -- one instruction instead of fence + atomic + fence.
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 // Non-blocking probe of an mbarrier phase (no suspend).
 __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;

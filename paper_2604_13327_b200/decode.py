@@ -96,8 +96,8 @@ LLAMA3_70B = DecoderConfig("llama3-70b", hidden=8192, layers=80, heads=64, kv_he
 CONFIGS = {c.name: c for c in (TINY, LLAMA3_8B, LLAMA3_70B)}
 
 
-def build_graph(cfg, tasks, lm_tasks):
-    return etsim.Graph.from_json(json.dumps(graph_spec(cfg, tasks, lm_tasks)))
+def build_graph(cfg, tasks, lm_tasks, fused_merge=False):
+    return etsim.Graph.from_json(json.dumps(graph_spec(cfg, tasks, lm_tasks, fused_merge)))
 
 
 def rope_inv_freq(cfg):
@@ -177,7 +177,7 @@ class DecodeModel:
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
-                 l2_prefetch=-1, residual="split"):
+                 l2_prefetch=-1, residual="split", fused_merge=True):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -193,7 +193,8 @@ class DecodeModel:
 
         import time
         t0 = time.perf_counter()
-        self.graph = build_graph(cfg, self.tasks, self.lm_tasks)
+        self.fused_merge = fused_merge
+        self.graph = build_graph(cfg, self.tasks, self.lm_tasks, fused_merge)
         self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3
 
@@ -212,6 +213,7 @@ class DecodeModel:
         self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=dev)
         self.h_b = torch.zeros_like(self.h_a) if residual == "double" else self.h_a
         self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        self.arrive = torch.zeros(cfg.layers, cfg.kv_heads, dtype=torch.int32, device=dev)  # split arrivals (fused merge)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
 
         t1 = time.perf_counter()
@@ -235,10 +237,12 @@ class DecodeModel:
                                f=[cfg.eps], p=[ptr(L["wqkv"]), 0, ptr(self.h_a), ptr(L["attn_norm"]), ptr(self.q), 0,
                                                ptr(kc), ptr(vc), ptr(self.inv_freq)]))
             attn_i = [dh, G, CH, self.capacity, s_slot, self.max_splits, cfg.kv_heads]
-            ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale],
-                               p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials)]))
-            ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale],
-                               p=[ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn)]))
+            attn_p = [ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(self.arrive[l])]
+            if self.fused_merge:  # flags bit 1: the last split of a kv head merges it
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p, flags=2))
+            else:
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p))
+                ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale], p=attn_p))
             if self.residual == "split":
                 # row-parallel products add into the residual stream in place: split-K
                 # spans (every task streams the same bytes), red.global.add epilogue

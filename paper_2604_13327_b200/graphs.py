@@ -4,7 +4,7 @@ fixture generator can build the same graphs for the reference implementation.
 """
 
 
-def graph_spec(cfg, tasks: int, lm_tasks: int):
+def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False):
     """Reference-format graph spec of one decode step (symbol `s`)."""
     CH = cfg.attn_chunk
     fns, events, calls = [], [], []
@@ -33,8 +33,12 @@ def graph_spec(cfg, tasks: int, lm_tasks: int):
         qkv, a, m, o, g, d = (ev(f"{x}{l}", ["1"]) for x in ("QKV", "A", "M", "O", "G", "D"))
         events[-5]["shape"] = [kv]  # A_l has one element per kv head
         call(fn(f"L{l}.qkv", [T]), ins=[(prev, ["0"])], outs=[(qkv, ["0"])])
-        call(fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
-        call(fn(f"L{l}.merge", [kv]), ins=[(a, ["t0"]), (qkv, ["0"])], outs=[(m, ["0"])])
+        if fused_merge:  # the last split of each kv head merges the group (no merge stage)
+            events.remove(next(e for e in events if e["name"] == a))
+            call(fn(f"L{l}.attn", [kv, f"max((s + {CH - 1}) // {CH}, 1)"]), ins=[(qkv, ["0"])], outs=[(m, ["0"])])
+        else:
+            call(fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
+            call(fn(f"L{l}.merge", [kv]), ins=[(a, ["t0"]), (qkv, ["0"])], outs=[(m, ["0"])])
         call(fn(f"L{l}.oproj", [T]), ins=[(m, ["0"])], outs=[(o, ["0"])])
         call(fn(f"L{l}.gateup", [T]), ins=[(o, ["0"])], outs=[(g, ["0"])])
         call(fn(f"L{l}.down", [T]), ins=[(g, ["0"])], outs=[(d, ["0"])])
