@@ -216,7 +216,21 @@ def run_ours(args):
 
     t_start = time.perf_counter()
     cfg = CONFIGS[args.config]
-    model = DecodeModel(cfg, device=f"cuda:{local}", samples=tuple(args.samples), seed=0)
+    tp_mode = args.tp > 0 or cfg.name == "llama3-70b"
+    tp = args.tp or world
+    if tp_mode:
+        # tensor parallel over all ranks: in-megakernel NVLink allreduce tasks;
+        # NCCL (torch.distributed) only exchanges the peer buffers' IPC handles
+        from paper_2604_13327_b200.tp import TPDecodeModel, exchange_peers
+
+        assert tp == world, "tensor parallelism spans every rank of the launch"
+        model = TPDecodeModel(cfg, rank, world, device=f"cuda:{local}", samples=tuple(args.samples), seed=0)
+        peers = exchange_peers(model.local_buffers(), rank, world) if world > 1 else [model.local_buffers()]
+        model.connect(peers)
+        model.vocab_local = model.local.vocab
+    else:
+        model = DecodeModel(cfg, device=f"cuda:{local}", samples=tuple(args.samples), seed=0)
+        model.vocab_local = cfg.vocab
     model.fill_cache(args.seq, seed=1)
     model.set_token(1)
     # a dedicated (non-default) stream: the executor launches on exactly this
@@ -266,7 +280,7 @@ def run_ours(args):
 
     # ---- end-to-end through the public API (host buffers) ------------------------
     tok_host = torch.ones(1, dtype=torch.int32).pin_memory()
-    logits_host = torch.empty(1, cfg.vocab, dtype=torch.float32).pin_memory()
+    logits_host = torch.empty(1, model.vocab_local, dtype=torch.float32).pin_memory()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -285,9 +299,11 @@ def run_ours(args):
 
     peak, peak_src = measured_peak()
     step_bytes = cfg.step_bytes(args.seq)
+    if tp_mode:  # per-GPU algorithmic bytes: the rank's weight shard plus its kv heads' cache
+        step_bytes = model.local.step_bytes(args.seq)
     med_ms = statistics.median(step_ms)
     achieved = step_bytes / (med_ms * 1e-3) / 1e9
-    tokens_total = args.steps * world
+    tokens_total = args.steps * (1 if tp_mode else world)  # TP: all ranks serve one token per step
     value = total_ms * 1e3 / tokens_total
     line = None
     if rank == 0:
@@ -303,11 +319,13 @@ def run_ours(args):
                    "detail": detail}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+            "scaling": "strong" if tp_mode else "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init bf16 weights N(0,0.02), KV cache N(0,1) for positions [0,s))",
             "config": {"workload": f"{cfg.name} decode bs=1 seq {args.seq}", "seq_len": args.seq, "batch": 1,
-                       "samples": list(args.samples), "parallelism": f"replicas{world}",
+                       "samples": list(args.samples),
+                       "parallelism": f"tp{world}" if tp_mode else f"replicas{world}",
                        "l2": "inputs larger than L2 (15 GB of weights per step), no flush",
                        "step_us_median": med_ms * 1e3, "step_us_p10": sorted(step_ms)[len(step_ms) // 10] * 1e3,
                        "step_us_p90": sorted(step_ms)[(len(step_ms) * 9) // 10] * 1e3,
@@ -320,7 +338,7 @@ def run_ours(args):
                          "frac_of_8TBps": achieved / 8000.0},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_ms * 1e3 / tokens_total, "unit": UNIT, "h2d_bytes_per_step": 4,
-                    "d2h_bytes_per_step": 4 * cfg.vocab},
+                    "d2h_bytes_per_step": 4 * model.vocab_local},
             "gpu_launches": args.steps,
             "clocks": clocks.summary(),
         }
@@ -341,6 +359,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--count-tasks", action="store_true")
+    ap.add_argument("--tp", type=int, default=0, help="tensor-parallel degree (default: world for llama3-70b, else 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -240,6 +240,16 @@ int et_read_counters(et_runtime* rt, int64_t* out, int64_t n);
 /* Trace of the last step: fills up to *n records and sets *n to the count. */
 int et_read_trace(et_runtime* rt, et_trace_rec* out, int64_t* n);
 
+/* Peer memory for tensor parallelism (setup only; the handles are exchanged by
+ * the caller, e.g. over torch.distributed).  The row-parallel allreduce task
+ * (ET_OP_ALLREDUCE) then reads peers' partials and stores peers' Event Tensor
+ * flags through these mappings over NVLink -- no NCCL on the data path.  The
+ * reference has no counterpart (it models TP only as task graphs, ref
+ * workloads.cpp:30-79; SPEC.md:8 excludes multi-GPU). */
+int et_ipc_get_handle(const void* dev_ptr, void* handle /* 64 bytes */);
+int et_ipc_open_handle(const void* handle /* 64 bytes */, int32_t device, void** dev_ptr);
+int et_ipc_close_handle(void* dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

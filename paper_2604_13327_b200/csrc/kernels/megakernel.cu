@@ -1020,6 +1020,62 @@ __device__ uint64_t body_moe_expert(const StaticParams& P, const et_op& op, cons
     return t_pro;
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-parallel allreduce task (row-parallel output projection / down
+// projection).  Every rank wrote its partial product of the stage into its own
+// `part` slot (EPI_F32); this task adds the partials of all TP ranks into rows
+// [r0, r1) of the local residual stream.  The cross-GPU dependency is an Event
+// Tensor element per (stage slot, source rank) living in each destination
+// rank's memory: the first allreduce task of a rank to run (its local stage is
+// complete -- the task waited on it) stores the step epoch into that element
+// on every rank with st.release.sys; every task spins with ld.acquire.sys until
+// all TP sources reached the epoch, then reads the peers' partials over NVLink.
+// Epochs (the step id, identical on all ranks) make resets unnecessary.
+__device__ void body_allreduce(const StaticParams& P, const et_op& op, const SlotView& si, int ctid, int worker) {
+    const int H = op.i[0], TP = op.i[1], rank = op.i[2], slot = op.i[3];
+    const uint32_t epoch = static_cast<uint32_t>(P.step_id);
+    float* h = reinterpret_cast<float*>(op.p[0]);
+    uint32_t* flags = reinterpret_cast<uint32_t*>(op.p[1]);          // local [slots][TP]
+    uint32_t* once = reinterpret_cast<uint32_t*>(op.p[2]);           // local [slots]
+    const unsigned long long* peers = reinterpret_cast<const unsigned long long*>(op.p[3]);  // [TP][2]: part, flags
+    if (ctid == 0 && atomicMax(once + slot, epoch) < epoch) {
+        for (int p = 0; p < TP; ++p) {
+            uint32_t* pf = reinterpret_cast<uint32_t*>(__ldg(peers + 2 * p + 1)) + slot * TP + rank;
+            st_release_sys(pf, epoch);
+        }
+    }
+    if (ctid < TP) {
+        const uint32_t* f = flags + slot * TP + ctid;
+        const uint64_t t0 = globaltimer();
+        uint32_t it = 0;
+        while (static_cast<int>(ld_acquire_sys(f) - epoch) < 0) {
+            if ((++it & 255u) == 0) {
+                if (aborted(P.status)) break;
+                if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                    report(P.status, ET_ERR_DEADLOCK, worker, -5, slot * TP + ctid, static_cast<int>(epoch));
+                    break;
+                }
+            }
+        }
+    }
+    bar_sync(1, kConsumers);
+    const int T = si.ext0, t = si.coord[0];
+    const int n4 = H / 4;
+    const int a = static_cast<int>(static_cast<long long>(t) * n4 / T), b = static_cast<int>(static_cast<long long>(t + 1) * n4 / T);
+    for (int i = a + ctid; i < b; i += kConsumers) {
+        float4 acc = ldcg_f4(h + 4 * i);
+        for (int p = 0; p < TP; ++p) {
+            const float* part = reinterpret_cast<const float*>(__ldg(peers + 2 * p)) + static_cast<long long>(slot) * H;
+            const float4 v = ld_cv_f4(part + 4 * i);
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        *reinterpret_cast<float4*>(h + 4 * i) = acc;
+    }
+}
+
 __device__ void body_embed(const StaticParams& P, const et_op& op, int ctid) {
     const int H = op.i[0];
     const int nb = op.i[1] >= 0 ? static_cast<int>(P.binding[op.i[1]]) : 1;
@@ -1104,6 +1160,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
+                case ET_OP_ALLREDUCE: body_allreduce(P, op, v, ctid, worker); break;
                 case ET_OP_MOE_ROUTE:
                     if constexpr (kMoE) body_moe_route(P, op, v, xs, acc, red, ring, ctid, &t_pro);
                     break;

@@ -52,6 +52,12 @@
 //   i8 = top_k, i10 = E; p0/p1 = Wgate/Wup (frag16 [E][I][H]), p2 = Wdown blocks (frag16
 //   [E][RS][H][IR]), p3 = xn (bf16 [b][H]), p4 = slot weights, p5 = h (fp32 [b][H]),
 //   p6 = tile table (from ET_OP_MOE_ROUTE)
+// ET_OP_ALLREDUCE       task t of T (static scheduler): h[r0:r1] += sum over TP ranks of their
+//   stage partials (rows split evenly over the T tasks); cross-GPU Event Tensor elements
+//   flags[slot][src] (epoch = step id; st.release.sys / ld.acquire.sys).
+//   i0 = H, i1 = TP, i2 = this rank, i3 = slot (stage index); p0 = h (fp32 [H]),
+//   p1 = local flags (uint32 [slots][TP]), p2 = local once-counters (uint32 [slots]),
+//   p3 = peer table (uint64 [TP][2]: rank p's part buffer base (fp32 [slots][H]), its flags)
 // ET_OP_EMBED           task (0): h[b][:] = float(table[tokens[b]][:]) for every batch row
 //   i0 = hidden, i1 = batch symbol slot (-1: 1); p0 = table (bf16 [vocab][hidden]),
 //   p1 = token ids (int32 [b]), p2 = out (fp32 [b][hidden])

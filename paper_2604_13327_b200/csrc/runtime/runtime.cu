@@ -637,3 +637,25 @@ int et_read_trace(et_runtime* rt, et_trace_rec* out, int64_t* n) {
 }
 
 }  // extern "C"
+
+int et_ipc_get_handle(const void* dev_ptr, void* handle) {
+    if (!dev_ptr || !handle) return ET_ERR_INVALID;
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)) != cudaSuccess) return ET_ERR_CUDA;
+    std::memcpy(handle, &h, sizeof(h));
+    return ET_OK;
+}
+
+int et_ipc_open_handle(const void* handle, int32_t device, void** dev_ptr) {
+    if (!handle || !dev_ptr) return ET_ERR_INVALID;
+    cudaSetDevice(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    if (cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return ET_ERR_CUDA;
+    return ET_OK;
+}
+
+int et_ipc_close_handle(void* dev_ptr) {
+    return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? ET_OK : ET_ERR_CUDA;
+}

@@ -139,8 +139,10 @@ def device_layout(W, keep_logical=False):
     return D
 
 
-def init_weights(cfg: DecoderConfig, device, seed=0, std=0.02):
-    """Random-init weights of the architecture (bf16, N(0, std)); norms ~ 1 + N(0, 0.01)."""
+def init_weights(cfg: DecoderConfig, device, seed=0, std=0.02, layer_hook=None):
+    """Random-init weights of the architecture (bf16, N(0, std)); norms ~ 1 + N(0, 0.01).
+    `layer_hook(d)` (optional) may replace each layer dict as soon as it is drawn
+    (tensor-parallel ranks keep only their shard; the draw order is unchanged)."""
     g = torch.Generator(device=device)
     g.manual_seed(seed)
 
@@ -155,8 +157,10 @@ def init_weights(cfg: DecoderConfig, device, seed=0, std=0.02):
         return t
 
     W = {"embed": w(cfg.vocab, cfg.hidden), "final_norm": norm(), "lm_head": w(cfg.vocab, cfg.hidden), "layers": []}
+    if layer_hook is not None:
+        W = layer_hook(W)
     for _ in range(cfg.layers):
-        W["layers"].append({
+        d = {
             "attn_norm": norm(),
             "wqkv": w(cfg.q_rows + 2 * cfg.kv_rows, cfg.hidden),
             "wo": w(cfg.hidden, cfg.q_rows),
@@ -164,7 +168,8 @@ def init_weights(cfg: DecoderConfig, device, seed=0, std=0.02):
             "wgate": w(cfg.intermediate, cfg.hidden),
             "wup": w(cfg.intermediate, cfg.hidden),
             "wdown": w(cfg.hidden, cfg.intermediate),
-        })
+        }
+        W["layers"].append(layer_hook(d) if layer_hook is not None else d)
     return W
 
 

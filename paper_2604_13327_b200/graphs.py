@@ -4,7 +4,7 @@ fixture generator can build the same graphs for the reference implementation.
 """
 
 
-def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False):
+def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allreduce_tasks: int = 0):
     """Reference-format graph spec of one decode step (symbol `s`)."""
     CH = cfg.attn_chunk
     fns, events, calls = [], [], []
@@ -40,8 +40,16 @@ def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False):
             call(fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
             call(fn(f"L{l}.merge", [kv]), ins=[(a, ["t0"]), (qkv, ["0"])], outs=[(m, ["0"])])
         call(fn(f"L{l}.oproj", [T]), ins=[(m, ["0"])], outs=[(o, ["0"])])
+        if allreduce_tasks:  # tensor parallel: row-parallel partials summed across ranks
+            ao = ev(f"AO{l}", ["1"])
+            call(fn(f"L{l}.ar_o", [str(allreduce_tasks)]), ins=[(o, ["0"])], outs=[(ao, ["0"])])
+            o = ao
         call(fn(f"L{l}.gateup", [T]), ins=[(o, ["0"])], outs=[(g, ["0"])])
         call(fn(f"L{l}.down", [T]), ins=[(g, ["0"])], outs=[(d, ["0"])])
+        if allreduce_tasks:
+            ad = ev(f"AD{l}", ["1"])
+            call(fn(f"L{l}.ar_d", [str(allreduce_tasks)]), ins=[(d, ["0"])], outs=[(ad, ["0"])])
+            d = ad
         prev = d
     ev("LM", ["1"])
     call(fn("lm_head", [str(lm_tasks)]), ins=[(prev, ["0"])], outs=[("LM", ["0"])])
