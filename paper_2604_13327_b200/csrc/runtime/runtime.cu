@@ -474,9 +474,11 @@ static int collect(et_runtime* rt, et_step_info* info) {
         cudaMemset(rt->d_cnt.ptr, 0, rt->d_cnt.n * sizeof(uint32_t));
         cudaMemset(rt->d_status.ptr, 0, 2 * sizeof(etk::DevStatus));
         rt->prepared[0] = rt->prepared[1] = -1;
-        rt->err = st.code == ET_ERR_DEADLOCK    ? "deadlock"
-                  : st.code == ET_ERR_UNDERFLOW ? "counter underflow"
-                                                : "step limit exceeded";
+        rt->err = st.code == ET_ERR_DEADLOCK     ? "deadlock"
+                  : st.code == ET_ERR_UNDERFLOW  ? "counter underflow"
+                  : st.code == ET_ERR_STEP_LIMIT ? "step limit exceeded"
+                                                 : "invalid tile operation (a GEMV's activations exceed shared "
+                                                   "memory: batch * K * 2 > 32 KB, or batch > 8)";
         return st.code;
     }
     return ET_OK;

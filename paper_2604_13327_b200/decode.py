@@ -96,8 +96,22 @@ LLAMA3_70B = DecoderConfig("llama3-70b", hidden=8192, layers=80, heads=64, kv_he
 CONFIGS = {c.name: c for c in (TINY, LLAMA3_8B, LLAMA3_70B)}
 
 
-def build_graph(cfg, tasks, lm_tasks, fused_merge=False):
-    return etsim.Graph.from_json(json.dumps(graph_spec(cfg, tasks, lm_tasks, fused_merge)))
+def build_graph(cfg, tasks, lm_tasks, fused_merge=False, call_tasks=None):
+    return etsim.Graph.from_json(json.dumps(graph_spec(cfg, tasks, lm_tasks, fused_merge, call_tasks=call_tasks)))
+
+
+def balanced_tasks(rows, workers, tile=16):
+    """Largest task count <= workers that splits rows into equal whole tiles (a stage
+    ends with its slowest task: 384 tiles over 148 tasks leaves 3-tile tasks beside
+    2-tile ones, over 128 tasks every task streams 3 tiles)."""
+    tiles = rows // tile
+    best = workers
+    for t in range(workers, max(1, workers // 2) - 1, -1):
+        if tiles % t == 0:
+            return t
+        if tiles / t <= 1:
+            continue
+    return best
 
 
 def rope_inv_freq(cfg):
@@ -182,7 +196,7 @@ class DecodeModel:
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
-                 l2_prefetch=-1, residual="split", fused_merge=True):
+                 l2_prefetch=-1, residual="split", fused_merge=True, balance=True):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -199,7 +213,14 @@ class DecodeModel:
         import time
         t0 = time.perf_counter()
         self.fused_merge = fused_merge
-        self.graph = build_graph(cfg, self.tasks, self.lm_tasks, fused_merge)
+        self.call_tasks = None
+        if balance:  # whole-row GEMVs get a task count that divides their row tiles evenly
+            self.call_tasks = {"qkv": balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.tasks),
+                               "gateup": balanced_tasks(cfg.intermediate, self.tasks)}
+            if residual == "double":  # whole-row residual GEMVs too (split-K spans are balanced already)
+                self.call_tasks.update(oproj=balanced_tasks(cfg.hidden, self.tasks),
+                                       down=balanced_tasks(cfg.hidden, self.tasks))
+        self.graph = build_graph(cfg, self.tasks, self.lm_tasks, fused_merge, self.call_tasks)
         self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3
 

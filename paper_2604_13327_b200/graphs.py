@@ -4,7 +4,8 @@ fixture generator can build the same graphs for the reference implementation.
 """
 
 
-def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allreduce_tasks: int = 0):
+def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allreduce_tasks: int = 0,
+               call_tasks=None):
     """Reference-format graph spec of one decode step (symbol `s`)."""
     CH = cfg.attn_chunk
     fns, events, calls = [], [], []
@@ -26,26 +27,27 @@ def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allred
         calls.append(c)
 
     T, kv = str(tasks), str(cfg.kv_heads)
+    ct = {k: str(v) for k, v in (call_tasks or {}).items()}  # per-call task counts (whole-tile balance)
     ev("EMB", ["1"])
     call(fn("embed", ["1"]), outs=[("EMB", ["0"])])
     prev = "EMB"
     for l in range(cfg.layers):
         qkv, a, m, o, g, d = (ev(f"{x}{l}", ["1"]) for x in ("QKV", "A", "M", "O", "G", "D"))
         events[-5]["shape"] = [kv]  # A_l has one element per kv head
-        call(fn(f"L{l}.qkv", [T]), ins=[(prev, ["0"])], outs=[(qkv, ["0"])])
+        call(fn(f"L{l}.qkv", [ct.get("qkv", T)]), ins=[(prev, ["0"])], outs=[(qkv, ["0"])])
         if fused_merge:  # the last split of each kv head merges the group (no merge stage)
             events.remove(next(e for e in events if e["name"] == a))
             call(fn(f"L{l}.attn", [kv, f"max((s + {CH - 1}) // {CH}, 1)"]), ins=[(qkv, ["0"])], outs=[(m, ["0"])])
         else:
             call(fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
             call(fn(f"L{l}.merge", [kv]), ins=[(a, ["t0"]), (qkv, ["0"])], outs=[(m, ["0"])])
-        call(fn(f"L{l}.oproj", [T]), ins=[(m, ["0"])], outs=[(o, ["0"])])
+        call(fn(f"L{l}.oproj", [ct.get("oproj", T)]), ins=[(m, ["0"])], outs=[(o, ["0"])])
         if allreduce_tasks:  # tensor parallel: row-parallel partials summed across ranks
             ao = ev(f"AO{l}", ["1"])
             call(fn(f"L{l}.ar_o", [str(allreduce_tasks)]), ins=[(o, ["0"])], outs=[(ao, ["0"])])
             o = ao
-        call(fn(f"L{l}.gateup", [T]), ins=[(o, ["0"])], outs=[(g, ["0"])])
-        call(fn(f"L{l}.down", [T]), ins=[(g, ["0"])], outs=[(d, ["0"])])
+        call(fn(f"L{l}.gateup", [ct.get("gateup", T)]), ins=[(o, ["0"])], outs=[(g, ["0"])])
+        call(fn(f"L{l}.down", [ct.get("down", T)]), ins=[(g, ["0"])], outs=[(d, ["0"])])
         if allreduce_tasks:
             ad = ev(f"AD{l}", ["1"])
             call(fn(f"L{l}.ar_d", [str(allreduce_tasks)]), ins=[(d, ["0"])], outs=[(ad, ["0"])])

@@ -12,7 +12,7 @@ from paper_2604_13327_b200.decode import CONFIGS, DecodeModel, init_weights  # n
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "llama3-8b"]
 W = init_weights(cfg, torch.device("cuda:0"), 0)
-variants = [dict(fused_merge=True), dict(fused_merge=False)]
+variants = [dict(residual="split"), dict(residual="double")]
 models = []
 for kw in variants:
     m = DecodeModel(cfg, samples=(1024,), weights=W, **kw)
