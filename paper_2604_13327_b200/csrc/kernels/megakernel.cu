@@ -512,7 +512,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
-    const int nspl = static_cast<int>((s + CH - 1) / CH);
+    const int nspl = (static_cast<int>(s) + CH - 1) / CH;
     const float scale = op.f[0];
     const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);
     const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + (static_cast<long long>(g) * cap + s) * dh;
@@ -599,7 +599,7 @@ __device__ __forceinline__ void qk_norm_rope(float* v, int dh, const float* w, f
 }
 
 __device__ void body_attn_split(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, Ring& ring,
-                                int ctid) {
+                                int ctid, uint64_t* t_split = nullptr) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
@@ -696,11 +696,12 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         bar_sync(1, kConsumers);
         if (ctid == Ring::owner(cv) * 32) ring.release(cv);
     }
+    if (t_split && ctid == 0) *t_split = globaltimer();  // split work done (trace: prologue stamp)
     if (op.flags & 2) {  // fused merge: the split of group g that arrives last merges it
         volatile int* flag = reinterpret_cast<volatile int*>(sc + G * CH);
         if (ctid == 0) {
             int* arrive = reinterpret_cast<int*>(op.p[5]) + g;
-            const int ntask = s > 0 ? static_cast<int>((s + CH - 1) / CH) : 1;  // grid max(ceil(s/CH), 1)
+            const int ntask = s > 0 ? (static_cast<int>(s) + CH - 1) / CH : 1;  // grid max(ceil(s/CH), 1)
             // release: this split's partial (CTA writes ordered by the bar above) before
             // the arrival; acquire: the other splits' partials after it
             const bool last = atom_add_acq_rel(arrive, 1) == ntask - 1;
@@ -708,7 +709,10 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             *flag = last ? 1 : 0;
         }
         bar_sync(1, kConsumers);
-        if (*flag) attn_merge_group(P, op, g, qs, qstride, sc + G * CH + 4, ctid);
+        if (*flag) {
+            if ((P.debug & 16) && ctid == 0) ring.stall = globaltimer() - *t_split;  // arrival round trip
+            attn_merge_group(P, op, g, qs, qstride, sc + G * CH + 4, ctid);
+        }
     }
 }
 
@@ -720,7 +724,7 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
-    const int nspl = static_cast<int>((s + CH - 1) / CH);
+    const int nspl = (static_cast<int>(s) + CH - 1) / CH;
     const int g = si.coord[0];
     const float scale = op.f[0];
     const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);
@@ -1112,13 +1116,13 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         uint64_t t_begin = 0, t_wait = 0, t_pro = 0, t_exec = 0;
         if (ctid == 0) t_begin = globaltimer();
         SlotView v = view_slot(P, T, s, qb);
-        const et_op& op = P.ops[v.call];
-        // operands that do not depend on the Event Tensors (RMSNorm gamma) are
-        // pulled into L1 while thread 0 spins on the dependency
-        if (op.kind == ET_OP_GEMV && op.i[3] == 1 && !v.masked) {
-            const char* gam = reinterpret_cast<const char*>(op.p[3]);
-            for (int off = ctid * 128; off < op.i[1] * 4; off += kConsumers * 128) prefetch_l1(gam + off);
-        }
+        // The op record is copied into shared memory while thread 0 spins on the
+        // dependency: the acquire that ends the wait invalidates L1, and every
+        // body reads its op fields first (an L2 round trip on the critical path).
+        const et_op& opg = P.ops[v.call];
+        if (ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
+            reinterpret_cast<int*>(smem + kSmemOp)[ctid - 32] = reinterpret_cast<const int*>(&opg)[ctid - 32];
+        const et_op& op = *reinterpret_cast<const et_op*>(smem + kSmemOp);
         if (ctid == 0) {
             misc[2] = 1;  // consumers blocked on an Event Tensor: HBM idles, the producer may fill L2
             bool ok = (P.debug & 1) ? true : wait_range(P, v.wb, v.we, s, worker);
@@ -1157,7 +1161,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                     }
                     t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid);
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_ALLREDUCE: body_allreduce(P, op, v, ctid, worker); break;
@@ -1185,7 +1189,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 r.worker = worker;
                 r.flags = v.masked ? 1 : 0;
                 r.task = s;
-                r.pad = (P.debug & 8) ? static_cast<int>(ring.busy) : (P.debug & 2) ? static_cast<int>(ring.stall) : 0;
+                r.pad = (P.debug & 8) ? static_cast<int>(ring.busy) : (P.debug & 18) ? static_cast<int>(ring.stall) : 0;
                 ring.stall = 0;
                 ring.busy = 0;
                 P.trace[s] = r;
@@ -1711,7 +1715,10 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
         const int task = misc[3];
         if (task < 0) break;
         SlotView v = dyn_view(P, D, task);
-        const et_op& op = P.ops[v.call];
+        const et_op& opg = P.ops[v.call];  // shared-memory copy, as in the static loop
+        if (ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
+            reinterpret_cast<int*>(smem + kSmemOp)[ctid - 32] = reinterpret_cast<const int*>(&opg)[ctid - 32];
+        const et_op& op = *reinterpret_cast<const et_op*>(smem + kSmemOp);
         if (ctid < 32) {
             int ok = 1;
             if (ctid == 0) {

@@ -38,7 +38,8 @@ constexpr int kSmemTable = kSmemAcc + kAccFloats * 4;
 constexpr int kSmemExt0 = kSmemTable + (kMaxTableSlots + 1) * 16;
 constexpr int kSmemBar = kSmemExt0 + kMaxTableCalls * 4;
 constexpr int kSmemMisc = kSmemBar + 2 * kStages * 8;
-constexpr int kSmemTotal = kSmemMisc + 512;
+constexpr int kSmemOp = kSmemMisc + 512;      // the running task's et_op record (copied before its waits)
+constexpr int kSmemTotal = kSmemOp + 256;
 
 // Device status word block (one per runtime).
 struct DevStatus {
