@@ -137,10 +137,12 @@ __device__ bool wait_range(const StaticParams& P, int b, int e, int s, int worke
 
 // Release increments: the consumer warps' writes precede this thread's
 // release through the barrier the caller executed just before.
-__device__ bool notify_range(const StaticParams& P, int b, int e, int s, int worker) {
+// `first` (>= 0): the element of notify b, read before the slot's waits (the
+// wait's acquire invalidates L1, so reading it here would add a round trip).
+__device__ bool notify_range(const StaticParams& P, int b, int e, int s, int worker, int first = -1) {
     bool ok = true;
     for (int n = b; n < e; ++n) {
-        const int el = __ldg(P.notifies + n);
+        const int el = (n == b && first >= 0) ? first : __ldg(P.notifies + n);
         const uint32_t old = atom_add_release(P.cnt + el, 1u);
         if (old >= static_cast<uint32_t>(__ldg(P.initial_counts + el))) {
             report(P.status, ET_ERR_UNDERFLOW, worker, s, el, -1);
@@ -306,6 +308,15 @@ __device__ void body_splitk(const StaticParams& P, const et_op& op, const int* c
     }
 }
 
+// RMSNorm gamma of a GEMV is staged in shared memory right after the bf16
+// activations (16-byte aligned) when both fit.
+__device__ __forceinline__ int gamma_offset(const et_op& op, const StaticParams& P) {
+    return ((batch_of(op, P) * op.i[1] + 7) / 8) * 8;  // in bf16 elements
+}
+__device__ __forceinline__ bool gemv_gamma_staged(const et_op& op, const StaticParams& P) {
+    return op.i[3] == 1 && (gamma_offset(op, P) * 2 + op.i[1] * 4) <= kXBytes;
+}
+
 // ---- GEMV main loop (tensor cores).  Weights sit in HBM as m16n8k16
 // A-fragment tiles (decode.py `frag16`): tile (t, j) = rows [16t, 16t+16) x
 // k-step j is 512 B = 32 lanes x 16 B, lane (g = lane/4, q = lane%4) holding
@@ -368,8 +379,11 @@ __device__ __forceinline__ void gemv_stream(Ring& ring, int warp, int lane, int 
 // weight tiles stream through the shared-memory ring; activations are staged
 // once per task in shared memory (with the fused RMSNorm when x is the fp32
 // residual stream); the epilogue applies the op's fused tail.
+// `pre` (static scheduler): shared memory holding the task's constant operands
+// staged during its dependency wait (RoPE inverse frequencies; gamma sits behind
+// the activations), or nullptr to read them from global memory.
 __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
-                              float* red, Ring& ring, int ctid) {
+                              float* red, Ring& ring, int ctid, const float* pre = nullptr) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int N = op.i[0], K = op.i[1], nseg = op.i[2];
     const int nb = batch_of(op, P);
@@ -386,7 +400,8 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
         // RMSNorm prologue: one pass over the fp32 residual stream held in
         // registers (K <= 8192), sum of squares reduced across the CTA
         const float* h = reinterpret_cast<const float*>(op.p[2]);
-        const float* gam = reinterpret_cast<const float*>(op.p[3]);
+        const float* gam = (pre && gemv_gamma_staged(op, P)) ? reinterpret_cast<const float*>(xs + gamma_offset(op, P))
+                                                             : reinterpret_cast<const float*>(op.p[3]);
         const int stride = op.i[9];
         constexpr int kMaxPer = 8;  // float4 per thread: K <= 8192
         for (int bi = 0; bi < nb; ++bi) {
@@ -412,7 +427,7 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
             for (int j = 0; j < kMaxPer; ++j) {
                 const int k = (ctid + j * kConsumers) * 4;
                 if (k < K) {
-                    const float4 g = __ldg(reinterpret_cast<const float4*>(gam + k));
+                    const float4 g = *reinterpret_cast<const float4*>(gam + k);
                     uint2 o;
                     o.x = static_cast<uint32_t>(f2bf(hv[j].x * scale * g.x)) |
                           (static_cast<uint32_t>(f2bf(hv[j].y * scale * g.y)) << 16);
@@ -448,7 +463,7 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     if (epi == EPI_QKV_ROPE) {
         const int dh = op.i[8], nq = op.i[10], nkv = op.i[11], cap = op.i[12];
         const long long pos = P.binding[op.i[6]];
-        const float* invf = reinterpret_cast<const float*>(op.p[8]);  // RoPE inverse frequencies [dh/2]
+        const float* invf = pre ? pre : reinterpret_cast<const float*>(op.p[8]);  // RoPE inverse frequencies [dh/2]
         float* qout = reinterpret_cast<float*>(op.p[4]);
         uint16_t* kc = reinterpret_cast<uint16_t*>(op.p[6]);
         uint16_t* vc = reinterpret_cast<uint16_t*>(op.p[7]);
@@ -457,7 +472,7 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
             float a = acc[(2 * pr) * nb], b = acc[(2 * pr + 1) * nb];
             if (row < nq + nkv) {  // q or k: rotate the interleaved pair
                 const int d = row % dh;
-                const float inv = __ldg(invf + d / 2);
+                const float inv = invf[d / 2];
                 float sn, cs;
                 sincosf(static_cast<float>(pos) * inv, &sn, &cs);
                 const float ra = a * cs - b * sn, rb = a * sn + b * cs;
@@ -1122,8 +1137,23 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         const et_op& opg = P.ops[v.call];
         if (ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
             reinterpret_cast<int*>(smem + kSmemOp)[ctid - 32] = reinterpret_cast<const int*>(&opg)[ctid - 32];
+        // likewise the constant operands of a GEMV: RMSNorm gamma (behind the staged
+        // activations) and the RoPE inverse frequencies
+        if (opg.kind == ET_OP_GEMV && !v.masked && ctid > 0) {
+            if (gemv_gamma_staged(opg, P)) {
+                const int K = opg.i[1];
+                float4* dst = reinterpret_cast<float4*>(xs + gamma_offset(opg, P));
+                const float4* src = reinterpret_cast<const float4*>(opg.p[3]);
+                for (int i = ctid - 1; i < K / 4; i += kConsumers - 1) dst[i] = __ldg(src + i);
+            }
+            if (opg.i[4] == EPI_QKV_ROPE)
+                for (int i = ctid - 1; i < opg.i[8] / 2; i += kConsumers - 1)
+                    reinterpret_cast<float*>(smem + kSmemPre)[i] = __ldg(reinterpret_cast<const float*>(opg.p[8]) + i);
+        }
         const et_op& op = *reinterpret_cast<const et_op*>(smem + kSmemOp);
+        int first_notify = -1;
         if (ctid == 0) {
+            if (v.ne > v.nb) first_notify = __ldg(P.notifies + v.nb);
             misc[2] = 1;  // consumers blocked on an Event Tensor: HBM idles, the producer may fill L2
             bool ok = (P.debug & 1) ? true : wait_range(P, v.wb, v.we, s, worker);
             misc[2] = 0;
@@ -1159,7 +1189,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                         if (ctid == 0) report(P.status, ET_ERR_INVALID, worker, s, -1, batch_of(op, P));
                         break;
                     }
-                    t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid);
+                    t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid, reinterpret_cast<const float*>(smem + kSmemPre));
                     break;
                 case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro); break;
                 case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
@@ -1177,7 +1207,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         bar_sync(1, kConsumers);
         if (ctid == 0) {
             t_exec = globaltimer();
-            notify_range(P, v.nb, v.ne, s, worker);
+            notify_range(P, v.nb, v.ne, s, worker, first_notify);
             if (P.record) {
                 et_trace_rec r;
                 r.t_push = 0;

@@ -39,7 +39,8 @@ constexpr int kSmemExt0 = kSmemTable + (kMaxTableSlots + 1) * 16;
 constexpr int kSmemBar = kSmemExt0 + kMaxTableCalls * 4;
 constexpr int kSmemMisc = kSmemBar + 2 * kStages * 8;
 constexpr int kSmemOp = kSmemMisc + 512;      // the running task's et_op record (copied before its waits)
-constexpr int kSmemTotal = kSmemOp + 256;
+constexpr int kSmemPre = kSmemOp + 256;       // small constant operands staged before the waits (RoPE freqs)
+constexpr int kSmemTotal = kSmemPre + 512;
 
 // Device status word block (one per runtime).
 struct DevStatus {
