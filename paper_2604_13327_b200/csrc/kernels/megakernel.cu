@@ -514,6 +514,24 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     return t_pro;
 }
 
+// Qwen3-style per-head RMSNorm (weight w[dh]) followed by the pair rotation at
+// position pos, in place on one head vector in shared memory; one warp.
+__device__ __noinline__ void qk_norm_rope(float* v, int dh, const float* w, float eps, const float* invf,
+                                             long long pos, int lane) {
+    float ss = 0.f;
+    for (int d = lane; d < dh; d += 32) ss += v[d] * v[d];
+    ss = warp_sum(ss);
+    const float sc = rsqrtf(ss / static_cast<float>(dh) + eps);
+    for (int j = lane; j < dh / 2; j += 32) {
+        const float a = v[2 * j] * sc * __ldg(w + 2 * j), b = v[2 * j + 1] * sc * __ldg(w + 2 * j + 1);
+        float sn, cs;
+        sincosf(static_cast<float>(pos) * __ldg(invf + j), &sn, &cs);
+        v[2 * j] = a * cs - b * sn;
+        v[2 * j + 1] = a * sn + b * cs;
+    }
+    __syncwarp();
+}
+
 // Merge of the splits of kv head g's q heads with the new token at position s
 // (K/V row s of the cache):
 //   O = (sum_c e^(m_c-M) o_c + e^(s_new-M) v_new) / (sum_c e^(m_c-M) l_c + e^(s_new-M)).
@@ -521,9 +539,12 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
 // operand -- split statistics, the new K/V row and this thread's o partials
 // (in registers, up to 16 splits per pass) -- is requested before the first
 // use, so a pass costs one L2 round trip.
+// kQK: the Qwen3 q/k-norm variant (MoE instantiation only; G * dh <= 1024), else
+// G * dh <= 512 -- the register footprint of the dense kernel stays spill-free.
+template <bool kQK>
 __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op& op, int g, const float* qs,
-                                                 int qstride, float* scr, int ctid) {
-    constexpr int kPass = 16, kOut = 2;  // splits per pass; outputs per thread (G * dh <= 512)
+                                              int qstride, float* scr, int ctid) {
+    constexpr int kPass = kQK ? 8 : 16, kOut = kQK ? 4 : 2;  // splits in registers; outputs per thread
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
@@ -537,13 +558,15 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     float* wts = ml + 2 * G * nspl;     // [G][nspl]
     float* hs = wts + G * nspl;         // [G]: weight of the new token
     float* kns = hs + G;                // [dh]
+    float* vns = kns + dh;              // [dh] (q/k-norm mode)
+    const bool qk = kQK && (op.flags & 1) != 0;
     float ov[kOut][kPass];
     float vv[kOut];
 #pragma unroll
     for (int j = 0; j < kOut; ++j) {
         const int idx = ctid + j * kConsumers;
         const int hh = idx / dh, d = idx - hh * dh;
-        vv[j] = idx < G * dh ? bf2f(__ldcg(vn + d)) : 0.f;
+        vv[j] = (idx < G * dh && !qk) ? bf2f(__ldcg(vn + d)) : 0.f;
 #pragma unroll
         for (int c = 0; c < kPass; ++c)
             ov[j][c] = (idx < G * dh && c < nspl) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d)
@@ -554,8 +577,40 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
         ml[2 * i] = __ldcg(pr);
         ml[2 * i + 1] = __ldcg(pr + 1);
     }
-    for (int d = ctid; d < dh; d += kConsumers) kns[d] = bf2f(__ldcg(kn + d));
+    if (!qk) {
+        for (int d = ctid; d < dh; d += kConsumers) kns[d] = bf2f(__ldcg(kn + d));
+    } else if constexpr (kQK) {
+        // Qwen3: the new k is the raw projection -> per-head RMSNorm + RoPE; k and v
+        // are appended to the cache (bf16) and used rounded, as any cached row
+        const float* kr = reinterpret_cast<const float*>(op.p[8]) + static_cast<long long>(g) * dh;
+        const float* vr = kr + static_cast<long long>(op.i[6]) * dh;
+        for (int d = ctid; d < dh; d += kConsumers) {
+            kns[d] = __ldcg(kr + d);
+            vns[d] = __ldcg(vr + d);
+        }
+        bar_sync(1, kConsumers);
+        if (warp == 0)
+            qk_norm_rope(kns, dh, reinterpret_cast<const float*>(op.p[6]), op.f[1],
+                         reinterpret_cast<const float*>(op.p[7]), s, lane);
+        bar_sync(1, kConsumers);
+        uint16_t* kc = const_cast<uint16_t*>(kn);
+        uint16_t* vc = const_cast<uint16_t*>(vn);
+        for (int d = ctid; d < dh; d += kConsumers) {
+            const uint16_t kb = f2bf(kns[d]), vb = f2bf(vns[d]);
+            kc[d] = kb;
+            vc[d] = vb;
+            kns[d] = bf2f(kb);
+            vns[d] = bf2f(vb);
+        }
+    }
     bar_sync(1, kConsumers);
+    if (qk) {
+#pragma unroll
+        for (int j = 0; j < kOut; ++j) {
+            const int idx = ctid + j * kConsumers;
+            if (idx < G * dh) vv[j] = vns[idx % dh];
+        }
+    }
     for (int hh = warp; hh < G; hh += kConsumerWarps) {
         float dot = 0.f;
         for (int d = lane; d < dh; d += 32) dot += qs[hh * qstride + d] * kns[d];
@@ -595,24 +650,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     }
 }
 
-// Qwen3-style per-head RMSNorm (weight w[dh]) followed by the pair rotation at
-// position pos, in place on one head vector in shared memory; one warp.
-__device__ __forceinline__ void qk_norm_rope(float* v, int dh, const float* w, float eps, const float* invf,
-                                             long long pos, int lane) {
-    float ss = 0.f;
-    for (int d = lane; d < dh; d += 32) ss += v[d] * v[d];
-    ss = warp_sum(ss);
-    const float sc = rsqrtf(ss / static_cast<float>(dh) + eps);
-    for (int j = lane; j < dh / 2; j += 32) {
-        const float a = v[2 * j] * sc * __ldg(w + 2 * j), b = v[2 * j + 1] * sc * __ldg(w + 2 * j + 1);
-        float sn, cs;
-        sincosf(static_cast<float>(pos) * __ldg(invf + j), &sn, &cs);
-        v[2 * j] = a * cs - b * sn;
-        v[2 * j + 1] = a * sn + b * cs;
-    }
-    __syncwarp();
-}
-
+template <bool kQK>
 __device__ void body_attn_split(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, Ring& ring,
                                 int ctid, uint64_t* t_split = nullptr) {
     const int warp = ctid >> 5, lane = ctid & 31;
@@ -627,11 +665,13 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     float* sc = scratch + G * qstride;   // [G][CH]
     const float* q = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
     for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
-    if (op.flags & 1) {  // q-norm + RoPE applied here (q is the raw projection)
-        bar_sync(1, kConsumers);
-        for (int h = warp; h < G; h += kConsumerWarps)
-            qk_norm_rope(qs + h * qstride, dh, reinterpret_cast<const float*>(op.p[5]), op.f[1],
-                         reinterpret_cast<const float*>(op.p[7]), s, lane);
+    if constexpr (kQK) {
+        if (op.flags & 1) {  // q-norm + RoPE applied here (q is the raw projection)
+            bar_sync(1, kConsumers);
+            for (int h = warp; h < G; h += kConsumerWarps)
+                qk_norm_rope(qs + h * qstride, dh, reinterpret_cast<const float*>(op.p[(op.flags & 2) ? 9 : 5]),
+                             op.f[1], reinterpret_cast<const float*>(op.p[7]), s, lane);
+        }
     }
     bar_sync(1, kConsumers);
     const float scale = op.f[0];
@@ -726,7 +766,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         bar_sync(1, kConsumers);
         if (*flag) {
             if ((P.debug & 16) && ctid == 0) ring.stall = globaltimer() - *t_split;  // arrival round trip
-            attn_merge_group(P, op, g, qs, qstride, sc + G * CH + 4, ctid);
+            attn_merge_group<kQK>(P, op, g, qs, qstride, sc + G * CH + 4, ctid);
         }
     }
 }
@@ -735,6 +775,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
 //   O = (sum_c e^(m_c-M) o_c + e^(s_new-M) v_new) / (sum_c e^(m_c-M) l_c + e^(s_new-M)).
 // Split statistics are staged in shared memory with independent loads, then
 // every (head, dim) output is one thread's dot product over the splits.
+template <bool kQK>
 __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
@@ -754,7 +795,7 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
         ml[2 * idx] = __ldcg(pr);
         ml[2 * idx + 1] = __ldcg(pr + 1);
     }
-    if (op.flags & 1) {
+    if (kQK && (op.flags & 1)) {
         // Qwen3 mode: q, k, v of the new token are raw projections.  q and k get
         // the per-head RMSNorm + RoPE here; k and v are appended to the cache
         // (bf16) for later steps and read back below like any cached row.
@@ -839,19 +880,18 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
         for (int v = ctid; v < nb * H / 8; v += kConsumers)
             reinterpret_cast<uint4*>(op.p[5])[v] = reinterpret_cast<const uint4*>(xs)[v];
     volatile int* flag = reinterpret_cast<volatile int*>(red + kConsumerWarps);
-    bar_sync(1, kConsumers);
-    if (ctid == 0) {
-        __threadfence();
-        int* arrive = reinterpret_cast<int*>(op.p[7]);
-        const bool last = atomicAdd(arrive, 1) == si.ext0 - 1;
-        if (last) {
-            *reinterpret_cast<volatile int*>(arrive) = 0;
-            __threadfence();
+    const bool single = si.ext0 == 1;  // one route task: no arrival, logits still in shared memory
+    if (!single) {
+        bar_sync(1, kConsumers);
+        if (ctid == 0) {
+            int* arrive = reinterpret_cast<int*>(op.p[7]);
+            const bool last = atom_add_acq_rel(arrive, 1) == si.ext0 - 1;
+            if (last) *reinterpret_cast<volatile int*>(arrive) = 0;
+            *flag = last ? 1 : 0;
         }
-        *flag = last ? 1 : 0;
+        bar_sync(1, kConsumers);
+        if (!*flag) return;
     }
-    bar_sync(1, kConsumers);
-    if (!*flag) return;
 
     const int rb = op.i[10];  // the layer's routing tensors: topk, cnt, ind, tind, elist, eoff
     int* topk = P.rt[rb];
@@ -863,7 +903,7 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
     const float* logits = reinterpret_cast<const float*>(op.p[4]);
     float* wslot = reinterpret_cast<float*>(op.p[6]);
     int4* tinfo = reinterpret_cast<int4*>(op.p[8]);   // [tiles] (expert, first slot, tokens)
-    int* scnt = reinterpret_cast<int*>(acc);          // [E] counts
+    int* scnt = reinterpret_cast<int*>(acc + E * nb);  // [E] counts (the logits stay in acc[0, E*nb))
     int* stop = scnt + 256;                           // [nb*K] experts per slot
     for (int e = ctid; e < E; e += kConsumers) scnt[e] = 0;
     bar_sync(1, kConsumers);
@@ -875,7 +915,7 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int e = lane + 32 * u;
-            lg[u] = e < E ? __ldcg(logits + static_cast<long long>(t) * E + e) : -INFINITY;
+            lg[u] = e < E ? (single ? acc[e * nb + t] : __ldcg(logits + static_cast<long long>(t) * E + e)) : -INFINITY;
             m = fmaxf(m, lg[u]);
         }
         m = warp_max(m);
@@ -917,7 +957,8 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
         __syncwarp();
         // weights p_e / sum of the selected p, recomputed from the logits
         const int ej = lane < K ? stop[t * K + lane] : 0;
-        const float wj = lane < K ? __expf(__ldcg(logits + static_cast<long long>(t) * E + ej) - m) / z : 0.f;
+        const float lj = lane < K ? (single ? acc[ej * nb + t] : __ldcg(logits + static_cast<long long>(t) * E + ej)) : 0.f;
+        const float wj = lane < K ? __expf(lj - m) / z : 0.f;
         const float wsum = warp_sum(wj);
         if (lane < K) {
             const int slot = t * K + lane;
@@ -1191,8 +1232,8 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                     }
                     t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid, reinterpret_cast<const float*>(smem + kSmemPre));
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro); break;
-                case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro); break;
+                case ET_OP_ATTN_MERGE: body_attn_merge<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_ALLREDUCE: body_allreduce(P, op, v, ctid, worker); break;
                 case ET_OP_MOE_ROUTE:
@@ -1790,8 +1831,8 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     }
                     tp = body_gemv(P, op, v, xs, acc, red, ring, ctid);
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
-                case ET_OP_ATTN_MERGE: body_attn_merge(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
+                case ET_OP_ATTN_MERGE: body_attn_merge<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_MOE_ROUTE:
                     if constexpr (kMoE) body_moe_route(P, op, v, xs, acc, red, ring, ctid, &tp);

@@ -33,7 +33,8 @@
 //   the per-head RMSNorm (p5 = q-norm weight, p6 = k-norm weight, fp32 [head_dim], f1 = eps)
 //   and RoPE (p7 = inverse frequencies) themselves; MERGE also normalises + rotates the raw
 //   new k at p8 + g*head_dim (v at p8 + (kv_heads + g)*head_dim) and appends k/v (bf16) to
-//   the cache at position s before using them.
+//   the cache at position s before using them.  With both bits (fused q/k-norm split) p5 holds the
+//   arrival counters and the q-norm weight moves to p9.
 // ET_OP_MOE_ROUTE       task t of E/16: router logits rows [16t, 16t+16) (GEMV, RMSNorm prologue,
 //   GEMV fields i0..i9 as ET_OP_GEMV with i3 = 1, i4 = EPI_F32); task 0 also stores the
 //   normalised activations; the last task to arrive computes the routing for every token:
@@ -116,6 +117,14 @@ struct ExpertTask {
     int slot[8];
 };
 
+// Expert id and row split of a task (the streaming plan needs nothing else).
+__device__ __forceinline__ void expert_of(const et_op& op, int flat, int* e, int* r) {
+    const int RS = op.i[2];
+    const int tile = flat / RS;
+    *r = flat - tile * RS;
+    *e = __ldcg(reinterpret_cast<const int*>(op.p[6]) + 4 * tile);
+}
+
 __device__ __forceinline__ ExpertTask expert_task(const et_op& op, int flat, int* const* rt) {
     const int RS = op.i[2];
     const int* elist = rt[op.i[6]];
@@ -188,13 +197,14 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
         pl.bytes[0] = (sp.u1 - sp.u0) * 512;
     } else if (op.kind == ET_OP_MOE_EXPERT) {
         // gate rows, up rows (rows [r*IR, r*IR+IR) of expert e), then down block (e, r)
-        const ExpertTask t = expert_task(op, coord[0], rt);
+        int e, r;
+        expert_of(op, coord[0], &e, &r);
         const long long I = op.i[0], H = op.i[1], RS = op.i[2], IR = I / RS;
         const long long rows = IR * H * 2;
         pl.nseg = 3;
-        pl.base[0] = reinterpret_cast<const uint8_t*>(op.p[0]) + (t.e * I + t.r * IR) * H * 2;
-        pl.base[1] = reinterpret_cast<const uint8_t*>(op.p[1]) + (t.e * I + t.r * IR) * H * 2;
-        pl.base[2] = reinterpret_cast<const uint8_t*>(op.p[2]) + (t.e * RS + t.r) * rows;
+        pl.base[0] = reinterpret_cast<const uint8_t*>(op.p[0]) + (e * I + r * IR) * H * 2;
+        pl.base[1] = reinterpret_cast<const uint8_t*>(op.p[1]) + (e * I + r * IR) * H * 2;
+        pl.base[2] = reinterpret_cast<const uint8_t*>(op.p[2]) + (e * RS + r) * rows;
         pl.bytes[0] = pl.bytes[1] = pl.bytes[2] = rows;
     } else if (op.kind == ET_OP_ATTN_SPLIT) {
         // K rows then V rows of positions [c*CH, min(s, c*CH+CH)), one chunk each

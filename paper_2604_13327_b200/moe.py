@@ -112,7 +112,8 @@ MOE_CONFIGS = {c.name: c for c in (TINY_MOE, QWEN3_30B_A3B)}
 RT_PER_LAYER = ("topk", "cnt", "ind", "tind", "elist", "eoff")
 
 
-def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1):
+def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=None, route_tasks=1,
+                   group_stage=True):
     """Reference-format graph spec (ref json_io.cpp:115-230) of one MoE decode step."""
     CH = cfg.attn_chunk
     E, K, RS = cfg.experts, cfg.top_k, cfg.row_splits
@@ -141,25 +142,39 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1):
                 {"name": rt["eoff"], "shape": [str(E + 1)], "role": "indptr", "writer": route}]
         qkv, a, m, o, r, x, d = (f"{n}{l}" for n in ("QKV", "A", "M", "O", "R", "EXP", "D"))
         ev(qkv, ["1"])
-        ev(a, [kv])
+        if not fused_merge:
+            ev(a, [kv])
         ev(m, ["1"])
         ev(o, ["1"])
         ev(r, ["1"])
-        ev(x, [str(E)], data_dependent=True, counts=rt["cnt"], writer=route)
+        if group_stage:
+            ev(x, [str(E)], data_dependent=True, counts=rt["cnt"], writer=route)
         ev(d, ["1"])
+        calls.append({"fn": fn(f"L{l}.qkv", [str(qkv_tasks or tasks)]), "in": [{"event": prev, "map": ["0"]}],
+                      "out": [{"event": qkv, "map": ["0"]}]})
+        if fused_merge:  # the last split of each kv head merges the group
+            calls.append({"fn": fn(f"L{l}.attn", [kv, f"max((s + {CH - 1}) // {CH}, 1)"]),
+                          "in": [{"event": qkv, "map": ["0"]}], "out": [{"event": m, "map": ["0"]}]})
+        else:
+            calls += [
+                {"fn": fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), "in": [{"event": qkv, "map": ["0"]}],
+                 "out": [{"event": a, "map": ["t0"]}]},
+                {"fn": fn(f"L{l}.merge", [kv]), "in": [{"event": a, "map": ["t0"]}, {"event": qkv, "map": ["0"]}],
+                 "out": [{"event": m, "map": ["0"]}]}]
         calls += [
-            {"fn": fn(f"L{l}.qkv", [T]), "in": [{"event": prev, "map": ["0"]}], "out": [{"event": qkv, "map": ["0"]}]},
-            {"fn": fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), "in": [{"event": qkv, "map": ["0"]}],
-             "out": [{"event": a, "map": ["t0"]}]},
-            {"fn": fn(f"L{l}.merge", [kv]), "in": [{"event": a, "map": ["t0"]}, {"event": qkv, "map": ["0"]}],
-             "out": [{"event": m, "map": ["0"]}]},
             {"fn": fn(f"L{l}.oproj", [T]), "in": [{"event": m, "map": ["0"]}], "out": [{"event": o, "map": ["0"]}]},
-            {"fn": fn(route, [str(E // 16)]), "in": [{"event": o, "map": ["0"]}], "out": [{"event": r, "map": ["0"]}]},
-            {"fn": fn(f"L{l}.group", [str(tokens * K)]), "in": [{"event": r, "map": ["0"]}],
-             "out": [{"event": x, "routed_by": rt["topk"]}]},
-            {"fn": fn(f"L{l}.expert", [str(tokens * K * RS)]), "extent_from": rt["tind"],
-             "in": [{"event": x, "indptr": rt["tind"]}], "out": [{"event": d, "map": ["0"]}]},
-        ]
+            {"fn": fn(route, [str(route_tasks)]), "in": [{"event": o, "map": ["0"]}],
+             "out": [{"event": r, "map": ["0"]}]}]
+        if group_stage:  # the reference structure: routed notify + range trigger (dynamic scheduler)
+            calls += [
+                {"fn": fn(f"L{l}.group", [str(tokens * K)]), "in": [{"event": r, "map": ["0"]}],
+                 "out": [{"event": x, "routed_by": rt["topk"]}]},
+                {"fn": fn(f"L{l}.expert", [str(tokens * K * RS)]), "extent_from": rt["tind"],
+                 "in": [{"event": x, "indptr": rt["tind"]}], "out": [{"event": d, "map": ["0"]}]}]
+        else:  # static scheduler: the worst-case rewrite makes EXP a barrier over the no-op
+            # group tasks anyway; the expert tiles wait on the routing itself (extent_from masks)
+            calls.append({"fn": fn(f"L{l}.expert", [str(tokens * K * RS)]), "extent_from": rt["tind"],
+                          "in": [{"event": r, "map": ["0"]}], "out": [{"event": d, "map": ["0"]}]})
         prev = d
     ev("LM", ["1"])
     calls.append({"fn": fn("lm_head", [str(lm_tasks)]), "in": [{"event": prev, "map": ["0"]}],
@@ -217,7 +232,8 @@ class MoEDecodeModel:
     """One MoE decoder + its lowered megakernel (static or dynamic scheduler)."""
 
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
-                 scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False):
+                 scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=False,
+                 balance=False, route_tasks=None, group_stage=None):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
@@ -231,7 +247,14 @@ class MoEDecodeModel:
         self.max_splits = max(1, (self.samples[-1] + cfg.attn_chunk - 1) // cfg.attn_chunk)
         self.scheduler = scheduler
         t0 = time.perf_counter()
-        self.spec = moe_graph_spec(cfg, self.num_workers, self.num_workers, self.tokens)
+        from .decode import balanced_tasks
+
+        self.fused_merge = fused_merge
+        self.group_stage = (scheduler == "dynamic") if group_stage is None else group_stage
+        self.route_tasks = route_tasks or max(1, cfg.experts // 16)
+        self.spec = moe_graph_spec(cfg, self.num_workers, self.num_workers, self.tokens, fused_merge=fused_merge,
+                                   qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
+                                   if balance else None, route_tasks=self.route_tasks, group_stage=self.group_stage)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.rt_index = {r["name"]: i for i, r in enumerate(self.spec["runtime_tensors"])}
         if scheduler == "dynamic":
@@ -260,6 +283,7 @@ class MoEDecodeModel:
         self.xn = torch.zeros(cfg.layers, b, cfg.hidden, dtype=torch.bfloat16, device=dev)
         self.wslot = torch.zeros(cfg.layers, b * K, dtype=torch.float32, device=dev)
         self.arrive = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
+        self.arrive_attn = torch.zeros(cfg.layers, cfg.kv_heads, dtype=torch.int32, device=dev)
         self.tiles = torch.zeros(cfg.layers, b * K, 4, dtype=torch.int32, device=dev)  # expert tile table
         self.logits = torch.zeros(b, cfg.vocab, dtype=torch.float32, device=dev)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
@@ -294,8 +318,15 @@ class MoEDecodeModel:
             attn_i = [dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads]
             attn_p = [ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(L["q_norm"]),
                       ptr(L["k_norm"]), ptr(self.inv_freq), ptr(self.qkv) + 4 * nq]
-            ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
-            ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
+            if self.fused_merge:  # flags: 1 = q/k-norm mode, 2 = the last split merges; p5 of the split
+                # op carries the arrival counters, so the norm weights move to the merge-compatible slots
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], flags=3,
+                                   p=[ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn),
+                                      ptr(self.arrive_attn[l]), ptr(L["k_norm"]), ptr(self.inv_freq),
+                                      ptr(self.qkv) + 4 * nq, ptr(L["q_norm"])]))
+            else:
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
+                ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
             ops.append(make_op(OP_GEMV, i=[H, nq, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],
                                p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h)]))
             assert [ri[n] for n in RT_PER_LAYER] == list(range(ri["topk"], ri["topk"] + len(RT_PER_LAYER)))
@@ -304,7 +335,8 @@ class MoEDecodeModel:
                                p=[ptr(L["router"]), 0, ptr(self.h), ptr(L["ffn_norm"]), ptr(self.logits_r[l]),
                                   ptr(self.xn[l]), ptr(self.wslot[l]), ptr(self.arrive[l:l + 1]), ptr(self.tiles[l])],
                                flags=1 if self.injected else 0))
-            ops.append(make_op(OP_NONE))  # group: the routed notify is the Event Tensor edge itself
+            if self.group_stage:
+                ops.append(make_op(OP_NONE))  # group: the routed notify is the Event Tensor edge itself
             ops.append(make_op(OP_MOE_EXPERT,
                                i=[cfg.expert_inter, H, RS, TS, ri["ind"], ri["cnt"], ri["elist"], ri["eoff"], K, 0, E],
                                p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(L["wdown"]), ptr(self.xn[l]), ptr(self.wslot[l]),
