@@ -548,7 +548,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
-    const int nspl = (static_cast<int>(s) + CH - 1) / CH;
+    const int nspl = attn_splits_with_data(op, P.binding);
     const float scale = op.f[0];
     const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);
     const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + (static_cast<long long>(g) * cap + s) * dh;
@@ -653,18 +653,30 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
 template <bool kQK>
 __device__ void body_attn_split(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, Ring& ring,
                                 int ctid, uint64_t* t_split = nullptr) {
+    // Flash-decoding split c of kv head g: its run of CH-position K/V blocks
+    // (attn_blocks) arrives through the ring interleaved K0 V0 K1 V1 ...; each
+    // block updates an online softmax (scores one (position, head) dot product per
+    // thread; per-head running max / sum by one warp; P.V accumulated in registers
+    // by the thread owning (head, dim pair)).  The unnormalised partial (m, l, o)
+    // per q head goes to the partials buffer; the merge combines the splits.
+    constexpr int kOutMax = kQK ? 2 : 1;  // (head, dim pair) outputs per thread: G * dh / 2 <= 256 * kOutMax
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
     const int g = si.coord[0], c = si.coord[1];
-    const long long p0 = static_cast<long long>(c) * CH;
-    const int np = p0 < s ? static_cast<int>((p0 + CH < s ? p0 + CH : s) - p0) : 0;
+    const AttnBlocks ab = attn_blocks(op, c, P.binding);
     const int qstride = dh + 4;          // padded rows: heads land on different banks
     const int nvec = dh / 8;             // 16-byte vectors per K/V row
+    const int half = dh / 2;
     float* qs = scratch;                 // [G][dh+4]
     float* sc = scratch + G * qstride;   // [G][CH]
+    float* st = sc + G * CH;             // [G][4]: running max, running sum, block rescale
     const float* q = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
     for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
+    if (ctid < G) {
+        st[4 * ctid] = -INFINITY;
+        st[4 * ctid + 1] = 0.f;
+    }
     if constexpr (kQK) {
         if (op.flags & 1) {  // q-norm + RoPE applied here (q is the raw projection)
             bar_sync(1, kConsumers);
@@ -675,12 +687,16 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     }
     bar_sync(1, kConsumers);
     const float scale = op.f[0];
-    if (np > 0) {  // an empty split (s == 0, fused merge) only arrives
+    float o0[kOutMax], o1[kOutMax];
+#pragma unroll
+    for (int j = 0; j < kOutMax; ++j) o0[j] = o1[j] = 0.f;
+    for (int blk = 0; blk < ab.nblk; ++blk) {
+        const long long pb = ab.p0 + static_cast<long long>(blk) * CH;
+        const int np = static_cast<int>(pb + CH < s ? CH : s - pb);
         const unsigned long long ck = ring.seq, cv = ring.seq + 1;
         ring.seq += 2;
-
-        // scores: one (position, head) dot product per thread; each position starts
-        // its walk over the row at a different 16-byte vector (bank rotation)
+        // scores; each position starts its walk over the row at a different 16-byte
+        // vector (bank rotation)
         const uint8_t* kb = ring.wait(ck);
         if (!kb) return;
         for (int t = ctid; t < G * np; t += kConsumers) {
@@ -706,67 +722,92 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         }
         bar_sync(1, kConsumers);
         if (ctid == Ring::owner(ck) * 32) ring.release(ck);
-
-        // softmax statistics per head (warp h), probabilities in place
-        float* part = reinterpret_cast<float*>(op.p[3]);
+        // online softmax statistics per head (warp h), probabilities in place
         for (int h = warp; h < G; h += kConsumerWarps) {
             float m = -INFINITY;
             for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
             m = warp_max(m);
+            const float mo = st[4 * h], mn = fmaxf(mo, m);
             float l = 0.f;
             for (int p = lane; p < np; p += 32) {
-                const float e = __expf(sc[h * CH + p] - m);
+                const float e = __expf(sc[h * CH + p] - mn);
                 sc[h * CH + p] = e;
                 l += e;
             }
             l = warp_sum(l);
             if (lane == 0) {
-                float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2);
-                pr[0] = m;
-                pr[1] = l;
+                const float alpha = __expf(mo - mn);  // 0 on the first block (mo = -inf)
+                st[4 * h] = mn;
+                st[4 * h + 1] = st[4 * h + 1] * alpha + l;
+                st[4 * h + 2] = alpha;
             }
         }
         bar_sync(1, kConsumers);
-
-        // o = P V: one (head, dim pair) per thread
+        // o = alpha * o + P V: one (head, dim pair) per thread (two when G * dh > 512)
         const uint8_t* vb = ring.wait(cv);
         if (!vb) return;
         const uint32_t* v2 = reinterpret_cast<const uint32_t*>(vb);
-        const int half = dh / 2;
-        for (int idx = ctid; idx < G * half; idx += kConsumers) {
-            const int h = idx / half, dp = idx % half;
+#pragma unroll
+        for (int j = 0; j < kOutMax; ++j) {
+            const int idx = ctid + j * kConsumers;
+            if (idx >= G * half) break;
+            const int h = idx / half, dp = idx - h * half;
             const float* ph = sc + h * CH;
-            float o0 = 0.f, o1 = 0.f;
-    #pragma unroll 8
-            for (int p = 0; p < np; ++p) {
-                const uint32_t vv = v2[p * half + dp];
-                const float w = ph[p];
-                o0 = fmaf(w, bf16lo(vv), o0);
-                o1 = fmaf(w, bf16hi(vv), o1);
+            const float alpha = st[4 * h + 2];
+            float a0 = o0[j] * alpha, a1 = o1[j] * alpha, a2 = 0.f, a3 = 0.f;
+            int p = 0;
+#pragma unroll 4
+            for (; p + 2 <= np; p += 2) {
+                const uint32_t va = v2[p * half + dp], vb2 = v2[(p + 1) * half + dp];
+                const float wa = ph[p], wb = ph[p + 1];
+                a0 = fmaf(wa, bf16lo(va), a0);
+                a1 = fmaf(wa, bf16hi(va), a1);
+                a2 = fmaf(wb, bf16lo(vb2), a2);
+                a3 = fmaf(wb, bf16hi(vb2), a3);
             }
-            float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2) + 2 + 2 * dp;
-            pr[0] = o0;
-            pr[1] = o1;
+            if (p < np) {
+                const uint32_t va = v2[p * half + dp];
+                a0 = fmaf(ph[p], bf16lo(va), a0);
+                a1 = fmaf(ph[p], bf16hi(va), a1);
+            }
+            o0[j] = a0 + a2;
+            o1[j] = a1 + a3;
         }
-        bar_sync(1, kConsumers);
+        bar_sync(1, kConsumers);  // sc / st are reused by the next block
         if (ctid == Ring::owner(cv) * 32) ring.release(cv);
+    }
+    // the unnormalised partial (m, l, o) of every q head of the group
+    float* part = reinterpret_cast<float*>(op.p[3]);
+#pragma unroll
+    for (int j = 0; j < kOutMax; ++j) {
+        const int idx = ctid + j * kConsumers;
+        if (idx >= G * half) break;
+        const int h = idx / half, dp = idx - h * half;
+        float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2);
+        pr[2 + 2 * dp] = o0[j];
+        pr[3 + 2 * dp] = o1[j];
+        if (dp == 0) {
+            pr[0] = st[4 * h];
+            pr[1] = st[4 * h + 1];
+        }
     }
     if (t_split && ctid == 0) *t_split = globaltimer();  // split work done (trace: prologue stamp)
     if (op.flags & 2) {  // fused merge: the split of group g that arrives last merges it
-        volatile int* flag = reinterpret_cast<volatile int*>(sc + G * CH);
+        volatile int* flag = reinterpret_cast<volatile int*>(st + 4 * G);
+        bar_sync(1, kConsumers);
         if (ctid == 0) {
             int* arrive = reinterpret_cast<int*>(op.p[5]) + g;
-            const int ntask = s > 0 ? (static_cast<int>(s) + CH - 1) / CH : 1;  // grid max(ceil(s/CH), 1)
             // release: this split's partial (CTA writes ordered by the bar above) before
             // the arrival; acquire: the other splits' partials after it
-            const bool last = atom_add_acq_rel(arrive, 1) == ntask - 1;
+            const int ntask = attn_tasks(op, P.binding);  // grid max(splits, 1)
+            const bool last = atom_add_acq_rel(arrive, 1) == (ntask > 0 ? ntask : 1) - 1;
             if (last) *reinterpret_cast<volatile int*>(arrive) = 0;  // every split of this step arrived
             *flag = last ? 1 : 0;
         }
         bar_sync(1, kConsumers);
         if (*flag) {
             if ((P.debug & 16) && ctid == 0) ring.stall = globaltimer() - *t_split;  // arrival round trip
-            attn_merge_group<kQK>(P, op, g, qs, qstride, sc + G * CH + 4, ctid);
+            attn_merge_group<kQK>(P, op, g, qs, qstride, st + 4 * G + 4, ctid);
         }
     }
 }
@@ -780,7 +821,7 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
-    const int nspl = (static_cast<int>(s) + CH - 1) / CH;
+    const int nspl = attn_splits_with_data(op, P.binding);
     const int g = si.coord[0];
     const float scale = op.f[0];
     const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);

@@ -18,9 +18,10 @@
 //   p0/p1 = weights (bf16 [N][K], frag16 tile order) of segment 0/1, p4 = out,
 //   p5 = residual in (fp32), p6/p7 = K/V cache of the layer (bf16 [kv_heads][cap][head_dim]);
 //   p8 = RoPE inverse frequencies (fp32 [head_dim/2], pair j rotates dims 2j, 2j+1); f0 = RMSNorm eps
-// ET_OP_ATTN_SPLIT      task (kv_head g, split c): flash-decoding partial over cached
-//   positions [c*CH, min(s, c*CH+CH)); i0 = head_dim, i1 = q heads per kv head, i2 = CH,
-//   i3 = KV capacity, i4 = position symbol slot, i5 = max splits, i6 = kv heads;
+// ET_OP_ATTN_SPLIT      task (kv_head g, split c) of grid [kv, min(ceil(s/CH), i5)]: flash-decoding
+//   partial over its run of CH-position blocks (attn_blocks), online softmax across blocks;
+//   i0 = head_dim, i1 = q heads per kv head, i2 = CH (block positions), i3 = KV capacity,
+//   i4 = position symbol slot, i5 = split cap (partials' split dimension), i6 = kv heads;
 //   p0 = q (fp32 [q_heads*head_dim], RoPE applied), p1/p2 = K/V cache, p3 = partials
 //   (fp32 [q_heads][max_splits][head_dim+2]); f0 = softmax scale
 // ET_OP_ATTN_MERGE      task (g): merges the splits and the new token at position s
@@ -176,6 +177,38 @@ __device__ __forceinline__ GemvSpan gemv_span(const et_op& op, int t, int T) {
     return sp;
 }
 
+// Attention splits: the s cached positions form ceil(s/CH) blocks of CH; the
+// call runs min(blocks, cap) split tasks per kv head (cap = i5, the partials'
+// split dimension; at least one with the fused merge) and split c streams blocks
+// [c*bps, min(blocks, (c+1)*bps)), bps = ceil(blocks / splits).
+struct AttnBlocks {
+    long long p0;  // first position
+    int nblk;      // blocks (the last one may be partial)
+};
+
+__device__ __forceinline__ int attn_tasks(const et_op& op, const long long* binding) {
+    const int s = static_cast<int>(binding[op.i[4]]), CH = op.i[2], cap = op.i[5];
+    const int nb = (s + CH - 1) / CH;
+    return nb < cap ? nb : cap;
+}
+__device__ __forceinline__ int attn_splits_with_data(const et_op& op, const long long* binding) {
+    return attn_tasks(op, binding);  // empty splits leave a neutral partial (m = -inf, l = 0)
+}
+__device__ __forceinline__ AttnBlocks attn_blocks(const et_op& op, int c, const long long* binding) {
+    const int s = static_cast<int>(binding[op.i[4]]), CH = op.i[2];
+    const int nb = (s + CH - 1) / CH;
+    const int ns = attn_tasks(op, binding);
+    AttnBlocks a;
+    a.p0 = 0;
+    a.nblk = 0;
+    if (ns <= 0) return a;
+    const int bps = (nb + ns - 1) / ns;
+    const int b0 = c * bps, b1 = (c + 1) * bps < nb ? (c + 1) * bps : nb;
+    a.p0 = static_cast<long long>(b0) * CH;
+    a.nblk = b1 > b0 ? b1 - b0 : 0;
+    return a;
+}
+
 // Plan for a task of `call` at row-major `flat` with sample coords `coord`.
 __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coord, int T, const long long* binding,
                                                 int* const* rt) {
@@ -207,17 +240,20 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
         pl.base[2] = reinterpret_cast<const uint8_t*>(op.p[2]) + (e * RS + r) * rows;
         pl.bytes[0] = pl.bytes[1] = pl.bytes[2] = rows;
     } else if (op.kind == ET_OP_ATTN_SPLIT) {
-        // K rows then V rows of positions [c*CH, min(s, c*CH+CH)), one chunk each
+        // the split's K/V blocks, interleaved K0 V0 K1 V1 ... (one block per chunk)
+        const AttnBlocks a = attn_blocks(op, coord[1], binding);
         const int dh = op.i[0], CH = op.i[2], cap = op.i[3];
         const long long s = binding[op.i[4]];
-        const long long p0 = static_cast<long long>(coord[1]) * CH;
-        const long long p1 = p0 + CH < s ? p0 + CH : s;
-        if (p1 > p0) {
-            const long long off = (static_cast<long long>(coord[0]) * cap + p0) * dh * 2;
+        long long p1 = a.p0 + static_cast<long long>(a.nblk) * CH;
+        if (p1 > s) p1 = s;
+        if (p1 > a.p0) {
+            const long long off = (static_cast<long long>(coord[0]) * cap + a.p0) * dh * 2;
             pl.nseg = 2;
+            pl.interleave = true;
+            pl.cbytes = CH * dh * 2;
             pl.base[0] = reinterpret_cast<const uint8_t*>(op.p[1]) + off;
             pl.base[1] = reinterpret_cast<const uint8_t*>(op.p[2]) + off;
-            pl.bytes[0] = pl.bytes[1] = (p1 - p0) * dh * 2;
+            pl.bytes[0] = pl.bytes[1] = (p1 - a.p0) * dh * 2;
         }
     }
     pl.finish();

@@ -96,8 +96,14 @@ LLAMA3_70B = DecoderConfig("llama3-70b", hidden=8192, layers=80, heads=64, kv_he
 CONFIGS = {c.name: c for c in (TINY, LLAMA3_8B, LLAMA3_70B)}
 
 
-def build_graph(cfg, tasks, lm_tasks, fused_merge=False, call_tasks=None):
-    return etsim.Graph.from_json(json.dumps(graph_spec(cfg, tasks, lm_tasks, fused_merge, call_tasks=call_tasks)))
+def build_graph(cfg, tasks, lm_tasks, fused_merge=False, call_tasks=None, attn_cap=None):
+    return etsim.Graph.from_json(json.dumps(graph_spec(cfg, tasks, lm_tasks, fused_merge, call_tasks=call_tasks,
+                                                       attn_cap=attn_cap)))
+
+
+def attn_split_cap(cfg, max_seq, workers):
+    """Splits per kv head: one per 64-position block up to ~one task per SM."""
+    return max(1, min((max_seq + cfg.attn_chunk - 1) // cfg.attn_chunk, workers // cfg.kv_heads))
 
 
 def balanced_tasks(rows, workers, tile=16):
@@ -207,7 +213,7 @@ class DecodeModel:
         self.lm_tasks = lm_tasks or self.num_workers
         self.samples = sorted(int(s) for s in samples)
         self.capacity = capacity or (self.samples[-1] + 1)
-        self.max_splits = max(1, (self.samples[-1] + cfg.attn_chunk - 1) // cfg.attn_chunk)
+        self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
         self.residual = residual
 
         import time
@@ -220,7 +226,7 @@ class DecodeModel:
             if residual == "double":  # whole-row residual GEMVs too (split-K spans are balanced already)
                 self.call_tasks.update(oproj=balanced_tasks(cfg.hidden, self.tasks),
                                        down=balanced_tasks(cfg.hidden, self.tasks))
-        self.graph = build_graph(cfg, self.tasks, self.lm_tasks, fused_merge, self.call_tasks)
+        self.graph = build_graph(cfg, self.tasks, self.lm_tasks, fused_merge, self.call_tasks, self.max_splits)
         self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3
 

@@ -5,7 +5,7 @@ fixture generator can build the same graphs for the reference implementation.
 
 
 def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allreduce_tasks: int = 0,
-               call_tasks=None):
+               call_tasks=None, attn_cap=None):
     """Reference-format graph spec of one decode step (symbol `s`)."""
     CH = cfg.attn_chunk
     fns, events, calls = [], [], []
@@ -35,11 +35,14 @@ def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allred
         qkv, a, m, o, g, d = (ev(f"{x}{l}", ["1"]) for x in ("QKV", "A", "M", "O", "G", "D"))
         events[-5]["shape"] = [kv]  # A_l has one element per kv head
         call(fn(f"L{l}.qkv", [ct.get("qkv", T)]), ins=[(prev, ["0"])], outs=[(qkv, ["0"])])
+        nsplit = f"(s + {CH - 1}) // {CH}"
+        if attn_cap:  # long contexts: at most attn_cap splits per kv head, each a run of blocks
+            nsplit = f"min({nsplit}, {attn_cap})"
         if fused_merge:  # the last split of each kv head merges the group (no merge stage)
             events.remove(next(e for e in events if e["name"] == a))
-            call(fn(f"L{l}.attn", [kv, f"max((s + {CH - 1}) // {CH}, 1)"]), ins=[(qkv, ["0"])], outs=[(m, ["0"])])
+            call(fn(f"L{l}.attn", [kv, f"max({nsplit}, 1)"]), ins=[(qkv, ["0"])], outs=[(m, ["0"])])
         else:
-            call(fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
+            call(fn(f"L{l}.attn", [kv, nsplit]), ins=[(qkv, ["0"])], outs=[(a, ["t0"])])
             call(fn(f"L{l}.merge", [kv]), ins=[(a, ["t0"]), (qkv, ["0"])], outs=[(m, ["0"])])
         call(fn(f"L{l}.oproj", [ct.get("oproj", T)]), ins=[(m, ["0"])], outs=[(o, ["0"])])
         if allreduce_tasks:  # tensor parallel: row-parallel partials summed across ranks

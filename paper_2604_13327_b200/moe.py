@@ -113,7 +113,7 @@ RT_PER_LAYER = ("topk", "cnt", "ind", "tind", "elist", "eoff")
 
 
 def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=None, route_tasks=1,
-                   group_stage=True):
+                   group_stage=True, attn_cap=None):
     """Reference-format graph spec (ref json_io.cpp:115-230) of one MoE decode step."""
     CH = cfg.attn_chunk
     E, K, RS = cfg.experts, cfg.top_k, cfg.row_splits
@@ -150,14 +150,15 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
         if group_stage:
             ev(x, [str(E)], data_dependent=True, counts=rt["cnt"], writer=route)
         ev(d, ["1"])
+        nsplit = f"(s + {CH - 1}) // {CH}" if not attn_cap else f"min((s + {CH - 1}) // {CH}, {attn_cap})"
         calls.append({"fn": fn(f"L{l}.qkv", [str(qkv_tasks or tasks)]), "in": [{"event": prev, "map": ["0"]}],
                       "out": [{"event": qkv, "map": ["0"]}]})
         if fused_merge:  # the last split of each kv head merges the group
-            calls.append({"fn": fn(f"L{l}.attn", [kv, f"max((s + {CH - 1}) // {CH}, 1)"]),
+            calls.append({"fn": fn(f"L{l}.attn", [kv, f"max({nsplit}, 1)"]),
                           "in": [{"event": qkv, "map": ["0"]}], "out": [{"event": m, "map": ["0"]}]})
         else:
             calls += [
-                {"fn": fn(f"L{l}.attn", [kv, f"(s + {CH - 1}) // {CH}"]), "in": [{"event": qkv, "map": ["0"]}],
+                {"fn": fn(f"L{l}.attn", [kv, nsplit]), "in": [{"event": qkv, "map": ["0"]}],
                  "out": [{"event": a, "map": ["t0"]}]},
                 {"fn": fn(f"L{l}.merge", [kv]), "in": [{"event": a, "map": ["t0"]}, {"event": qkv, "map": ["0"]}],
                  "out": [{"event": m, "map": ["0"]}]}]
@@ -244,7 +245,9 @@ class MoEDecodeModel:
         self.tokens = 1
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
-        self.max_splits = max(1, (self.samples[-1] + cfg.attn_chunk - 1) // cfg.attn_chunk)
+        from .decode import attn_split_cap
+
+        self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
         self.scheduler = scheduler
         t0 = time.perf_counter()
         from .decode import balanced_tasks
@@ -254,7 +257,8 @@ class MoEDecodeModel:
         self.route_tasks = route_tasks or max(1, cfg.experts // 16)
         self.spec = moe_graph_spec(cfg, self.num_workers, self.num_workers, self.tokens, fused_merge=fused_merge,
                                    qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
-                                   if balance else None, route_tasks=self.route_tasks, group_stage=self.group_stage)
+                                   if balance else None, route_tasks=self.route_tasks, group_stage=self.group_stage,
+                                   attn_cap=self.max_splits)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.rt_index = {r["name"]: i for i, r in enumerate(self.spec["runtime_tensors"])}
         if scheduler == "dynamic":

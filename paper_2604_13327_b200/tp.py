@@ -30,7 +30,7 @@ import time
 import torch
 
 from . import etsim
-from .decode import frag16, init_weights, rope_inv_freq
+from .decode import attn_split_cap, frag16, init_weights, rope_inv_freq
 from .graphs import graph_spec
 from .ops import (
     EPI_F32,
@@ -101,13 +101,13 @@ class TPDecodeModel:
         self.num_workers = num_workers or props.multi_processor_count
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
-        self.max_splits = max(1, (self.samples[-1] + cfg.attn_chunk - 1) // cfg.attn_chunk)
         self.local = dataclasses.replace(cfg, heads=cfg.heads // world, kv_heads=cfg.kv_heads // world,
                                          intermediate=cfg.intermediate // world, vocab=cfg.vocab // world)
         self.ar_tasks = ar_tasks or self.num_workers
+        self.max_splits = attn_split_cap(self.local, self.samples[-1], self.num_workers)
         t0 = time.perf_counter()
         spec = graph_spec(self.local, self.num_workers, self.num_workers, fused_merge=True,
-                          allreduce_tasks=self.ar_tasks)
+                          allreduce_tasks=self.ar_tasks, attn_cap=self.max_splits)
         self.graph = etsim.Graph.from_json(json.dumps(spec))
         self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3

@@ -51,3 +51,28 @@ def test_tiny_logits_match_oracle(tiny, s):
     assert mg.check(t) == []
     assert all(c == 0 for c in m.executor.final_counters())
     assert m.last_stats["tasks_executed"] == mg.num_tasks
+
+
+@pytest.fixture(scope="module")
+def tiny_long():
+    # 4 workers -> at most 2 attention splits per kv head: every split streams a run
+    # of 64-position blocks with the online softmax (flash-decoding across blocks)
+    return DecodeModel(TINY, samples=(512,), num_workers=4, seed=0, record_trace=True, keep_logical=True)
+
+
+@pytest.mark.parametrize("s", [300, 512, 65, 1])
+def test_tiny_multi_block_splits_match_oracle(tiny_long, s):
+    m = tiny_long
+    assert m.max_splits == 2
+    m.fill_cache(s, seed=3)
+    m.set_token(11)
+    cpu_k = [k.cpu() for k in m.kcache]
+    cpu_v = [v.cpu() for v in m.vcache]
+    logits = m.step(s)[0].cpu()
+    ref, _, _ = decode_step(m.cfg, weights_to_cpu(m.W_logical), cpu_k, cpu_v, 11, s, m.inv_freq.cpu(),
+                            emulate_bf16=True)
+    err, scale = _errs(logits, ref)
+    assert err <= 2e-3 * scale + 2e-3, (s, err, scale)
+    mg = m.graph.instantiate({"s": s})
+    assert mg.check(m.executor.trace()) == []
+    assert all(c == 0 for c in m.executor.final_counters())
