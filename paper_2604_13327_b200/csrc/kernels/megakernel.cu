@@ -539,12 +539,12 @@ __device__ __noinline__ void qk_norm_rope(float* v, int dh, const float* w, floa
 // operand -- split statistics, the new K/V row and this thread's o partials
 // (in registers, up to 16 splits per pass) -- is requested before the first
 // use, so a pass costs one L2 round trip.
-// kQK: the Qwen3 q/k-norm variant (MoE instantiation only; G * dh <= 1024), else
-// G * dh <= 512 -- the register footprint of the dense kernel stays spill-free.
-template <bool kQK>
+// kWide: G * dh <= 1024 (MoE instantiation: 8 q heads per kv head), else G * dh
+// <= 512 -- the register footprint of the dense kernel stays spill-free.
+template <bool kWide>
 __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op& op, int g, const float* qs,
                                               int qstride, float* scr, int ctid) {
-    constexpr int kPass = kQK ? 8 : 16, kOut = kQK ? 4 : 2;  // splits in registers; outputs per thread
+    constexpr int kPass = kWide ? 8 : 16, kOut = kWide ? 4 : 2;  // splits in registers; outputs per thread
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
     const long long s = P.binding[op.i[4]];
@@ -558,15 +558,13 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     float* wts = ml + 2 * G * nspl;     // [G][nspl]
     float* hs = wts + G * nspl;         // [G]: weight of the new token
     float* kns = hs + G;                // [dh]
-    float* vns = kns + dh;              // [dh] (q/k-norm mode)
-    const bool qk = kQK && (op.flags & 1) != 0;
     float ov[kOut][kPass];
     float vv[kOut];
 #pragma unroll
     for (int j = 0; j < kOut; ++j) {
         const int idx = ctid + j * kConsumers;
         const int hh = idx / dh, d = idx - hh * dh;
-        vv[j] = (idx < G * dh && !qk) ? bf2f(__ldcg(vn + d)) : 0.f;
+        vv[j] = idx < G * dh ? bf2f(__ldcg(vn + d)) : 0.f;
 #pragma unroll
         for (int c = 0; c < kPass; ++c)
             ov[j][c] = (idx < G * dh && c < nspl) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d)
@@ -577,40 +575,8 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
         ml[2 * i] = __ldcg(pr);
         ml[2 * i + 1] = __ldcg(pr + 1);
     }
-    if (!qk) {
-        for (int d = ctid; d < dh; d += kConsumers) kns[d] = bf2f(__ldcg(kn + d));
-    } else if constexpr (kQK) {
-        // Qwen3: the new k is the raw projection -> per-head RMSNorm + RoPE; k and v
-        // are appended to the cache (bf16) and used rounded, as any cached row
-        const float* kr = reinterpret_cast<const float*>(op.p[8]) + static_cast<long long>(g) * dh;
-        const float* vr = kr + static_cast<long long>(op.i[6]) * dh;
-        for (int d = ctid; d < dh; d += kConsumers) {
-            kns[d] = __ldcg(kr + d);
-            vns[d] = __ldcg(vr + d);
-        }
-        bar_sync(1, kConsumers);
-        if (warp == 0)
-            qk_norm_rope(kns, dh, reinterpret_cast<const float*>(op.p[6]), op.f[1],
-                         reinterpret_cast<const float*>(op.p[7]), s, lane);
-        bar_sync(1, kConsumers);
-        uint16_t* kc = const_cast<uint16_t*>(kn);
-        uint16_t* vc = const_cast<uint16_t*>(vn);
-        for (int d = ctid; d < dh; d += kConsumers) {
-            const uint16_t kb = f2bf(kns[d]), vb = f2bf(vns[d]);
-            kc[d] = kb;
-            vc[d] = vb;
-            kns[d] = bf2f(kb);
-            vns[d] = bf2f(vb);
-        }
-    }
+    for (int d = ctid; d < dh; d += kConsumers) kns[d] = bf2f(__ldcg(kn + d));
     bar_sync(1, kConsumers);
-    if (qk) {
-#pragma unroll
-        for (int j = 0; j < kOut; ++j) {
-            const int idx = ctid + j * kConsumers;
-            if (idx < G * dh) vv[j] = vns[idx % dh];
-        }
-    }
     for (int hh = warp; hh < G; hh += kConsumerWarps) {
         float dot = 0.f;
         for (int d = lane; d < dh; d += 32) dot += qs[hh * qstride + d] * kns[d];
@@ -679,10 +645,33 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     }
     if constexpr (kQK) {
         if (op.flags & 1) {  // q-norm + RoPE applied here (q is the raw projection)
+            // fused merge: split 0 also normalises + rotates the new k and appends the
+            // new k/v (bf16) to the cache row s before it arrives, so the merger reads
+            // them like any cached row
+            const bool knew = (op.flags & 2) && c == 0;
+            float* kv = sc;  // [2][dh] scratch before the blocks use sc
+            if (knew) {
+                const float* kr = reinterpret_cast<const float*>(op.p[8]) + static_cast<long long>(g) * dh;
+                const float* vr = kr + static_cast<long long>(op.i[6]) * dh;
+                for (int d = ctid; d < dh; d += kConsumers) {
+                    kv[d] = __ldcg(kr + d);
+                    kv[dh + d] = __ldcg(vr + d);
+                }
+            }
             bar_sync(1, kConsumers);
-            for (int h = warp; h < G; h += kConsumerWarps)
-                qk_norm_rope(qs + h * qstride, dh, reinterpret_cast<const float*>(op.p[(op.flags & 2) ? 9 : 5]),
-                             op.f[1], reinterpret_cast<const float*>(op.p[7]), s, lane);
+            for (int h = warp; h < G + (knew ? 1 : 0); h += kConsumerWarps)
+                qk_norm_rope(h < G ? qs + h * qstride : kv, dh,
+                             reinterpret_cast<const float*>(op.p[h < G ? ((op.flags & 2) ? 9 : 5) : 6]), op.f[1],
+                             reinterpret_cast<const float*>(op.p[7]), s, lane);
+            if (knew) {
+                bar_sync(1, kConsumers);
+                uint16_t* kc = reinterpret_cast<uint16_t*>(op.p[1]) + (static_cast<long long>(g) * op.i[3] + s) * dh;
+                uint16_t* vc = reinterpret_cast<uint16_t*>(op.p[2]) + (static_cast<long long>(g) * op.i[3] + s) * dh;
+                for (int d = ctid; d < dh; d += kConsumers) {
+                    kc[d] = f2bf(kv[d]);
+                    vc[d] = f2bf(kv[dh + d]);
+                }
+            }
         }
     }
     bar_sync(1, kConsumers);
@@ -1051,7 +1040,20 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
     bar_sync(1, kConsumers);
     if (ctid == 0)  // slots grouped by expert, stable in slot order
         for (int sl = 0; sl < nb * K; ++sl) elist[scnt[stop[sl]]++] = sl;
-    __threadfence();
+    // The selected experts' weights cannot be streamed before this point (their ids
+    // exist only now); start pulling them into L2 while the expert tasks get
+    // released.  (Plain writes above are published by the task's NOTIFY release.)
+    if (op.p[9]) {
+        const long long mat = static_cast<long long>(op.i[8]) * H * 2;  // one expert matrix: I x H bf16
+        for (int i = ctid; i < 3 * E; i += kConsumers) {
+            const int e = i / 3, m = i - 3 * e;
+            if (cnt[e] > 0) {
+                const uint8_t* base = reinterpret_cast<const uint8_t*>(op.p[9 + m]) + e * mat;
+                for (long long off = 0; off < mat; off += (1 << 20))
+                    bulk_prefetch_l2(base + off, static_cast<uint32_t>(mat - off < (1 << 20) ? mat - off : (1 << 20)));
+            }
+        }
+    }
 }
 
 // Routed expert task (see expert_task): gate/up rows of its row split for the

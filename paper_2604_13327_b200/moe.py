@@ -233,8 +233,8 @@ class MoEDecodeModel:
     """One MoE decoder + its lowered megakernel (static or dynamic scheduler)."""
 
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
-                 scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=False,
-                 balance=False, route_tasks=None, group_stage=None):
+                 scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=True,
+                 balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
@@ -254,6 +254,7 @@ class MoEDecodeModel:
 
         self.fused_merge = fused_merge
         self.group_stage = (scheduler == "dynamic") if group_stage is None else group_stage
+        self.l2_prefetch_experts = l2_prefetch_experts
         self.route_tasks = route_tasks or max(1, cfg.experts // 16)
         self.spec = moe_graph_spec(cfg, self.num_workers, self.num_workers, self.tokens, fused_merge=fused_merge,
                                    qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
@@ -334,10 +335,13 @@ class MoEDecodeModel:
             ops.append(make_op(OP_GEMV, i=[H, nq, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],
                                p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h)]))
             assert [ri[n] for n in RT_PER_LAYER] == list(range(ri["topk"], ri["topk"] + len(RT_PER_LAYER)))
-            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, -1, K, 16, 0, H, ri["topk"], 0, RS, TS],
+            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, -1, K, 16, cfg.expert_inter, H, ri["topk"], 0, RS,
+                                                TS],
                                f=[cfg.eps],
                                p=[ptr(L["router"]), 0, ptr(self.h), ptr(L["ffn_norm"]), ptr(self.logits_r[l]),
-                                  ptr(self.xn[l]), ptr(self.wslot[l]), ptr(self.arrive[l:l + 1]), ptr(self.tiles[l])],
+                                  ptr(self.xn[l]), ptr(self.wslot[l]), ptr(self.arrive[l:l + 1]), ptr(self.tiles[l]),
+                                  ptr(L["wgate"]) if self.l2_prefetch_experts else 0, ptr(L["wup"]),
+                                  ptr(L["wdown"])],
                                flags=1 if self.injected else 0))
             if self.group_stage:
                 ops.append(make_op(OP_NONE))  # group: the routed notify is the Event Tensor edge itself
