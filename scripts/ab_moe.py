@@ -10,8 +10,12 @@ CODE = r'''
 import json, statistics, sys
 sys.path.insert(0, sys.argv[1])
 from paper_2604_13327_b200.moe import MOE_CONFIGS, MoEDecodeModel
+import dataclasses
 kw = json.loads(sys.argv[2])
-m = MoEDecodeModel(MOE_CONFIGS["qwen3-30b-a3b"], samples=(1024,), **kw)
+cfg = MOE_CONFIGS["qwen3-30b-a3b"]
+if "attn_chunk" in kw:
+    cfg = dataclasses.replace(cfg, attn_chunk=kw.pop("attn_chunk"))
+m = MoEDecodeModel(cfg, samples=(1024,), **kw)
 m.fill_cache(1024); m.set_token(1)
 ts = [m.executor.run({"s": 1024})["kernel_ms"] for _ in range(12)]
 print(json.dumps({"median_ms": statistics.median(ts[3:])}))
