@@ -1482,9 +1482,9 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
 __device__ __forceinline__ void fence_sc_gpu() { asm volatile("fence.sc.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t dyn_init(const StaticParams& P, const DynParams& D, int el) {
-    const int t = __ldg(D.el_dd + el);
-    if (t < 0) return static_cast<uint32_t>(__ldg(P.initial_counts + el));
-    return static_cast<uint32_t>(__ldcg(P.rt[D.dd_counts_rt[t]] + (el - D.dd_base[t])));
+    const int4 info = __ldg(D.el_info + el);
+    if (info.z < 0) return static_cast<uint32_t>(info.w);
+    return static_cast<uint32_t>(__ldcg(P.rt[D.dd_counts_rt[info.z]] + (el - D.dd_base[info.z])));
 }
 
 __device__ __forceinline__ bool dyn_visible(const DynParams& D, int el) {
@@ -1504,8 +1504,8 @@ __device__ void dyn_push(const StaticParams& P, const DynParams& D, int task) {
 __device__ void dyn_fire(const StaticParams& P, const DynParams& D, int el) {
     if (atomicExch(&D.fired[el], 1u) != 0u) return;
     for (int k = __ldg(D.consumer_off + el), e = __ldg(D.consumer_off + el + 1); k < e; ++k) {
-        const int c = __ldg(D.consumers + k);
-        if (atomicSub(&D.rem[c], 1) == 1) dyn_push(P, D, c);
+        const int ce = __ldg(D.consumers + k), c = ce & 0x7fffffff;
+        if (ce < 0 || atomicSub(&D.rem[c], 1) == 1) dyn_push(P, D, c);
     }
     const int t = __ldg(D.el_dd + el);
     if (t >= 0 && D.dd_range_call[t] >= 0) {
@@ -1582,17 +1582,22 @@ __device__ __forceinline__ void dyn_push_warp(const StaticParams& P, const DynPa
 }
 
 __device__ __noinline__ void dyn_fire_warp(const StaticParams& P, const DynParams& D, int el, int lane) {
-    int first = 0;
-    if (lane == 0) first = atomicExch(&D.fired[el], 1u) == 0u;
-    if (!__shfl_sync(0xffffffffu, first, 0)) return;
-    const int cb = __ldg(D.consumer_off + el), ce = __ldg(D.consumer_off + el + 1);
+    const int4 info = __ldg(D.el_info + el);  // (consumers begin, end, dd tensor, initial count)
+    if (info.z >= 0) {  // a data-dependent element can be fired by its count and by the reveal
+        int first = 0;
+        if (lane == 0) first = atomicExch(&D.fired[el], 1u) == 0u;
+        if (!__shfl_sync(0xffffffffu, first, 0)) return;
+    }
+    const int cb = info.x, ce = info.y;
     for (int k0 = cb; k0 < ce; k0 += 32) {
         const int k = k0 + lane;
-        const int c = k < ce ? __ldg(D.consumers + k) : -1;
-        const bool ready = c >= 0 && atomicSub(&D.rem[c], 1) == 1;
+        const int e = k < ce ? __ldg(D.consumers + k) : 0;
+        const int c = e & 0x7fffffff;
+        // bit 31: this element is the consumer's only pending wait -> ready now
+        const bool ready = k < ce && (e < 0 || atomicSub(&D.rem[c], 1) == 1);
         dyn_push_warp(P, D, c, ready, lane);
     }
-    const int t = __ldg(D.el_dd + el);
+    const int t = info.z;
     if (t >= 0 && D.dd_range_call[t] >= 0) {
         const int call = D.dd_range_call[t];
         const int* ip = P.rt[__ldg(D.call_range_rt + call)];
@@ -1658,8 +1663,12 @@ __device__ void dyn_count_warp(const StaticParams& P, const DynParams& D, unsign
         const uint32_t need = dyn_init(P, D, el);
         if (ctr == P.cnt && old >= need) report(P.status, ET_ERR_UNDERFLOW, worker, task, el, -1);
         if (may_fire && old + 1 == need) {
-            fence_sc_gpu();
-            fire = dyn_visible(D, el);
+            if (__ldg(D.el_dd + el) < 0) {
+                fire = 1;  // static element: only this notify can complete it
+            } else {
+                fence_sc_gpu();  // ordered against the reveal of the data-dependent tensor
+                fire = dyn_visible(D, el);
+            }
         }
     }
     if (__shfl_sync(0xffffffffu, fire, 0)) dyn_fire_warp(P, D, el, lane);
@@ -1706,30 +1715,32 @@ __device__ int dyn_pop(const StaticParams& P, const DynParams& D, int cls, int w
     }
 }
 
-__device__ SlotView dyn_view(const StaticParams& P, const DynParams& D, int task) {
+// A task's slot view from its packed records; masking compares the coordinates
+// with the call's grid extents at this launch's binding (shared-memory table
+// filled at kernel start when the graph has <= kMaxCallExt calls of rank <= 2).
+__device__ SlotView dyn_view(const StaticParams& P, const DynParams& D, int task, const int2* cext = nullptr) {
     SlotView v;
-    v.call = __ldg(D.task_call + task);
-    const int rank = __ldg(P.call_rank + v.call);
-    int flat = __ldg(D.task_flat + task);
-    int ext[kMaxRank];
-    for (int d = 0; d < kMaxRank; ++d) ext[d] = d < rank ? __ldg(P.call_extents + v.call * 4 + d) : 1;
-    v.ext0 = ext[0];
-    for (int d = kMaxRank - 1; d >= 0; --d) {
-        if (d >= rank) {
-            v.coord[d] = 0;
-            continue;
-        }
-        v.coord[d] = flat % ext[d];
-        flat /= ext[d];
+    const int4 d = __ldg(D.task_desc + task);
+    const int4 r = __ldg(D.task_rng + task);
+    v.call = d.x;
+    v.coord[0] = d.y;
+    v.coord[1] = d.z;
+    v.coord[2] = v.coord[3] = 0;
+    v.ext0 = d.w;
+    if (cext) {
+        const int2 e = cext[v.call];
+        v.masked = v.coord[0] >= e.x || v.coord[1] >= e.y;
+    } else {
+        const int rank = __ldg(P.call_rank + v.call);
+        v.masked = false;
+        for (int k = 0; k < rank && k < 2; ++k)
+            if (v.coord[k] >= eval_code(P, v.call, k)) v.masked = true;
     }
-    v.masked = false;
-    for (int d = 0; d < rank; ++d)
-        if (v.coord[d] >= eval_code(P, v.call, d)) v.masked = true;
     v.lazy = false;
-    v.wb = __ldg(D.task_wait_off + task);
-    v.we = __ldg(D.task_wait_off + task + 1);
-    v.nb = __ldg(D.task_notify_off + task);
-    v.ne = __ldg(D.task_notify_off + task + 1);
+    v.wb = r.x;
+    v.we = r.y;
+    v.nb = r.z;
+    v.ne = r.w;
     return v;
 }
 
@@ -1808,6 +1819,7 @@ __device__ void dyn_record(const StaticParams& P, const DynParams& D, int task, 
 template <bool kMoE>
 __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
     const int ctid = threadIdx.x;
+    const int2* cext = P.num_calls <= kMaxCallExt ? reinterpret_cast<const int2*>(smem + kSmemCallExt) : nullptr;
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
     float* acc = reinterpret_cast<float*>(smem + kSmemAcc);
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
@@ -1828,7 +1840,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
         bar_sync(1, kConsumers);
         const int task = misc[3];
         if (task < 0) break;
-        SlotView v = dyn_view(P, D, task);
+        SlotView v = dyn_view(P, D, task, cext);
         const et_op& opg = P.ops[v.call];  // shared-memory copy, as in the static loop
         if (ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
             reinterpret_cast<int*>(smem + kSmemOp)[ctid - 32] = reinterpret_cast<const int*>(&opg)[ctid - 32];
@@ -1904,6 +1916,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
 
 __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
     if ((threadIdx.x & 31) != 0) return;
+    const int2* cext = P.num_calls <= kMaxCallExt ? reinterpret_cast<const int2*>(smem + kSmemCallExt) : nullptr;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
     uint64_t* empty = full + kStages;
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
@@ -1917,7 +1930,7 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
         gen = misc[5];
         const int task = misc[4];
         if (task < 0) return;
-        const SlotView v = dyn_view(P, D, task);
+        const SlotView v = dyn_view(P, D, task, cext);
         if (v.masked) continue;
         const et_op& op = P.ops[v.call];
         if (!op_streams(op.kind)) continue;
@@ -1938,14 +1951,14 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
 }
 
 // DMA-class tasks: popped from their own queue by worker 0's DMA warp.
-__device__ void dyn_dma_loop(const StaticParams& P, const DynParams& D) {
+__device__ void dyn_dma_loop(const StaticParams& P, const DynParams& D, const int2* cext) {
     if ((threadIdx.x & 31) != 0) return;
     const int worker = P.num_queues;
     for (;;) {
         const int task = dyn_pop(P, D, 1, worker);
         if (task < 0) return;
         const uint64_t tb = globaltimer();
-        const SlotView v = dyn_view(P, D, task);
+        const SlotView v = dyn_view(P, D, task, cext);
         if (!dyn_prepare(P, D, v, task, worker)) return;
         const uint64_t tw = globaltimer();
         if (!v.masked && P.tick_ns > 0 && D.task_duration) {
@@ -2009,6 +2022,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         misc[3] = misc[4] = misc[5] = 0;
         if (worker == 0) atomicAdd(&P.status->pushes, static_cast<unsigned long long>(D.num_ready[0] + D.num_ready[1]));
     }
+    if (P.num_calls <= kMaxCallExt) {  // grid extents of every call at this binding (masking)
+        int2* cext = reinterpret_cast<int2*>(smem + kSmemCallExt);
+        for (int c = threadIdx.x; c < P.num_calls; c += blockDim.x) {
+            const int rank = __ldg(P.call_rank + c);
+            cext[c] = make_int2(rank > 0 ? static_cast<int>(eval_code(P, c, 0)) : 1,
+                                rank > 1 ? static_cast<int>(eval_code(P, c, 1)) : 1);
+        }
+    }
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     if (warp < kConsumerWarps) {
@@ -2016,7 +2037,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == kProducerWarp) {
         dyn_producer_loop(P, D, worker, smem);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
-        dyn_dma_loop(P, D);
+        dyn_dma_loop(P, D, P.num_calls <= kMaxCallExt ? reinterpret_cast<const int2*>(smem + kSmemCallExt) : nullptr);
     }
 }
 

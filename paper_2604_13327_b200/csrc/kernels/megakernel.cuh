@@ -159,7 +159,16 @@ struct DynParams {
     unsigned int* disp_other;
     unsigned long long* push_time;
     int writer_tasks[kMaxDd];    // task count of each dd tensor's writer call
+    // packed per-task / per-element records (one 16-byte load each on the hot path)
+    const int4* task_desc;       // (call, coord0, coord1, ext0 of the call at the sample)
+    const int4* task_rng;        // (wait_off, wait_end, notify_off, notify_end)
+    const int4* el_info;         // (consumer_off, consumer_end, dd tensor or -1, initial count)
+    // consumers[] entries carry bit 31 when that consumer has exactly one pending
+    // wait (it is ready the moment the element fires: no rem[] decrement needed)
 };
+
+constexpr int kSmemCallExt = kSmemTable;       // dynamic kernel: per-call grid extents at the binding (int2)
+constexpr int kMaxCallExt = (kSmemBar - kSmemTable) / 8;
 
 }  // namespace etk
 

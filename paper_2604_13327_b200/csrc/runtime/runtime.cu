@@ -64,6 +64,7 @@ struct Sample {
     DevArray<int32_t> d_task_call, d_task_flat, d_task_duration, d_task_wait_off, d_task_waits, d_task_notify_off,
         d_task_notifies, d_task_rem_init, d_task_class, d_consumer_off, d_consumers, d_call_first_task, d_call_routed_rt,
         d_call_routed_base, d_call_range_rt, d_call_range_base, d_el_dd, d_ready;
+    DevArray<int4> d_task_desc, d_task_rng, d_el_info;
     DevArray<uint8_t> d_task_wait_armed, d_call_range_armed;
 };
 
@@ -301,6 +302,9 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
     int rc = et_upload_static(rt, s, num_samples);  // sample bindings, extents, counters, status
     if (rc != ET_OK) return rc;
     rt->mode = ET_MODE_DYNAMIC;
+    for (int c = 0; c < rt->num_calls; ++c)
+        if (rt->call_rank[static_cast<size_t>(c)] > 2)
+            return rt->fail(ET_ERR_INVALID, "the dynamic scheduler supports grids of rank <= 2");
     int max_tasks = 1;
     for (int i = 0; i < num_samples; ++i) {
         const et_dynamic_desc& d = dyn[i];
@@ -347,6 +351,33 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
         ET_CUDA(S.d_call_range_base.upload(d.call_range_base, ncall), "upload dynamic");
         ET_CUDA(S.d_call_range_armed.upload(d.call_range_armed, ncall), "upload dynamic");
         ET_CUDA(S.d_el_dd.upload(d.el_dd, static_cast<size_t>(std::max(1, S.num_counters))), "upload dynamic");
+        {  // packed records for the device hot path
+            std::vector<int4> desc(nt), rng(nt), info(static_cast<size_t>(std::max(1, S.num_counters)));
+            for (int t = 0; t < d.num_tasks; ++t) {
+                const int c = d.task_call[t];
+                const int rank = rt->call_rank[static_cast<size_t>(c)];
+                int flat = d.task_flat[t];
+                int coord[4] = {0, 0, 0, 0};
+                for (int k = rank - 1; k >= 0; --k) {
+                    const int e = S.call_extents[static_cast<size_t>(c * 4 + k)];
+                    coord[k] = e > 0 ? flat % e : 0;
+                    flat = e > 0 ? flat / e : 0;
+                }
+                desc[static_cast<size_t>(t)] = make_int4(c, coord[0], coord[1], S.call_extents[static_cast<size_t>(c * 4)]);
+                rng[static_cast<size_t>(t)] = make_int4(d.task_wait_off[t], d.task_wait_off[t + 1], d.task_notify_off[t],
+                                                        d.task_notify_off[t + 1]);
+            }
+            for (int el = 0; el < S.num_counters; ++el)
+                info[static_cast<size_t>(el)] = make_int4(d.consumer_off[el], d.consumer_off[el + 1], d.el_dd[el],
+                                                          s[i].initial_counts[el]);
+            std::vector<int32_t> cons(d.consumers, d.consumers + d.consumer_off[S.num_counters]);
+            for (auto& c : cons)
+                if (d.task_rem_init[c] == 1 && d.call_range_rt[d.task_call[c]] < 0) c |= static_cast<int32_t>(0x80000000u);
+            ET_CUDA(S.d_consumers.upload(cons.empty() ? nullptr : cons.data(), nc), "upload dynamic");
+            ET_CUDA(S.d_task_desc.upload(desc.data(), nt), "upload dynamic");
+            ET_CUDA(S.d_task_rng.upload(rng.data(), nt), "upload dynamic");
+            ET_CUDA(S.d_el_info.upload(info.data(), info.size()), "upload dynamic");
+        }
         ET_CUDA(S.d_ready.upload(ready.empty() ? nullptr : ready.data(), std::max<size_t>(1, ready.size())),
                 "upload dynamic");
         etk::DynParams& P = S.dyn;
@@ -385,6 +416,9 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
             P.writer_tasks[t] = wt;
         }
         P.el_dd = S.d_el_dd.ptr;
+        P.task_desc = S.d_task_desc.ptr;
+        P.task_rng = S.d_task_rng.ptr;
+        P.el_info = S.d_el_info.ptr;
         P.num_ready[0] = static_cast<int>(ready0.size());
         P.num_ready[1] = static_cast<int>(ready1.size());
         P.class_total[0] = totals[0];
