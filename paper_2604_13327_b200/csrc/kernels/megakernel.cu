@@ -387,12 +387,15 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     const int warp = ctid >> 5, lane = ctid & 31;
     const int N = op.i[0], K = op.i[1], nseg = op.i[2];
     const int nb = batch_of(op, P);
-    const GemvSpan sp = gemv_span(op, si.coord[0], si.ext0);
+    // flags bit 4: grouped GEMV -- coord 0 selects the group's weight matrix and
+    // activation slice, coord 1 the row span among i9 tasks per group
+    const bool grouped = (op.flags & 16) != 0;
+    const GemvSpan sp = gemv_span(op, grouped ? si.coord[1] : si.coord[0], grouped ? op.i[9] : si.ext0);
     const int r0 = sp.row0, R = sp.rows;
 
     // ---- prologue: activations into shared memory (bf16 [nb][K]), accumulators zeroed
     if (op.i[3] == 0) {
-        const uint16_t* x = reinterpret_cast<const uint16_t*>(op.p[2]);
+        const uint16_t* x = reinterpret_cast<const uint16_t*>(op.p[2]) + (grouped ? static_cast<long long>(si.coord[0]) * K : 0);
         const int nv = nb * K / 8;
         for (int v = ctid; v < nv; v += kConsumers)
             reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x) + v);
@@ -467,8 +470,14 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
         float* qout = reinterpret_cast<float*>(op.p[4]);
         uint16_t* kc = reinterpret_cast<uint16_t*>(op.p[6]);
         uint16_t* vc = reinterpret_cast<uint16_t*>(op.p[7]);
+        const int G = nq / nkv, grows = (G + 2) * dh;  // flags bit 3: rows grouped by kv head
         for (int pr = ctid; pr < R / 2; pr += kConsumers) {
-            const int row = r0 + 2 * pr;
+            int row = r0 + 2 * pr;
+            if (op.flags & 8) {  // (q heads of group g, k head g, v head g) -> the global row order
+                const int g = row / grows, w = row - g * grows;
+                row = w < G * dh ? g * G * dh + w : w < (G + 1) * dh ? nq + g * dh + (w - G * dh)
+                                                                    : nq + nkv + g * dh + (w - (G + 1) * dh);
+            }
             float a = acc[(2 * pr) * nb], b = acc[(2 * pr + 1) * nb];
             if (row < nq + nkv) {  // q or k: rotate the interleaved pair
                 const int d = row % dh;

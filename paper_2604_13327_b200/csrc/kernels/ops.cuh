@@ -9,7 +9,10 @@
 //   i1 = parts; p1 = partials, p2 = out (int32 [n])
 // ET_OP_GEMV            task t of T computes its span (gemv_span) of every segment (T = call grid
 //   extent); epilogues: F32/BF16 store, RESID out = p5 + y, SILU_MUL out = silu(y0) * y1,
-//   QKV_ROPE (RoPE on q/k pairs, k/v appended to the cache), ADD out += y (red.global.add)
+//   QKV_ROPE (RoPE on q/k pairs, k/v appended to the cache), ADD out += y (red.global.add).
+//   flags bit 3 (QKV_ROPE): the weight rows are grouped per kv head (G q heads, k head, v head);
+//   flags bit 4: grouped GEMV -- task (g, t) of grid [groups, i9]: matrix g (bf16 [N][K] frag16, the
+//   matrices stacked at p0) times activation slice g (p2 + g*K), rows split over i9 tasks
 //   i0 = N rows per segment, i1 = K, i2 = segments (1|2), i3 = x mode (0 bf16 [b][K] at p2,
 //   1 fp32 residual stream at p2 normalised with RMSNorm gamma p3), i4 = epilogue (GemvEpi),
 //   i5 = batch symbol slot (-1: b = 1), i6 = position symbol slot, i7 = row alignment,
@@ -217,10 +220,12 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
     pl.cbytes = kStageBytes;
     pl.interleave = false;
     if (op.kind == ET_OP_GEMV) {
-        const GemvSpan sp = gemv_span(op, coord[0], T);
+        const bool grouped = (op.flags & 16) != 0;  // coord 0 = group (its own matrix), coord 1 = row span
+        const GemvSpan sp = gemv_span(op, grouped ? coord[1] : coord[0], grouped ? op.i[9] : T);
+        const long long gofs = grouped ? static_cast<long long>(coord[0]) * op.i[0] * op.i[1] * 2 : 0;
         pl.nseg = op.i[2];
         for (int s = 0; s < pl.nseg; ++s) {
-            pl.base[s] = reinterpret_cast<const uint8_t*>(op.p[s]) + sp.u0 * 512;
+            pl.base[s] = reinterpret_cast<const uint8_t*>(op.p[s]) + gofs + sp.u0 * 512;
             pl.bytes[s] = (sp.u1 - sp.u0) * 512;
         }
     } else if (op.kind == ET_OP_MOE_ROUTE) {

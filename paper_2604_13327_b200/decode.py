@@ -144,15 +144,39 @@ def frag16(w):
 GEMV_WEIGHTS = ("wqkv", "wo", "wgate", "wup", "wdown")
 
 
-def device_layout(W, keep_logical=False):
-    """Weight dict the megakernel reads: every GEMV matrix in frag16 order.  With
-    keep_logical the row-major originals stay referenced (the CPU oracle reads
-    them); otherwise they are dropped as each layer is converted."""
+def group_qkv_rows(w, cfg):
+    """Wqkv rows reordered per kv head: (its G q heads, its k head, its v head)."""
+    dh, G, nkv = cfg.head_dim, cfg.heads // cfg.kv_heads, cfg.kv_heads
+    q = w[: cfg.q_rows].reshape(nkv, G * dh, -1)
+    k = w[cfg.q_rows: cfg.q_rows + cfg.kv_rows].reshape(nkv, dh, -1)
+    v = w[cfg.q_rows + cfg.kv_rows:].reshape(nkv, dh, -1)
+    return torch.cat([q, k, v], dim=1).reshape(w.shape[0], -1)
+
+
+def group_wo(w, cfg):
+    """Wo split by kv-head group along its input columns: [kv][H][G*dh], each frag16."""
+    cols = (cfg.heads // cfg.kv_heads) * cfg.head_dim
+    return torch.stack([frag16(w[:, g * cols:(g + 1) * cols].contiguous()) for g in range(cfg.kv_heads)])
+
+
+def device_layout(W, keep_logical=False, cfg=None, grouped=False):
+    """Weight dict the megakernel reads: every GEMV matrix in frag16 order (grouped:
+    Wqkv rows per kv head, Wo split per kv-head group).  With keep_logical the
+    row-major originals stay referenced (the CPU oracle reads them); otherwise
+    they are dropped as each layer is converted."""
     D = {"embed": W["embed"], "final_norm": W["final_norm"], "lm_head": frag16(W["lm_head"]), "layers": []}
     if not keep_logical:
         W["lm_head"] = None
     for L in W["layers"]:
-        D["layers"].append({k: (frag16(v) if k in GEMV_WEIGHTS else v) for k, v in L.items()})
+        d = {}
+        for k, v in L.items():
+            if grouped and k == "wqkv":
+                d[k] = frag16(group_qkv_rows(v, cfg).contiguous())
+            elif grouped and k == "wo":
+                d[k] = group_wo(v, cfg)
+            else:
+                d[k] = frag16(v) if k in GEMV_WEIGHTS else v
+        D["layers"].append(d)
         if not keep_logical:
             for k in GEMV_WEIGHTS:
                 L[k] = None
@@ -202,7 +226,7 @@ class DecodeModel:
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
-                 l2_prefetch=-1, residual="split", fused_merge=True, balance=True):
+                 l2_prefetch=-1, residual="split", fused_merge=True, balance=True, grouped=True):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -226,14 +250,22 @@ class DecodeModel:
             if residual == "double":  # whole-row residual GEMVs too (split-K spans are balanced already)
                 self.call_tasks.update(oproj=balanced_tasks(cfg.hidden, self.tasks),
                                        down=balanced_tasks(cfg.hidden, self.tasks))
-        self.graph = build_graph(cfg, self.tasks, self.lm_tasks, fused_merge, self.call_tasks, self.max_splits)
+        self.grouped = grouped and fused_merge and residual == "split" and balance and \
+            self.call_tasks["qkv"] % cfg.kv_heads == 0
+        self.oproj_group_tasks = max(1, self.tasks // cfg.kv_heads)
+        while (cfg.hidden // 16) % self.oproj_group_tasks:
+            self.oproj_group_tasks -= 1
+        self.graph = etsim.Graph.from_json(json.dumps(graph_spec(
+            cfg, self.tasks, self.lm_tasks, fused_merge, call_tasks=self.call_tasks, attn_cap=self.max_splits,
+            grouped=self.grouped, oproj_group_tasks=self.oproj_group_tasks)))
         self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3
 
         dev = self.device
         W = weights if weights is not None else init_weights(cfg, dev, seed)
         self.W_logical = W if keep_logical else None           # row-major bf16; the CPU oracle reads these
-        self.W = device_layout(W, keep_logical=keep_logical or weights is not None)  # what the megakernel reads
+        self.W = device_layout(W, keep_logical=keep_logical or weights is not None, cfg=cfg,
+                               grouped=self.grouped)  # what the megakernel reads
         self.kcache = [torch.zeros(cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
                        for _ in range(cfg.layers)]
         self.vcache = [torch.zeros_like(k) for k in self.kcache]
@@ -265,7 +297,7 @@ class DecodeModel:
         for l, L in enumerate(W["layers"]):
             kc, vc = self.kcache[l], self.vcache[l]
             ops.append(make_op(OP_GEMV, i=[cfg.q_rows + 2 * cfg.kv_rows, H, 1, 1, EPI_QKV_ROPE, -1, s_slot, 16, dh, H,
-                                           cfg.q_rows, cfg.kv_rows, self.capacity],
+                                           cfg.q_rows, cfg.kv_rows, self.capacity], flags=8 if self.grouped else 0,
                                f=[cfg.eps], p=[ptr(L["wqkv"]), 0, ptr(self.h_a), ptr(L["attn_norm"]), ptr(self.q), 0,
                                                ptr(kc), ptr(vc), ptr(self.inv_freq)]))
             attn_i = [dh, G, CH, self.capacity, s_slot, self.max_splits, cfg.kv_heads]
@@ -275,7 +307,12 @@ class DecodeModel:
             else:
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p))
                 ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale], p=attn_p))
-            if self.residual == "split":
+            if self.grouped:
+                # per kv-head group: h += Wo[:, group cols] a_group (red.global.add), each
+                # group's tasks released by its own merge
+                ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 0, EPI_ADD, -1, 0, 16, 0, self.oproj_group_tasks],
+                                   flags=16, p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_a)]))
+            elif self.residual == "split":
                 # row-parallel products add into the residual stream in place: split-K
                 # spans (every task streams the same bytes), red.global.add epilogue
                 ops.append(make_op(OP_GEMV, i=[H, cfg.q_rows, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],

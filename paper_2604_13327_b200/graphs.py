@@ -5,7 +5,7 @@ fixture generator can build the same graphs for the reference implementation.
 
 
 def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allreduce_tasks: int = 0,
-               call_tasks=None, attn_cap=None):
+               call_tasks=None, attn_cap=None, grouped=False, oproj_group_tasks=16):
     """Reference-format graph spec of one decode step (symbol `s`)."""
     CH = cfg.attn_chunk
     fns, events, calls = [], [], []
@@ -34,6 +34,26 @@ def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allred
     for l in range(cfg.layers):
         qkv, a, m, o, g, d = (ev(f"{x}{l}", ["1"]) for x in ("QKV", "A", "M", "O", "G", "D"))
         events[-5]["shape"] = [kv]  # A_l has one element per kv head
+        if grouped:
+            # fine-grained Event Tensors: QKV and M have one element per kv head, so a
+            # head group's attention starts when its own q/k/v rows are done and its
+            # output projection when its own merge is done
+            assert fused_merge, "grouped layers use the fused attention merge"
+            Tq = int(ct.get("qkv", T))
+            assert Tq % cfg.kv_heads == 0, (Tq, cfg.kv_heads)
+            events[-6]["shape"] = [kv]  # QKV_l
+            events[-4]["shape"] = [kv]  # M_l
+            call(fn(f"L{l}.qkv", [str(Tq)]), ins=[(prev, ["0"])], outs=[(qkv, [f"t0 // {Tq // cfg.kv_heads}"])])
+            events.remove(next(e for e in events if e["name"] == a))
+            nsplit = f"(s + {CH - 1}) // {CH}"
+            if attn_cap:
+                nsplit = f"min({nsplit}, {attn_cap})"
+            call(fn(f"L{l}.attn", [kv, f"max({nsplit}, 1)"]), ins=[(qkv, ["t0"])], outs=[(m, ["t0"])])
+            call(fn(f"L{l}.oproj", [kv, str(oproj_group_tasks)]), ins=[(m, ["t0"])], outs=[(o, ["0"])])
+            call(fn(f"L{l}.gateup", [ct.get("gateup", T)]), ins=[(o, ["0"])], outs=[(g, ["0"])])
+            call(fn(f"L{l}.down", [ct.get("down", T)]), ins=[(g, ["0"])], outs=[(d, ["0"])])
+            prev = d
+            continue
         call(fn(f"L{l}.qkv", [ct.get("qkv", T)]), ins=[(prev, ["0"])], outs=[(qkv, ["0"])])
         nsplit = f"(s + {CH - 1}) // {CH}"
         if attn_cap:  # long contexts: at most attn_cap splits per kv head, each a run of blocks
