@@ -105,7 +105,11 @@ def cpu_reference_step_us(cfg, seq, budget_s=12.0):
     Returns (us_per_token, detail dict)."""
     import torch
 
-    from paper_2604_13327_b200.decode import attn_split_cap, balanced_tasks, build_graph
+    from paper_2604_13327_b200 import etsim
+    from paper_2604_13327_b200.decode import decode_graph_spec
+
+    def etsim_graph_from_spec(spec):
+        return etsim.Graph.from_json(json.dumps(spec))
 
     detail = {}
     sim_us = None
@@ -124,10 +128,7 @@ def cpu_reference_step_us(cfg, seq, budget_s=12.0):
     )
     try:
         # the same decode graph DecodeModel lowers (148 workers)
-        g = build_graph(cfg, 148, 148, fused_merge=True,
-                        call_tasks={"qkv": balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, 148),
-                                    "gateup": balanced_tasks(cfg.intermediate, 148)},
-                        attn_cap=attn_split_cap(cfg, seq, 148))
+        g = etsim_graph_from_spec(decode_graph_spec(cfg, 148, seq)[0])
         detail["graph_tasks"] = g.instantiate({"s": seq}).num_tasks
         out = subprocess.run([sys.executable, "-c", code], input=g.to_json(),
                              capture_output=True, text=True, timeout=budget_s * 3 + 60)

@@ -101,6 +101,28 @@ def build_graph(cfg, tasks, lm_tasks, fused_merge=False, call_tasks=None, attn_c
                                                        attn_cap=attn_cap)))
 
 
+def decode_graph_spec(cfg, workers, max_seq, lm_tasks=None, residual="split", fused_merge=True, balance=True,
+                      grouped=True):
+    """The decode-step graph DecodeModel lowers (reference JSON spec) and the
+    layout choices it implies: per-call task counts, kv-head grouping, the
+    attention split cap."""
+    call_tasks = None
+    if balance:  # whole-row GEMVs get a task count that divides their row tiles evenly
+        call_tasks = {"qkv": balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, workers),
+                      "gateup": balanced_tasks(cfg.intermediate, workers)}
+        if residual == "double":  # whole-row residual GEMVs too (split-K spans are balanced already)
+            call_tasks.update(oproj=balanced_tasks(cfg.hidden, workers), down=balanced_tasks(cfg.hidden, workers))
+    grouped = bool(grouped and fused_merge and residual == "split" and balance and
+                   call_tasks["qkv"] % cfg.kv_heads == 0)
+    og = max(1, workers // cfg.kv_heads)
+    while (cfg.hidden // 16) % og:
+        og -= 1
+    cap = attn_split_cap(cfg, max_seq, workers)
+    spec = graph_spec(cfg, workers, lm_tasks or workers, fused_merge, call_tasks=call_tasks, attn_cap=cap,
+                      grouped=grouped, oproj_group_tasks=og)
+    return spec, {"call_tasks": call_tasks, "grouped": grouped, "oproj_group_tasks": og, "attn_cap": cap}
+
+
 def attn_split_cap(cfg, max_seq, workers):
     """Splits per kv head: one per 64-position block up to ~one task per SM."""
     return max(1, min((max_seq + cfg.attn_chunk - 1) // cfg.attn_chunk, workers // cfg.kv_heads))
@@ -226,7 +248,8 @@ class DecodeModel:
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
-                 l2_prefetch=-1, residual="split", fused_merge=True, balance=True, grouped=True):
+                 l2_prefetch=-1, residual="split", fused_merge=True, balance=True, grouped=True,
+                 scheduler="static", early_push=False):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -243,22 +266,18 @@ class DecodeModel:
         import time
         t0 = time.perf_counter()
         self.fused_merge = fused_merge
-        self.call_tasks = None
-        if balance:  # whole-row GEMVs get a task count that divides their row tiles evenly
-            self.call_tasks = {"qkv": balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.tasks),
-                               "gateup": balanced_tasks(cfg.intermediate, self.tasks)}
-            if residual == "double":  # whole-row residual GEMVs too (split-K spans are balanced already)
-                self.call_tasks.update(oproj=balanced_tasks(cfg.hidden, self.tasks),
-                                       down=balanced_tasks(cfg.hidden, self.tasks))
-        self.grouped = grouped and fused_merge and residual == "split" and balance and \
-            self.call_tasks["qkv"] % cfg.kv_heads == 0
-        self.oproj_group_tasks = max(1, self.tasks // cfg.kv_heads)
-        while (cfg.hidden // 16) % self.oproj_group_tasks:
-            self.oproj_group_tasks -= 1
-        self.graph = etsim.Graph.from_json(json.dumps(graph_spec(
-            cfg, self.tasks, self.lm_tasks, fused_merge, call_tasks=self.call_tasks, attn_cap=self.max_splits,
-            grouped=self.grouped, oproj_group_tasks=self.oproj_group_tasks)))
-        self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
+        spec, self.layout = decode_graph_spec(cfg, self.tasks, self.samples[-1], lm_tasks=self.lm_tasks,
+                                              residual=residual, fused_merge=fused_merge, balance=balance,
+                                              grouped=grouped)
+        self.call_tasks = self.layout["call_tasks"]
+        self.grouped = self.layout["grouped"]
+        self.oproj_group_tasks = self.layout["oproj_group_tasks"]
+        self.graph = etsim.Graph.from_json(json.dumps(spec))
+        self.scheduler = scheduler
+        if scheduler == "dynamic":  # on-GPU ready queues (Algorithm 2) instead of per-SM queues
+            self.kernel = etsim.lower_dynamic(self.graph, early_push=early_push)
+        else:
+            self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3
 
         dev = self.device
@@ -281,8 +300,12 @@ class DecodeModel:
         self.inv_freq = rope_inv_freq(cfg).to(dev)
 
         t1 = time.perf_counter()
-        self.executor = etsim.Executor(self.kernel, device=self.device.index or 0, num_workers=self.num_workers,
-                                       record_trace=record_trace, prefetch=prefetch, l2_prefetch=l2_prefetch)
+        if scheduler == "dynamic":
+            self.executor = etsim.Executor(self.kernel, [{"s": s} for s in self.samples], device=self.device.index or 0,
+                                           num_workers=self.num_workers, record_trace=record_trace, prefetch=prefetch)
+        else:
+            self.executor = etsim.Executor(self.kernel, device=self.device.index or 0, num_workers=self.num_workers,
+                                           record_trace=record_trace, prefetch=prefetch, l2_prefetch=l2_prefetch)
         self.executor.bind_ops(pack(self._ops()))
         self.upload_ms = (time.perf_counter() - t1) * 1e3
 

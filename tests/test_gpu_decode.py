@@ -76,3 +76,23 @@ def test_tiny_multi_block_splits_match_oracle(tiny_long, s):
     mg = m.graph.instantiate({"s": s})
     assert mg.check(m.executor.trace()) == []
     assert all(c == 0 for c in m.executor.final_counters())
+
+
+@pytest.mark.parametrize("early", [False, True])
+def test_tiny_dynamic_scheduler_matches_oracle(early):
+    """The same decode graph under the on-GPU dynamic scheduler (push/pop ready
+    queues, optional early push): logits and Event Tensor accounting."""
+    m = DecodeModel(TINY, samples=(16, 64), num_workers=16, seed=0, record_trace=True, keep_logical=True,
+                    scheduler="dynamic", early_push=early)
+    for s in (16, 40):
+        m.fill_cache(s, seed=1)
+        m.set_token(5)
+        cpu_k = [k.cpu() for k in m.kcache]
+        cpu_v = [v.cpu() for v in m.vcache]
+        logits = m.step(s)[0].cpu()
+        ref, _, _ = decode_step(m.cfg, weights_to_cpu(m.W_logical), cpu_k, cpu_v, 5, s, m.inv_freq.cpu())
+        err, scale = _errs(logits, ref)
+        assert err <= 2e-3 * scale + 2e-3, (s, err, scale)
+        mg = m.graph.instantiate({"s": s})
+        assert mg.check(m.executor.trace()) == []
+        assert m.last_stats["pushes"] == m.last_stats["pops"] == mg.num_tasks
