@@ -623,6 +623,20 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
             o = fmaf(w[c], __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d), o);
         out[idx] = f2bf(o + o2);
     }
+    if constexpr (kWide) {
+        if ((op.flags & 33) == 33) {
+            // split-K q/k/v projection (flags bit 5): its fp32 accumulators of this group are
+            // consumed (every split arrived, split 0 appended k/v) -- zero them for the next step
+            float* q = reinterpret_cast<float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
+            float* kr = reinterpret_cast<float*>(op.p[8]) + static_cast<long long>(g) * dh;
+            float* vr = kr + static_cast<long long>(op.i[6]) * dh;
+            for (int i = ctid; i < G * dh; i += kConsumers) q[i] = 0.f;
+            for (int i = ctid; i < dh; i += kConsumers) {
+                kr[i] = 0.f;
+                vr[i] = 0.f;
+            }
+        }
+    }
 }
 
 template <bool kQK>

@@ -234,7 +234,7 @@ class MoEDecodeModel:
 
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
                  scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=True,
-                 balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False):
+                 balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False, qkv_split=True):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
@@ -255,6 +255,7 @@ class MoEDecodeModel:
         self.fused_merge = fused_merge
         self.group_stage = (scheduler == "dynamic") if group_stage is None else group_stage
         self.l2_prefetch_experts = l2_prefetch_experts
+        self.qkv_split = qkv_split and fused_merge
         self.route_tasks = route_tasks or max(1, cfg.experts // 16)
         self.spec = moe_graph_spec(cfg, self.num_workers, self.num_workers, self.tokens, fused_merge=fused_merge,
                                    qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
@@ -318,14 +319,18 @@ class MoEDecodeModel:
         for l, L in enumerate(W["layers"]):
             ri = {n: self.rt_index[f"{n}{l}"] for n in RT_PER_LAYER}
             kc, vc = self.kcache[l], self.vcache[l]
-            ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
-                               p=[ptr(L["wqkv"]), 0, ptr(self.h), ptr(L["attn_norm"]), ptr(self.qkv)]))
+            if self.qkv_split:  # split-K spans, red.add into the raw q/k/v accumulators (the merger zeroes them)
+                ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_ADD, -1, 0, 16, 0, H, 0, 0, 0, 1],
+                                   f=[cfg.eps], p=[ptr(L["wqkv"]), 0, ptr(self.h), ptr(L["attn_norm"]), ptr(self.qkv)]))
+            else:
+                ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
+                                   p=[ptr(L["wqkv"]), 0, ptr(self.h), ptr(L["attn_norm"]), ptr(self.qkv)]))
             attn_i = [dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads]
             attn_p = [ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(L["q_norm"]),
                       ptr(L["k_norm"]), ptr(self.inv_freq), ptr(self.qkv) + 4 * nq]
             if self.fused_merge:  # flags: 1 = q/k-norm mode, 2 = the last split merges; p5 of the split
                 # op carries the arrival counters, so the norm weights move to the merge-compatible slots
-                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], flags=3,
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], flags=3 | (32 if self.qkv_split else 0),
                                    p=[ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn),
                                       ptr(self.arrive_attn[l]), ptr(L["k_norm"]), ptr(self.inv_freq),
                                       ptr(self.qkv) + 4 * nq, ptr(L["q_norm"])]))
