@@ -390,15 +390,18 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     // flags bit 4: grouped GEMV -- coord 0 selects the group's weight matrix and
     // activation slice, coord 1 the row span among i9 tasks per group
     const bool grouped = (op.flags & 16) != 0;
-    const GemvSpan sp = gemv_span(op, grouped ? si.coord[1] : si.coord[0], grouped ? op.i[9] : si.ext0);
+    const GemvSpan sp = gemv_span(op, grouped ? si.coord[1] : si.coord[0], grouped ? op.i[13] : si.ext0);
     const int r0 = sp.row0, R = sp.rows;
 
     // ---- prologue: activations into shared memory (bf16 [nb][K]), accumulators zeroed
     if (op.i[3] == 0) {
+        // activation rows are i9 elements apart (0: packed [nb][K]); a grouped GEMV reads slice g
         const uint16_t* x = reinterpret_cast<const uint16_t*>(op.p[2]) + (grouped ? static_cast<long long>(si.coord[0]) * K : 0);
-        const int nv = nb * K / 8;
-        for (int v = ctid; v < nv; v += kConsumers)
-            reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x) + v);
+        const int xstride = op.i[9] > 0 ? op.i[9] : K, k8 = K / 8;
+        for (int v = ctid; v < nb * k8; v += kConsumers) {
+            const int bi = v / k8, kk = v - bi * k8;
+            reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x + static_cast<long long>(bi) * xstride) + kk);
+        }
     } else {
         // RMSNorm prologue: one pass over the fp32 residual stream held in
         // registers (K <= 8192), sum of squares reduced across the CTA
@@ -551,18 +554,21 @@ __device__ __noinline__ void qk_norm_rope(float* v, int dh, const float* w, floa
 // kWide: G * dh <= 1024 (MoE instantiation: 8 q heads per kv head), else G * dh
 // <= 512 -- the register footprint of the dense kernel stays spill-free.
 template <bool kWide>
-__device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op& op, int g, const float* qs,
+__device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op& op, int gi, const float* qs,
                                               int qstride, float* scr, int ctid) {
     constexpr int kPass = kWide ? 8 : 16, kOut = kWide ? 4 : 2;  // splits in registers; outputs per thread
     const int warp = ctid >> 5, lane = ctid & 31;
-    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5], kvh = op.i[6];
+    const int g = gi % kvh, bq = gi / kvh;  // kv head, sequence of the batch
     const long long s = P.binding[op.i[4]];
     const int nspl = attn_splits_with_data(op, P.binding);
     const float scale = op.f[0];
-    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);
-    const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + (static_cast<long long>(g) * cap + s) * dh;
-    const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + (static_cast<long long>(g) * cap + s) * dh;
-    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) + static_cast<long long>(g) * G * dh;
+    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(gi) * G * maxs * (dh + 2);
+    const long long cb = static_cast<long long>(bq) * op.i[8];  // this sequence's cache
+    const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + cb + (static_cast<long long>(g) * cap + s) * dh;
+    const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + cb + (static_cast<long long>(g) * cap + s) * dh;
+    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) + static_cast<long long>(bq) * kvh * G * dh +
+                    static_cast<long long>(g) * G * dh;
     float* ml = scr;                    // [G][nspl][2]
     float* wts = ml + 2 * G * nspl;     // [G][nspl]
     float* hs = wts + G * nspl;         // [G]: weight of the new token
@@ -627,9 +633,10 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
         if ((op.flags & 33) == 33) {
             // split-K q/k/v projection (flags bit 5): its fp32 accumulators of this group are
             // consumed (every split arrived, split 0 appended k/v) -- zero them for the next step
-            float* q = reinterpret_cast<float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
-            float* kr = reinterpret_cast<float*>(op.p[8]) + static_cast<long long>(g) * dh;
-            float* vr = kr + static_cast<long long>(op.i[6]) * dh;
+            const long long rb = static_cast<long long>(bq) * op.i[7];  // this sequence's projection row
+            float* q = reinterpret_cast<float*>(op.p[0]) + rb + static_cast<long long>(g) * G * dh;
+            float* kr = reinterpret_cast<float*>(op.p[8]) + rb + static_cast<long long>(g) * dh;
+            float* vr = kr + static_cast<long long>(kvh) * dh;
             for (int i = ctid; i < G * dh; i += kConsumers) q[i] = 0.f;
             for (int i = ctid; i < dh; i += kConsumers) {
                 kr[i] = 0.f;
@@ -650,9 +657,11 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     // per q head goes to the partials buffer; the merge combines the splits.
     constexpr int kOutMax = kQK ? 2 : 1;  // (head, dim pair) outputs per thread: G * dh / 2 <= 256 * kOutMax
     const int warp = ctid >> 5, lane = ctid & 31;
-    const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5];
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5], kvh = op.i[6];
     const long long s = P.binding[op.i[4]];
-    const int g = si.coord[0], c = si.coord[1];
+    const int gi = si.coord[0], c = si.coord[1];   // gi = sequence * kv_heads + kv head
+    const int g = gi % kvh, bq = gi / kvh;
+    const long long rb = static_cast<long long>(bq) * op.i[7];  // this sequence's q / projection row
     const AttnBlocks ab = attn_blocks(op, c, P.binding);
     const int qstride = dh + 4;          // padded rows: heads land on different banks
     const int nvec = dh / 8;             // 16-byte vectors per K/V row
@@ -660,7 +669,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     float* qs = scratch;                 // [G][dh+4]
     float* sc = scratch + G * qstride;   // [G][CH]
     float* st = sc + G * CH;             // [G][4]: running max, running sum, block rescale
-    const float* q = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(g) * G * dh;
+    const float* q = reinterpret_cast<const float*>(op.p[0]) + rb + static_cast<long long>(g) * G * dh;
     for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
     if (ctid < G) {
         st[4 * ctid] = -INFINITY;
@@ -674,8 +683,8 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             const bool knew = (op.flags & 2) && c == 0;
             float* kv = sc;  // [2][dh] scratch before the blocks use sc
             if (knew) {
-                const float* kr = reinterpret_cast<const float*>(op.p[8]) + static_cast<long long>(g) * dh;
-                const float* vr = kr + static_cast<long long>(op.i[6]) * dh;
+                const float* kr = reinterpret_cast<const float*>(op.p[8]) + rb + static_cast<long long>(g) * dh;
+                const float* vr = kr + static_cast<long long>(kvh) * dh;
                 for (int d = ctid; d < dh; d += kConsumers) {
                     kv[d] = __ldcg(kr + d);
                     kv[dh + d] = __ldcg(vr + d);
@@ -688,8 +697,9 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
                              reinterpret_cast<const float*>(op.p[7]), s, lane);
             if (knew) {
                 bar_sync(1, kConsumers);
-                uint16_t* kc = reinterpret_cast<uint16_t*>(op.p[1]) + (static_cast<long long>(g) * op.i[3] + s) * dh;
-                uint16_t* vc = reinterpret_cast<uint16_t*>(op.p[2]) + (static_cast<long long>(g) * op.i[3] + s) * dh;
+                const long long cb = static_cast<long long>(bq) * op.i[8];
+                uint16_t* kc = reinterpret_cast<uint16_t*>(op.p[1]) + cb + (static_cast<long long>(g) * op.i[3] + s) * dh;
+                uint16_t* vc = reinterpret_cast<uint16_t*>(op.p[2]) + cb + (static_cast<long long>(g) * op.i[3] + s) * dh;
                 for (int d = ctid; d < dh; d += kConsumers) {
                     kc[d] = f2bf(kv[d]);
                     vc[d] = f2bf(kv[dh + d]);
@@ -795,7 +805,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         const int idx = ctid + j * kConsumers;
         if (idx >= G * half) break;
         const int h = idx / half, dp = idx - h * half;
-        float* pr = part + ((static_cast<long long>(g) * G + h) * maxs + c) * (dh + 2);
+        float* pr = part + ((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + 2);
         pr[2 + 2 * dp] = o0[j];
         pr[3 + 2 * dp] = o1[j];
         if (dp == 0) {
@@ -808,7 +818,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         volatile int* flag = reinterpret_cast<volatile int*>(st + 4 * G);
         bar_sync(1, kConsumers);
         if (ctid == 0) {
-            int* arrive = reinterpret_cast<int*>(op.p[5]) + g;
+            int* arrive = reinterpret_cast<int*>(op.p[5]) + gi;
             // release: this split's partial (CTA writes ordered by the bar above) before
             // the arrival; acquire: the other splits' partials after it
             const int ntask = attn_tasks(op, P.binding);  // grid max(splits, 1)
@@ -819,7 +829,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         bar_sync(1, kConsumers);
         if (*flag) {
             if ((P.debug & 16) && ctid == 0) ring.stall = globaltimer() - *t_split;  // arrival round trip
-            attn_merge_group<kQK>(P, op, g, qs, qstride, st + 4 * G + 4, ctid);
+            attn_merge_group<kQK>(P, op, gi, qs, qstride, st + 4 * G + 4, ctid);
         }
     }
 }
@@ -1635,6 +1645,9 @@ __device__ __noinline__ void dyn_fire_warp(const StaticParams& P, const DynParam
     }
 }
 
+__device__ void dyn_count_warp(const StaticParams& P, const DynParams& D, unsigned int* ctr, int el, bool may_fire,
+                               int worker, int task, int lane);
+
 __device__ void dyn_reveal_warp(const StaticParams& P, const DynParams& D, int t, int lane) {
     if (lane == 0) {
         st_release(reinterpret_cast<uint32_t*>(&D.ctl->revealed[t]), 1u);
@@ -1674,6 +1687,26 @@ __device__ void dyn_reveal_warp(const StaticParams& P, const DynParams& D, int t
             const int b = __ffs(m) - 1;
             m &= m - 1;
             dyn_fire_warp(P, D, e0 + b, lane);
+        }
+    }
+    // Range-call tasks at or beyond indptr[last] never exist (extent_from): the
+    // static-map notifies the sample's worst-case counts expect from them are
+    // credited here, once the live count is known (the reference instantiates the
+    // actual grid instead, ref materialize.cpp:166-174).
+    const int rcall = D.dd_range_call[t];
+    if (rcall >= 0) {
+        const int live = __ldcg(P.rt[__ldg(D.call_range_rt + rcall)] + D.dd_count[t]);
+        long long worst = 1;
+        for (int d = 0, r = __ldg(P.call_rank + rcall); d < r; ++d) worst *= __ldg(P.call_extents + rcall * 4 + d);
+        const int first = __ldg(D.call_first_task + rcall);
+        for (long long f = live; f < worst; ++f) {
+            const int task = first + static_cast<int>(f);
+            const int4 rg = __ldg(D.task_rng + task);
+            for (int n = rg.z; n < rg.w; ++n) {
+                const int el = __ldg(D.task_notifies + n);
+                if (D.early_push) dyn_count_warp(P, D, D.disp, el, true, -1, task, lane);
+                dyn_count_warp(P, D, P.cnt, el, !D.early_push, -1, task, lane);
+            }
         }
     }
 }
@@ -1783,7 +1816,7 @@ __device__ bool dyn_prepare(const StaticParams& P, const DynParams& D, const Slo
     }
     if (D.early_push && dispatch) {
         for (int n = v.nb; n < v.ne; ++n) dyn_count(P, D, D.disp, __ldg(D.task_notifies + n), true, worker, task);
-        const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+        const int rel = v.masked ? -1 : dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));  // masked: no routing
         if (rel >= 0) dyn_count(P, D, D.disp, rel, true, worker, task);
     }
     return true;
@@ -1796,7 +1829,7 @@ __device__ void dyn_finish(const StaticParams& P, const DynParams& D, const Slot
         if (D.dd_writer_call[t] == v.call && atomicSub(&D.ctl->writer_rem[t], 1) == 1) dyn_reveal(P, D, t);
     const bool fire = !D.early_push;
     for (int n = v.nb; n < v.ne; ++n) dyn_count(P, D, P.cnt, __ldg(D.task_notifies + n), fire, worker, task);
-    const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+    const int rel = v.masked ? -1 : dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));  // masked: no routing
     if (rel >= 0) dyn_count(P, D, P.cnt, rel, fire, worker, task);
 }
 
@@ -1804,7 +1837,7 @@ __device__ void dyn_finish(const StaticParams& P, const DynParams& D, const Slot
 __device__ void dyn_dispatch_warp(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker,
                                   int lane) {
     for (int n = v.nb; n < v.ne; ++n) dyn_count_warp(P, D, D.disp, __ldg(D.task_notifies + n), true, worker, task, lane);
-    const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+    const int rel = v.masked ? -1 : dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));  // masked: no routing
     if (rel >= 0) dyn_count_warp(P, D, D.disp, rel, true, worker, task, lane);
 }
 
@@ -1818,7 +1851,7 @@ __device__ void dyn_finish_warp(const StaticParams& P, const DynParams& D, const
     }
     const bool fire = !D.early_push;
     for (int n = v.nb; n < v.ne; ++n) dyn_count_warp(P, D, P.cnt, __ldg(D.task_notifies + n), fire, worker, task, lane);
-    const int rel = dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));
+    const int rel = v.masked ? -1 : dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));  // masked: no routing
     if (rel >= 0) dyn_count_warp(P, D, P.cnt, rel, fire, worker, task, lane);
 }
 

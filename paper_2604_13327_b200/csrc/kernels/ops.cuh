@@ -11,8 +11,9 @@
 //   extent); epilogues: F32/BF16 store, RESID out = p5 + y, SILU_MUL out = silu(y0) * y1,
 //   QKV_ROPE (RoPE on q/k pairs, k/v appended to the cache), ADD out += y (red.global.add).
 //   flags bit 3 (QKV_ROPE): the weight rows are grouped per kv head (G q heads, k head, v head);
-//   flags bit 4: grouped GEMV -- task (g, t) of grid [groups, i9]: matrix g (bf16 [N][K] frag16, the
-//   matrices stacked at p0) times activation slice g (p2 + g*K), rows split over i9 tasks
+//   flags bit 4: grouped GEMV -- task (g, t) of grid [groups, i13]: matrix g (bf16 [N][K] frag16, the
+//   matrices stacked at p0) times activation slice g (p2 + g*K), rows split over i13 tasks;
+//   x mode 0: activation rows i9 elements apart (0 = K)
 //   i0 = N rows per segment, i1 = K, i2 = segments (1|2), i3 = x mode (0 bf16 [b][K] at p2,
 //   1 fp32 residual stream at p2 normalised with RMSNorm gamma p3), i4 = epilogue (GemvEpi),
 //   i5 = batch symbol slot (-1: b = 1), i6 = position symbol slot, i7 = row alignment,
@@ -24,7 +25,9 @@
 // ET_OP_ATTN_SPLIT      task (kv_head g, split c) of grid [kv, min(ceil(s/CH), i5)]: flash-decoding
 //   partial over its run of CH-position blocks (attn_blocks), online softmax across blocks;
 //   i0 = head_dim, i1 = q heads per kv head, i2 = CH (block positions), i3 = KV capacity,
-//   i4 = position symbol slot, i5 = split cap (partials' split dimension), i6 = kv heads;
+//   i4 = position symbol slot, i5 = split cap (partials' split dimension), i6 = kv heads,
+//   i7 = q / projection row stride of a batch sequence, i8 = per-sequence cache stride (elements);
+//   batch: grid dim 0 is sequence * kv_heads + kv head (partials / arrival counters per such group);
 //   p0 = q (fp32 [q_heads*head_dim], RoPE applied), p1/p2 = K/V cache, p3 = partials
 //   (fp32 [q_heads][max_splits][head_dim+2]); f0 = softmax scale
 // ET_OP_ATTN_MERGE      task (g): merges the splits and the new token at position s
@@ -160,7 +163,7 @@ struct GemvSpan {
 __device__ __forceinline__ GemvSpan gemv_span(const et_op& op, int t, int T) {
     const long long kst = op.i[1] / 16;
     GemvSpan sp;
-    if (op.i[13]) {
+    if (op.i[13] && !(op.flags & 16)) {
         const long long pairs = static_cast<long long>(op.i[0] / 16) * kst / 2;
         sp.u0 = (static_cast<long long>(t) * pairs / T) * 2;
         sp.u1 = (static_cast<long long>(t + 1) * pairs / T) * 2;
@@ -221,7 +224,7 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
     pl.interleave = false;
     if (op.kind == ET_OP_GEMV) {
         const bool grouped = (op.flags & 16) != 0;  // coord 0 = group (its own matrix), coord 1 = row span
-        const GemvSpan sp = gemv_span(op, grouped ? coord[1] : coord[0], grouped ? op.i[9] : T);
+        const GemvSpan sp = gemv_span(op, grouped ? coord[1] : coord[0], grouped ? op.i[13] : T);
         const long long gofs = grouped ? static_cast<long long>(coord[0]) * op.i[0] * op.i[1] * 2 : 0;
         pl.nseg = op.i[2];
         for (int s = 0; s < pl.nseg; ++s) {
@@ -252,7 +255,8 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
         long long p1 = a.p0 + static_cast<long long>(a.nblk) * CH;
         if (p1 > s) p1 = s;
         if (p1 > a.p0) {
-            const long long off = (static_cast<long long>(coord[0]) * cap + a.p0) * dh * 2;
+            const int kvh = op.i[6], g = coord[0] % kvh, bq = coord[0] / kvh;  // coord 0 = sequence * kv + head
+            const long long off = static_cast<long long>(bq) * op.i[8] * 2 + (static_cast<long long>(g) * cap + a.p0) * dh * 2;
             pl.nseg = 2;
             pl.interleave = true;
             pl.cbytes = CH * dh * 2;

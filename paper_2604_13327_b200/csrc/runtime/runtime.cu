@@ -123,6 +123,7 @@ struct et_runtime {
     DevArray<et_op> d_ops;
     int has_moe = 0;  // bound ops include MoE bodies: launch the MoE instantiation
     int ops_bound = 0;
+    std::vector<et_op> h_ops;  // host copy of the bound op table (launch-time capacity checks)
 
     int mode = ET_MODE_STATIC;
     // dynamic scheduler state, two parities
@@ -141,6 +142,7 @@ struct et_runtime {
     int last_sample = -1;
     bool launched = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timed = false;  // ev0/ev1 bracket the last launch (synchronous steps only)
 
     int fail(int code, const std::string& m) {
         err = m;
@@ -439,6 +441,28 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
     return ET_OK;
 }
 
+namespace {
+// A GEMV task accumulates nseg x rows x b fp32 values in shared memory (kAccFloats);
+// bound the rows of the widest task from the span arithmetic of ops.cuh gemv_span.
+bool gemv_acc_fits(const et_op& op, int64_t grid0, const int64_t* binding) {
+    if (op.kind != ET_OP_GEMV) return true;
+    const bool grouped = (op.flags & 16) != 0;
+    const int64_t T = grouped ? op.i[13] : grid0;
+    if (T <= 0) return true;
+    const int64_t nb = op.i[5] >= 0 ? binding[op.i[5]] : 1;
+    const int64_t kst = op.i[1] / 16;
+    int64_t rows;
+    if (op.i[13] && !grouped) {  // split-K: an even span of k-step pairs may straddle row tiles
+        const int64_t pairs = static_cast<int64_t>(op.i[0] / 16) * kst / 2;
+        rows = ((2 * ((pairs + T - 1) / T) + kst - 1) / kst + 1) * 16;
+    } else {
+        const int64_t align = op.i[7] > 16 ? op.i[7] : 16;
+        rows = ((op.i[0] / align + T - 1) / T) * align;
+    }
+    return op.i[2] * rows * nb <= etk::kAccFloats;
+}
+}  // namespace
+
 int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     if (!rt || (!ops && num_calls > 0)) return ET_ERR_INVALID;
     if (num_calls != rt->num_calls) return rt->fail(ET_ERR_INVALID, "op table must have one entry per call");
@@ -446,6 +470,7 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     cudaStreamSynchronize(rt->stream);
     ET_CUDA(rt->d_ops.upload(ops, static_cast<size_t>(std::max(1, num_calls))), "bind ops");
     rt->has_moe = 0;
+    rt->h_ops.assign(ops, ops + num_calls);
     for (int32_t c = 0; c < num_calls; ++c)
         if (ops[c].kind == ET_OP_MOE_ROUTE || ops[c].kind == ET_OP_MOE_EXPERT) rt->has_moe = 1;
     rt->ops_bound = 1;
@@ -500,7 +525,10 @@ static int collect(et_runtime* rt, et_step_info* info) {
         info->pushes = static_cast<int64_t>(st.pushes);
         info->pops = static_cast<int64_t>(st.pops);
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, rt->ev0, rt->ev1) == cudaSuccess) info->kernel_ms = ms;
+        if (rt->timed) {
+            if (cudaEventElapsedTime(&ms, rt->ev0, rt->ev1) == cudaSuccess) info->kernel_ms = ms;
+            else (void)cudaGetLastError();  // never leave a stale error for the next launch check
+        }
         info->step_id = rt->steps;
     }
     if (st.code != 0) {
@@ -543,6 +571,10 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
             if (!ok) return rt->fail(ET_ERR_INVALID, "grid of call " + std::to_string(c) + " is invalid at the binding");
             if (a > S.call_extents[static_cast<size_t>(c * 4 + d)])
                 return rt->fail(ET_ERR_INVALID, "sampled shape does not cover the actual grid of call " + std::to_string(c));
+            if (d == 0 && !gemv_acc_fits(rt->h_ops[static_cast<size_t>(c)], a, binding))
+                return rt->fail(ET_ERR_INVALID, "GEMV call " + std::to_string(c) +
+                                                    ": rows per task x batch exceed the shared-memory accumulators "
+                                                    "(give the call more tasks)");
         }
 
     etk::StaticParams p{};
@@ -622,6 +654,7 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
         rt->prepared[oth] = pick;  // the launch rebuilds the other parity for this sample
         rt->prepared[cur] = -1;
     }
+    rt->timed = synchronous;
     if (synchronous) cudaEventRecord(rt->ev0, st);
     if (rt->mode == ET_MODE_DYNAMIC)
         e = et_launch_dynamic(p, dp, S.num_queues, rt->has_moe, st);

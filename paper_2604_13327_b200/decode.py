@@ -333,7 +333,8 @@ class DecodeModel:
             if self.grouped:
                 # per kv-head group: h += Wo[:, group cols] a_group (red.global.add), each
                 # group's tasks released by its own merge
-                ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 0, EPI_ADD, -1, 0, 16, 0, self.oproj_group_tasks],
+                ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 0, EPI_ADD, -1, 0, 16, 0, cfg.q_rows, 0, 0, 0,
+                                               self.oproj_group_tasks],
                                    flags=16, p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_a)]))
             elif self.residual == "split":
                 # row-parallel products add into the residual stream in place: split-K

@@ -113,8 +113,15 @@ RT_PER_LAYER = ("topk", "cnt", "ind", "tind", "elist", "eoff")
 
 
 def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=None, route_tasks=1,
-                   group_stage=True, attn_cap=None):
-    """Reference-format graph spec (ref json_io.cpp:115-230) of one MoE decode step."""
+                   group_stage=True, attn_cap=None, oproj_group_tasks=None):
+    """Reference-format graph spec (ref json_io.cpp:115-230) of one MoE decode step.
+
+    tokens: an int (fixed batch) or "b" -- the batch is then a graph symbol next
+    to `s`, and the attention, group and expert grids scale with it at run time
+    (one lowered artifact serves every batch up to the largest sample).
+    oproj_group_tasks: the output projection runs per kv-head group (grid [kv, n]),
+    each group released by its own attention merge (needed for batch > 4: the
+    full attention row would not fit the staged activations)."""
     CH = cfg.attn_chunk
     E, K, RS = cfg.experts, cfg.top_k, cfg.row_splits
     fns, events, calls, rts = [], [], [], []
@@ -138,13 +145,13 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
                 {"name": rt["cnt"], "shape": [str(E)], "role": "counts", "writer": route},
                 {"name": rt["ind"], "shape": [str(E + 1)], "role": "indptr", "writer": route},
                 {"name": rt["tind"], "shape": [str(E + 1)], "role": "indptr", "writer": route},
-                {"name": rt["elist"], "shape": [str(tokens * K)], "role": "routing", "writer": route},
+                {"name": rt["elist"], "shape": [f"{tokens} * {K}"], "role": "routing", "writer": route},
                 {"name": rt["eoff"], "shape": [str(E + 1)], "role": "indptr", "writer": route}]
         qkv, a, m, o, r, x, d = (f"{n}{l}" for n in ("QKV", "A", "M", "O", "R", "EXP", "D"))
         ev(qkv, ["1"])
         if not fused_merge:
             ev(a, [kv])
-        ev(m, ["1"])
+        ev(m, [kv] if oproj_group_tasks else ["1"])
         ev(o, ["1"])
         ev(r, ["1"])
         if group_stage:
@@ -153,34 +160,41 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
         nsplit = f"(s + {CH - 1}) // {CH}" if not attn_cap else f"min((s + {CH - 1}) // {CH}, {attn_cap})"
         calls.append({"fn": fn(f"L{l}.qkv", [str(qkv_tasks or tasks)]), "in": [{"event": prev, "map": ["0"]}],
                       "out": [{"event": qkv, "map": ["0"]}]})
-        if fused_merge:  # the last split of each kv head merges the group
-            calls.append({"fn": fn(f"L{l}.attn", [kv, f"max({nsplit}, 1)"]),
-                          "in": [{"event": qkv, "map": ["0"]}], "out": [{"event": m, "map": ["0"]}]})
+        if fused_merge:  # the last split of each (sequence, kv head) merges the group
+            calls.append({"fn": fn(f"L{l}.attn", [f"{tokens} * {kv}", f"max({nsplit}, 1)"]),
+                          "in": [{"event": qkv, "map": ["0"]}],
+                          "out": [{"event": m, "map": [f"t0 % {kv}" if oproj_group_tasks else "0"]}]})
         else:
             calls += [
                 {"fn": fn(f"L{l}.attn", [kv, nsplit]), "in": [{"event": qkv, "map": ["0"]}],
                  "out": [{"event": a, "map": ["t0"]}]},
                 {"fn": fn(f"L{l}.merge", [kv]), "in": [{"event": a, "map": ["t0"]}, {"event": qkv, "map": ["0"]}],
                  "out": [{"event": m, "map": ["0"]}]}]
+        if oproj_group_tasks:
+            calls.append({"fn": fn(f"L{l}.oproj", [kv, str(oproj_group_tasks)]), "in": [{"event": m, "map": ["t0"]}],
+                          "out": [{"event": o, "map": ["0"]}]})
+        else:
+            calls.append({"fn": fn(f"L{l}.oproj", [T]), "in": [{"event": m, "map": ["0"]}],
+                          "out": [{"event": o, "map": ["0"]}]})
         calls += [
-            {"fn": fn(f"L{l}.oproj", [T]), "in": [{"event": m, "map": ["0"]}], "out": [{"event": o, "map": ["0"]}]},
             {"fn": fn(route, [str(route_tasks)]), "in": [{"event": o, "map": ["0"]}],
              "out": [{"event": r, "map": ["0"]}]}]
         if group_stage:  # the reference structure: routed notify + range trigger (dynamic scheduler)
             calls += [
-                {"fn": fn(f"L{l}.group", [str(tokens * K)]), "in": [{"event": r, "map": ["0"]}],
+                {"fn": fn(f"L{l}.group", [f"{tokens} * {K}"]), "in": [{"event": r, "map": ["0"]}],
                  "out": [{"event": x, "routed_by": rt["topk"]}]},
-                {"fn": fn(f"L{l}.expert", [str(tokens * K * RS)]), "extent_from": rt["tind"],
+                {"fn": fn(f"L{l}.expert", [f"{tokens} * {K * RS}"]), "extent_from": rt["tind"],
                  "in": [{"event": x, "indptr": rt["tind"]}], "out": [{"event": d, "map": ["0"]}]}]
         else:  # static scheduler: the worst-case rewrite makes EXP a barrier over the no-op
             # group tasks anyway; the expert tiles wait on the routing itself (extent_from masks)
-            calls.append({"fn": fn(f"L{l}.expert", [str(tokens * K * RS)]), "extent_from": rt["tind"],
+            calls.append({"fn": fn(f"L{l}.expert", [f"{tokens} * {K * RS}"]), "extent_from": rt["tind"],
                           "in": [{"event": r, "map": ["0"]}], "out": [{"event": d, "map": ["0"]}]})
         prev = d
     ev("LM", ["1"])
     calls.append({"fn": fn("lm_head", [str(lm_tasks)]), "in": [{"event": prev, "map": ["0"]}],
                   "out": [{"event": "LM", "map": ["0"]}]})
-    return {"symbols": ["s"], "size_symbol": "s", "duration_models": {"unit": {"kind": "constant", "value": 1}},
+    symbols = ["s", "b"] if tokens == "b" else ["s"]
+    return {"symbols": symbols, "size_symbol": "s", "duration_models": {"unit": {"kind": "constant", "value": 1}},
             "device_functions": fns, "event_tensors": events, "runtime_tensors": rts, "calls": calls}
 
 
@@ -225,6 +239,9 @@ def moe_device_layout(cfg, W):
         blocks = L["wdown"].reshape(E, H, RS, IR).permute(0, 2, 1, 3)  # [E][RS][H][IR]
         d["wdown"] = torch.stack([torch.stack([frag16(blocks[e, r].contiguous()) for r in range(RS)])
                                   for e in range(E)])
+        cols = (cfg.heads // cfg.kv_heads) * cfg.head_dim  # Wo per kv-head group (batched decode)
+        d["wo_grouped"] = torch.stack([frag16(L["wo"][:, g * cols:(g + 1) * cols].contiguous())
+                                       for g in range(cfg.kv_heads)])
         D["layers"].append(d)
     return D
 
@@ -234,7 +251,8 @@ class MoEDecodeModel:
 
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
                  scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=True,
-                 balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False, qkv_split=True):
+                 balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False, qkv_split=True,
+                 max_batch=1, batch_samples=None):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
@@ -242,7 +260,13 @@ class MoEDecodeModel:
         self.device = torch.device(device)
         props = torch.cuda.get_device_properties(self.device)
         self.num_workers = num_workers or props.multi_processor_count
-        self.tokens = 1
+        # batch: a graph symbol `b` (1 <= b <= max_batch <= 8, the mma N dimension);
+        # every (s, b) at or below a sample runs on the lowered artifact
+        assert 1 <= max_batch <= 8
+        self.max_batch = max_batch
+        self.batched = max_batch > 1
+        self.tokens = "b" if self.batched else 1
+        self.batch_samples = sorted(set(batch_samples or (1, max_batch))) if self.batched else [1]
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
         from .decode import attn_split_cap
@@ -257,18 +281,30 @@ class MoEDecodeModel:
         self.l2_prefetch_experts = l2_prefetch_experts
         self.qkv_split = qkv_split and fused_merge
         self.route_tasks = route_tasks or max(1, cfg.experts // 16)
-        self.spec = moe_graph_spec(cfg, self.num_workers, self.num_workers, self.tokens, fused_merge=fused_merge,
+        assert fused_merge or not self.batched, "batched decode uses the fused attention merge"
+        self.oproj_group_tasks = None
+        if self.batched:  # per kv-head-group output projection (a batch of full attention rows would not fit)
+            og = max(1, self.num_workers // cfg.kv_heads)
+            while (cfg.hidden // 16) % og:
+                og -= 1
+            self.oproj_group_tasks = og
+        # the lm_head task's rows x batch accumulate in shared memory (2048 fp32): a large
+        # vocabulary at batch 8 needs more, smaller row spans than one per worker
+        tiles, cap_tiles = cfg.vocab // 16, max(1, 2048 // (16 * max_batch))
+        self.lm_tasks = max(self.num_workers, -(-tiles // cap_tiles))
+        self.spec = moe_graph_spec(cfg, self.num_workers, self.lm_tasks, self.tokens, fused_merge=fused_merge,
                                    qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
                                    if balance else None, route_tasks=self.route_tasks, group_stage=self.group_stage,
-                                   attn_cap=self.max_splits)
+                                   attn_cap=self.max_splits, oproj_group_tasks=self.oproj_group_tasks)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.rt_index = {r["name"]: i for i, r in enumerate(self.spec["runtime_tensors"])}
+        self.bindings = [self._binding(s, b) for s in self.samples for b in self.batch_samples]
         if scheduler == "dynamic":
             self.kernel = etsim.lower_dynamic(self.graph, early_push=early_push)
         else:
             # static: data-dependent events collapse to worst-case barriers (ref
             # sched_static.cpp:13-47); extent_from still masks dead expert tiles on device
-            self.kernel = etsim.lower_static(etsim.worst_case_rewrite(self.graph), [{"s": s} for s in self.samples],
+            self.kernel = etsim.lower_static(etsim.worst_case_rewrite(self.graph), self.bindings,
                                              num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3
 
@@ -276,20 +312,21 @@ class MoEDecodeModel:
         W = weights if weights is not None else init_moe_weights(cfg, dev, seed)
         self.W_logical = W if keep_logical else None
         self.W = moe_device_layout(cfg, W)
-        b, E, K = self.tokens, cfg.experts, cfg.top_k
-        self.kcache = [torch.zeros(cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
+        b, E, K = self.max_batch, cfg.experts, cfg.top_k
+        # per-sequence KV caches [b][kv][cap][dh]
+        self.kcache = [torch.zeros(b, cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
                        for _ in range(cfg.layers)]
         self.vcache = [torch.zeros_like(k) for k in self.kcache]
         self.tok = torch.zeros(b, dtype=torch.int32, device=dev)
         self.h = torch.zeros(b, cfg.hidden, dtype=torch.float32, device=dev)
         self.qkv = torch.zeros(b, cfg.q_rows + 2 * cfg.kv_rows, dtype=torch.float32, device=dev)
         self.attn = torch.zeros(b, cfg.q_rows, dtype=torch.bfloat16, device=dev)
-        self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        self.partials = torch.zeros(b * cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
         self.logits_r = torch.zeros(cfg.layers, b, E, dtype=torch.float32, device=dev)   # router logits per layer
         self.xn = torch.zeros(cfg.layers, b, cfg.hidden, dtype=torch.bfloat16, device=dev)
         self.wslot = torch.zeros(cfg.layers, b * K, dtype=torch.float32, device=dev)
         self.arrive = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
-        self.arrive_attn = torch.zeros(cfg.layers, cfg.kv_heads, dtype=torch.int32, device=dev)
+        self.arrive_attn = torch.zeros(cfg.layers, b * cfg.kv_heads, dtype=torch.int32, device=dev)
         self.tiles = torch.zeros(cfg.layers, b * K, 4, dtype=torch.int32, device=dev)  # expert tile table
         self.logits = torch.zeros(b, cfg.vocab, dtype=torch.float32, device=dev)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
@@ -297,11 +334,12 @@ class MoEDecodeModel:
 
         t1 = time.perf_counter()
         if scheduler == "dynamic":
-            self.executor = etsim.Executor(self.kernel, [{"s": s} for s in self.samples], device=dev.index or 0,
-                                           num_workers=self.num_workers, record_trace=record_trace)
+            self.executor = etsim.Executor(self.kernel, self.bindings, device=dev.index or 0,
+                                           num_workers=self.num_workers, record_trace=record_trace,
+                                           max_batch=self.max_batch)
         else:
             self.executor = etsim.Executor(self.kernel, device=dev.index or 0, num_workers=self.num_workers,
-                                           record_trace=record_trace)
+                                           record_trace=record_trace, max_batch=self.max_batch)
         self.bind()
         self.upload_ms = (time.perf_counter() - t1) * 1e3
 
@@ -315,17 +353,19 @@ class MoEDecodeModel:
         G = cfg.heads // cfg.kv_heads
         scale = 1.0 / math.sqrt(dh)
         nq = cfg.q_rows
-        ops = [make_op(OP_EMBED, i=[H, -1], p=[ptr(W["embed"]), ptr(self.tok), ptr(self.h)])]
+        bs = 1 if self.batched else -1  # binding slot of the batch symbol (-1: one sequence)
+        ops = [make_op(OP_EMBED, i=[H, bs], p=[ptr(W["embed"]), ptr(self.tok), ptr(self.h)])]
         for l, L in enumerate(W["layers"]):
             ri = {n: self.rt_index[f"{n}{l}"] for n in RT_PER_LAYER}
             kc, vc = self.kcache[l], self.vcache[l]
             if self.qkv_split:  # split-K spans, red.add into the raw q/k/v accumulators (the merger zeroes them)
-                ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_ADD, -1, 0, 16, 0, H, 0, 0, 0, 1],
+                ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_ADD, bs, 0, 16, 0, H, 0, 0, 0, 1],
                                    f=[cfg.eps], p=[ptr(L["wqkv"]), 0, ptr(self.h), ptr(L["attn_norm"]), ptr(self.qkv)]))
             else:
-                ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
+                ops.append(make_op(OP_GEMV, i=[nq + 2 * cfg.kv_rows, H, 1, 1, EPI_F32, bs, 0, 16, 0, H], f=[cfg.eps],
                                    p=[ptr(L["wqkv"]), 0, ptr(self.h), ptr(L["attn_norm"]), ptr(self.qkv)]))
-            attn_i = [dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads]
+            attn_i = [dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, nq + 2 * cfg.kv_rows,
+                      cfg.kv_heads * self.capacity * dh]
             attn_p = [ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(L["q_norm"]),
                       ptr(L["k_norm"]), ptr(self.inv_freq), ptr(self.qkv) + 4 * nq]
             if self.fused_merge:  # flags: 1 = q/k-norm mode, 2 = the last split merges; p5 of the split
@@ -337,10 +377,15 @@ class MoEDecodeModel:
             else:
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
                 ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
-            ops.append(make_op(OP_GEMV, i=[H, nq, 1, 0, EPI_ADD, -1, 0, 16, 0, 0, 0, 0, 0, 1],
-                               p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h)]))
+            if self.oproj_group_tasks:  # per kv-head group, activation rows nq apart
+                ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 0, EPI_ADD, bs, 0, 16, 0, nq, 0, 0, 0,
+                                               self.oproj_group_tasks], flags=16,
+                                   p=[ptr(L["wo_grouped"]), 0, ptr(self.attn), 0, ptr(self.h)]))
+            else:
+                ops.append(make_op(OP_GEMV, i=[H, nq, 1, 0, EPI_ADD, bs, 0, 16, 0, 0, 0, 0, 0, 1],
+                                   p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h)]))
             assert [ri[n] for n in RT_PER_LAYER] == list(range(ri["topk"], ri["topk"] + len(RT_PER_LAYER)))
-            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, -1, K, 16, cfg.expert_inter, H, ri["topk"], 0, RS,
+            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, bs, K, 16, cfg.expert_inter, H, ri["topk"], 0, RS,
                                                 TS],
                                f=[cfg.eps],
                                p=[ptr(L["router"]), 0, ptr(self.h), ptr(L["ffn_norm"]), ptr(self.logits_r[l]),
@@ -354,7 +399,7 @@ class MoEDecodeModel:
                                i=[cfg.expert_inter, H, RS, TS, ri["ind"], ri["cnt"], ri["elist"], ri["eoff"], K, 0, E],
                                p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(L["wdown"]), ptr(self.xn[l]), ptr(self.wslot[l]),
                                   ptr(self.h), ptr(self.tiles[l])]))
-        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
+        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, bs, 0, 16, 0, H], f=[cfg.eps],
                            p=[ptr(W["lm_head"]), 0, ptr(self.h), ptr(W["final_norm"]), ptr(self.logits)]))
         return ops
 
@@ -368,11 +413,15 @@ class MoEDecodeModel:
             self.injected = True
             self.bind()
 
-    def routing(self, l):
-        """Device-written routing tensors of layer l (after a step)."""
+    def _binding(self, s, b=1):
+        return {"s": int(s), "b": int(b)} if self.batched else {"s": int(s)}
+
+    def routing(self, l, b=None):
+        """Device-written routing tensors of layer l (after a step with batch b)."""
         cfg = self.cfg
-        n = {"topk": self.tokens * cfg.top_k, "cnt": cfg.experts, "ind": cfg.experts + 1, "tind": cfg.experts + 1,
-             "elist": self.tokens * cfg.top_k, "eoff": cfg.experts + 1}
+        b = b if b is not None else getattr(self, "last_b", 1)
+        n = {"topk": b * cfg.top_k, "cnt": cfg.experts, "ind": cfg.experts + 1, "tind": cfg.experts + 1,
+             "elist": b * cfg.top_k, "eoff": cfg.experts + 1}
         return {k: self.executor.runtime_tensor(f"{k}{l}", v) for k, v in n.items()}
 
     def realization(self):
@@ -384,23 +433,29 @@ class MoEDecodeModel:
         return out
 
     def fill_cache(self, s, seed=1):
+        """Synthetic prefilled caches, N(0, 1) bf16 for positions [0, s) of every sequence."""
         g = torch.Generator(device=self.device)
         g.manual_seed(seed)
         for k, v in zip(self.kcache, self.vcache):
             k.zero_()
             v.zero_()
-            k[:, :s].normal_(0.0, 1.0, generator=g)
-            v[:, :s].normal_(0.0, 1.0, generator=g)
+            k[..., :s, :].normal_(0.0, 1.0, generator=g)
+            v[..., :s, :].normal_(0.0, 1.0, generator=g)
 
     def set_token(self, token):
-        self.tok.fill_(int(token))
+        if isinstance(token, (list, tuple)):
+            self.tok[: len(token)].copy_(torch.tensor(token, dtype=torch.int32))
+        else:
+            self.tok.fill_(int(token))
 
-    def step(self, s):
-        self.last_stats = self.executor.run({"s": int(s)})
+    def step(self, s, b=1):
+        self.last_b = b
+        self.last_stats = self.executor.run(self._binding(s, b))
         return self.logits
 
-    def launch(self, s, stream=0):
-        self.executor.launch({"s": int(s)}, stream)
+    def launch(self, s, stream=0, b=1):
+        self.last_b = b
+        self.executor.launch(self._binding(s, b), stream)
 
     def active_experts(self):
         return [sum(1 for c in self.routing(l)["cnt"] if c > 0) for l in range(self.cfg.layers)]

@@ -37,7 +37,9 @@ def _check(logits, ref):
 
 
 def _cpu(m):
-    return [k.cpu() for k in m.kcache], [v.cpu() for v in m.vcache]
+    """CPU caches of the (first) sequence, [kv][cap][dh] per layer."""
+    pick = (lambda t: t[0]) if m.kcache[0].dim() == 4 else (lambda t: t)
+    return [pick(k).cpu() for k in m.kcache], [pick(v).cpu() for v in m.vcache]
 
 
 @pytest.mark.parametrize("s", [1024, 777])

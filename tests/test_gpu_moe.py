@@ -31,8 +31,9 @@ def model(request):
                           record_trace=True, keep_logical=True)
 
 
-def _cpu_cache(m):
-    return [k.cpu() for k in m.kcache], [v.cpu() for v in m.vcache]
+def _cpu_cache(m, seq=0):
+    """CPU copy of one sequence's caches ([kv][cap][dh] per layer)."""
+    return [k[seq].cpu() for k in m.kcache], [v[seq].cpu() for v in m.vcache]
 
 
 @pytest.mark.parametrize("s,token", [(16, 3), (40, 11), (0, 5)])
@@ -87,3 +88,41 @@ def test_moe_injected_routing_matches_reference_realization():
     mg = m.kernel.graph.instantiate({"s": 16}, routing=m.realization())
     assert mg.check(t) == []
     assert m.last_stats["tasks_executed"] == mg.num_tasks
+
+
+@pytest.mark.parametrize("scheduler", ["static", "dynamic"])
+def test_moe_batched_decode_no_recompile(scheduler):
+    """One lowered artifact (batch symbol b <= 8) runs b = 1, 3, 8 sequences, each
+    with its own KV cache and token: per-token routing bit-exact, per-sequence
+    logits vs the oracle, and the Event Tensor accounting of the exact (s, b)."""
+    cfg = TINY_MOE
+    m = MoEDecodeModel(cfg, samples=(64,), num_workers=16, seed=0, scheduler=scheduler, record_trace=True,
+                       keep_logical=True, max_batch=8, batch_samples=(2, 8))
+    Wc = weights_to_cpu(m.W_logical)
+    toks = [3, 9, 27, 81, 243, 729, 1000, 17]
+    for b, s in ((1, 16), (3, 40), (8, 64)):
+        m.fill_cache(s, seed=b)
+        m.set_token(toks)
+        kc = [k.cpu() for k in m.kcache]
+        vc = [v.cpu() for v in m.vcache]
+        logits = m.step(s, b).cpu()
+        for l in range(cfg.layers):
+            r = m.routing(l, b)
+            want_topk = []
+            for t in range(b):
+                want_topk += topk_ref(m.logits_r[l, t].cpu().tolist(), cfg.top_k)
+            assert r["topk"] == want_topk, (b, l)
+            want = moe_routing_tensors(r["topk"], cfg.experts, cfg.tile_tokens, cfg.row_splits)
+            for key in ("cnt", "ind", "tind", "eoff", "elist"):
+                assert r[key] == want[key], (b, l, key)
+        for t in range(b):
+            routing = [m.routing(l, b)["topk"][t * cfg.top_k:(t + 1) * cfg.top_k] for l in range(cfg.layers)]
+            ref, _, _ = moe_decode_step(cfg, Wc, [k[t] for k in kc], [v[t] for v in vc], toks[t], s,
+                                        m.inv_freq.cpu(), routing=routing)
+            err = (logits[t] - ref).abs().max().item()
+            scale = ref.abs().max().item()
+            assert err <= 2e-3 * scale + 2e-3, (b, t, err, scale)
+        mg = m.kernel.graph.instantiate(m._binding(s, b), routing=m.realization())
+        assert mg.check(m.executor.trace()) == []
+        assert m.last_stats["tasks_executed"] == mg.num_tasks
+        assert all(c == 0 for c in m.executor.final_counters())
