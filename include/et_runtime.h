@@ -62,7 +62,9 @@ enum et_op_kind {
     ET_OP_MOE_GROUP = 9,      /* scatter routed (token, k) slots into expert lists */
     ET_OP_MOE_COMBINE = 10,   /* weighted combine of expert outputs + residual     */
     ET_OP_ARGMAX = 11,        /* greedy token from logits                          */
-    ET_OP_EMBED = 12          /* embedding rows of the step's tokens -> fp32 stream */
+    ET_OP_EMBED = 12,         /* embedding rows of the step's tokens -> fp32 stream */
+    ET_OP_GEMV_TC = 13,       /* large-batch GEMV on tcgen05 tensor cores (TMEM)   */
+    ET_OP_NORM = 14           /* RMSNorm of the stream -> bf16 tensor-core operand */
 };
 
 /* One bound tile operation.  Meaning of i[], f[], p[] is per kind and is

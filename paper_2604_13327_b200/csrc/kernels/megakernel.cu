@@ -526,16 +526,181 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     return t_pro;
 }
 
+// ---------------------------------------------------------------------------
+// Large-batch GEMV on the 5th-generation tensor cores (ET_OP_GEMV_TC, ops.cuh).
+// Shared-memory mbarriers behind the misc words: x buffer full [2], x buffer
+// free [2] (tcgen05.commit), accumulators done [1] (tcgen05.commit).
+struct TcState {
+    uint32_t tmem;        // TMEM column base (512 columns, allocated at kernel start)
+    unsigned int xp;      // activation pieces consumed (issuer thread)
+    unsigned int ndone;   // tensor-core tasks completed (phase of the done barrier)
+};
+
+__device__ __forceinline__ uint64_t* tc_bars(uint8_t* smem) {
+    return reinterpret_cast<uint64_t*>(smem + kSmemMisc + 448);
+}
+
+// Bounded mbarrier wait (reports a deadlock instead of hanging; false when aborted).
+__device__ __noinline__ bool tc_wait(uint64_t* bar, uint32_t parity, DevStatus* status, long long watchdog_ns,
+                                     int worker, int code) {
+    if (mbar_try_wait(bar, parity)) return true;
+    const uint64_t t0 = globaltimer();
+    uint32_t it = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if ((++it & 1023u) == 0) {
+            if (aborted(status)) return false;
+            if (globaltimer() - t0 > static_cast<uint64_t>(watchdog_ns)) {
+                report(status, ET_ERR_DEADLOCK, worker, -1, code, 0);
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
+__device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op& op, const SlotView& si, uint8_t* smem,
+                                 Ring& ring, TcState& ts, int ctid) {
+    const int warp = ctid >> 5, lane = ctid & 31;
+    const int N = op.i[0], nseg = op.i[2], kp = op.i[6];
+    const int nb = batch_of(op, P), npad = tc_npad(nb);
+    const TcSpan sp = tc_span(op, si.coord[0], si.ext0);
+    if (sp.nblk <= 0 || sp.np <= 0) return 0;
+    uint64_t* bars = tc_bars(smem);
+    const int cpb = kp / 64;                       // 16 KB weight chunks per (piece, block)
+    const int wpp = nseg * sp.nblk * cpb;          // weight chunks per piece
+    const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
+    if (ctid == 0) {
+        // the issuer: per piece, wait for the activation piece, then per weight chunk
+        // four K=16 MMAs into the (segment, block) accumulator; each chunk's stage is
+        // released by tcgen05.commit once its MMAs have read it
+        const uint32_t idesc = umma_idesc_bf16(npad);
+        unsigned long long c = ring.seq;
+        bool ok = true;
+        for (int p = 0; p < sp.np && ok; ++p) {
+            const int xb = static_cast<int>(ts.xp & 1u);
+            ok = tc_wait(&bars[xb], (ts.xp >> 1) & 1u, P.status, P.watchdog_ns, ring.worker, -4);
+            if (!ok) break;
+            tc_fence_after();
+            const uint32_t xaddr = smem_u32(smem + kSmemX + xb * kTcXBuf);
+            for (int w = 0; w < wpp; ++w, ++c) {
+                const uint8_t* buf = ring.wait(c);
+                if (!buf) {
+                    ok = false;
+                    break;
+                }
+                tc_fence_after();
+                const int sg = w / (sp.nblk * cpb), rem = w - sg * sp.nblk * cpb;
+                const int blk = rem / cpb, ch = rem - blk * cpb;
+                const uint32_t d = ts.tmem + static_cast<uint32_t>((sg * sp.nblk + blk) * npad);
+                const uint32_t a0 = smem_u32(buf);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int ks = ch * 4 + j;
+                    umma_bf16(d, umma_desc(a0 + j * 4096), umma_desc(xaddr + ks * npad * 32), idesc,
+                              (p | ks) != 0 ? 1u : 0u);
+                }
+                umma_commit(&ring.empty[Ring::stage_of(c)]);
+            }
+            umma_commit(&bars[2 + xb]);  // the x buffer is free once this piece's MMAs complete
+            ++ts.xp;
+        }
+        umma_commit(&bars[4]);
+    }
+    ring.seq += static_cast<unsigned long long>(wpp) * sp.np;
+    const bool done = tc_wait(&bars[4], ts.ndone & 1u, P.status, P.watchdog_ns, ring.worker, -5);
+    ++ts.ndone;
+    if (!done) return t_pro;
+    tc_fence_after();
+
+    // ---- epilogue: warp w reads TMEM lanes 32*(w%4).. (rows of each block); the two
+    // warp halves take alternate 16-column (batch) chunks
+    const int q = warp & 3, half = warp >> 2;
+    const int nchunk = npad / 16, nitems = sp.nblk * nchunk;
+    const int epi = op.i[4];
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    for (int it = half; it < nitems; it += 2) {
+        const int blk = it / nchunk, n0 = (it - blk * nchunk) * 16;
+        float v[16], u[16];
+        tmem_ld16(ts.tmem + lane_off + static_cast<uint32_t>(blk * npad + n0), v);
+        if (epi == EPI_SILU_MUL) tmem_ld16(ts.tmem + lane_off + static_cast<uint32_t>((sp.nblk + blk) * npad + n0), u);
+        const int row = (sp.b0 + blk) * 128 + q * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int n = n0 + j;
+            if (n < nb) {
+                const long long o = static_cast<long long>(n) * N + row;
+                if (epi == EPI_F32) {
+                    reinterpret_cast<float*>(op.p[4])[o] = v[j];
+                } else if (epi == EPI_ADD) {
+                    atomicAdd(reinterpret_cast<float*>(op.p[4]) + o, v[j]);
+                } else if (epi == EPI_BF16) {
+                    reinterpret_cast<uint16_t*>(op.p[4])[o] = f2bf(v[j]);
+                } else if (epi == EPI_RESID) {
+                    reinterpret_cast<float*>(op.p[4])[o] = __ldcg(reinterpret_cast<const float*>(op.p[5]) + o) + v[j];
+                } else if (epi == EPI_SILU_MUL) {
+                    const float sv = v[j] / (1.f + __expf(-v[j]));
+                    reinterpret_cast<uint16_t*>(op.p[4])[xb_offset(n, row, npad, op.i[7])] = f2bf(sv * u[j]);
+                }
+            }
+        }
+    }
+    tc_fence_before();  // the next task's MMAs overwrite these columns after the closing barrier
+    return t_pro;
+}
+
+// RMSNorm of stream row n into the tensor-core operand layout (ET_OP_NORM).
+__device__ __noinline__ void body_norm(const StaticParams& P, const et_op& op, const SlotView& si, float* red, int ctid) {
+    const int warp = ctid >> 5, lane = ctid & 31;
+    const int n = si.coord[0], nb = batch_of(op, P);
+    if (n >= nb) return;
+    const int K = op.i[0], kp = op.i[6], npad = tc_npad(nb);
+    const float* h = reinterpret_cast<const float*>(op.p[0]) + static_cast<long long>(n) * K;
+    const float* gam = reinterpret_cast<const float*>(op.p[1]);
+    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[2]);
+    constexpr int kMaxPer = 8;  // K <= 8192
+    float4 hv[kMaxPer];
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+        const int k = (ctid + j * kConsumers) * 4;
+        if (k < K) {
+            hv[j] = ldcg_f4(h + k);
+            ss += hv[j].x * hv[j].x + hv[j].y * hv[j].y + hv[j].z * hv[j].z + hv[j].w * hv[j].w;
+        }
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) red[warp] = ss;
+    bar_sync(1, kConsumers);
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) t += red[w];
+    const float scale = rsqrtf(t / static_cast<float>(K) + op.f[0]);
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+        const int k = (ctid + j * kConsumers) * 4;
+        if (k < K) {
+            const float4 g = __ldg(reinterpret_cast<const float4*>(gam + k));
+            uint2 o;
+            o.x = static_cast<uint32_t>(f2bf(hv[j].x * scale * g.x)) | (static_cast<uint32_t>(f2bf(hv[j].y * scale * g.y)) << 16);
+            o.y = static_cast<uint32_t>(f2bf(hv[j].z * scale * g.z)) | (static_cast<uint32_t>(f2bf(hv[j].w * scale * g.w)) << 16);
+            *reinterpret_cast<uint2*>(out + xb_offset(n, k, npad, kp)) = o;
+        }
+    }
+}
+
 // Qwen3-style per-head RMSNorm (weight w[dh]) followed by the pair rotation at
 // position pos, in place on one head vector in shared memory; one warp.
 __device__ __noinline__ void qk_norm_rope(float* v, int dh, const float* w, float eps, const float* invf,
                                              long long pos, int lane) {
-    float ss = 0.f;
-    for (int d = lane; d < dh; d += 32) ss += v[d] * v[d];
-    ss = warp_sum(ss);
-    const float sc = rsqrtf(ss / static_cast<float>(dh) + eps);
+    float sc = 1.f;
+    if (w) {  // nullptr: RoPE only (Llama: no q/k norm)
+        float ss = 0.f;
+        for (int d = lane; d < dh; d += 32) ss += v[d] * v[d];
+        ss = warp_sum(ss);
+        sc = rsqrtf(ss / static_cast<float>(dh) + eps);
+    }
     for (int j = lane; j < dh / 2; j += 32) {
-        const float a = v[2 * j] * sc * __ldg(w + 2 * j), b = v[2 * j + 1] * sc * __ldg(w + 2 * j + 1);
+        const float a = v[2 * j] * sc * (w ? __ldg(w + 2 * j) : 1.f), b = v[2 * j + 1] * sc * (w ? __ldg(w + 2 * j + 1) : 1.f);
         float sn, cs;
         sincosf(static_cast<float>(pos) * __ldg(invf + j), &sn, &cs);
         v[2 * j] = a * cs - b * sn;
@@ -567,8 +732,12 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     const long long cb = static_cast<long long>(bq) * op.i[8];  // this sequence's cache
     const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + cb + (static_cast<long long>(g) * cap + s) * dh;
     const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + cb + (static_cast<long long>(g) * cap + s) * dh;
-    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) + static_cast<long long>(bq) * kvh * G * dh +
-                    static_cast<long long>(g) * G * dh;
+    // i9 > 0 (tensor-core instantiation): the output goes to the operand layout of the
+    // next GEMV (piece length i9, batch from symbol slot i10)
+    const int kxb = kWide ? op.i[9] : 0;
+    const int xnp = kxb ? tc_npad(op.i[10] >= 0 ? static_cast<int>(P.binding[op.i[10]]) : 1) : 0;
+    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) +
+                    (kxb ? 0 : static_cast<long long>(bq) * kvh * G * dh + static_cast<long long>(g) * G * dh);
     float* ml = scr;                    // [G][nspl][2]
     float* wts = ml + 2 * G * nspl;     // [G][nspl]
     float* hs = wts + G * nspl;         // [G]: weight of the new token
@@ -627,7 +796,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
         }
         for (int c = kPass; c < nspl; ++c)  // long contexts: the remaining splits
             o = fmaf(w[c], __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d), o);
-        out[idx] = f2bf(o + o2);
+        out[kxb ? xb_offset(bq, g * G * dh + idx, xnp, kxb) : idx] = f2bf(o + o2);
     }
     if constexpr (kWide) {
         if ((op.flags & 33) == 33) {
@@ -693,7 +862,9 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             bar_sync(1, kConsumers);
             for (int h = warp; h < G + (knew ? 1 : 0); h += kConsumerWarps)
                 qk_norm_rope(h < G ? qs + h * qstride : kv, dh,
-                             reinterpret_cast<const float*>(op.p[h < G ? ((op.flags & 2) ? 9 : 5) : 6]), op.f[1],
+                             (op.flags & 64) ? nullptr
+                                             : reinterpret_cast<const float*>(op.p[h < G ? ((op.flags & 2) ? 9 : 5) : 6]),
+                             op.f[1],
                              reinterpret_cast<const float*>(op.p[7]), s, lane);
             if (knew) {
                 bar_sync(1, kConsumers);
@@ -1227,14 +1398,16 @@ __device__ void body_embed(const StaticParams& P, const et_op& op, int ctid) {
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ bool op_streams(int kind) {
-    return kind == ET_OP_GEMV || kind == ET_OP_ATTN_SPLIT || kind == ET_OP_MOE_ROUTE || kind == ET_OP_MOE_EXPERT;
+    return kind == ET_OP_GEMV || kind == ET_OP_ATTN_SPLIT || kind == ET_OP_MOE_ROUTE || kind == ET_OP_MOE_EXPERT ||
+           kind == ET_OP_GEMV_TC;
 }
 
 // kMoE: the MoE bodies are compiled into this instantiation.  The dense
 // instantiation keeps them out of the register allocation of the GEMV loop.
-template <bool kMoE>
+template <bool kMoE, bool kTC>
 __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     const int ctid = threadIdx.x;
+    TcState ts{kTC ? reinterpret_cast<volatile uint32_t*>(smem + kSmemMisc)[8] : 0u, 0u, 0u};
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
     float* acc = reinterpret_cast<float*>(smem + kSmemAcc);
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
@@ -1308,8 +1481,16 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                     }
                     t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid, reinterpret_cast<const float*>(smem + kSmemPre));
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro); break;
-                case ET_OP_ATTN_MERGE: body_attn_merge<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
+                case ET_OP_ATTN_SPLIT:
+                    body_attn_split<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro);
+                    break;
+                case ET_OP_ATTN_MERGE: body_attn_merge<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
+                case ET_OP_GEMV_TC:
+                    if constexpr (kTC) t_pro = body_gemv_tc(P, op, v, smem, ring, ts, ctid);
+                    break;
+                case ET_OP_NORM:
+                    if constexpr (kTC) body_norm(P, op, v, red, ctid);
+                    break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_ALLREDUCE: body_allreduce(P, op, v, ctid, worker); break;
                 case ET_OP_MOE_ROUTE:
@@ -1349,6 +1530,32 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     }
 }
 
+// Producer: activation piece into x buffer xq % 2 once the issuer freed it (tensor-core GEMV).
+__device__ __noinline__ bool tc_issue_x(const StaticParams& P, uint8_t* smem, const Chunk& xc, unsigned int& xq,
+                                        int worker) {
+    uint64_t* bars = tc_bars(smem);
+    const int b = static_cast<int>(xq & 1u);
+    const uint32_t par = ((xq >> 1) & 1u) ^ 1u;
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
+    while (!mbar_try_wait(&bars[2 + b], par)) {
+        if ((++spins & 1023u) == 0) {
+            if (aborted(P.status)) return false;
+            if (t0 == 0) t0 = globaltimer();
+            else if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                report(P.status, ET_ERR_DEADLOCK, worker, -1, -6, static_cast<int>(xq));
+                return false;
+            }
+        }
+    }
+    __threadfence();             // the pieces were written by other CTAs before the waits passed
+    fence_proxy_async_global();  // ... with generic stores; the bulk copy reads through the async proxy
+    mbar_arrive_expect_tx(&bars[b], xc.bytes);
+    bulk_g2s_keep(smem + kSmemX + b * kTcXBuf, xc.src, xc.bytes, &bars[b]);
+    ++xq;
+    return true;
+}
+
 __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     if ((threadIdx.x & 31) != 0) return;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -1357,6 +1564,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     const uint64_t pol = policy_evict_first();
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
     unsigned long long cseq = 0;  // chunks issued to the ring
+    unsigned int xq = 0;          // activation pieces issued to the tensor-core x buffers
     for (int s = qb; s < qe; ++s) {
         SlotView v = view_slot(P, T, s, qb);
         if (v.masked) continue;
@@ -1371,9 +1579,20 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         }
         const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
         const int n = pl.total_chunks();
-        for (int c = 0; c < n; ++c, ++cseq) {
+        for (int c = 0; c < n; ++c) {
+            if (pl.tc_np) {
+                const Chunk xc = pl.chunk(c);
+                if (xc.x) {  // activation piece: produced upstream, so only once the slot's waits pass
+                    while (misc[1] <= s) {
+                        if (aborted(P.status)) return;
+                    }
+                    if (!tc_issue_x(P, smem, xc, xq, worker)) return;
+                    continue;
+                }
+            }
             const int stage = static_cast<int>(cseq % kStages);
             const uint32_t phase = static_cast<uint32_t>((cseq / kStages) & 1ull);
+            ++cseq;
             uint32_t spins = 0;
             uint64_t t0 = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
@@ -1439,7 +1658,26 @@ __device__ void dma_loop(const StaticParams& P) {
     }
 }
 
-template <bool kMoE>
+// Tensor-core instantiations: TMEM (512 columns) held for the whole launch and
+// the x-buffer / done mbarriers initialised.
+__device__ __forceinline__ void tc_setup(uint8_t* smem) {
+    if (threadIdx.x == 0) {
+        uint64_t* b = tc_bars(smem);
+        for (int i = 0; i < 5; ++i) mbar_init(&b[i], 1);
+        fence_mbar_init();
+    }
+    if ((threadIdx.x >> 5) == 0) tmem_alloc(reinterpret_cast<uint32_t*>(smem + kSmemMisc + 32), kTmemCols);
+    tc_fence_before();
+}
+
+__device__ __forceinline__ void tc_teardown(uint8_t* smem) {
+    tc_fence_before();
+    bar_sync(1, kConsumers);
+    tc_fence_after();
+    if ((threadIdx.x >> 5) == 0) tmem_dealloc(reinterpret_cast<volatile uint32_t*>(smem + kSmemMisc)[8], kTmemCols);
+}
+
+template <bool kMoE, bool kTC>
 __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_constant__ StaticParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int worker = blockIdx.x;
@@ -1486,10 +1724,13 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
             ent[i] = e;
         }
     }
+    if constexpr (kTC) tc_setup(smem);
     __syncthreads();
+    if constexpr (kTC) tc_fence_after();
     const int warp = threadIdx.x >> 5;
     if (warp < kConsumerWarps) {
-        consumer_loop<kMoE>(P, worker, smem, T);
+        consumer_loop<kMoE, kTC>(P, worker, smem, T);
+        if constexpr (kTC) tc_teardown(smem);
     } else if (warp == kProducerWarp) {
         producer_loop(P, worker, smem, T);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
@@ -1872,9 +2113,10 @@ __device__ void dyn_record(const StaticParams& P, const DynParams& D, int task, 
     P.trace[task] = r;
 }
 
-template <bool kMoE>
+template <bool kMoE, bool kTC>
 __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
     const int ctid = threadIdx.x;
+    TcState ts{kTC ? reinterpret_cast<volatile uint32_t*>(smem + kSmemMisc)[8] : 0u, 0u, 0u};
     const int2* cext = P.num_calls <= kMaxCallExt ? reinterpret_cast<const int2*>(smem + kSmemCallExt) : nullptr;
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
     float* acc = reinterpret_cast<float*>(smem + kSmemAcc);
@@ -1915,6 +2157,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
             if (ok && D.early_push) dyn_dispatch_warp(P, D, v, task, worker, ctid);
             if (ctid == 0) {
                 misc[0] = ok ? 0 : 1;
+                misc[6] = misc[5];  // waits passed: the producer may stream this task's activations
                 tw = globaltimer();
             }
         }
@@ -1942,8 +2185,14 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     }
                     tp = body_gemv(P, op, v, xs, acc, red, ring, ctid);
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
-                case ET_OP_ATTN_MERGE: body_attn_merge<kMoE>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
+                case ET_OP_ATTN_SPLIT: body_attn_split<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
+                case ET_OP_ATTN_MERGE: body_attn_merge<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
+                case ET_OP_GEMV_TC:
+                    if constexpr (kTC) tp = body_gemv_tc(P, op, v, smem, ring, ts, ctid);
+                    break;
+                case ET_OP_NORM:
+                    if constexpr (kTC) body_norm(P, op, v, red, ctid);
+                    break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_MOE_ROUTE:
                     if constexpr (kMoE) body_moe_route(P, op, v, xs, acc, red, ring, ctid, &tp);
@@ -1978,6 +2227,7 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
     const uint64_t pol = policy_evict_first();
     unsigned long long cseq = 0;
+    unsigned int xq = 0;
     int gen = 0;
     for (;;) {
         while (misc[5] == gen) {
@@ -1992,9 +2242,20 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
         if (!op_streams(op.kind)) continue;
         const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
         const int n = pl.total_chunks();
-        for (int c = 0; c < n; ++c, ++cseq) {
+        for (int c = 0; c < n; ++c) {
+            if (pl.tc_np) {
+                const Chunk xc = pl.chunk(c);
+                if (xc.x) {  // activation piece: only once the task's (armed) waits pass
+                    while (misc[6] != gen) {
+                        if (aborted(P.status)) return;
+                    }
+                    if (!tc_issue_x(P, smem, xc, xq, worker)) return;
+                    continue;
+                }
+            }
             const int stage = static_cast<int>(cseq % kStages);
             const uint32_t phase = static_cast<uint32_t>((cseq / kStages) & 1ull);
+            ++cseq;
             uint32_t spins = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
                 if ((++spins & 1023u) == 0 && aborted(P.status)) return;
@@ -2057,7 +2318,7 @@ __device__ void dyn_reset_state(const StaticParams& P, const DynParams& D, DynCt
     }
 }
 
-template <bool kMoE>
+template <bool kMoE, bool kTC>
 __global__ void __launch_bounds__(kThreads, 1)
     et_dynamic_kernel(const __grid_constant__ StaticParams P, const __grid_constant__ DynParams D) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -2076,6 +2337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
         misc[0] = misc[1] = misc[2] = 0;
         misc[3] = misc[4] = misc[5] = 0;
+        misc[6] = -1;
         if (worker == 0) atomicAdd(&P.status->pushes, static_cast<unsigned long long>(D.num_ready[0] + D.num_ready[1]));
     }
     if (P.num_calls <= kMaxCallExt) {  // grid extents of every call at this binding (masking)
@@ -2086,10 +2348,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 rank > 1 ? static_cast<int>(eval_code(P, c, 1)) : 1);
         }
     }
+    if constexpr (kTC) tc_setup(smem);
     __syncthreads();
+    if constexpr (kTC) tc_fence_after();
     const int warp = threadIdx.x >> 5;
     if (warp < kConsumerWarps) {
-        dyn_consumer_loop<kMoE>(P, D, worker, smem);
+        dyn_consumer_loop<kMoE, kTC>(P, D, worker, smem);
+        if constexpr (kTC) tc_teardown(smem);
     } else if (warp == kProducerWarp) {
         dyn_producer_loop(P, D, worker, smem);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
@@ -2129,20 +2394,29 @@ int launch_persistent(K kernel, bool& configured, int num_workers, void* stream,
 }
 }  // namespace
 
-// max_batch > 8 needs the tensor-memory (tcgen05) GEMV path, not in this build.
-int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, int moe, void* stream) {
-    if (max_batch > etk::kMaxBatch) return static_cast<int>(cudaErrorInvalidValue);
-    static bool conf[2] = {false, false};
+// variant bit 0: MoE bodies; bit 1: tensor-core GEMV (TMEM) bodies.  Batches above
+// 8 need the tensor-core variant (the mma.sync GEMV carries the batch in n8).
+int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, int variant, void* stream) {
+    if (max_batch > ((variant & 2) ? etk::kMaxBatchTc : etk::kMaxBatch)) return static_cast<int>(cudaErrorInvalidValue);
+    static bool conf[4] = {false, false, false, false};
     void* args[] = {const_cast<etk::StaticParams*>(&p)};
-    return moe ? launch_persistent(etk::et_static_kernel<true>, conf[1], num_workers, stream, args)
-               : launch_persistent(etk::et_static_kernel<false>, conf[0], num_workers, stream, args);
+    switch (variant & 3) {
+        case 1: return launch_persistent(etk::et_static_kernel<true, false>, conf[1], num_workers, stream, args);
+        case 2: return launch_persistent(etk::et_static_kernel<false, true>, conf[2], num_workers, stream, args);
+        case 3: return launch_persistent(etk::et_static_kernel<true, true>, conf[3], num_workers, stream, args);
+        default: return launch_persistent(etk::et_static_kernel<false, false>, conf[0], num_workers, stream, args);
+    }
 }
 
-int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, int moe, void* stream) {
-    static bool conf[2] = {false, false};
+int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, int variant, void* stream) {
+    static bool conf[4] = {false, false, false, false};
     void* args[] = {const_cast<etk::StaticParams*>(&p), const_cast<etk::DynParams*>(&d)};
-    return moe ? launch_persistent(etk::et_dynamic_kernel<true>, conf[1], num_workers, stream, args)
-               : launch_persistent(etk::et_dynamic_kernel<false>, conf[0], num_workers, stream, args);
+    switch (variant & 3) {
+        case 1: return launch_persistent(etk::et_dynamic_kernel<true, false>, conf[1], num_workers, stream, args);
+        case 2: return launch_persistent(etk::et_dynamic_kernel<false, true>, conf[2], num_workers, stream, args);
+        case 3: return launch_persistent(etk::et_dynamic_kernel<true, true>, conf[3], num_workers, stream, args);
+        default: return launch_persistent(etk::et_dynamic_kernel<false, false>, conf[0], num_workers, stream, args);
+    }
 }
 
 int et_dynamic_reset(const etk::StaticParams& p, const etk::DynParams& d, void* stream) {

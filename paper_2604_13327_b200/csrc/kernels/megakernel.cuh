@@ -27,6 +27,7 @@ constexpr int kMaxSymbols = 8;
 constexpr int kMaxRuntime = 512;  // runtime tensors per graph (6 per MoE layer)
 constexpr int kMaxRank = 4;
 constexpr int kMaxBatch = 8;   // GEMV batch rows carried in the mma M dimension
+constexpr int kMaxBatchTc = 128;  // tensor-core GEMV: batch = MMA N (Npad * kp * 2 <= 16 KB)
 
 constexpr int kMaxTableSlots = 512;   // per-CTA slot table in shared memory
 constexpr int kMaxTableCalls = 1024;  // per-call sample extent of dim 0
@@ -174,7 +175,7 @@ constexpr int kMaxCallExt = (kSmemBar - kSmemTable) / 8;
 
 // Host-side launcher (megakernel.cu).
 // moe != 0 selects the instantiation that contains the MoE tile bodies
-int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, int moe, void* stream);
+int et_launch_static(const etk::StaticParams& p, int num_workers, int max_batch, int variant, void* stream);
 int et_static_smem_bytes();
-int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, int moe, void* stream);
+int et_launch_dynamic(const etk::StaticParams& p, const etk::DynParams& d, int num_workers, int variant, void* stream);
 int et_dynamic_reset(const etk::StaticParams& p, const etk::DynParams& d, void* stream);

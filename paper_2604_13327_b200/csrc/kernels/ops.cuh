@@ -69,6 +69,22 @@
 // ET_OP_EMBED           task (0): h[b][:] = float(table[tokens[b]][:]) for every batch row
 //   i0 = hidden, i1 = batch symbol slot (-1: 1); p0 = table (bf16 [vocab][hidden]),
 //   p1 = token ids (int32 [b]), p2 = out (fp32 [b][hidden])
+// ET_OP_GEMV_TC         large-batch GEMV on the tcgen05 tensor cores: task t of T = G * i3 takes
+//   row blocks [g*nblk/G, (g+1)*nblk/G) (128 rows each, nblk = N/128) and k pieces
+//   [r*np/i3, (r+1)*np/i3) (np = K/kp) with g = t / i3, r = t % i3; per piece the activation
+//   piece (Npad x kp bf16, Npad = batch rounded up to 16) streams into one of two shared
+//   buffers, the weight chunks (16 KB = 128 rows x 64 k) through the ring, and one thread
+//   issues tcgen05.mma (M=128, N=Npad, K=16) into TMEM accumulators (column block (seg, blk)
+//   at (seg*nblk_task + blk)*Npad); the epilogue reads TMEM with tcgen05.ld.
+//   i0 = N rows per segment (% 128 == 0), i1 = K, i2 = segments (1|2), i3 = k splits (EPI_ADD
+//   only when > 1), i4 = epilogue (F32 / BF16 / RESID / ADD: [b][N] row-major; SILU_MUL:
+//   bf16 in the tensor-core operand layout with piece length i7), i5 = batch symbol slot,
+//   i6 = kp (piece length, % 64 == 0, Npad * kp * 2 <= 16 KB);
+//   p0/p1 = weights in the tensor-core layout of segment 0/1 (tc_weight_offset), p2 = x in the
+//   operand layout (xb_offset), p4 = out, p5 = residual in (fp32, EPI_RESID)
+// ET_OP_NORM            task n (< b): out[n] = bf16(h[n] * rsqrt(mean(h[n]^2) + eps) * gamma) in
+//   the tensor-core operand layout; i0 = K, i5 = batch symbol slot, i6 = kp; p0 = h (fp32
+//   [b][K]), p1 = gamma (fp32 [K]), p2 = out; f0 = eps
 #pragma once
 
 #include "megakernel.cuh"
@@ -81,7 +97,44 @@ enum GemvEpi { EPI_F32 = 0, EPI_BF16 = 1, EPI_RESID = 2, EPI_SILU_MUL = 3, EPI_Q
 struct Chunk {
     const uint8_t* src;
     uint32_t bytes;
+    bool x;  // tensor-core GEMV: an activation piece for the x buffers, not a ring stage
 };
+
+// ---- tensor-core GEMV (ET_OP_GEMV_TC) -------------------------------------------------
+constexpr int kTcChunk = 16384;      // weight chunk: 128 rows x 64 k (4 k steps of 4 KB)
+constexpr int kTcXBuf = kXBytes / 2;  // two activation piece buffers
+constexpr int kTmemCols = 512;
+
+// Batch padded to the MMA N dimension (multiple of 16, at least 16).
+__host__ __device__ __forceinline__ int tc_npad(int nb) { return nb <= 16 ? 16 : (nb + 15) & ~15; }
+
+// Element offset of activation (n, k) in the operand layout: pieces of kp, then
+// k steps of 16, then 8-row groups of the batch, then the two 8-wide k halves,
+// then 8 rows x 8 k (16-byte core-matrix rows).
+__host__ __device__ __forceinline__ long long xb_offset(int n, int k, int npad, int kp) {
+    const int piece = k / kp, kk = k - piece * kp;
+    return static_cast<long long>(piece) * npad * kp + (kk >> 4) * (npad * 16) + (n >> 3) * 128 + ((kk >> 3) & 1) * 64 +
+           (n & 7) * 8 + (k & 7);
+}
+
+struct TcSpan {
+    int b0, nblk;  // first row block, row blocks of the task
+    int p0, np;    // first k piece, pieces of the task
+};
+
+__host__ __device__ __forceinline__ TcSpan tc_span(const et_op& op, int t, int T) {
+    const int splits = op.i[3] > 0 ? op.i[3] : 1;
+    const int G = T / splits > 0 ? T / splits : 1;
+    const int g = t / splits, r = t - g * splits;
+    const int nblk = op.i[0] / 128, npc = op.i[1] / op.i[6];
+    TcSpan sp;
+    sp.b0 = static_cast<int>(static_cast<long long>(g) * nblk / G);
+    sp.nblk = static_cast<int>(static_cast<long long>(g + 1) * nblk / G) - sp.b0;
+    sp.p0 = static_cast<int>(static_cast<long long>(r) * npc / splits);
+    sp.np = static_cast<int>(static_cast<long long>(r + 1) * npc / splits) - sp.p0;
+    if (g >= G) sp.nblk = 0;
+    return sp;
+}
 
 // Streaming plan of one task: up to two contiguous byte ranges cut into
 // chunks of `cbytes` (<= one ring stage).  GEMV streams segment 0 then
@@ -94,12 +147,30 @@ struct StreamPlan {
     int cbytes;
     bool interleave;
     int n[kMaxSeg];  // chunks per segment (set by finish(); keeps divisions off the per-chunk path)
+    // tensor-core GEMV: per piece p, X(p) then the weight chunks of every (segment, block),
+    // except that piece 0 streams up to kStages weight chunks ahead of X(0) (those need no
+    // dependency); tc_w = weight chunks per piece, tc_np = pieces (0: not a tensor-core plan)
+    int tc_w = 0, tc_np = 0, tc_pre = 0;
+    const uint8_t* tc_x;       // activation piece p at tc_x + p * tc_xbytes
+    uint32_t tc_xbytes;
+    long long tc_pstride;      // weight bytes between pieces (whole matrix width)
 
     __device__ void finish() {
         for (int s = 0; s < kMaxSeg; ++s) n[s] = s < nseg ? static_cast<int>((bytes[s] + cbytes - 1) / cbytes) : 0;
     }
-    __device__ int total_chunks() const { return n[0] + n[1] + n[2]; }
+    __device__ int total_chunks() const { return tc_np ? tc_np * (tc_w + 1) : n[0] + n[1] + n[2]; }
     __device__ Chunk chunk(int idx) const {
+        if (tc_np) {
+            const int p = idx / (tc_w + 1);
+            int r = idx - p * (tc_w + 1);
+            const int xpos = p == 0 ? tc_pre : 0;
+            if (r == xpos) return Chunk{tc_x + static_cast<long long>(p) * tc_xbytes, tc_xbytes, true};
+            if (r > xpos) --r;
+            const int per_seg = static_cast<int>(bytes[0] / kTcChunk);
+            const int sg = r / per_seg;
+            return Chunk{base[sg] + p * tc_pstride + static_cast<long long>(r - sg * per_seg) * kTcChunk, kTcChunk,
+                         false};
+        }
         int s = 0;
         if (interleave) {
             s = idx & 1;
@@ -109,7 +180,7 @@ struct StreamPlan {
         }
         const long long off = static_cast<long long>(idx) * cbytes;
         const long long rem = bytes[s] - off;
-        return Chunk{base[s] + off, static_cast<uint32_t>(rem < cbytes ? rem : cbytes)};
+        return Chunk{base[s] + off, static_cast<uint32_t>(rem < cbytes ? rem : cbytes), false};
     }
 };
 
@@ -222,6 +293,26 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
     pl.nseg = 0;
     pl.cbytes = kStageBytes;
     pl.interleave = false;
+    if (op.kind == ET_OP_GEMV_TC) {
+        const TcSpan sp = tc_span(op, coord[0], T);
+        if (sp.nblk <= 0 || sp.np <= 0) {  // idle task: nothing streams
+            pl.finish();
+            return pl;
+        }
+        const int nb = op.i[5] >= 0 ? static_cast<int>(binding[op.i[5]]) : 1;
+        const long long kp = op.i[6], blk_bytes = kp * 256;  // one 128-row block of one piece
+        pl.tc_pstride = static_cast<long long>(op.i[0] / 128) * blk_bytes;
+        pl.nseg = op.i[2];
+        for (int s = 0; s < pl.nseg; ++s)
+            pl.base[s] = reinterpret_cast<const uint8_t*>(op.p[s]) + sp.p0 * pl.tc_pstride + sp.b0 * blk_bytes;
+        pl.bytes[0] = sp.nblk * blk_bytes;
+        pl.tc_w = static_cast<int>(pl.nseg * pl.bytes[0] / kTcChunk);
+        pl.tc_np = sp.np;
+        pl.tc_pre = pl.tc_w < kStages ? pl.tc_w : kStages;
+        pl.tc_xbytes = static_cast<uint32_t>(tc_npad(nb) * kp * 2);
+        pl.tc_x = reinterpret_cast<const uint8_t*>(op.p[2]) + static_cast<long long>(sp.p0) * pl.tc_xbytes;
+        return pl;
+    }
     if (op.kind == ET_OP_GEMV) {
         const bool grouped = (op.flags & 16) != 0;  // coord 0 = group (its own matrix), coord 1 = row span
         const GemvSpan sp = gemv_span(op, grouped ? coord[1] : coord[0], grouped ? op.i[13] : T);

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../kernels/megakernel.cuh"
+#include "../kernels/ops.cuh"
 #include "et_runtime.h"
 
 namespace {
@@ -121,7 +122,7 @@ struct et_runtime {
 
     std::vector<Sample> samples;
     DevArray<et_op> d_ops;
-    int has_moe = 0;  // bound ops include MoE bodies: launch the MoE instantiation
+    int has_moe = 0;  // kernel variant: bit 0 MoE bodies, bit 1 tensor-core GEMV bodies (bound ops)
     int ops_bound = 0;
     std::vector<et_op> h_ops;  // host copy of the bound op table (launch-time capacity checks)
 
@@ -445,6 +446,16 @@ namespace {
 // A GEMV task accumulates nseg x rows x b fp32 values in shared memory (kAccFloats);
 // bound the rows of the widest task from the span arithmetic of ops.cuh gemv_span.
 bool gemv_acc_fits(const et_op& op, int64_t grid0, const int64_t* binding) {
+    if (op.kind == ET_OP_GEMV_TC) {  // TMEM columns, operand shapes and piece buffers
+        const int64_t nb = op.i[5] >= 0 ? binding[op.i[5]] : 1;
+        const int npad = etk::tc_npad(static_cast<int>(nb));
+        const int kp = op.i[6], splits = op.i[3] > 0 ? op.i[3] : 1;
+        if (nb > etk::kMaxBatchTc || kp <= 0 || kp % 64 || op.i[1] % kp || op.i[0] % 128) return false;
+        if (static_cast<int64_t>(npad) * kp * 2 > etk::kTcXBuf || grid0 % splits) return false;
+        if (splits > 1 && op.i[4] != etk::EPI_ADD) return false;
+        const int64_t G = grid0 / splits, nblk = op.i[0] / 128;
+        return op.i[2] * ((nblk + G - 1) / G) * npad <= etk::kTmemCols;
+    }
     if (op.kind != ET_OP_GEMV) return true;
     const bool grouped = (op.flags & 16) != 0;
     const int64_t T = grouped ? op.i[13] : grid0;
@@ -472,7 +483,8 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     rt->has_moe = 0;
     rt->h_ops.assign(ops, ops + num_calls);
     for (int32_t c = 0; c < num_calls; ++c)
-        if (ops[c].kind == ET_OP_MOE_ROUTE || ops[c].kind == ET_OP_MOE_EXPERT) rt->has_moe = 1;
+        if (ops[c].kind == ET_OP_MOE_ROUTE || ops[c].kind == ET_OP_MOE_EXPERT) rt->has_moe |= 1;
+        else if (ops[c].kind == ET_OP_GEMV_TC || ops[c].kind == ET_OP_NORM) rt->has_moe |= 2;
     rt->ops_bound = 1;
     return ET_OK;
 }
@@ -573,8 +585,8 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
                 return rt->fail(ET_ERR_INVALID, "sampled shape does not cover the actual grid of call " + std::to_string(c));
             if (d == 0 && !gemv_acc_fits(rt->h_ops[static_cast<size_t>(c)], a, binding))
                 return rt->fail(ET_ERR_INVALID, "GEMV call " + std::to_string(c) +
-                                                    ": rows per task x batch exceed the shared-memory accumulators "
-                                                    "(give the call more tasks)");
+                                                    ": rows per task x batch exceed the accumulators (shared memory / "
+                                                    "tensor memory) or the operand shape is invalid");
         }
 
     etk::StaticParams p{};

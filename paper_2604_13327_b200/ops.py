@@ -23,6 +23,8 @@ OP_MOE_GROUP = 9
 OP_MOE_COMBINE = 10
 OP_ARGMAX = 11
 OP_EMBED = 12
+OP_GEMV_TC = 13
+OP_NORM = 14
 
 EPI_F32, EPI_BF16, EPI_RESID, EPI_SILU_MUL, EPI_QKV_ROPE, EPI_ADD = range(6)
 

@@ -20,9 +20,10 @@ def test_persistent_kernels_do_not_spill():
                          r"(\d+) bytes spill loads", text):
         found[m.group(1)] = (int(m.group(3)), int(m.group(4)))
     kernels = {k: v for k, v in found.items() if "et_static_kernel" in k or "et_dynamic_kernel" in k}
-    assert len(kernels) == 4, found  # dense + MoE instantiation of each scheduler
+    # <kMoE, kTC> instantiations of each scheduler: dense, MoE, tensor-core, MoE + tensor-core
+    assert len(kernels) == 8, found
     for name, (st, ld) in kernels.items():
-        if "ILb0E" in name:  # dense instantiation (the Llama decode path): spill-free
+        if "ILb0ELb0E" in name:  # dense mma.sync instantiation (the Llama bs=1 decode path): spill-free
             assert st == 0 and ld == 0, (name, st, ld)
-        else:  # MoE instantiation: bounded (once-per-task routing / slot decoding code)
-            assert st <= 160 and ld <= 160, (name, st, ld)
+        else:  # bounded (once-per-task routing / slot decoding / epilogue code)
+            assert st <= 256 and ld <= 256, (name, st, ld)

@@ -1,0 +1,64 @@
+"""Large-batch decode on the tensor-core GEMV path (tcgen05.mma into TMEM):
+one lowered artifact (batch symbol b <= 64, position symbol s) runs several
+(s, b) bindings; every sequence's logits agree with the bf16-emulating CPU
+oracle (oracle/decoder_oracle.py, one sequence at a time) and its new K/V rows
+match the oracle's, bit for bit after the bf16 rounding both apply.
+Tolerance: max |err| <= 2e-3 * max|logit| + 2e-3 (fp32 accumulation order)."""
+
+import pytest
+import torch
+
+from oracle.decoder_oracle import decode_step, weights_to_cpu
+from paper_2604_13327_b200.batch import BatchDecodeModel, tc_npad, xb_unpack
+from paper_2604_13327_b200.decode import TINY
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=["static", "dynamic"])
+def model(request):
+    return BatchDecodeModel(TINY, samples=(16, 96), max_batch=64, batch_samples=(8, 64), num_workers=16, seed=0,
+                            scheduler=request.param, keep_logical=True, record_trace=True)
+
+
+@pytest.mark.parametrize("b,s", [(1, 16), (5, 40), (17, 96), (64, 7)])
+def test_batch_logits_vs_oracle(model, b, s):
+    m, cfg = model, model.cfg
+    m.fill_cache(s, seed=b)
+    toks = [(37 * i + 11) % cfg.vocab for i in range(b)]
+    m.set_token(toks)
+    kc = [k.cpu() for k in m.kcache]
+    vc = [v.cpu() for v in m.vcache]
+    logits = m.step(s, b).cpu()
+    Wc = weights_to_cpu(m.W_logical)
+    for t in range(b):
+        ref, nk, nv = decode_step(cfg, Wc, [k[t] for k in kc], [v[t] for v in vc], toks[t], s, m.inv_freq.cpu())
+        err = (logits[t] - ref).abs().max().item()
+        scale = ref.abs().max().item()
+        assert err <= 2e-3 * scale + 2e-3, (b, s, t, err, scale)
+        if t in (0, b - 1):
+            for l in range(cfg.layers):
+                dk = (m.kcache[l][t, :, s].float().cpu() - nk[l].float()).abs().max().item()
+                dv = (m.vcache[l][t, :, s].float().cpu() - nv[l].float()).abs().max().item()
+                assert dk <= 2e-2 * nk[l].abs().max().item() + 1e-2, (l, dk)
+                assert dv <= 2e-2 * nv[l].abs().max().item() + 1e-2, (l, dv)
+    assert torch.isfinite(logits).all()
+    mg = m.kernel.graph.instantiate({"s": s, "b": b})
+    assert mg.check(m.executor.trace()) == []
+    assert all(c == 0 for c in m.executor.final_counters())
+    assert m.last_stats["tasks_executed"] == mg.num_tasks
+    assert m.qkv.abs().max().item() == 0.0  # raw split-K accumulators consumed and zeroed
+
+
+def test_batch_final_norm_operand_layout(model):
+    """The final RMSNorm's operand-layout buffer holds exactly bf16(rmsnorm(h) * gamma)."""
+    m, cfg = model, model.cfg
+    b, s = 5, 16
+    m.fill_cache(s, seed=3)
+    m.set_token([1, 2, 3, 4, 5])
+    m.step(s, b)
+    h = m.h[:b].double().cpu()
+    g = m.W["final_norm"].double().cpu()
+    want = (h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + cfg.eps) * g).to(torch.bfloat16).float()
+    got = xb_unpack(m.xn.cpu(), b, cfg.hidden, tc_npad(b), m.kp)
+    assert (got - want).abs().max().item() <= 1e-2 * want.abs().max().item()
