@@ -83,11 +83,12 @@ def xb_unpack(buf, b, K, npad, kp):
 def tc_tasks(nblk, workers, splittable, nseg=1, npad=64, pieces=1):
     """(tasks, k splits) of a projection: one 128-row block per group and enough
     k splits to cover the workers when the epilogue adds (split-K); otherwise
-    groups of blocks sized to the TMEM columns."""
+    groups of blocks small enough that two MMA issuers fit their accumulators
+    in TMEM (ops.cuh kTcIssuers)."""
     if splittable:
         splits = max(1, min(pieces, round(workers / nblk)))
         return nblk * splits, splits
-    per = max(1, TMEM_COLS // (nseg * npad))
+    per = max(1, TMEM_COLS // (2 * nseg * npad))  # blocks per task that leave TMEM for 2 MMA issuers
     groups = max(min(workers, nblk), -(-nblk // per))
     return groups, 1
 
@@ -138,7 +139,10 @@ class BatchDecodeModel:
         props = torch.cuda.get_device_properties(self.device)
         self.num_workers = num_workers or props.multi_processor_count
         self.max_batch = max_batch
-        self.batch_samples = sorted(set(batch_samples or (max_batch,)) | {max_batch})
+        # batch samples: powers of two up to max_batch by default, so a small batch runs on a
+        # schedule at most twice its size (masked tasks still wait and notify)
+        default = [1 << i for i in range(8) if (1 << i) < max_batch]
+        self.batch_samples = sorted(set(batch_samples or default) | {max_batch})
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
         self.kp = kp = tc_piece(max_batch)
@@ -153,6 +157,8 @@ class BatchDecodeModel:
                                       ("gateup", I, H, False, 2), ("down", H, I, True, 1),
                                       ("lm", cfg.vocab, H, False, 1)):
             self.tasks[name], self.splits[name] = tc_tasks(n // 128, w, add, nseg, npad, k // kp)
+        # attention splits per (sequence, kv head): the batch-1 cap (a split is a run of
+        # 64-position blocks; at large batch the extra tasks only shorten the tail)
         self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
         self.scheduler = scheduler
         t0 = time.perf_counter()

@@ -228,6 +228,7 @@ struct Ring {
     unsigned long long stall = 0;  // ns spent waiting for filled stages (ET_DEBUG bit 2)
     bool dbg = false;
     unsigned long long busy = 0;   // ns between a stage's arrival and its release (ET_DEBUG bit 8)
+    unsigned long long xwait = 0;  // tensor-core GEMV: ns the issuer waited for activation pieces
     uint64_t t_ret = 0;
 
     __device__ __forceinline__ static int stage_of(unsigned long long c) { return static_cast<int>(c % kStages); }
@@ -528,8 +529,8 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
 
 // ---------------------------------------------------------------------------
 // Large-batch GEMV on the 5th-generation tensor cores (ET_OP_GEMV_TC, ops.cuh).
-// Shared-memory mbarriers behind the misc words: x buffer full [2], x buffer
-// free [2] (tcgen05.commit), accumulators done [1] (tcgen05.commit).
+// Shared-memory mbarriers behind the misc words: x slot full [kTcXSlots], x slot
+// free [kTcXSlots] (tcgen05.commit), accumulators done [1] (tcgen05.commit).
 struct TcState {
     uint32_t tmem;        // TMEM column base (512 columns, allocated at kernel start)
     unsigned int xp;      // activation pieces consumed (issuer thread)
@@ -537,7 +538,7 @@ struct TcState {
 };
 
 __device__ __forceinline__ uint64_t* tc_bars(uint8_t* smem) {
-    return reinterpret_cast<uint64_t*>(smem + kSmemMisc + 448);
+    return reinterpret_cast<uint64_t*>(smem + kSmemMisc + 384);
 }
 
 // Bounded mbarrier wait (reports a deadlock instead of hanging; false when aborted).
@@ -558,6 +559,68 @@ __device__ __noinline__ bool tc_wait(uint64_t* bar, uint32_t parity, DevStatus* 
     return true;
 }
 
+// Sum of the nis issuers' accumulators (cols apart) for 16 columns of this lane.
+__device__ __forceinline__ void tc_sum16(uint32_t taddr, int nis, int cols, float* v) {
+    tmem_ld16(taddr, v);
+    for (int k = 1; k < nis; ++k) {
+        float w[16];
+        tmem_ld16(taddr + static_cast<uint32_t>(k * cols), w);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += w[j];
+    }
+}
+
+// Issuer k (one thread) of a tensor-core GEMV task: for pieces k, k + nis, ...,
+// wait for the activation piece, then per weight chunk four K=16 MMAs into its
+// own (segment, block) accumulators; each chunk's ring stage is released by
+// tcgen05.commit once its MMAs have read it.  Everything lives in registers:
+// the mbarrier round trips of one thread bound its streaming rate, so up to
+// kTcIssuers threads (in different warps) take alternate pieces.
+__device__ __noinline__ void tc_issue(uint8_t* smem, uint32_t tmem, unsigned long long c0, unsigned int xp0, int k,
+                                      int nis, int np, int nsb, int cpb, int npad, int kp, unsigned long long* xwait,
+                                      DevStatus* status, long long watchdog_ns, int worker) {
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+    uint64_t* empty = full + kStages;
+    uint64_t* bars = tc_bars(smem);
+    const uint32_t ring0 = smem_u32(smem + kSmemRing);
+    const uint32_t idesc = umma_idesc_bf16(npad);
+    const uint32_t xbytes = static_cast<uint32_t>(npad * kp * 2);
+    const int nxs = tc_xslots(xbytes);
+    const int wpp = nsb * cpb;                               // chunks per piece
+    const uint64_t xstep = static_cast<uint64_t>(npad * 2);  // one k step of the piece (npad*32 B >> 4)
+    for (int p = k; p < np; p += nis) {
+        const unsigned int gx = xp0 + static_cast<unsigned int>(p);  // the CTA's piece sequence number
+        const int xb = static_cast<int>(gx % nxs);
+        const uint64_t tx0 = xwait ? globaltimer() : 0;
+        if (!tc_wait(&bars[xb], (gx / nxs) & 1u, status, watchdog_ns, worker, -4)) return;
+        if (xwait) xwait[0] += globaltimer() - tx0;
+        tc_fence_after();
+        const uint64_t xd = umma_desc(smem_u32(smem + kSmemX) + xb * xbytes);
+        unsigned long long c = c0 + static_cast<unsigned long long>(p) * wpp;
+        uint32_t d = tmem;
+        for (int sb = 0; sb < nsb; ++sb, d += npad) {  // (segment, block) accumulators
+            uint64_t xk = xd;
+            for (int ch = 0; ch < cpb; ++ch, ++c, xk += 4 * xstep) {
+                const int st = static_cast<int>(c & (kStages - 1));
+                const uint32_t par = static_cast<uint32_t>(c / kStages) & 1u;
+                if (!mbar_try_wait(&full[st], par)) {
+                    const uint64_t tw0 = xwait ? globaltimer() : 0;
+                    if (!tc_wait(&full[st], par, status, watchdog_ns, worker, -2)) return;
+                    if (xwait) xwait[1] += globaltimer() - tw0;
+                }
+                tc_fence_after();
+                const uint64_t a = umma_desc(ring0 + st * kStageBytes);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    umma_bf16(d, a + j * 256, xk + j * xstep, idesc, (p != k || ch != 0 || j != 0) ? 1u : 0u);
+                umma_commit(&empty[st]);
+            }
+        }
+        umma_commit(&bars[kTcXSlots + xb]);  // the x slot is free once these MMAs complete
+    }
+    umma_commit(&bars[2 * kTcXSlots]);  // one of the kTcIssuers arrivals on the done barrier
+}
+
 __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op& op, const SlotView& si, uint8_t* smem,
                                  Ring& ring, TcState& ts, int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
@@ -568,52 +631,40 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
     uint64_t* bars = tc_bars(smem);
     const int cpb = kp / 64;                       // 16 KB weight chunks per (piece, block)
     const int wpp = nseg * sp.nblk * cpb;          // weight chunks per piece
+    const int cols = nseg * sp.nblk * npad;        // TMEM columns of one issuer's accumulators
+    // issuers: lane 0 of warps 0..nis-1 take pieces k, k + nis, ... into their own
+    // accumulator columns (the protocol round trips of one thread bound its rate).
+    // Parity waits are exact only while no waiter runs two phases ahead of the fills:
+    // an issuer's next piece must lie within one ring lap (nis * wpp <= kStages) and
+    // one x-slot lap (nis <= slots) of its previous one -- the producer fills in order.
+    const int nxs = tc_xslots(static_cast<uint32_t>(npad * kp * 2));
+    int nis = kTmemCols / cols;
+    nis = nis < kTcIssuers ? nis : kTcIssuers;
+    nis = nis < sp.np ? nis : sp.np;
+    nis = nis < kStages / wpp ? nis : kStages / wpp;
+    nis = nis < nxs ? nis : nxs;
+    nis = nis > 1 ? nis : 1;
     const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
-    if (ctid == 0) {
-        // the issuer: per piece, wait for the activation piece, then per weight chunk
-        // four K=16 MMAs into the (segment, block) accumulator; each chunk's stage is
-        // released by tcgen05.commit once its MMAs have read it
-        const uint32_t idesc = umma_idesc_bf16(npad);
-        unsigned long long c = ring.seq;
-        bool ok = true;
-        for (int p = 0; p < sp.np && ok; ++p) {
-            const int xb = static_cast<int>(ts.xp & 1u);
-            ok = tc_wait(&bars[xb], (ts.xp >> 1) & 1u, P.status, P.watchdog_ns, ring.worker, -4);
-            if (!ok) break;
-            tc_fence_after();
-            const uint32_t xaddr = smem_u32(smem + kSmemX + xb * kTcXBuf);
-            for (int w = 0; w < wpp; ++w, ++c) {
-                const uint8_t* buf = ring.wait(c);
-                if (!buf) {
-                    ok = false;
-                    break;
-                }
-                tc_fence_after();
-                const int sg = w / (sp.nblk * cpb), rem = w - sg * sp.nblk * cpb;
-                const int blk = rem / cpb, ch = rem - blk * cpb;
-                const uint32_t d = ts.tmem + static_cast<uint32_t>((sg * sp.nblk + blk) * npad);
-                const uint32_t a0 = smem_u32(buf);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int ks = ch * 4 + j;
-                    umma_bf16(d, umma_desc(a0 + j * 4096), umma_desc(xaddr + ks * npad * 32), idesc,
-                              (p | ks) != 0 ? 1u : 0u);
-                }
-                umma_commit(&ring.empty[Ring::stage_of(c)]);
-            }
-            umma_commit(&bars[2 + xb]);  // the x buffer is free once this piece's MMAs complete
-            ++ts.xp;
-        }
-        umma_commit(&bars[4]);
+    if (lane == 0 && warp < kTcIssuers) {  // the rest of each issuer warp parks on the closing barrier
+        unsigned long long xw[2] = {0, 0};  // debug: ns waiting for activation pieces / ring stages
+        tc_issue(smem, ts.tmem + static_cast<uint32_t>(warp * cols), ring.seq, ts.xp, warp, nis, warp < nis ? sp.np : 0,
+                 nseg * sp.nblk, cpb, npad, kp, ring.dbg ? xw : nullptr, P.status, P.watchdog_ns, ring.worker);
+        ring.xwait += xw[0];
+        ring.stall += xw[1];
     }
+    // the other consumer threads block on the named barrier while the issuers run (spinning
+    // on the done mbarrier would contend with the issuers' mbarrier traffic)
+    bar_sync(1, kConsumers);
     ring.seq += static_cast<unsigned long long>(wpp) * sp.np;
-    const bool done = tc_wait(&bars[4], ts.ndone & 1u, P.status, P.watchdog_ns, ring.worker, -5);
+    ts.xp += static_cast<unsigned int>(sp.np);
+    const bool done = tc_wait(&bars[2 * kTcXSlots], ts.ndone & 1u, P.status, P.watchdog_ns, ring.worker, -5);
     ++ts.ndone;
     if (!done) return t_pro;
     tc_fence_after();
 
     // ---- epilogue: warp w reads TMEM lanes 32*(w%4).. (rows of each block); the two
-    // warp halves take alternate 16-column (batch) chunks
+    // warp halves take alternate 16-column (batch) chunks; the issuers' partial
+    // accumulators are summed
     const int q = warp & 3, half = warp >> 2;
     const int nchunk = npad / 16, nitems = sp.nblk * nchunk;
     const int epi = op.i[4];
@@ -621,8 +672,9 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
     for (int it = half; it < nitems; it += 2) {
         const int blk = it / nchunk, n0 = (it - blk * nchunk) * 16;
         float v[16], u[16];
-        tmem_ld16(ts.tmem + lane_off + static_cast<uint32_t>(blk * npad + n0), v);
-        if (epi == EPI_SILU_MUL) tmem_ld16(ts.tmem + lane_off + static_cast<uint32_t>((sp.nblk + blk) * npad + n0), u);
+        tc_sum16(ts.tmem + lane_off + static_cast<uint32_t>(blk * npad + n0), nis, cols, v);
+        if (epi == EPI_SILU_MUL)
+            tc_sum16(ts.tmem + lane_off + static_cast<uint32_t>((sp.nblk + blk) * npad + n0), nis, cols, u);
         const int row = (sp.b0 + blk) * 128 + q * 32 + lane;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -1414,7 +1466,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     float* red = reinterpret_cast<float*>(smem + kSmemMisc + 64);
     Ring ring{smem + kSmemRing, reinterpret_cast<uint64_t*>(smem + kSmemBar),
               reinterpret_cast<uint64_t*>(smem + kSmemBar) + kStages, 0ull, P.status, P.watchdog_ns, worker};
-    ring.dbg = (P.debug & 10) != 0 && P.record;
+    ring.dbg = (P.debug & 522) != 0 && P.record;
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
     unsigned long long executed = 0, noops = 0;
     for (int s = qb; s < qe; ++s) {
@@ -1517,9 +1569,12 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 r.worker = worker;
                 r.flags = v.masked ? 1 : 0;
                 r.task = s;
-                r.pad = (P.debug & 8) ? static_cast<int>(ring.busy) : (P.debug & 18) ? static_cast<int>(ring.stall) : 0;
+                r.pad = (P.debug & 512) ? static_cast<int>(ring.xwait)
+                        : (P.debug & 8) ? static_cast<int>(ring.busy)
+                        : (P.debug & 18) ? static_cast<int>(ring.stall) : 0;
                 ring.stall = 0;
                 ring.busy = 0;
+                ring.xwait = 0;
                 P.trace[s] = r;
             }
         }
@@ -1530,29 +1585,102 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     }
 }
 
-// Producer: activation piece into x buffer xq % 2 once the issuer freed it (tensor-core GEMV).
-__device__ __noinline__ bool tc_issue_x(const StaticParams& P, uint8_t* smem, const Chunk& xc, unsigned int& xq,
-                                        int worker) {
+// Producer side of a tensor-core GEMV task: per piece p, the activation piece X(p)
+// into x slot xq % nxs (once the issuer freed it) and the weight chunks of every
+// (segment, block) into the ring; piece 0 streams up to kStages weight chunks
+// before X(0), which -- produced upstream -- may only load once the task's waits
+// passed (dep 0: static slot `key` done waiting, misc[1] > key; dep 1: dynamic
+// task generation `key`, misc[6] == key).  Pointer walks only: this thread's
+// scalar work is on the streaming critical path.
+__device__ __noinline__ bool tc_produce(const StaticParams& P, uint8_t* smem, const StreamPlan& pl,
+                                        volatile int* misc, int dep, int key, unsigned long long& cseq,
+                                        unsigned int& xq, int worker, uint64_t pol) {
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+    uint64_t* empty = full + kStages;
     uint64_t* bars = tc_bars(smem);
-    const int b = static_cast<int>(xq & 1u);
-    const uint32_t par = ((xq >> 1) & 1u) ^ 1u;
-    uint32_t spins = 0;
-    uint64_t t0 = 0;
-    while (!mbar_try_wait(&bars[2 + b], par)) {
-        if ((++spins & 1023u) == 0) {
-            if (aborted(P.status)) return false;
-            if (t0 == 0) t0 = globaltimer();
-            else if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
-                report(P.status, ET_ERR_DEADLOCK, worker, -1, -6, static_cast<int>(xq));
-                return false;
+    // the plan's fields in registers (the plan itself sits in local memory)
+    const uint8_t* const base0 = pl.base[0];
+    const uint8_t* const base1 = pl.nseg > 1 ? pl.base[1] : pl.base[0];
+    const long long pstride = pl.tc_pstride;
+    const uint8_t* const xsrc = pl.tc_x;
+    const uint32_t xbytes = pl.tc_xbytes;
+    const int np = pl.tc_np, tw = pl.tc_w, pre = pl.tc_pre, nseg = pl.nseg;
+    const int nxs = tc_xslots(xbytes);
+    const int per_seg = static_cast<int>(pl.bytes[0] >> 14);  // 16 KB chunks per segment and piece
+    const bool fast = (P.debug & 4) != 0, xfast = (P.debug & 256) != 0;
+    const uint32_t ring0 = smem_u32(smem + kSmemRing);
+    bool fenced = false;
+    for (int p = 0; p < np; ++p) {
+        int w = 0;
+        const uint8_t* src = base0 + p * pstride;
+        int sg = 0, left = per_seg;
+        for (int half = 0; half < 2; ++half) {
+            const int stop = half ? tw : (p == 0 ? pre : 0);
+            for (; w < stop; ++w) {
+                const int stage = static_cast<int>(cseq % kStages);
+                const uint32_t phase = static_cast<uint32_t>((cseq / kStages) & 1ull);
+                ++cseq;
+                uint32_t spins = 0;
+                uint64_t t0 = 0;
+                while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
+                    if ((++spins & 1023u) == 0) {
+                        if (aborted(P.status)) return false;
+                        if (t0 == 0) t0 = globaltimer();
+                        else if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                            report(P.status, ET_ERR_DEADLOCK, worker, -1, -3, w);
+                            return false;
+                        }
+                    }
+                }
+                if (fast) {
+                    mbar_arrive(&full[stage]);
+                } else {
+                    mbar_arrive_expect_tx(&full[stage], kTcChunk);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+                        "[%3], %4;" ::"r"(ring0 + stage * kStageBytes),
+                        "l"(src), "r"(kTcChunk), "r"(smem_u32(&full[stage])), "l"(pol)
+                        : "memory");
+                }
+                src += kTcChunk;
+                if (--left == 0 && ++sg < nseg) {
+                    src = base1 + p * pstride;
+                    left = per_seg;
+                }
             }
+            if (half) break;
+            // X(p)
+            if (!fenced) {
+                while (dep == 0 ? misc[1] <= key : misc[6] != key) {
+                    if (aborted(P.status)) return false;
+                }
+                __threadfence();             // the pieces were written by other CTAs before the waits passed
+                fence_proxy_async_global();  // ... with generic stores; the bulk copy reads through the async proxy
+                fenced = true;
+            }
+            const int b = static_cast<int>(xq % nxs);
+            const uint32_t par = ((xq / nxs) & 1u) ^ 1u;
+            uint32_t spins = 0;
+            uint64_t t0 = 0;
+            while (!mbar_try_wait(&bars[kTcXSlots + b], par)) {
+                if ((++spins & 1023u) == 0) {
+                    if (aborted(P.status)) return false;
+                    if (t0 == 0) t0 = globaltimer();
+                    else if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                        report(P.status, ET_ERR_DEADLOCK, worker, -1, -6, static_cast<int>(xq));
+                        return false;
+                    }
+                }
+            }
+            if (xfast) {  // timing experiment: x slots "fill" instantly
+                mbar_arrive(&bars[b]);
+            } else {
+                mbar_arrive_expect_tx(&bars[b], xbytes);
+                bulk_g2s_keep(smem + kSmemX + b * xbytes, xsrc + static_cast<long long>(p) * xbytes, xbytes, &bars[b]);
+            }
+            ++xq;
         }
     }
-    __threadfence();             // the pieces were written by other CTAs before the waits passed
-    fence_proxy_async_global();  // ... with generic stores; the bulk copy reads through the async proxy
-    mbar_arrive_expect_tx(&bars[b], xc.bytes);
-    bulk_g2s_keep(smem + kSmemX + b * kTcXBuf, xc.src, xc.bytes, &bars[b]);
-    ++xq;
     return true;
 }
 
@@ -1578,21 +1706,14 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             if (v.lazy && extent_masked(P, v.call, v.coord)) continue;
         }
         const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
+        if (pl.tc_np) {  // tensor-core GEMV: weight chunks + activation pieces (gated on the waits)
+            if (!tc_produce(P, smem, pl, misc, 0, s, cseq, xq, worker, pol)) return;
+            continue;
+        }
         const int n = pl.total_chunks();
-        for (int c = 0; c < n; ++c) {
-            if (pl.tc_np) {
-                const Chunk xc = pl.chunk(c);
-                if (xc.x) {  // activation piece: produced upstream, so only once the slot's waits pass
-                    while (misc[1] <= s) {
-                        if (aborted(P.status)) return;
-                    }
-                    if (!tc_issue_x(P, smem, xc, xq, worker)) return;
-                    continue;
-                }
-            }
+        for (int c = 0; c < n; ++c, ++cseq) {
             const int stage = static_cast<int>(cseq % kStages);
             const uint32_t phase = static_cast<uint32_t>((cseq / kStages) & 1ull);
-            ++cseq;
             uint32_t spins = 0;
             uint64_t t0 = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
@@ -1663,7 +1784,8 @@ __device__ void dma_loop(const StaticParams& P) {
 __device__ __forceinline__ void tc_setup(uint8_t* smem) {
     if (threadIdx.x == 0) {
         uint64_t* b = tc_bars(smem);
-        for (int i = 0; i < 5; ++i) mbar_init(&b[i], 1);
+        for (int i = 0; i < 2 * kTcXSlots; ++i) mbar_init(&b[i], 1);
+        mbar_init(&b[2 * kTcXSlots], kTcIssuers);  // done: one commit per issuer
         fence_mbar_init();
     }
     if ((threadIdx.x >> 5) == 0) tmem_alloc(reinterpret_cast<uint32_t*>(smem + kSmemMisc + 32), kTmemCols);
@@ -2241,21 +2363,14 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
         const et_op& op = P.ops[v.call];
         if (!op_streams(op.kind)) continue;
         const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
+        if (pl.tc_np) {  // tensor-core GEMV: activation pieces once the task's (armed) waits pass
+            if (!tc_produce(P, smem, pl, misc, 1, gen, cseq, xq, worker, pol)) return;
+            continue;
+        }
         const int n = pl.total_chunks();
-        for (int c = 0; c < n; ++c) {
-            if (pl.tc_np) {
-                const Chunk xc = pl.chunk(c);
-                if (xc.x) {  // activation piece: only once the task's (armed) waits pass
-                    while (misc[6] != gen) {
-                        if (aborted(P.status)) return;
-                    }
-                    if (!tc_issue_x(P, smem, xc, xq, worker)) return;
-                    continue;
-                }
-            }
+        for (int c = 0; c < n; ++c, ++cseq) {
             const int stage = static_cast<int>(cseq % kStages);
             const uint32_t phase = static_cast<uint32_t>((cseq / kStages) & 1ull);
-            ++cseq;
             uint32_t spins = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
                 if ((++spins & 1023u) == 0 && aborted(P.status)) return;

@@ -97,12 +97,18 @@ enum GemvEpi { EPI_F32 = 0, EPI_BF16 = 1, EPI_RESID = 2, EPI_SILU_MUL = 3, EPI_Q
 struct Chunk {
     const uint8_t* src;
     uint32_t bytes;
-    bool x;  // tensor-core GEMV: an activation piece for the x buffers, not a ring stage
 };
 
 // ---- tensor-core GEMV (ET_OP_GEMV_TC) -------------------------------------------------
 constexpr int kTcChunk = 16384;      // weight chunk: 128 rows x 64 k (4 k steps of 4 KB)
-constexpr int kTcXBuf = kXBytes / 2;  // two activation piece buffers
+constexpr int kTcXBuf = kXBytes / 2;  // largest activation piece (two slots at least)
+constexpr int kTcXSlots = 4;          // activation piece slots (as many as fit, up to 4)
+constexpr int kTcIssuers = 4;         // MMA issuer threads (lane 0 of consumer warps 0..3)
+
+__host__ __device__ __forceinline__ int tc_xslots(uint32_t xbytes) {
+    const int n = static_cast<int>(kXBytes / xbytes);
+    return n < kTcXSlots ? n : kTcXSlots;
+}
 constexpr int kTmemCols = 512;
 
 // Batch padded to the MMA N dimension (multiple of 16, at least 16).
@@ -147,9 +153,8 @@ struct StreamPlan {
     int cbytes;
     bool interleave;
     int n[kMaxSeg];  // chunks per segment (set by finish(); keeps divisions off the per-chunk path)
-    // tensor-core GEMV: per piece p, X(p) then the weight chunks of every (segment, block),
-    // except that piece 0 streams up to kStages weight chunks ahead of X(0) (those need no
-    // dependency); tc_w = weight chunks per piece, tc_np = pieces (0: not a tensor-core plan)
+    // tensor-core GEMV (streamed by tc_produce, not chunk()): tc_w = weight chunks per piece,
+    // tc_np = pieces (0: not a tensor-core plan), tc_pre = weight chunks streamed before X(0)
     int tc_w = 0, tc_np = 0, tc_pre = 0;
     const uint8_t* tc_x;       // activation piece p at tc_x + p * tc_xbytes
     uint32_t tc_xbytes;
@@ -158,19 +163,8 @@ struct StreamPlan {
     __device__ void finish() {
         for (int s = 0; s < kMaxSeg; ++s) n[s] = s < nseg ? static_cast<int>((bytes[s] + cbytes - 1) / cbytes) : 0;
     }
-    __device__ int total_chunks() const { return tc_np ? tc_np * (tc_w + 1) : n[0] + n[1] + n[2]; }
+    __device__ int total_chunks() const { return n[0] + n[1] + n[2]; }
     __device__ Chunk chunk(int idx) const {
-        if (tc_np) {
-            const int p = idx / (tc_w + 1);
-            int r = idx - p * (tc_w + 1);
-            const int xpos = p == 0 ? tc_pre : 0;
-            if (r == xpos) return Chunk{tc_x + static_cast<long long>(p) * tc_xbytes, tc_xbytes, true};
-            if (r > xpos) --r;
-            const int per_seg = static_cast<int>(bytes[0] / kTcChunk);
-            const int sg = r / per_seg;
-            return Chunk{base[sg] + p * tc_pstride + static_cast<long long>(r - sg * per_seg) * kTcChunk, kTcChunk,
-                         false};
-        }
         int s = 0;
         if (interleave) {
             s = idx & 1;
@@ -180,7 +174,7 @@ struct StreamPlan {
         }
         const long long off = static_cast<long long>(idx) * cbytes;
         const long long rem = bytes[s] - off;
-        return Chunk{base[s] + off, static_cast<uint32_t>(rem < cbytes ? rem : cbytes), false};
+        return Chunk{base[s] + off, static_cast<uint32_t>(rem < cbytes ? rem : cbytes)};
     }
 };
 
