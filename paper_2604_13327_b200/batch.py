@@ -65,6 +65,15 @@ def tc_piece(max_batch):
     return min(512, kp // 64 * 64)
 
 
+def tc_piece_for(max_batch, ks):
+    """tc_piece(max_batch), reduced until it divides every projection input width in ks."""
+    kp = tc_piece(max_batch)
+    while any(k % kp for k in ks):
+        kp -= 64
+    assert kp >= 64, ks
+    return kp
+
+
 def tc_pack(w, kp):
     """[N][K] bf16 -> the tensor-core layout [K/kp][N/128][kp/16][16][2][8][8]
     (piece, row block, k step, 8-row group, k half, row, k)."""
@@ -145,7 +154,7 @@ class BatchDecodeModel:
         self.batch_samples = sorted(set(batch_samples or default) | {max_batch})
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
-        self.kp = kp = tc_piece(max_batch)
+        self.kp = kp = tc_piece_for(max_batch, (cfg.hidden, cfg.q_rows, cfg.intermediate))
         npad = tc_npad(max_batch)
         H, I, nq, nkv = cfg.hidden, cfg.intermediate, cfg.q_rows, cfg.kv_rows
         rows = nq + 2 * nkv

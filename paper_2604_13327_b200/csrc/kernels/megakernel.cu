@@ -668,6 +668,7 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
     const int q = warp & 3, half = warp >> 2;
     const int nchunk = npad / 16, nitems = sp.nblk * nchunk;
     const int epi = op.i[4];
+    const int ostride = op.i[8] > 0 ? op.i[8] : N;  // output rows (a padded block's tail rows are dropped)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     for (int it = half; it < nitems; it += 2) {
         const int blk = it / nchunk, n0 = (it - blk * nchunk) * 16;
@@ -679,8 +680,8 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const int n = n0 + j;
-            if (n < nb) {
-                const long long o = static_cast<long long>(n) * N + row;
+            if (n < nb && row < ostride) {
+                const long long o = static_cast<long long>(n) * ostride + row;
                 if (epi == EPI_F32) {
                     reinterpret_cast<float*>(op.p[4])[o] = v[j];
                 } else if (epi == EPI_ADD) {
@@ -736,6 +737,8 @@ __device__ __noinline__ void body_norm(const StaticParams& P, const et_op& op, c
             o.x = static_cast<uint32_t>(f2bf(hv[j].x * scale * g.x)) | (static_cast<uint32_t>(f2bf(hv[j].y * scale * g.y)) << 16);
             o.y = static_cast<uint32_t>(f2bf(hv[j].z * scale * g.z)) | (static_cast<uint32_t>(f2bf(hv[j].w * scale * g.w)) << 16);
             *reinterpret_cast<uint2*>(out + xb_offset(n, k, npad, kp)) = o;
+            if (op.p[3])  // also row-major bf16 [b][K] (the MoE expert tiles read their tokens' rows)
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(op.p[3]) + static_cast<long long>(n) * K + k) = o;
         }
     }
 }
@@ -1156,18 +1159,30 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
 // eoff and elist for the expert call).  Everything is written before this
 // task's NOTIFY (release), and the dynamic scheduler reveals the counts when
 // the whole writer call has finished (ref simulate.cpp:632-649).
-__device__ void body_moe_route(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
+__device__ __noinline__ void body_moe_route(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
                                float* red, Ring& ring, int ctid, uint64_t* t_pro) {
-    *t_pro = body_gemv(P, op, si, xs, acc, red, ring, ctid);
+    // flags bit 1: the router logits were accumulated by a tensor-core GEMV (large batch)
+    // into p1 (fp32 [b][E], split-K adds): one route task copies them to p4 and zeroes p1
+    const bool pre = (op.flags & 2) != 0;
     const int warp = ctid >> 5, lane = ctid & 31;
     const int E = op.i[0], H = op.i[1], K = op.i[6], RS = op.i[12], TS = op.i[13];
     const int nb = batch_of(op, P);
-    if (si.coord[0] == 0)  // the normalised activations feed the experts
-        for (int v = ctid; v < nb * H / 8; v += kConsumers)
-            reinterpret_cast<uint4*>(op.p[5])[v] = reinterpret_cast<const uint4*>(xs)[v];
+    if (pre) {
+        float* lacc = reinterpret_cast<float*>(op.p[1]);
+        for (int i = ctid; i < nb * E; i += kConsumers) {
+            reinterpret_cast<float*>(op.p[4])[i] = __ldcg(lacc + i);
+            lacc[i] = 0.f;
+        }
+        bar_sync(1, kConsumers);
+    } else {
+        *t_pro = body_gemv(P, op, si, xs, acc, red, ring, ctid);
+        if (si.coord[0] == 0)  // the normalised activations feed the experts
+            for (int v = ctid; v < nb * H / 8; v += kConsumers)
+                reinterpret_cast<uint4*>(op.p[5])[v] = reinterpret_cast<const uint4*>(xs)[v];
+    }
     volatile int* flag = reinterpret_cast<volatile int*>(red + kConsumerWarps);
-    const bool single = si.ext0 == 1;  // one route task: no arrival, logits still in shared memory
-    if (!single) {
+    const bool single = !pre && si.ext0 == 1;  // one route task: no arrival, logits still in shared memory
+    if (!single && !pre) {
         bar_sync(1, kConsumers);
         if (ctid == 0) {
             int* arrive = reinterpret_cast<int*>(op.p[7]);
@@ -1189,7 +1204,7 @@ __device__ void body_moe_route(const StaticParams& P, const et_op& op, const Slo
     const float* logits = reinterpret_cast<const float*>(op.p[4]);
     float* wslot = reinterpret_cast<float*>(op.p[6]);
     int4* tinfo = reinterpret_cast<int4*>(op.p[8]);   // [tiles] (expert, first slot, tokens)
-    int* scnt = reinterpret_cast<int*>(acc + E * nb);  // [E] counts (the logits stay in acc[0, E*nb))
+    int* scnt = reinterpret_cast<int*>(acc + (single ? E * nb : 0));  // [E] counts (single: logits in acc[0, E*nb))
     int* stop = scnt + 256;                           // [nb*K] experts per slot
     for (int e = ctid; e < E; e += kConsumers) scnt[e] = 0;
     bar_sync(1, kConsumers);

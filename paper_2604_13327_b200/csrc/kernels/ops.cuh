@@ -52,7 +52,9 @@
 //   i6 = top_k, i10 = index of the layer's first routing runtime tensor (in order topk,
 //   counts, exp_indptr, task_indptr, elist, eoff), i12 = RS, i13 = TS; p0 = router weight (frag16
 //   [E][H]), p2 = h (fp32 [b][H]), p3 = gamma, p4 = logits (fp32 [b][E]), p5 = xn out
-//   (bf16 [b][H]), p6 = slot weights out (fp32 [b*top_k]), p7 = arrival counter (int32)
+//   (bf16 [b][H]), p6 = slot weights out (fp32 [b*top_k]), p7 = arrival counter (int32);
+//   flags bit 1 (large batch): no GEMV -- one task reads the logits a tensor-core GEMV
+//   accumulated at p1 (fp32 [b][E]), copies them to p4 and zeroes p1
 // ET_OP_MOE_EXPERT      task flat = tile * RS + r (range-triggered on task_indptr, extent_from):
 //   for the tile's tokens x = xn[token]: act = silu(Wg_e x) * (Wu_e x) on rows [r*IR, r*IR+IR)
 //   (IR = I / RS), then h[token] += w_slot * Wd_e[:, rows] act (red.global.add).
@@ -79,12 +81,13 @@
 //   i0 = N rows per segment (% 128 == 0), i1 = K, i2 = segments (1|2), i3 = k splits (EPI_ADD
 //   only when > 1), i4 = epilogue (F32 / BF16 / RESID / ADD: [b][N] row-major; SILU_MUL:
 //   bf16 in the tensor-core operand layout with piece length i7), i5 = batch symbol slot,
-//   i6 = kp (piece length, % 64 == 0, Npad * kp * 2 <= 16 KB);
+//   i6 = kp (piece length, % 64 == 0, Npad * kp * 2 <= 16 KB), i8 = output rows / row stride
+//   of the row-major epilogues (0 = N; rows of a zero-padded last block beyond it are dropped);
 //   p0/p1 = weights in the tensor-core layout of segment 0/1 (tc_weight_offset), p2 = x in the
 //   operand layout (xb_offset), p4 = out, p5 = residual in (fp32, EPI_RESID)
 // ET_OP_NORM            task n (< b): out[n] = bf16(h[n] * rsqrt(mean(h[n]^2) + eps) * gamma) in
 //   the tensor-core operand layout; i0 = K, i5 = batch symbol slot, i6 = kp; p0 = h (fp32
-//   [b][K]), p1 = gamma (fp32 [K]), p2 = out; f0 = eps
+//   [b][K]), p1 = gamma (fp32 [K]), p2 = out, p3 = optional row-major copy (bf16 [b][K]); f0 = eps
 #pragma once
 
 #include "megakernel.cuh"
@@ -317,6 +320,10 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
             pl.bytes[s] = (sp.u1 - sp.u0) * 512;
         }
     } else if (op.kind == ET_OP_MOE_ROUTE) {
+        if (op.flags & 2) {  // logits precomputed by a tensor-core GEMV: nothing streams
+            pl.finish();
+            return pl;
+        }
         const GemvSpan sp = gemv_span(op, coord[0], T);
         pl.nseg = 1;
         pl.base[0] = reinterpret_cast<const uint8_t*>(op.p[0]) + sp.u0 * 512;

@@ -113,7 +113,7 @@ RT_PER_LAYER = ("topk", "cnt", "ind", "tind", "elist", "eoff")
 
 
 def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=None, route_tasks=1,
-                   group_stage=True, attn_cap=None, oproj_group_tasks=None):
+                   group_stage=True, attn_cap=None, oproj_group_tasks=None, tc=None):
     """Reference-format graph spec (ref json_io.cpp:115-230) of one MoE decode step.
 
     tokens: an int (fixed batch) or "b" -- the batch is then a graph symbol next
@@ -121,7 +121,10 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
     (one lowered artifact serves every batch up to the largest sample).
     oproj_group_tasks: the output projection runs per kv-head group (grid [kv, n]),
     each group released by its own attention merge (needed for batch > 4: the
-    full attention row would not fit the staged activations)."""
+    full attention row would not fit the staged activations).
+    tc: task counts of the tensor-core projections (batches above 8): every
+    RMSNorm becomes its own [b] call feeding the tensor-core operand layout, and
+    the router logits come from a tensor-core GEMV call before the route task."""
     CH = cfg.attn_chunk
     E, K, RS = cfg.experts, cfg.top_k, cfg.row_splits
     fns, events, calls, rts = [], [], [], []
@@ -158,8 +161,13 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
             ev(x, [str(E)], data_dependent=True, counts=rt["cnt"], writer=route)
         ev(d, ["1"])
         nsplit = f"(s + {CH - 1}) // {CH}" if not attn_cap else f"min((s + {CH - 1}) // {CH}, {attn_cap})"
-        calls.append({"fn": fn(f"L{l}.qkv", [str(qkv_tasks or tasks)]), "in": [{"event": prev, "map": ["0"]}],
-                      "out": [{"event": qkv, "map": ["0"]}]})
+        if tc:  # RMSNorm of the stream into the tensor-core operand layout, one task per token
+            n1 = ev(f"N1{l}", ["1"])
+            calls.append({"fn": fn(f"L{l}.norm1", [str(tokens)]), "in": [{"event": prev, "map": ["0"]}],
+                          "out": [{"event": n1, "map": ["0"]}]})
+            prev = n1
+        calls.append({"fn": fn(f"L{l}.qkv", [str(tc["qkv"] if tc else qkv_tasks or tasks)]),
+                      "in": [{"event": prev, "map": ["0"]}], "out": [{"event": qkv, "map": ["0"]}]})
         if fused_merge:  # the last split of each (sequence, kv head) merges the group
             calls.append({"fn": fn(f"L{l}.attn", [f"{tokens} * {kv}", f"max({nsplit}, 1)"]),
                           "in": [{"event": qkv, "map": ["0"]}],
@@ -174,10 +182,18 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
             calls.append({"fn": fn(f"L{l}.oproj", [kv, str(oproj_group_tasks)]), "in": [{"event": m, "map": ["t0"]}],
                           "out": [{"event": o, "map": ["0"]}]})
         else:
-            calls.append({"fn": fn(f"L{l}.oproj", [T]), "in": [{"event": m, "map": ["0"]}],
+            calls.append({"fn": fn(f"L{l}.oproj", [str(tc["oproj"]) if tc else T]), "in": [{"event": m, "map": ["0"]}],
                           "out": [{"event": o, "map": ["0"]}]})
+        rin = o
+        if tc:  # norm2 -> router logits (tensor cores) -> route (top-k, counts, indptr)
+            n2, rl = ev(f"N2{l}", ["1"]), ev(f"RL{l}", ["1"])
+            calls += [{"fn": fn(f"L{l}.norm2", [str(tokens)]), "in": [{"event": o, "map": ["0"]}],
+                       "out": [{"event": n2, "map": ["0"]}]},
+                      {"fn": fn(f"L{l}.router", [str(tc["router"])]), "in": [{"event": n2, "map": ["0"]}],
+                       "out": [{"event": rl, "map": ["0"]}]}]
+            rin = rl
         calls += [
-            {"fn": fn(route, [str(route_tasks)]), "in": [{"event": o, "map": ["0"]}],
+            {"fn": fn(route, [str(1 if tc else route_tasks)]), "in": [{"event": rin, "map": ["0"]}],
              "out": [{"event": r, "map": ["0"]}]}]
         if group_stage:  # the reference structure: routed notify + range trigger (dynamic scheduler)
             calls += [
@@ -190,8 +206,13 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
             calls.append({"fn": fn(f"L{l}.expert", [f"{tokens} * {K * RS}"]), "extent_from": rt["tind"],
                           "in": [{"event": r, "map": ["0"]}], "out": [{"event": d, "map": ["0"]}]})
         prev = d
+    if tc:
+        ev("NF", ["1"])
+        calls.append({"fn": fn("normf", [str(tokens)]), "in": [{"event": prev, "map": ["0"]}],
+                      "out": [{"event": "NF", "map": ["0"]}]})
+        prev = "NF"
     ev("LM", ["1"])
-    calls.append({"fn": fn("lm_head", [str(lm_tasks)]), "in": [{"event": prev, "map": ["0"]}],
+    calls.append({"fn": fn("lm_head", [str(tc["lm"] if tc else lm_tasks)]), "in": [{"event": prev, "map": ["0"]}],
                   "out": [{"event": "LM", "map": ["0"]}]})
     symbols = ["s", "b"] if tokens == "b" else ["s"]
     return {"symbols": symbols, "size_symbol": "s", "duration_models": {"unit": {"kind": "constant", "value": 1}},
@@ -224,24 +245,34 @@ def init_moe_weights(cfg: MoEConfig, device, seed=0, std=0.02):
     return W
 
 
-def moe_device_layout(cfg, W):
+def moe_device_layout(cfg, W, kp=0):
     """frag16 tiles for every GEMV matrix; expert down projections cut into RS
-    column blocks [E][RS][H][IR], each its own frag16 matrix."""
+    column blocks [E][RS][H][IR], each its own frag16 matrix.  kp > 0 (batches
+    above 8): the dense projections in the tensor-core layout instead (batch.tc_pack;
+    router rows padded to a 128-row block)."""
     E, H, I, RS = cfg.experts, cfg.hidden, cfg.expert_inter, cfg.row_splits
     IR = I // RS
-    D = {"embed": W["embed"], "final_norm": W["final_norm"], "lm_head": frag16(W["lm_head"]), "layers": []}
+    if kp:
+        from .batch import tc_pack
+
+        def pad128(w):
+            n = -(-w.shape[0] // 128) * 128
+            return w if n == w.shape[0] else torch.cat([w, w.new_zeros(n - w.shape[0], w.shape[1])])
+    D = {"embed": W["embed"], "final_norm": W["final_norm"],
+         "lm_head": tc_pack(W["lm_head"], kp) if kp else frag16(W["lm_head"]), "layers": []}
     for L in W["layers"]:
         d = dict(L)
         for k in ("wqkv", "wo", "router"):
-            d[k] = frag16(L[k])
+            d[k] = tc_pack(pad128(L[k]), kp) if kp else frag16(L[k])
         d["wgate"] = torch.stack([frag16(L["wgate"][e]) for e in range(E)])
         d["wup"] = torch.stack([frag16(L["wup"][e]) for e in range(E)])
         blocks = L["wdown"].reshape(E, H, RS, IR).permute(0, 2, 1, 3)  # [E][RS][H][IR]
         d["wdown"] = torch.stack([torch.stack([frag16(blocks[e, r].contiguous()) for r in range(RS)])
                                   for e in range(E)])
-        cols = (cfg.heads // cfg.kv_heads) * cfg.head_dim  # Wo per kv-head group (batched decode)
-        d["wo_grouped"] = torch.stack([frag16(L["wo"][:, g * cols:(g + 1) * cols].contiguous())
-                                       for g in range(cfg.kv_heads)])
+        if not kp:
+            cols = (cfg.heads // cfg.kv_heads) * cfg.head_dim  # Wo per kv-head group (batched decode)
+            d["wo_grouped"] = torch.stack([frag16(L["wo"][:, g * cols:(g + 1) * cols].contiguous())
+                                           for g in range(cfg.kv_heads)])
         D["layers"].append(d)
     return D
 
@@ -260,13 +291,16 @@ class MoEDecodeModel:
         self.device = torch.device(device)
         props = torch.cuda.get_device_properties(self.device)
         self.num_workers = num_workers or props.multi_processor_count
-        # batch: a graph symbol `b` (1 <= b <= max_batch <= 8, the mma N dimension);
-        # every (s, b) at or below a sample runs on the lowered artifact
-        assert 1 <= max_batch <= 8
+        # batch: a graph symbol `b`; every (s, b) at or below a sample runs on the lowered
+        # artifact.  Up to 8 the projections carry the batch in the mma.sync N dimension;
+        # above, they run on the tcgen05 tensor cores (batch.py layouts)
+        assert 1 <= max_batch <= 64
         self.max_batch = max_batch
         self.batched = max_batch > 1
+        self.tc = max_batch > 8
         self.tokens = "b" if self.batched else 1
-        self.batch_samples = sorted(set(batch_samples or (1, max_batch))) if self.batched else [1]
+        default = [1 << i for i in range(7) if (1 << i) < max_batch] if self.tc else [1]
+        self.batch_samples = sorted(set(batch_samples or default) | {max_batch}) if self.batched else [1]
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
         from .decode import attn_split_cap
@@ -292,10 +326,24 @@ class MoEDecodeModel:
         # vocabulary at batch 8 needs more, smaller row spans than one per worker
         tiles, cap_tiles = cfg.vocab // 16, max(1, 2048 // (16 * max_batch))
         self.lm_tasks = max(self.num_workers, -(-tiles // cap_tiles))
+        self.kp, self.tc_tasks, self.tc_splits = 0, None, None
+        if self.tc:
+            from .batch import tc_npad, tc_piece_for, tc_tasks
+
+            assert fused_merge
+            self.oproj_group_tasks = None
+            H, nq = cfg.hidden, cfg.q_rows
+            self.kp = tc_piece_for(max_batch, (H, nq))
+            npad, w = tc_npad(max_batch), self.num_workers
+            self.tc_tasks, self.tc_splits = {}, {}
+            for name, n, k, add in (("qkv", nq + 2 * cfg.kv_rows, H, True), ("oproj", H, nq, True),
+                                    ("router", -(-cfg.experts // 128) * 128, H, True), ("lm", cfg.vocab, H, False)):
+                self.tc_tasks[name], self.tc_splits[name] = tc_tasks(n // 128, w, add, 1, npad, k // self.kp)
         self.spec = moe_graph_spec(cfg, self.num_workers, self.lm_tasks, self.tokens, fused_merge=fused_merge,
                                    qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
                                    if balance else None, route_tasks=self.route_tasks, group_stage=self.group_stage,
-                                   attn_cap=self.max_splits, oproj_group_tasks=self.oproj_group_tasks)
+                                   attn_cap=self.max_splits, oproj_group_tasks=self.oproj_group_tasks,
+                                   tc=self.tc_tasks)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.rt_index = {r["name"]: i for i, r in enumerate(self.spec["runtime_tensors"])}
         self.bindings = [self._binding(s, b) for s in self.samples for b in self.batch_samples]
@@ -311,7 +359,7 @@ class MoEDecodeModel:
         dev = self.device
         W = weights if weights is not None else init_moe_weights(cfg, dev, seed)
         self.W_logical = W if keep_logical else None
-        self.W = moe_device_layout(cfg, W)
+        self.W = moe_device_layout(cfg, W, self.kp)
         b, E, K = self.max_batch, cfg.experts, cfg.top_k
         # per-sequence KV caches [b][kv][cap][dh]
         self.kcache = [torch.zeros(b, cfg.kv_heads, self.capacity, cfg.head_dim, dtype=torch.bfloat16, device=dev)
@@ -329,6 +377,13 @@ class MoEDecodeModel:
         self.arrive_attn = torch.zeros(cfg.layers, b * cfg.kv_heads, dtype=torch.int32, device=dev)
         self.tiles = torch.zeros(cfg.layers, b * K, 4, dtype=torch.int32, device=dev)  # expert tile table
         self.logits = torch.zeros(b, cfg.vocab, dtype=torch.float32, device=dev)
+        if self.tc:  # operand-layout activations and the router accumulators (zeroed by the route task)
+            from .batch import tc_npad
+
+            npad = tc_npad(b)
+            self.xn_tc = torch.zeros(npad * cfg.hidden, dtype=torch.bfloat16, device=dev)
+            self.attn_tc = torch.zeros(npad * cfg.q_rows, dtype=torch.bfloat16, device=dev)
+            self.logits_acc = torch.zeros(b, E, dtype=torch.float32, device=dev)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
         self.injected = False
 
@@ -346,7 +401,62 @@ class MoEDecodeModel:
     def bind(self):
         self.executor.bind_ops(pack(self._ops()))
 
+    def _ops_tc(self):
+        """Op table of the tensor-core variant (batches above 8)."""
+        from .ops import OP_GEMV_TC, OP_NORM
+
+        cfg, W, kp = self.cfg, self.W, self.kp
+        H, dh, CH, nq = cfg.hidden, cfg.head_dim, cfg.attn_chunk, cfg.q_rows
+        E, K, RS, TS = cfg.experts, cfg.top_k, cfg.row_splits, cfg.tile_tokens
+        G = cfg.heads // cfg.kv_heads
+        rows = nq + 2 * cfg.kv_rows
+        bs, sp = 1, self.tc_splits
+
+        def tc(n, k, epi, w, x, out, splits, ostride=0):
+            return make_op(OP_GEMV_TC, i=[n, k, 1, splits, epi, bs, kp, 0, ostride],
+                           p=[ptr(w), 0, ptr(x), 0, ptr(out)])
+
+        def norm(gamma, rowmajor=None):
+            return make_op(OP_NORM, i=[H, 0, 0, 0, 0, bs, kp], f=[cfg.eps],
+                           p=[ptr(self.h), ptr(gamma), ptr(self.xn_tc), ptr(rowmajor)])
+
+        ops = [make_op(OP_EMBED, i=[H, bs], p=[ptr(W["embed"]), ptr(self.tok), ptr(self.h)])]
+        for l, L in enumerate(W["layers"]):
+            ri = {n: self.rt_index[f"{n}{l}"] for n in RT_PER_LAYER}
+            ops.append(norm(L["attn_norm"]))
+            ops.append(tc(rows, H, EPI_ADD, L["wqkv"], self.xn_tc, self.qkv, sp["qkv"]))
+            # flags: 1 q/k-norm mode, 2 fused merge, 32 zero the raw q/k/v after use; out in operand layout
+            ops.append(make_op(OP_ATTN_SPLIT,
+                               i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
+                                  cfg.kv_heads * self.capacity * dh, kp, bs],
+                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32,
+                               p=[ptr(self.qkv), ptr(self.kcache[l]), ptr(self.vcache[l]), ptr(self.partials),
+                                  ptr(self.attn_tc), ptr(self.arrive_attn[l]), ptr(L["k_norm"]), ptr(self.inv_freq),
+                                  ptr(self.qkv) + 4 * nq, ptr(L["q_norm"])]))
+            ops.append(tc(H, nq, EPI_ADD, L["wo"], self.attn_tc, self.h, sp["oproj"]))
+            ops.append(norm(L["ffn_norm"], self.xn[l]))
+            ops.append(tc(-(-E // 128) * 128, H, EPI_ADD, L["router"], self.xn_tc, self.logits_acc, sp["router"],
+                          ostride=E))
+            assert [ri[n] for n in RT_PER_LAYER] == list(range(ri["topk"], ri["topk"] + len(RT_PER_LAYER)))
+            ops.append(make_op(OP_MOE_ROUTE, i=[E, H, 1, 1, EPI_F32, bs, K, 16, cfg.expert_inter, H, ri["topk"], 0, RS,
+                                                TS],
+                               f=[cfg.eps],
+                               p=[0, ptr(self.logits_acc), ptr(self.h), 0, ptr(self.logits_r[l]), ptr(self.xn[l]),
+                                  ptr(self.wslot[l]), ptr(self.arrive[l:l + 1]), ptr(self.tiles[l])],
+                               flags=2 | (1 if self.injected else 0)))
+            if self.group_stage:
+                ops.append(make_op(OP_NONE))
+            ops.append(make_op(OP_MOE_EXPERT,
+                               i=[cfg.expert_inter, H, RS, TS, ri["ind"], ri["cnt"], ri["elist"], ri["eoff"], K, 0, E],
+                               p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(L["wdown"]), ptr(self.xn[l]), ptr(self.wslot[l]),
+                                  ptr(self.h), ptr(self.tiles[l])]))
+        ops.append(norm(W["final_norm"]))
+        ops.append(tc(cfg.vocab, H, EPI_F32, W["lm_head"], self.xn_tc, self.logits, 1))
+        return ops
+
     def _ops(self):
+        if self.tc:
+            return self._ops_tc()
         cfg, W = self.cfg, self.W
         H, dh, CH = cfg.hidden, cfg.head_dim, cfg.attn_chunk
         E, K, RS, TS = cfg.experts, cfg.top_k, cfg.row_splits, cfg.tile_tokens

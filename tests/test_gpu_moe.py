@@ -90,17 +90,24 @@ def test_moe_injected_routing_matches_reference_realization():
     assert m.last_stats["tasks_executed"] == mg.num_tasks
 
 
-@pytest.mark.parametrize("scheduler", ["static", "dynamic"])
-def test_moe_batched_decode_no_recompile(scheduler):
-    """One lowered artifact (batch symbol b <= 8) runs b = 1, 3, 8 sequences, each
-    with its own KV cache and token: per-token routing bit-exact, per-sequence
-    logits vs the oracle, and the Event Tensor accounting of the exact (s, b)."""
+@pytest.mark.parametrize("scheduler,max_batch,cases", [
+    ("static", 8, ((1, 16), (3, 40), (8, 64))),
+    ("dynamic", 8, ((1, 16), (3, 40), (8, 64))),
+    ("static", 16, ((1, 16), (5, 40), (16, 64))),    # tensor-core projections (batch above 8)
+    ("dynamic", 16, ((2, 16), (11, 64), (16, 40))),
+])
+def test_moe_batched_decode_no_recompile(scheduler, max_batch, cases):
+    """One lowered artifact (batch symbol b <= max_batch) runs several batches, each
+    sequence with its own KV cache and token: per-token routing bit-exact, per-sequence
+    logits vs the oracle, and the Event Tensor accounting of the exact (s, b).  Above
+    8 the dense projections run on tcgen05 (GEMV_TC) and the router logits come from
+    a tensor-core GEMV before the route task."""
     cfg = TINY_MOE
     m = MoEDecodeModel(cfg, samples=(64,), num_workers=16, seed=0, scheduler=scheduler, record_trace=True,
-                       keep_logical=True, max_batch=8, batch_samples=(2, 8))
+                       keep_logical=True, max_batch=max_batch, batch_samples=(2, max_batch))
     Wc = weights_to_cpu(m.W_logical)
-    toks = [3, 9, 27, 81, 243, 729, 1000, 17]
-    for b, s in ((1, 16), (3, 40), (8, 64)):
+    toks = [(3 ** i + 7 * i) % cfg.vocab for i in range(max_batch)]
+    for b, s in cases:
         m.fill_cache(s, seed=b)
         m.set_token(toks)
         kc = [k.cpu() for k in m.kcache]
