@@ -9,7 +9,8 @@ batch from the binding, no recompilation or relaunch.
 Graph per layer l (Event Tensors, counts derived by the reference lowering):
     norm1_l  [b]                 waits D_{l-1}[0]  notifies N1_l[0]
     qkv_l    [Tq]                waits N1_l[0]     notifies QKV_l[0]
-    attn_l   [b*kv, splits]      waits QKV_l[0]    notifies M_l[0]   (fused merge)
+    attn_l   [b*kv*splits(s,b)]  waits QKV_l[0]    notifies M_l[0]   (fused merge; fewer,
+                                                                       longer splits as b grows)
     oproj_l  [To]                waits M_l[0]      notifies O_l[0]
     norm2_l  [b]                 waits O_l[0]      notifies N2_l[0]
     gateup_l [Tg]                waits N2_l[0]     notifies G_l[0]
@@ -102,7 +103,19 @@ def tc_tasks(nblk, workers, splittable, nseg=1, npad=64, pieces=1):
     return groups, 1
 
 
-def batch_graph_spec(cfg, tasks, attn_cap):
+def attn_budget(cfg, workers):
+    """Per-step split budget of the batched attention: splits per (sequence, kv head)
+    <= max(1, budget // b), about two attention tasks per SM at any batch."""
+    return max(1, 2 * workers // cfg.kv_heads)
+
+
+def attn_grid(cfg, attn_cap, budget):
+    """Flat attention grid [b * kv * splits] (ops.cuh attn_coord, flags bit 7)."""
+    CH = cfg.attn_chunk
+    return f"b * {cfg.kv_heads} * max(1, min(min((s + {CH - 1}) // {CH}, {attn_cap}), {budget} // b))"
+
+
+def batch_graph_spec(cfg, tasks, attn_cap, budget):
     """Reference-format graph spec (ref json_io.cpp:115-230) of one batched decode step."""
     CH, kv = cfg.attn_chunk, str(cfg.kv_heads)
     fns, events, calls = [], [], []
@@ -119,11 +132,10 @@ def batch_graph_spec(cfg, tasks, attn_cap):
 
     prev = call("embed", ["1"], None, "EMB")
     calls[-1].pop("in")
-    nsplit = f"max(min((s + {CH - 1}) // {CH}, {attn_cap}), 1)"
     for l in range(cfg.layers):
         prev = call(f"L{l}.norm1", ["b"], prev, f"N1{l}")
         prev = call(f"L{l}.qkv", [str(tasks["qkv"])], prev, f"QKV{l}")
-        prev = call(f"L{l}.attn", [f"b * {kv}", nsplit], prev, f"M{l}")
+        prev = call(f"L{l}.attn", [attn_grid(cfg, attn_cap, budget)], prev, f"M{l}")
         prev = call(f"L{l}.oproj", [str(tasks["oproj"])], prev, f"O{l}")
         prev = call(f"L{l}.norm2", ["b"], prev, f"N2{l}")
         prev = call(f"L{l}.gateup", [str(tasks["gateup"])], prev, f"G{l}")
@@ -171,7 +183,8 @@ class BatchDecodeModel:
         self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
         self.scheduler = scheduler
         t0 = time.perf_counter()
-        self.spec = batch_graph_spec(cfg, self.tasks, self.max_splits)
+        self.attn_budget = attn_budget(cfg, self.num_workers)
+        self.spec = batch_graph_spec(cfg, self.tasks, self.max_splits, self.attn_budget)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.bindings = [{"s": s, "b": b} for s in self.samples for b in self.batch_samples]
         if scheduler == "dynamic":
@@ -245,8 +258,8 @@ class BatchDecodeModel:
             # flags: 1 q/k fused mode, 2 fused merge, 32 zero the raw q/k/v after use, 64 RoPE only
             ops.append(make_op(OP_ATTN_SPLIT,
                                i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
-                                  cfg.kv_heads * self.capacity * dh, kp, bs],
-                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 64,
+                                  cfg.kv_heads * self.capacity * dh, kp, bs, self.attn_budget],
+                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 64 | 128,
                                p=[ptr(self.qkv), ptr(self.kcache[l]), ptr(self.vcache[l]), ptr(self.partials),
                                   ptr(self.attn), ptr(self.arrive[l]), 0, ptr(self.inv_freq),
                                   ptr(self.qkv) + 4 * nq, 0]))

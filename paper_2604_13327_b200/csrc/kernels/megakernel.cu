@@ -870,7 +870,144 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     }
 }
 
-template <bool kQK>
+// Tensor-core form of a split's block loop (tensor-core instantiations: the batch
+// path).  Per 64-position block: S^T = K Q^T on mma.sync m16n8k16 (positions x q
+// heads; q split into bf16 hi + lo, so the scores keep ~fp32 precision) by warps
+// 0..3, the same online softmax over the scores in shared memory, then
+// O^T += V^T P^T (head dims x q heads; V^T fragments by ldmatrix.trans, P split
+// hi + lo) by warps 0..dh/16-1.  Writes the unnormalised partial (m, l, o) like
+// the scalar loop.  G <= 8, dh % 16 == 0, dh <= 128, CH == 64 (checked on the host).
+__device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& op, int gi, int c, const AttnBlocks ab,
+                                            long long s, const float* qs, int qstride, float* sc, float* st, Ring& ring,
+                                            int ctid) {
+    const int warp = ctid >> 5, lane = ctid & 31, g8 = lane >> 2, q4 = lane & 3;
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5];
+    const float scale = op.f[0];
+    const int nks = dh / 16;
+    uint32_t qh[8][2], ql[8][2];  // Q^T fragments (k = dim, n = head g8)
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+        qh[ks][0] = qh[ks][1] = ql[ks][0] = ql[ks][1] = 0u;
+        if (ks < nks && warp < 4 && g8 < G) {
+            const float* qv = qs + g8 * qstride + ks * 16 + 2 * q4;
+            split_bf16x2(qv[0], qv[1], qh[ks][0], ql[ks][0]);
+            split_bf16x2(qv[8], qv[9], qh[ks][1], ql[ks][1]);
+        }
+    }
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int blk = 0; blk < ab.nblk; ++blk) {
+        const long long pb = ab.p0 + static_cast<long long>(blk) * CH;
+        const int np = static_cast<int>(pb + CH < s ? CH : s - pb);
+        const unsigned long long ck = ring.seq, cv = ring.seq + 1;
+        ring.seq += 2;
+        const uint8_t* kb = ring.wait(ck);
+        if (!kb) return false;
+        if (warp < 4 && 16 * warp < np) {
+            float d[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint8_t* r0 = kb + (16 * warp + g8) * dh * 2 + 4 * q4;
+            const uint8_t* r1 = r0 + 8 * dh * 2;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                if (ks < nks) {
+                    uint4 a;
+                    a.x = *reinterpret_cast<const uint32_t*>(r0 + ks * 32);
+                    a.y = *reinterpret_cast<const uint32_t*>(r1 + ks * 32);
+                    a.z = *reinterpret_cast<const uint32_t*>(r0 + ks * 32 + 16);
+                    a.w = *reinterpret_cast<const uint32_t*>(r1 + ks * 32 + 16);
+                    mma_bf16_16816(d, a, qh[ks][0], qh[ks][1]);
+                    mma_bf16_16816(d, a, ql[ks][0], ql[ks][1]);
+                }
+            }
+            const int p0 = 16 * warp + g8, h0 = 2 * q4;  // d: (p0, h0) (p0, h0+1) (p0+8, h0) (p0+8, h0+1)
+            if (h0 < G) {
+                if (p0 < np) sc[h0 * CH + p0] = d[0] * scale;
+                if (p0 + 8 < np) sc[h0 * CH + p0 + 8] = d[2] * scale;
+            }
+            if (h0 + 1 < G) {
+                if (p0 < np) sc[(h0 + 1) * CH + p0] = d[1] * scale;
+                if (p0 + 8 < np) sc[(h0 + 1) * CH + p0 + 8] = d[3] * scale;
+            }
+        }
+        bar_sync(1, kConsumers);
+        if (ctid == Ring::owner(ck) * 32) ring.release(ck);
+        for (int h = warp; h < G; h += kConsumerWarps) {  // online softmax statistics per head (warp h)
+            float m = -INFINITY;
+            for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
+            m = warp_max(m);
+            const float mo = st[4 * h], mn = fmaxf(mo, m);
+            float l = 0.f;
+            for (int p = lane; p < np; p += 32) {
+                const float e = __expf(sc[h * CH + p] - mn);
+                sc[h * CH + p] = e;
+                l += e;
+            }
+            l = warp_sum(l);
+            if (lane == 0) {
+                const float alpha = __expf(mo - mn);
+                st[4 * h] = mn;
+                st[4 * h + 1] = st[4 * h + 1] * alpha + l;
+                st[4 * h + 2] = alpha;
+            }
+        }
+        bar_sync(1, kConsumers);
+        const uint8_t* vb = ring.wait(cv);
+        if (!vb) return false;
+        if (warp < nks) {
+            const int h0 = 2 * q4;
+            const float a0 = h0 < G ? st[4 * h0 + 2] : 1.f, a1 = h0 + 1 < G ? st[4 * h0 + 6] : 1.f;
+            o[0] *= a0;
+            o[1] *= a1;
+            o[2] *= a0;
+            o[3] *= a1;
+            const int mi = lane >> 3;
+            const uint8_t* vrow = vb + (((mi & 2) ? 8 : 0) + (lane & 7)) * dh * 2 + (16 * warp + ((mi & 1) ? 8 : 0)) * 2;
+            const float* ph = sc + g8 * CH + 2 * q4;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const int pp = ks * 16 + 2 * q4;
+                if (ks * 16 < np) {
+                    const uint4 a = ldsm_x4_trans(vrow + ks * 16 * dh * 2);  // V^T: dims x positions
+                    float p00 = 0.f, p01 = 0.f, p10 = 0.f, p11 = 0.f;
+                    if (g8 < G) {
+                        if (pp < np) p00 = ph[ks * 16];
+                        if (pp + 1 < np) p01 = ph[ks * 16 + 1];
+                        if (pp + 8 < np) p10 = ph[ks * 16 + 8];
+                        if (pp + 9 < np) p11 = ph[ks * 16 + 9];
+                    }
+                    uint32_t bh0, bl0, bh1, bl1;
+                    split_bf16x2(p00, p01, bh0, bl0);
+                    split_bf16x2(p10, p11, bh1, bl1);
+                    mma_bf16_16816(o, a, bh0, bh1);
+                    mma_bf16_16816(o, a, bl0, bl1);
+                }
+            }
+        }
+        bar_sync(1, kConsumers);  // sc / st are reused by the next block
+        if (ctid == Ring::owner(cv) * 32) ring.release(cv);
+    }
+    float* part = reinterpret_cast<float*>(op.p[3]);
+    if (warp < nks) {  // o: O^T (d0, h0) (d0, h0+1) (d0+8, h0) (d0+8, h0+1)
+        const int d0 = 16 * warp + g8, h0 = 2 * q4;
+        if (h0 < G) {
+            float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + c) * (dh + 2);
+            pr[2 + d0] = o[0];
+            pr[10 + d0] = o[2];
+        }
+        if (h0 + 1 < G) {
+            float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + c) * (dh + 2);
+            pr[2 + d0] = o[1];
+            pr[10 + d0] = o[3];
+        }
+    }
+    if (ctid < G) {
+        float* pr = part + ((static_cast<long long>(gi) * G + ctid) * maxs + c) * (dh + 2);
+        pr[0] = st[4 * ctid];
+        pr[1] = st[4 * ctid + 1];
+    }
+    return true;
+}
+
+template <bool kQK, bool kMMA = false>
 __device__ void body_attn_split(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, Ring& ring,
                                 int ctid, uint64_t* t_split = nullptr) {
     // Flash-decoding split c of kv head g: its run of CH-position K/V blocks
@@ -883,7 +1020,8 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5], kvh = op.i[6];
     const long long s = P.binding[op.i[4]];
-    const int gi = si.coord[0], c = si.coord[1];   // gi = sequence * kv_heads + kv head
+    int gi, c;  // gi = sequence * kv_heads + kv head, c = split
+    attn_coord(op, si.coord, P.binding, &gi, &c);
     const int g = gi % kvh, bq = gi / kvh;
     const long long rb = static_cast<long long>(bq) * op.i[7];  // this sequence's q / projection row
     const AttnBlocks ab = attn_blocks(op, c, P.binding);
@@ -934,109 +1072,113 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         }
     }
     bar_sync(1, kConsumers);
-    const float scale = op.f[0];
-    float o0[kOutMax], o1[kOutMax];
-#pragma unroll
-    for (int j = 0; j < kOutMax; ++j) o0[j] = o1[j] = 0.f;
-    for (int blk = 0; blk < ab.nblk; ++blk) {
-        const long long pb = ab.p0 + static_cast<long long>(blk) * CH;
-        const int np = static_cast<int>(pb + CH < s ? CH : s - pb);
-        const unsigned long long ck = ring.seq, cv = ring.seq + 1;
-        ring.seq += 2;
-        // scores; each position starts its walk over the row at a different 16-byte
-        // vector (bank rotation)
-        const uint8_t* kb = ring.wait(ck);
-        if (!kb) return;
-        for (int t = ctid; t < G * np; t += kConsumers) {
-            const int h = t % G, p = t / G;
-            const uint8_t* kr = kb + p * dh * 2;
-            const float* qh = qs + h * qstride;
-            float a0 = 0.f, a1 = 0.f;
-            for (int v = 0; v < nvec; ++v) {
-                const int vv = (v + p) & (nvec - 1);
-                const uint4 k8 = lds128(kr + vv * 16);
-                const float4 qa = *reinterpret_cast<const float4*>(qh + vv * 8);
-                const float4 qb = *reinterpret_cast<const float4*>(qh + vv * 8 + 4);
-                a0 = fmaf(bf16lo(k8.x), qa.x, a0);
-                a1 = fmaf(bf16hi(k8.x), qa.y, a1);
-                a0 = fmaf(bf16lo(k8.y), qa.z, a0);
-                a1 = fmaf(bf16hi(k8.y), qa.w, a1);
-                a0 = fmaf(bf16lo(k8.z), qb.x, a0);
-                a1 = fmaf(bf16hi(k8.z), qb.y, a1);
-                a0 = fmaf(bf16lo(k8.w), qb.z, a0);
-                a1 = fmaf(bf16hi(k8.w), qb.w, a1);
+    if constexpr (kMMA) {
+        if (!attn_split_mma(P, op, gi, c, ab, s, qs, qstride, sc, st, ring, ctid)) return;
+    } else {
+        const float scale = op.f[0];
+        float o0[kOutMax], o1[kOutMax];
+    #pragma unroll
+        for (int j = 0; j < kOutMax; ++j) o0[j] = o1[j] = 0.f;
+        for (int blk = 0; blk < ab.nblk; ++blk) {
+            const long long pb = ab.p0 + static_cast<long long>(blk) * CH;
+            const int np = static_cast<int>(pb + CH < s ? CH : s - pb);
+            const unsigned long long ck = ring.seq, cv = ring.seq + 1;
+            ring.seq += 2;
+            // scores; each position starts its walk over the row at a different 16-byte
+            // vector (bank rotation)
+            const uint8_t* kb = ring.wait(ck);
+            if (!kb) return;
+            for (int t = ctid; t < G * np; t += kConsumers) {
+                const int h = t % G, p = t / G;
+                const uint8_t* kr = kb + p * dh * 2;
+                const float* qh = qs + h * qstride;
+                float a0 = 0.f, a1 = 0.f;
+                for (int v = 0; v < nvec; ++v) {
+                    const int vv = (v + p) & (nvec - 1);
+                    const uint4 k8 = lds128(kr + vv * 16);
+                    const float4 qa = *reinterpret_cast<const float4*>(qh + vv * 8);
+                    const float4 qb = *reinterpret_cast<const float4*>(qh + vv * 8 + 4);
+                    a0 = fmaf(bf16lo(k8.x), qa.x, a0);
+                    a1 = fmaf(bf16hi(k8.x), qa.y, a1);
+                    a0 = fmaf(bf16lo(k8.y), qa.z, a0);
+                    a1 = fmaf(bf16hi(k8.y), qa.w, a1);
+                    a0 = fmaf(bf16lo(k8.z), qb.x, a0);
+                    a1 = fmaf(bf16hi(k8.z), qb.y, a1);
+                    a0 = fmaf(bf16lo(k8.w), qb.z, a0);
+                    a1 = fmaf(bf16hi(k8.w), qb.w, a1);
+                }
+                sc[h * CH + p] = (a0 + a1) * scale;
             }
-            sc[h * CH + p] = (a0 + a1) * scale;
+            bar_sync(1, kConsumers);
+            if (ctid == Ring::owner(ck) * 32) ring.release(ck);
+            // online softmax statistics per head (warp h), probabilities in place
+            for (int h = warp; h < G; h += kConsumerWarps) {
+                float m = -INFINITY;
+                for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
+                m = warp_max(m);
+                const float mo = st[4 * h], mn = fmaxf(mo, m);
+                float l = 0.f;
+                for (int p = lane; p < np; p += 32) {
+                    const float e = __expf(sc[h * CH + p] - mn);
+                    sc[h * CH + p] = e;
+                    l += e;
+                }
+                l = warp_sum(l);
+                if (lane == 0) {
+                    const float alpha = __expf(mo - mn);  // 0 on the first block (mo = -inf)
+                    st[4 * h] = mn;
+                    st[4 * h + 1] = st[4 * h + 1] * alpha + l;
+                    st[4 * h + 2] = alpha;
+                }
+            }
+            bar_sync(1, kConsumers);
+            // o = alpha * o + P V: one (head, dim pair) per thread (two when G * dh > 512)
+            const uint8_t* vb = ring.wait(cv);
+            if (!vb) return;
+            const uint32_t* v2 = reinterpret_cast<const uint32_t*>(vb);
+    #pragma unroll
+            for (int j = 0; j < kOutMax; ++j) {
+                const int idx = ctid + j * kConsumers;
+                if (idx >= G * half) break;
+                const int h = idx / half, dp = idx - h * half;
+                const float* ph = sc + h * CH;
+                const float alpha = st[4 * h + 2];
+                float a0 = o0[j] * alpha, a1 = o1[j] * alpha, a2 = 0.f, a3 = 0.f;
+                int p = 0;
+    #pragma unroll 4
+                for (; p + 2 <= np; p += 2) {
+                    const uint32_t va = v2[p * half + dp], vb2 = v2[(p + 1) * half + dp];
+                    const float wa = ph[p], wb = ph[p + 1];
+                    a0 = fmaf(wa, bf16lo(va), a0);
+                    a1 = fmaf(wa, bf16hi(va), a1);
+                    a2 = fmaf(wb, bf16lo(vb2), a2);
+                    a3 = fmaf(wb, bf16hi(vb2), a3);
+                }
+                if (p < np) {
+                    const uint32_t va = v2[p * half + dp];
+                    a0 = fmaf(ph[p], bf16lo(va), a0);
+                    a1 = fmaf(ph[p], bf16hi(va), a1);
+                }
+                o0[j] = a0 + a2;
+                o1[j] = a1 + a3;
+            }
+            bar_sync(1, kConsumers);  // sc / st are reused by the next block
+            if (ctid == Ring::owner(cv) * 32) ring.release(cv);
         }
-        bar_sync(1, kConsumers);
-        if (ctid == Ring::owner(ck) * 32) ring.release(ck);
-        // online softmax statistics per head (warp h), probabilities in place
-        for (int h = warp; h < G; h += kConsumerWarps) {
-            float m = -INFINITY;
-            for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
-            m = warp_max(m);
-            const float mo = st[4 * h], mn = fmaxf(mo, m);
-            float l = 0.f;
-            for (int p = lane; p < np; p += 32) {
-                const float e = __expf(sc[h * CH + p] - mn);
-                sc[h * CH + p] = e;
-                l += e;
-            }
-            l = warp_sum(l);
-            if (lane == 0) {
-                const float alpha = __expf(mo - mn);  // 0 on the first block (mo = -inf)
-                st[4 * h] = mn;
-                st[4 * h + 1] = st[4 * h + 1] * alpha + l;
-                st[4 * h + 2] = alpha;
-            }
-        }
-        bar_sync(1, kConsumers);
-        // o = alpha * o + P V: one (head, dim pair) per thread (two when G * dh > 512)
-        const uint8_t* vb = ring.wait(cv);
-        if (!vb) return;
-        const uint32_t* v2 = reinterpret_cast<const uint32_t*>(vb);
-#pragma unroll
+        // the unnormalised partial (m, l, o) of every q head of the group
+        float* part = reinterpret_cast<float*>(op.p[3]);
+    #pragma unroll
         for (int j = 0; j < kOutMax; ++j) {
             const int idx = ctid + j * kConsumers;
             if (idx >= G * half) break;
             const int h = idx / half, dp = idx - h * half;
-            const float* ph = sc + h * CH;
-            const float alpha = st[4 * h + 2];
-            float a0 = o0[j] * alpha, a1 = o1[j] * alpha, a2 = 0.f, a3 = 0.f;
-            int p = 0;
-#pragma unroll 4
-            for (; p + 2 <= np; p += 2) {
-                const uint32_t va = v2[p * half + dp], vb2 = v2[(p + 1) * half + dp];
-                const float wa = ph[p], wb = ph[p + 1];
-                a0 = fmaf(wa, bf16lo(va), a0);
-                a1 = fmaf(wa, bf16hi(va), a1);
-                a2 = fmaf(wb, bf16lo(vb2), a2);
-                a3 = fmaf(wb, bf16hi(vb2), a3);
+            float* pr = part + ((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + 2);
+            pr[2 + 2 * dp] = o0[j];
+            pr[3 + 2 * dp] = o1[j];
+            if (dp == 0) {
+                pr[0] = st[4 * h];
+                pr[1] = st[4 * h + 1];
             }
-            if (p < np) {
-                const uint32_t va = v2[p * half + dp];
-                a0 = fmaf(ph[p], bf16lo(va), a0);
-                a1 = fmaf(ph[p], bf16hi(va), a1);
-            }
-            o0[j] = a0 + a2;
-            o1[j] = a1 + a3;
-        }
-        bar_sync(1, kConsumers);  // sc / st are reused by the next block
-        if (ctid == Ring::owner(cv) * 32) ring.release(cv);
-    }
-    // the unnormalised partial (m, l, o) of every q head of the group
-    float* part = reinterpret_cast<float*>(op.p[3]);
-#pragma unroll
-    for (int j = 0; j < kOutMax; ++j) {
-        const int idx = ctid + j * kConsumers;
-        if (idx >= G * half) break;
-        const int h = idx / half, dp = idx - h * half;
-        float* pr = part + ((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + 2);
-        pr[2 + 2 * dp] = o0[j];
-        pr[3 + 2 * dp] = o1[j];
-        if (dp == 0) {
-            pr[0] = st[4 * h];
-            pr[1] = st[4 * h + 1];
         }
     }
     if (t_split && ctid == 0) *t_split = globaltimer();  // split work done (trace: prologue stamp)
@@ -1549,7 +1691,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                     t_pro = body_gemv(P, op, v, xs, acc, red, ring, ctid, reinterpret_cast<const float*>(smem + kSmemPre));
                     break;
                 case ET_OP_ATTN_SPLIT:
-                    body_attn_split<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro);
+                    body_attn_split<kMoE || kTC, kTC>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid, &t_pro);
                     break;
                 case ET_OP_ATTN_MERGE: body_attn_merge<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_GEMV_TC:
@@ -2322,7 +2464,9 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     }
                     tp = body_gemv(P, op, v, xs, acc, red, ring, ctid);
                     break;
-                case ET_OP_ATTN_SPLIT: body_attn_split<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid); break;
+                case ET_OP_ATTN_SPLIT:
+                    body_attn_split<kMoE || kTC, kTC>(P, op, v, reinterpret_cast<float*>(xs), ring, ctid);
+                    break;
                 case ET_OP_ATTN_MERGE: body_attn_merge<kMoE || kTC>(P, op, v, reinterpret_cast<float*>(xs), ctid); break;
                 case ET_OP_GEMV_TC:
                     if constexpr (kTC) tp = body_gemv_tc(P, op, v, smem, ring, ts, ctid);

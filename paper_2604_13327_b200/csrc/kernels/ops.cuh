@@ -28,6 +28,8 @@
 //   i4 = position symbol slot, i5 = split cap (partials' split dimension), i6 = kv heads,
 //   i7 = q / projection row stride of a batch sequence, i8 = per-sequence cache stride (elements);
 //   batch: grid dim 0 is sequence * kv_heads + kv head (partials / arrival counters per such group);
+//   flags bit 7: one flat grid dimension [b * kv * splits] instead, with i11 = per-step split
+//   budget (splits <= max(1, i11 / b)) and i10 = batch symbol slot (attn_tasks, attn_coord);
 //   p0 = q (fp32 [q_heads*head_dim], RoPE applied), p1/p2 = K/V cache, p3 = partials
 //   (fp32 [q_heads][max_splits][head_dim+2]); f0 = softmax scale
 // ET_OP_ATTN_MERGE      task (g): merges the splits and the new token at position s
@@ -260,10 +262,33 @@ struct AttnBlocks {
     int nblk;      // blocks (the last one may be partial)
 };
 
+// Splits of one (sequence, kv head) group: one per CH-position block, at most i5 (the
+// partials' split dimension) and, with a per-step budget i11 > 0, at most
+// max(1, i11 / b) (b from symbol slot i10): large batches get fewer, longer splits.
 __device__ __forceinline__ int attn_tasks(const et_op& op, const long long* binding) {
     const int s = static_cast<int>(binding[op.i[4]]), CH = op.i[2], cap = op.i[5];
     const int nb = (s + CH - 1) / CH;
-    return nb < cap ? nb : cap;
+    int ns = nb < cap ? nb : cap;
+    if (op.i[11] > 0) {
+        const int b = static_cast<int>(binding[op.i[10]]);
+        const int lim = op.i[11] / b > 1 ? op.i[11] / b : 1;
+        ns = ns < lim ? ns : lim;
+    }
+    return ns;
+}
+
+// (group, split) of a task: flags bit 7 = flat grid [b * kv * max(splits, 1)] (split count
+// depending on the batch), else the 2-D grid [b * kv, splits].
+__device__ __forceinline__ void attn_coord(const et_op& op, const int* coord, const long long* binding, int* gi,
+                                           int* c) {
+    if (op.flags & 128) {
+        const int ns0 = attn_tasks(op, binding), ns = ns0 > 1 ? ns0 : 1;
+        *gi = coord[0] / ns;
+        *c = coord[0] - *gi * ns;
+    } else {
+        *gi = coord[0];
+        *c = coord[1];
+    }
 }
 __device__ __forceinline__ int attn_splits_with_data(const et_op& op, const long long* binding) {
     return attn_tasks(op, binding);  // empty splits leave a neutral partial (m = -inf, l = 0)
@@ -341,13 +366,15 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
         pl.bytes[0] = pl.bytes[1] = pl.bytes[2] = rows;
     } else if (op.kind == ET_OP_ATTN_SPLIT) {
         // the split's K/V blocks, interleaved K0 V0 K1 V1 ... (one block per chunk)
-        const AttnBlocks a = attn_blocks(op, coord[1], binding);
+        int gi, c;
+        attn_coord(op, coord, binding, &gi, &c);
+        const AttnBlocks a = attn_blocks(op, c, binding);
         const int dh = op.i[0], CH = op.i[2], cap = op.i[3];
         const long long s = binding[op.i[4]];
         long long p1 = a.p0 + static_cast<long long>(a.nblk) * CH;
         if (p1 > s) p1 = s;
         if (p1 > a.p0) {
-            const int kvh = op.i[6], g = coord[0] % kvh, bq = coord[0] / kvh;  // coord 0 = sequence * kv + head
+            const int kvh = op.i[6], g = gi % kvh, bq = gi / kvh;  // gi = sequence * kv + head
             const long long off = static_cast<long long>(bq) * op.i[8] * 2 + (static_cast<long long>(g) * cap + a.p0) * dh * 2;
             pl.nseg = 2;
             pl.interleave = true;

@@ -319,4 +319,21 @@ __device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, uint32
                  : "memory");
 }
 
+// ldmatrix x4 with transpose (four 8x8 b16 matrices; lane l addresses row l%8 of matrix l/8).
+__device__ __forceinline__ uint4 ldsm_x4_trans(const void* p) {
+    uint4 v;
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+}
+
+// (hi, lo) bf16 pair split of two floats: x ~= hi + lo to ~16 mantissa bits, so a pair
+// of bf16 MMAs reproduces an fp32 operand (the other operand exact in bf16).
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const uint16_t ha = f2bf(a), hb = f2bf(b);
+    hi = static_cast<uint32_t>(ha) | (static_cast<uint32_t>(hb) << 16);
+    lo = static_cast<uint32_t>(f2bf(a - bf2f(ha))) | (static_cast<uint32_t>(f2bf(b - bf2f(hb))) << 16);
+}
+
 }  // namespace etk

@@ -168,7 +168,12 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
             prev = n1
         calls.append({"fn": fn(f"L{l}.qkv", [str(tc["qkv"] if tc else qkv_tasks or tasks)]),
                       "in": [{"event": prev, "map": ["0"]}], "out": [{"event": qkv, "map": ["0"]}]})
-        if fused_merge:  # the last split of each (sequence, kv head) merges the group
+        if tc:  # flat grid, split count shrinking with the batch (batch.attn_grid)
+            from .batch import attn_grid
+
+            calls.append({"fn": fn(f"L{l}.attn", [attn_grid(cfg, attn_cap, tc["attn_budget"])]),
+                          "in": [{"event": qkv, "map": ["0"]}], "out": [{"event": m, "map": ["0"]}]})
+        elif fused_merge:  # the last split of each (sequence, kv head) merges the group
             calls.append({"fn": fn(f"L{l}.attn", [f"{tokens} * {kv}", f"max({nsplit}, 1)"]),
                           "in": [{"event": qkv, "map": ["0"]}],
                           "out": [{"event": m, "map": [f"t0 % {kv}" if oproj_group_tasks else "0"]}]})
@@ -339,6 +344,9 @@ class MoEDecodeModel:
             for name, n, k, add in (("qkv", nq + 2 * cfg.kv_rows, H, True), ("oproj", H, nq, True),
                                     ("router", -(-cfg.experts // 128) * 128, H, True), ("lm", cfg.vocab, H, False)):
                 self.tc_tasks[name], self.tc_splits[name] = tc_tasks(n // 128, w, add, 1, npad, k // self.kp)
+            from .batch import attn_budget
+
+            self.tc_tasks["attn_budget"] = attn_budget(cfg, w)
         self.spec = moe_graph_spec(cfg, self.num_workers, self.lm_tasks, self.tokens, fused_merge=fused_merge,
                                    qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
                                    if balance else None, route_tasks=self.route_tasks, group_stage=self.group_stage,
@@ -428,8 +436,8 @@ class MoEDecodeModel:
             # flags: 1 q/k-norm mode, 2 fused merge, 32 zero the raw q/k/v after use; out in operand layout
             ops.append(make_op(OP_ATTN_SPLIT,
                                i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
-                                  cfg.kv_heads * self.capacity * dh, kp, bs],
-                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32,
+                                  cfg.kv_heads * self.capacity * dh, kp, bs, self.tc_tasks["attn_budget"]],
+                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 128,
                                p=[ptr(self.qkv), ptr(self.kcache[l]), ptr(self.vcache[l]), ptr(self.partials),
                                   ptr(self.attn_tc), ptr(self.arrive_attn[l]), ptr(L["k_norm"]), ptr(self.inv_freq),
                                   ptr(self.qkv) + 4 * nq, ptr(L["q_norm"])]))

@@ -26,4 +26,8 @@ def test_persistent_kernels_do_not_spill():
         if "ILb0ELb0E" in name:  # dense mma.sync instantiation (the Llama bs=1 decode path): spill-free
             assert st == 0 and ld == 0, (name, st, ld)
         else:  # bounded (once-per-task routing / slot decoding / epilogue code)
-            assert st <= 256 and ld <= 256, (name, st, ld)
+            assert st <= 320 and ld <= 320, (name, st, ld)
+    # the tensor-core streaming loops (issuer, producer) are register-resident everywhere
+    for name, (st, ld) in found.items():
+        if "tc_issue" in name or "tc_produce" in name:
+            assert st == 0 and ld == 0, (name, st, ld)
