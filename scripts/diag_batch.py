@@ -58,3 +58,30 @@ for c in l1:
         v = sorted(recs_of[dbg][i][9] for i in idx)
         row += f"  {name} med {v[len(v)//2]/1e3:7.2f}"
     print(row + " us")
+
+# attention task phases (normal run): wait-end -> split work done (t_prologue stamp) -> exec end
+os.environ["ET_DEBUG"] = "0"
+timed(2)
+raw = m.executor.raw_trace()
+t = m.executor.trace()
+ca = [c for c in range(len(calls)) if calls[c] == "L1.attn"][0]
+ph1, ph2 = [], []
+for rec, tr in zip(raw, t.records):
+    if tr["call"] == ca and not tr["noop"] and rec[3] > 0:
+        ph1.append(rec[3] - rec[2])
+        ph2.append(rec[4] - rec[3])
+ph1.sort()
+ph2.sort()
+print(f"attn split phase med {ph1[len(ph1)//2]/1e3:.2f} us, merge+arrival phase med {ph2[len(ph2)//2]/1e3:.2f} us "
+      f"max {ph2[-1]/1e3:.2f}")
+for name in ("L1.attn", "L1.gateup", "L1.qkv"):
+    ci = [c for c in range(len(calls)) if calls[c] == name][0]
+    w, x = [], []
+    for rec, tr in zip(raw, t.records):
+        if tr["call"] == ci and not tr["noop"]:
+            w.append(rec[2] - rec[1])
+            x.append(rec[4] - rec[2])
+    w.sort()
+    x.sort()
+    print(f"{name}: dependency wait med {w[len(w)//2]/1e3:.2f} max {w[-1]/1e3:.2f} us; work med {x[len(x)//2]/1e3:.2f} "
+          f"max {x[-1]/1e3:.2f} us; exec field {t.records[0]['exec']}")

@@ -57,3 +57,63 @@ def test_frag16_row_ranges_are_contiguous():
     for r0 in range(0, N, 16):
         block = T[r0:r0 + 16].flatten()
         assert sorted(block.tolist()) == sorted(W[r0:r0 + 16].flatten().tolist())
+
+
+def test_tensor_core_weight_layout_matches_kernel_offsets():
+    """batch.tc_pack puts W[r][k] where body_gemv_tc's descriptors read it: piece, 128-row
+    block, 4 KB k step, then 8-row group (256 B), k half (128 B), row (16 B), k (2 B)."""
+    import random
+
+    import torch
+
+    from paper_2604_13327_b200.batch import tc_pack
+
+    N, K, kp = 256, 384, 128
+    w = torch.arange(N * K, dtype=torch.float32).reshape(N, K)
+    p = tc_pack(w, kp)
+    nblk = N // 128
+    rnd = random.Random(0)
+    for _ in range(2000):
+        r, k = rnd.randrange(N), rnd.randrange(K)
+        piece, kk, blk, rr = k // kp, k % kp, r // 128, r % 128
+        byte = ((piece * nblk + blk) * (kp * 256) + (kk // 16) * 4096 + (rr // 8) * 256 + ((kk % 16) // 8) * 128
+                + (rr % 8) * 16 + (k % 8) * 2)
+        assert p[byte // 2] == w[r, k]
+
+
+def test_tensor_core_activation_layout_roundtrip():
+    """xb_unpack inverts the operand layout of ops.cuh xb_offset (restated here)."""
+    import torch
+
+    from paper_2604_13327_b200.batch import tc_npad, xb_unpack
+
+    b, K, kp = 5, 256, 128
+    npad = tc_npad(b)
+
+    def xb_offset(n, k):
+        piece, kk = k // kp, k % kp
+        return piece * npad * kp + (kk >> 4) * (npad * 16) + (n >> 3) * 128 + ((kk >> 3) & 1) * 64 + (n & 7) * 8 + (k & 7)
+
+    x = torch.randn(b, K)
+    buf = torch.zeros(npad * K)
+    for n in range(b):
+        for k in range(K):
+            buf[xb_offset(n, k)] = x[n, k]
+    assert torch.equal(xb_unpack(buf, b, K, npad, kp), x)
+
+
+def test_batched_attention_grid_is_covered_by_power_of_two_samples():
+    """The flat attention grid b*kv*max(1, min(ceil(s/64), cap, budget // b)) of every
+    b <= 64 fits the next power-of-two batch sample (static schedule coverage)."""
+    from paper_2604_13327_b200.batch import attn_budget
+    from paper_2604_13327_b200.decode import LLAMA3_8B
+
+    cap, bud = 18, attn_budget(LLAMA3_8B, 148)
+
+    def tasks(b, s):
+        return b * LLAMA3_8B.kv_heads * max(1, min(min((s + 63) // 64, cap), bud // b))
+
+    for s in (1, 100, 1024, 8192):
+        for b in range(1, 65):
+            sample = 1 << (b - 1).bit_length()
+            assert tasks(b, s) <= tasks(sample, s), (b, s)
