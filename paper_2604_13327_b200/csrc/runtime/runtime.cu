@@ -566,28 +566,40 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     if (!rt->ops_bound) return rt->fail(ET_ERR_INVALID, "ops not bound");
     cudaSetDevice(rt->cfg.device);
     // next-larger covering sample (samples are uploaded in selection order)
-    int pick = -1;
-    for (size_t i = 0; i < rt->samples.size() && pick < 0; ++i) {
-        bool covers = true;
-        for (int k = 0; k < num_symbols; ++k) covers &= rt->samples[i].binding[static_cast<size_t>(k)] >= binding[k];
-        if (covers) pick = static_cast<int>(i);
-    }
-    if (pick < 0) return rt->fail(ET_ERR_INVALID, "binding exceeds every sampled shape");
-    const Sample& S = rt->samples[static_cast<size_t>(pick)];
-    // the actual grids must fit inside the sample's (ref sched_static.cpp:153-156)
+    // actual grid extents at this binding
+    std::vector<int64_t> ext(static_cast<size_t>(rt->num_calls) * 4, 0);
     for (int c = 0; c < rt->num_calls; ++c)
         for (int d = 0; d < rt->call_rank[static_cast<size_t>(c)]; ++d) {
             bool ok = true;
             const int64_t a = eval_host(rt->code_op, rt->code_arg, rt->grid_code_off[static_cast<size_t>(c * 4 + d)],
                                         rt->grid_code_off[static_cast<size_t>(c * 4 + d + 1)], binding, &ok);
             if (!ok) return rt->fail(ET_ERR_INVALID, "grid of call " + std::to_string(c) + " is invalid at the binding");
-            if (a > S.call_extents[static_cast<size_t>(c * 4 + d)])
-                return rt->fail(ET_ERR_INVALID, "sampled shape does not cover the actual grid of call " + std::to_string(c));
+            ext[static_cast<size_t>(c * 4 + d)] = a;
             if (d == 0 && !gemv_acc_fits(rt->h_ops[static_cast<size_t>(c)], a, binding))
                 return rt->fail(ET_ERR_INVALID, "GEMV call " + std::to_string(c) +
                                                     ": rows per task x batch exceed the accumulators (shared memory / "
                                                     "tensor memory) or the operand shape is invalid");
         }
+    // next-larger sample covering the binding (ref sched_static.cpp:111-175) whose grids
+    // also cover the actual ones (ref sched_static.cpp:153-156); a grid that is not
+    // monotone in the symbols (e.g. splits shrinking with the batch) falls through to
+    // the next covering sample instead of failing
+    int pick = -1, first = -1;
+    for (size_t i = 0; i < rt->samples.size() && pick < 0; ++i) {
+        bool covers = true;
+        for (int k = 0; k < num_symbols; ++k) covers &= rt->samples[i].binding[static_cast<size_t>(k)] >= binding[k];
+        if (!covers) continue;
+        if (first < 0) first = static_cast<int>(i);
+        bool grids = true;
+        for (int c = 0; c < rt->num_calls && grids; ++c)
+            for (int d = 0; d < rt->call_rank[static_cast<size_t>(c)]; ++d)
+                grids &= ext[static_cast<size_t>(c * 4 + d)] <= rt->samples[i].call_extents[static_cast<size_t>(c * 4 + d)];
+        if (grids) pick = static_cast<int>(i);
+    }
+    if (first < 0) return rt->fail(ET_ERR_INVALID, "binding exceeds every sampled shape");
+    if (pick < 0) return rt->fail(ET_ERR_INVALID, "sampled shape does not cover the actual grid of a call");
+    const Sample& S = rt->samples[static_cast<size_t>(pick)];
+    (void)S;
 
     etk::StaticParams p{};
     p.num_symbols = rt->num_symbols;

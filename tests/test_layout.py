@@ -103,8 +103,10 @@ def test_tensor_core_activation_layout_roundtrip():
 
 
 def test_batched_attention_grid_is_covered_by_power_of_two_samples():
-    """The flat attention grid b*kv*max(1, min(ceil(s/64), cap, budget // b)) of every
-    b <= 64 fits the next power-of-two batch sample (static schedule coverage)."""
+    """The flat attention grid b*kv*max(1, min(ceil(s/64), cap, budget // b)) is not
+    monotone in b (b=17, s=100: 272 tasks; b=32: 256), so the runtime takes the first
+    covering sample whose grids also cover (runtime.cu et_step); with power-of-two batch
+    samples up to 64 one always exists."""
     from paper_2604_13327_b200.batch import attn_budget
     from paper_2604_13327_b200.decode import LLAMA3_8B
 
@@ -115,5 +117,5 @@ def test_batched_attention_grid_is_covered_by_power_of_two_samples():
 
     for s in (1, 100, 1024, 8192):
         for b in range(1, 65):
-            sample = 1 << (b - 1).bit_length()
-            assert tasks(b, s) <= tasks(sample, s), (b, s)
+            samples = [1 << i for i in range(7) if (1 << i) >= b]
+            assert any(tasks(b, s) <= tasks(x, s) for x in samples), (b, s)
