@@ -27,7 +27,9 @@ Device layout (HBM):
     epilogue), so each piece reaches shared memory with one bulk copy;
   * residual stream fp32 [b][H] (row-parallel projections red.add into it),
     raw q/k/v fp32 [b][rows] (split-K adds; the attention merger zeroes them),
-    KV caches bf16 [b][kv][capacity][head_dim] per layer.
+    KV caches bf16 [b][kv][capacity][head_dim] per layer, each row's 16-byte chunks
+    XOR-swizzled by position % 8 (cache_swizzle) so the tensor-core attention reads
+    8 rows from 8 different bank groups.
 """
 
 import json
@@ -64,6 +66,17 @@ def tc_piece(max_batch):
     """Piece length kp: one activation piece (npad x kp bf16) fills a 16 KB x buffer."""
     kp = XBUF_BYTES // (2 * tc_npad(max_batch))
     return min(512, kp // 64 * 64)
+
+
+def cache_swizzle(t):
+    """K/V cache rows with their 16-byte (8-element) chunks XOR-permuted by position % 8
+    (attention flags bit 8): the device layout <-> the logical [.., cap, dh] rows.  An
+    involution, so the same call converts either way."""
+    *lead, cap, dh = t.shape
+    pos = torch.arange(cap, device=t.device).view(cap, 1)
+    chunk = torch.arange(dh // 8, device=t.device).view(1, dh // 8)
+    src = (chunk ^ (pos % 8)).view(*([1] * len(lead)), cap, dh // 8, 1).expand(*lead, cap, dh // 8, 8)
+    return torch.gather(t.reshape(*lead, cap, dh // 8, 8), -2, src).reshape(t.shape)
 
 
 def tc_piece_for(max_batch, ks):
@@ -255,11 +268,12 @@ class BatchDecodeModel:
         for l, L in enumerate(W["layers"]):
             ops.append(norm(L["attn_norm"]))
             ops.append(tc(rows, H, 1, EPI_ADD, L["wqkv"], None, self.xn, self.qkv, sp["qkv"]))
-            # flags: 1 q/k fused mode, 2 fused merge, 32 zero the raw q/k/v after use, 64 RoPE only
+            # flags: 1 q/k fused mode, 2 fused merge, 32 zero the raw q/k/v after use, 64 RoPE only,
+            # 128 flat batch-dependent grid, 256 chunk-swizzled cache rows (cache_swizzle)
             ops.append(make_op(OP_ATTN_SPLIT,
                                i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
                                   cfg.kv_heads * self.capacity * dh, kp, bs, self.attn_budget],
-                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 64 | 128,
+                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 64 | 128 | 256,
                                p=[ptr(self.qkv), ptr(self.kcache[l]), ptr(self.vcache[l]), ptr(self.partials),
                                   ptr(self.attn), ptr(self.arrive[l]), 0, ptr(self.inv_freq),
                                   ptr(self.qkv) + 4 * nq, 0]))

@@ -797,13 +797,16 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     float* wts = ml + 2 * G * nspl;     // [G][nspl]
     float* hs = wts + G * nspl;         // [G]: weight of the new token
     float* kns = hs + G;                // [dh]
+    // flags bit 8 (tensor-core instantiations): cache rows hold their 16-byte chunks
+    // XOR-swizzled by position % 8, so row-strided tensor-core reads are bank-conflict free
+    const int csw = (kWide && (op.flags & 256)) ? static_cast<int>(s & 7) : 0;
     float ov[kOut][kPass];
     float vv[kOut];
 #pragma unroll
     for (int j = 0; j < kOut; ++j) {
         const int idx = ctid + j * kConsumers;
         const int hh = idx / dh, d = idx - hh * dh;
-        vv[j] = idx < G * dh ? bf2f(__ldcg(vn + d)) : 0.f;
+        vv[j] = idx < G * dh ? bf2f(__ldcg(vn + ((((d >> 3) ^ csw)) << 3) + (d & 7))) : 0.f;
 #pragma unroll
         for (int c = 0; c < kPass; ++c)
             ov[j][c] = (idx < G * dh && c < nspl) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d)
@@ -814,7 +817,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
         ml[2 * i] = __ldcg(pr);
         ml[2 * i + 1] = __ldcg(pr + 1);
     }
-    for (int d = ctid; d < dh; d += kConsumers) kns[d] = bf2f(__ldcg(kn + d));
+    for (int d = ctid; d < dh; d += kConsumers) kns[d] = bf2f(__ldcg(kn + ((((d >> 3) ^ csw)) << 3) + (d & 7)));
     bar_sync(1, kConsumers);
     for (int hh = warp; hh < G; hh += kConsumerWarps) {
         float dot = 0.f;
@@ -884,6 +887,7 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5];
     const float scale = op.f[0];
     const int nks = dh / 16;
+    const bool swz = (op.flags & 256) != 0;  // cache rows chunk-swizzled by position % 8
     uint32_t qh[8][2], ql[8][2];  // Q^T fragments (k = dim, n = head g8)
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
@@ -895,40 +899,56 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
         }
     }
     float o[4] = {0.f, 0.f, 0.f, 0.f};
+    // ET_DEBUG 4096 (+ trace): thread 0 accumulates ns in ring waits / barriers / compute
+    const bool tdbg = ring.dbg && (P.debug & 4096) && ctid == 0;
+    uint64_t tw = 0, tb = 0, tcomp = 0, tt = tdbg ? globaltimer() : 0;
+#define ET_PHASE(acc)                          \
+    if (tdbg) {                                \
+        const uint64_t now_ = globaltimer();   \
+        acc += now_ - tt;                      \
+        tt = now_;                             \
+    }
     for (int blk = 0; blk < ab.nblk; ++blk) {
         const long long pb = ab.p0 + static_cast<long long>(blk) * CH;
         const int np = static_cast<int>(pb + CH < s ? CH : s - pb);
         const unsigned long long ck = ring.seq, cv = ring.seq + 1;
         ring.seq += 2;
+        ET_PHASE(tcomp)
         const uint8_t* kb = ring.wait(ck);
         if (!kb) return false;
+        ET_PHASE(tw)
         if (warp < 4 && 16 * warp < np) {
-            float d[4] = {0.f, 0.f, 0.f, 0.f};
+            float d[4] = {0.f, 0.f, 0.f, 0.f}, e[4] = {0.f, 0.f, 0.f, 0.f};  // two chains (hi / lo)
+            // rows 16w+g8 and +8 share position % 8 = g8: chunk j of either sits at j ^ sw
+            const int sw = swz ? g8 : 0;
             const uint8_t* r0 = kb + (16 * warp + g8) * dh * 2 + 4 * q4;
             const uint8_t* r1 = r0 + 8 * dh * 2;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 if (ks < nks) {
+                    const int c0 = ((2 * ks) ^ sw) * 16, c1 = ((2 * ks + 1) ^ sw) * 16;
                     uint4 a;
-                    a.x = *reinterpret_cast<const uint32_t*>(r0 + ks * 32);
-                    a.y = *reinterpret_cast<const uint32_t*>(r1 + ks * 32);
-                    a.z = *reinterpret_cast<const uint32_t*>(r0 + ks * 32 + 16);
-                    a.w = *reinterpret_cast<const uint32_t*>(r1 + ks * 32 + 16);
+                    a.x = *reinterpret_cast<const uint32_t*>(r0 + c0);
+                    a.y = *reinterpret_cast<const uint32_t*>(r1 + c0);
+                    a.z = *reinterpret_cast<const uint32_t*>(r0 + c1);
+                    a.w = *reinterpret_cast<const uint32_t*>(r1 + c1);
                     mma_bf16_16816(d, a, qh[ks][0], qh[ks][1]);
-                    mma_bf16_16816(d, a, ql[ks][0], ql[ks][1]);
+                    mma_bf16_16816(e, a, ql[ks][0], ql[ks][1]);
                 }
             }
             const int p0 = 16 * warp + g8, h0 = 2 * q4;  // d: (p0, h0) (p0, h0+1) (p0+8, h0) (p0+8, h0+1)
             if (h0 < G) {
-                if (p0 < np) sc[h0 * CH + p0] = d[0] * scale;
-                if (p0 + 8 < np) sc[h0 * CH + p0 + 8] = d[2] * scale;
+                if (p0 < np) sc[h0 * CH + p0] = (d[0] + e[0]) * scale;
+                if (p0 + 8 < np) sc[h0 * CH + p0 + 8] = (d[2] + e[2]) * scale;
             }
             if (h0 + 1 < G) {
-                if (p0 < np) sc[(h0 + 1) * CH + p0] = d[1] * scale;
-                if (p0 + 8 < np) sc[(h0 + 1) * CH + p0 + 8] = d[3] * scale;
+                if (p0 < np) sc[(h0 + 1) * CH + p0] = (d[1] + e[1]) * scale;
+                if (p0 + 8 < np) sc[(h0 + 1) * CH + p0 + 8] = (d[3] + e[3]) * scale;
             }
         }
+        ET_PHASE(tcomp)
         bar_sync(1, kConsumers);
+        ET_PHASE(tb)
         if (ctid == Ring::owner(ck) * 32) ring.release(ck);
         for (int h = warp; h < G; h += kConsumerWarps) {  // online softmax statistics per head (warp h)
             float m = -INFINITY;
@@ -937,9 +957,9 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
             const float mo = st[4 * h], mn = fmaxf(mo, m);
             float l = 0.f;
             for (int p = lane; p < np; p += 32) {
-                const float e = __expf(sc[h * CH + p] - mn);
-                sc[h * CH + p] = e;
-                l += e;
+                const float ex = __expf(sc[h * CH + p] - mn);
+                sc[h * CH + p] = ex;
+                l += ex;
             }
             l = warp_sum(l);
             if (lane == 0) {
@@ -949,9 +969,12 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
                 st[4 * h + 2] = alpha;
             }
         }
+        ET_PHASE(tcomp)
         bar_sync(1, kConsumers);
+        ET_PHASE(tb)
         const uint8_t* vb = ring.wait(cv);
         if (!vb) return false;
+        ET_PHASE(tw)
         if (warp < nks) {
             const int h0 = 2 * q4;
             const float a0 = h0 < G ? st[4 * h0 + 2] : 1.f, a1 = h0 + 1 < G ? st[4 * h0 + 6] : 1.f;
@@ -959,8 +982,9 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
             o[1] *= a1;
             o[2] *= a0;
             o[3] *= a1;
-            const int mi = lane >> 3;
-            const uint8_t* vrow = vb + (((mi & 2) ? 8 : 0) + (lane & 7)) * dh * 2 + (16 * warp + ((mi & 1) ? 8 : 0)) * 2;
+            const int mi = lane >> 3, prow = ((mi & 2) ? 8 : 0) + (lane & 7);  // this lane's row (position)
+            const int chunk = (2 * warp + (mi & 1)) ^ (swz ? (lane & 7) : 0);   // its 16-byte dim chunk
+            const uint8_t* vrow = vb + prow * dh * 2 + chunk * 16;
             const float* ph = sc + g8 * CH + 2 * q4;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
@@ -982,8 +1006,16 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
                 }
             }
         }
+        ET_PHASE(tcomp)
         bar_sync(1, kConsumers);  // sc / st are reused by the next block
+        ET_PHASE(tb)
         if (ctid == Ring::owner(cv) * 32) ring.release(cv);
+    }
+#undef ET_PHASE
+    if (tdbg) {  // reported through the trace pad (ring.stall: waits, busy: barriers, xwait: compute)
+        ring.stall += tw;
+        ring.busy += tb;
+        ring.xwait += tcomp;
     }
     float* part = reinterpret_cast<float*>(op.p[3]);
     if (warp < nks) {  // o: O^T (d0, h0) (d0, h0+1) (d0+8, h0) (d0+8, h0+1)
@@ -1064,9 +1096,11 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
                 const long long cb = static_cast<long long>(bq) * op.i[8];
                 uint16_t* kc = reinterpret_cast<uint16_t*>(op.p[1]) + cb + (static_cast<long long>(g) * op.i[3] + s) * dh;
                 uint16_t* vc = reinterpret_cast<uint16_t*>(op.p[2]) + cb + (static_cast<long long>(g) * op.i[3] + s) * dh;
+                const int sw = (op.flags & 256) ? static_cast<int>(s & 7) : 0;  // cache row chunk swizzle
                 for (int d = ctid; d < dh; d += kConsumers) {
-                    kc[d] = f2bf(kv[d]);
-                    vc[d] = f2bf(kv[dh + d]);
+                    const int dp = ((((d >> 3) ^ sw)) << 3) | (d & 7);
+                    kc[dp] = f2bf(kv[d]);
+                    vc[dp] = f2bf(kv[dh + d]);
                 }
             }
         }

@@ -28,6 +28,8 @@
 //   i4 = position symbol slot, i5 = split cap (partials' split dimension), i6 = kv heads,
 //   i7 = q / projection row stride of a batch sequence, i8 = per-sequence cache stride (elements);
 //   batch: grid dim 0 is sequence * kv_heads + kv head (partials / arrival counters per such group);
+//   flags bit 8: K/V cache rows store their 16-byte chunks XOR-swizzled by position % 8
+//   (chunk j of row p at j ^ (p % 8)): tensor-core reads of 8 rows hit 8 bank groups;
 //   flags bit 7: one flat grid dimension [b * kv * splits] instead, with i11 = per-step split
 //   budget (splits <= max(1, i11 / b)) and i10 = batch symbol slot (attn_tasks, attn_coord);
 //   p0 = q (fp32 [q_heads*head_dim], RoPE applied), p1/p2 = K/V cache, p3 = partials

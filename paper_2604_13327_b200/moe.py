@@ -433,11 +433,12 @@ class MoEDecodeModel:
             ri = {n: self.rt_index[f"{n}{l}"] for n in RT_PER_LAYER}
             ops.append(norm(L["attn_norm"]))
             ops.append(tc(rows, H, EPI_ADD, L["wqkv"], self.xn_tc, self.qkv, sp["qkv"]))
-            # flags: 1 q/k-norm mode, 2 fused merge, 32 zero the raw q/k/v after use; out in operand layout
+            # flags: 1 q/k-norm mode, 2 fused merge, 32 zero the raw q/k/v after use, 128 flat grid,
+            # 256 chunk-swizzled cache rows (batch.cache_swizzle); out in operand layout
             ops.append(make_op(OP_ATTN_SPLIT,
                                i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
                                   cfg.kv_heads * self.capacity * dh, kp, bs, self.tc_tasks["attn_budget"]],
-                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 128,
+                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 128 | 256,
                                p=[ptr(self.qkv), ptr(self.kcache[l]), ptr(self.vcache[l]), ptr(self.partials),
                                   ptr(self.attn_tc), ptr(self.arrive_attn[l]), ptr(L["k_norm"]), ptr(self.inv_freq),
                                   ptr(self.qkv) + 4 * nq, ptr(L["q_norm"])]))

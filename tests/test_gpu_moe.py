@@ -110,8 +110,11 @@ def test_moe_batched_decode_no_recompile(scheduler, max_batch, cases):
     for b, s in cases:
         m.fill_cache(s, seed=b)
         m.set_token(toks)
-        kc = [k.cpu() for k in m.kcache]
-        vc = [v.cpu() for v in m.vcache]
+        from paper_2604_13327_b200.batch import cache_swizzle
+
+        sw = cache_swizzle if m.tc else (lambda x: x)  # the tensor-core variant stores rows swizzled
+        kc = [sw(k).cpu() for k in m.kcache]
+        vc = [sw(v).cpu() for v in m.vcache]
         logits = m.step(s, b).cpu()
         for l in range(cfg.layers):
             r = m.routing(l, b)
