@@ -191,9 +191,9 @@ class BatchDecodeModel:
                                       ("gateup", I, H, False, 2), ("down", H, I, True, 1),
                                       ("lm", cfg.vocab, H, False, 1)):
             self.tasks[name], self.splits[name] = tc_tasks(n // 128, w, add, nseg, npad, k // kp)
-        # attention splits per (sequence, kv head): the batch-1 cap (a split is a run of
-        # 64-position blocks; at large batch the extra tasks only shorten the tail)
-        self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
+        # attention splits per (sequence, kv head): a quarter of the batch-1 cap -- every
+        # split already runs 8 warps on separate tiles and leaves 8 partials to merge
+        self.max_splits = max(1, attn_split_cap(cfg, self.samples[-1], self.num_workers) // 4)
         self.scheduler = scheduler
         t0 = time.perf_counter()
         self.attn_budget = attn_budget(cfg, self.num_workers)
@@ -220,7 +220,9 @@ class BatchDecodeModel:
         self.qkv = torch.zeros(B, rows, dtype=torch.float32, device=dev)        # raw projections (split-K adds)
         self.attn = torch.zeros(npad * nq, dtype=torch.bfloat16, device=dev)    # attention out (operand layout)
         self.act = torch.zeros(npad * I, dtype=torch.bfloat16, device=dev)      # silu(gate)*up (operand layout)
-        self.partials = torch.zeros(B * cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        # 8 partials per split (one per consumer warp: attention flags bit 9)
+        self.partials = torch.zeros(B * cfg.heads, 8 * self.max_splits, cfg.head_dim + 2, dtype=torch.float32,
+                                    device=dev)
         self.arrive = torch.zeros(cfg.layers, B * cfg.kv_heads, dtype=torch.int32, device=dev)
         self.logits = torch.zeros(B, cfg.vocab, dtype=torch.float32, device=dev)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
@@ -269,11 +271,12 @@ class BatchDecodeModel:
             ops.append(norm(L["attn_norm"]))
             ops.append(tc(rows, H, 1, EPI_ADD, L["wqkv"], None, self.xn, self.qkv, sp["qkv"]))
             # flags: 1 q/k fused mode, 2 fused merge, 32 zero the raw q/k/v after use, 64 RoPE only,
-            # 128 flat batch-dependent grid, 256 chunk-swizzled cache rows (cache_swizzle)
+            # 128 flat batch-dependent grid, 256 chunk-swizzled cache rows (cache_swizzle),
+            # 512 one partial per consumer warp
             ops.append(make_op(OP_ATTN_SPLIT,
                                i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
                                   cfg.kv_heads * self.capacity * dh, kp, bs, self.attn_budget],
-                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 64 | 128 | 256,
+                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 64 | 128 | 256 | 512,
                                p=[ptr(self.qkv), ptr(self.kcache[l]), ptr(self.vcache[l]), ptr(self.partials),
                                   ptr(self.attn), ptr(self.arrive[l]), 0, ptr(self.inv_freq),
                                   ptr(self.qkv) + 4 * nq, 0]))

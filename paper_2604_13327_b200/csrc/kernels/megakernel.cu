@@ -778,7 +778,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
                                               int qstride, float* scr, int ctid) {
     constexpr int kPass = kWide ? 8 : 16, kOut = kWide ? 4 : 2;  // splits in registers; outputs per thread
     const int warp = ctid >> 5, lane = ctid & 31;
-    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5], kvh = op.i[6];
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = attn_part_stride(op), kvh = op.i[6];
     const int g = gi % kvh, bq = gi / kvh;  // kv head, sequence of the batch
     const long long s = P.binding[op.i[4]];
     const int nspl = attn_splits_with_data(op, P.binding);
@@ -874,54 +874,54 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
 }
 
 // Tensor-core form of a split's block loop (tensor-core instantiations: the batch
-// path).  Per 64-position block: S^T = K Q^T on mma.sync m16n8k16 (positions x q
-// heads; q split into bf16 hi + lo, so the scores keep ~fp32 precision) by warps
-// 0..3, the same online softmax over the scores in shared memory, then
-// O^T += V^T P^T (head dims x q heads; V^T fragments by ldmatrix.trans, P split
-// hi + lo) by warps 0..dh/16-1.  Writes the unnormalised partial (m, l, o) like
-// the scalar loop.  G <= 8, dh % 16 == 0, dh <= 128, CH == 64 (checked on the host).
+// path), split along positions: warp w owns the 16-position tile (w % 4) of every
+// block of parity (w / 4) -- warps 0-3 take blocks 0, 2, 4, ..., warps 4-7 blocks
+// 1, 3, 5, ... -- and keeps its own online softmax (m, l per head) and O^T
+// accumulators in registers, so a block needs no CTA barrier: per tile,
+// S^T = K Q^T (mma.sync m16n8k16, positions x q heads, q split bf16 hi + lo), the
+// running max / sum by shuffles over the tile's 16 positions, P^T transposed
+// through a per-warp scratch, then O^T += V^T P^T for every 16-dim tile of the
+// head (V^T by ldmatrix.trans, P split hi + lo).  The four warps of a block meet
+// on a named barrier only to release its two ring stages.  Each warp leaves its own
+// partial (split c, sub-split w: flags bit 9), folded by the group merge.
+// G <= 8, dh % 16 == 0, dh <= 128, CH == 64 (checked on the host).
 __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& op, int gi, int c, const AttnBlocks ab,
                                             long long s, const float* qs, int qstride, float* sc, float* st, Ring& ring,
                                             int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31, g8 = lane >> 2, q4 = lane & 3;
-    const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5];
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = attn_part_stride(op);
     const float scale = op.f[0];
-    const int nks = dh / 16;
+    const int nks = dh / 16, half = warp >> 2, tile = warp & 3;
     const bool swz = (op.flags & 256) != 0;  // cache rows chunk-swizzled by position % 8
     uint32_t qh[8][2], ql[8][2];  // Q^T fragments (k = dim, n = head g8)
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
         qh[ks][0] = qh[ks][1] = ql[ks][0] = ql[ks][1] = 0u;
-        if (ks < nks && warp < 4 && g8 < G) {
+        if (ks < nks && g8 < G) {
             const float* qv = qs + g8 * qstride + ks * 16 + 2 * q4;
             split_bf16x2(qv[0], qv[1], qh[ks][0], ql[ks][0]);
             split_bf16x2(qv[8], qv[9], qh[ks][1], ql[ks][1]);
         }
     }
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    // ET_DEBUG 4096 (+ trace): thread 0 accumulates ns in ring waits / barriers / compute
-    const bool tdbg = ring.dbg && (P.debug & 4096) && ctid == 0;
-    uint64_t tw = 0, tb = 0, tcomp = 0, tt = tdbg ? globaltimer() : 0;
-#define ET_PHASE(acc)                          \
-    if (tdbg) {                                \
-        const uint64_t now_ = globaltimer();   \
-        acc += now_ - tt;                      \
-        tt = now_;                             \
-    }
-    for (int blk = 0; blk < ab.nblk; ++blk) {
+    const int h0 = 2 * q4;                       // this thread's two head columns
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    float o[8][4];                               // O^T per 16-dim tile: (d, h0) (d, h0+1) (d+8, h0) (d+8, h0+1)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+    float* pw = sc + warp * 16 * 9;              // per-warp P scratch [16 positions][8 heads] (+1 pad)
+    const unsigned long long seq0 = ring.seq;
+    ring.seq += 2ull * ab.nblk;
+    for (int blk = half; blk < ab.nblk; blk += 2) {
         const long long pb = ab.p0 + static_cast<long long>(blk) * CH;
         const int np = static_cast<int>(pb + CH < s ? CH : s - pb);
-        const unsigned long long ck = ring.seq, cv = ring.seq + 1;
-        ring.seq += 2;
-        ET_PHASE(tcomp)
+        const unsigned long long ck = seq0 + 2ull * blk, cv = ck + 1;
         const uint8_t* kb = ring.wait(ck);
         if (!kb) return false;
-        ET_PHASE(tw)
-        if (warp < 4 && 16 * warp < np) {
-            float d[4] = {0.f, 0.f, 0.f, 0.f}, e[4] = {0.f, 0.f, 0.f, 0.f};  // two chains (hi / lo)
-            // rows 16w+g8 and +8 share position % 8 = g8: chunk j of either sits at j ^ sw
+        const int t0 = 16 * tile;                // the tile's first position in the block
+        if (t0 < np) {
+            float d[4] = {0.f, 0.f, 0.f, 0.f}, e[4] = {0.f, 0.f, 0.f, 0.f};
             const int sw = swz ? g8 : 0;
-            const uint8_t* r0 = kb + (16 * warp + g8) * dh * 2 + 4 * q4;
+            const uint8_t* r0 = kb + (t0 + g8) * dh * 2 + 4 * q4;
             const uint8_t* r1 = r0 + 8 * dh * 2;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
@@ -936,105 +936,100 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
                     mma_bf16_16816(e, a, ql[ks][0], ql[ks][1]);
                 }
             }
-            const int p0 = 16 * warp + g8, h0 = 2 * q4;  // d: (p0, h0) (p0, h0+1) (p0+8, h0) (p0+8, h0+1)
-            if (h0 < G) {
-                if (p0 < np) sc[h0 * CH + p0] = (d[0] + e[0]) * scale;
-                if (p0 + 8 < np) sc[h0 * CH + p0 + 8] = (d[2] + e[2]) * scale;
-            }
-            if (h0 + 1 < G) {
-                if (p0 < np) sc[(h0 + 1) * CH + p0] = (d[1] + e[1]) * scale;
-                if (p0 + 8 < np) sc[(h0 + 1) * CH + p0 + 8] = (d[3] + e[3]) * scale;
-            }
-        }
-        ET_PHASE(tcomp)
-        bar_sync(1, kConsumers);
-        ET_PHASE(tb)
-        if (ctid == Ring::owner(ck) * 32) ring.release(ck);
-        for (int h = warp; h < G; h += kConsumerWarps) {  // online softmax statistics per head (warp h)
-            float m = -INFINITY;
-            for (int p = lane; p < np; p += 32) m = fmaxf(m, sc[h * CH + p]);
-            m = warp_max(m);
-            const float mo = st[4 * h], mn = fmaxf(mo, m);
-            float l = 0.f;
-            for (int p = lane; p < np; p += 32) {
-                const float ex = __expf(sc[h * CH + p] - mn);
-                sc[h * CH + p] = ex;
-                l += ex;
-            }
-            l = warp_sum(l);
-            if (lane == 0) {
-                const float alpha = __expf(mo - mn);
-                st[4 * h] = mn;
-                st[4 * h + 1] = st[4 * h + 1] * alpha + l;
-                st[4 * h + 2] = alpha;
-            }
-        }
-        ET_PHASE(tcomp)
-        bar_sync(1, kConsumers);
-        ET_PHASE(tb)
-        const uint8_t* vb = ring.wait(cv);
-        if (!vb) return false;
-        ET_PHASE(tw)
-        if (warp < nks) {
-            const int h0 = 2 * q4;
-            const float a0 = h0 < G ? st[4 * h0 + 2] : 1.f, a1 = h0 + 1 < G ? st[4 * h0 + 6] : 1.f;
-            o[0] *= a0;
-            o[1] *= a1;
-            o[2] *= a0;
-            o[3] *= a1;
-            const int mi = lane >> 3, prow = ((mi & 2) ? 8 : 0) + (lane & 7);  // this lane's row (position)
-            const int chunk = (2 * warp + (mi & 1)) ^ (swz ? (lane & 7) : 0);   // its 16-byte dim chunk
-            const uint8_t* vrow = vb + prow * dh * 2 + chunk * 16;
-            const float* ph = sc + g8 * CH + 2 * q4;
+            // scores of positions t0+g8 / t0+g8+8 for heads h0, h0+1 (invalid -> -inf)
+            const bool v0 = t0 + g8 < np, v1 = t0 + g8 + 8 < np;
+            const float s00 = v0 ? (d[0] + e[0]) * scale : -INFINITY, s01 = v0 ? (d[1] + e[1]) * scale : -INFINITY;
+            const float s10 = v1 ? (d[2] + e[2]) * scale : -INFINITY, s11 = v1 ? (d[3] + e[3]) * scale : -INFINITY;
+            float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-                const int pp = ks * 16 + 2 * q4;
-                if (ks * 16 < np) {
-                    const uint4 a = ldsm_x4_trans(vrow + ks * 16 * dh * 2);  // V^T: dims x positions
-                    float p00 = 0.f, p01 = 0.f, p10 = 0.f, p11 = 0.f;
-                    if (g8 < G) {
-                        if (pp < np) p00 = ph[ks * 16];
-                        if (pp + 1 < np) p01 = ph[ks * 16 + 1];
-                        if (pp + 8 < np) p10 = ph[ks * 16 + 8];
-                        if (pp + 9 < np) p11 = ph[ks * 16 + 9];
-                    }
-                    uint32_t bh0, bl0, bh1, bl1;
-                    split_bf16x2(p00, p01, bh0, bl0);
-                    split_bf16x2(p10, p11, bh1, bl1);
-                    mma_bf16_16816(o, a, bh0, bh1);
-                    mma_bf16_16816(o, a, bl0, bl1);
+            for (int off = 4; off < 32; off <<= 1) {  // over g8 (lanes with the same q4)
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+            }
+            const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);  // finite: the tile has a valid position
+            const float a0 = __expf(m0 - n0), a1 = __expf(m1 - n1);
+            const float p00 = __expf(s00 - n0), p01 = __expf(s01 - n1), p10 = __expf(s10 - n0), p11 = __expf(s11 - n1);
+            float r0s = p00 + p10, r1s = p01 + p11;
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) {
+                r0s += __shfl_xor_sync(0xffffffffu, r0s, off);
+                r1s += __shfl_xor_sync(0xffffffffu, r1s, off);
+            }
+            m0 = n0;
+            m1 = n1;
+            l0 = l0 * a0 + r0s;
+            l1 = l1 * a1 + r1s;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                o[mt][0] *= a0;
+                o[mt][1] *= a1;
+                o[mt][2] *= a0;
+                o[mt][3] *= a1;
+            }
+            // P^T fragments need (positions 2q4.., head g8): transpose through the warp scratch
+            pw[g8 * 9 + h0] = p00;
+            pw[g8 * 9 + h0 + 1] = p01;
+            pw[(g8 + 8) * 9 + h0] = p10;
+            pw[(g8 + 8) * 9 + h0 + 1] = p11;
+            __syncwarp();
+            const float q00 = g8 < G ? pw[(2 * q4) * 9 + g8] : 0.f, q01 = g8 < G ? pw[(2 * q4 + 1) * 9 + g8] : 0.f;
+            const float q10 = g8 < G ? pw[(2 * q4 + 8) * 9 + g8] : 0.f, q11 = g8 < G ? pw[(2 * q4 + 9) * 9 + g8] : 0.f;
+            __syncwarp();
+            uint32_t bh0, bl0, bh1, bl1;
+            split_bf16x2(q00, q01, bh0, bl0);
+            split_bf16x2(q10, q11, bh1, bl1);
+            const uint8_t* vb = ring.wait(cv);
+            if (!vb) return false;
+            const int mi = lane >> 3, prow = t0 + ((mi & 2) ? 8 : 0) + (lane & 7);  // this lane's V row
+            const uint8_t* vrow = vb + prow * dh * 2;
+            const int csw = swz ? (lane & 7) : 0;                                  // prow % 8 == lane % 8
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                if (mt < nks) {
+                    const uint4 a = ldsm_x4_trans(vrow + ((2 * mt + (mi & 1)) ^ csw) * 16);  // V^T: dims x positions
+                    mma_bf16_16816(o[mt], a, bh0, bh1);
+                    mma_bf16_16816(o[mt], a, bl0, bl1);
                 }
             }
+        } else {
+            if (!ring.wait(cv)) return false;
         }
-        ET_PHASE(tcomp)
-        bar_sync(1, kConsumers);  // sc / st are reused by the next block
-        ET_PHASE(tb)
-        if (ctid == Ring::owner(cv) * 32) ring.release(cv);
+        bar_sync(2 + half, 128);  // the block's four warps are done with its K and V stages
+        if ((ctid & 127) == 0) {
+            ring.release(ck);
+            ring.release(cv);
+        }
     }
-#undef ET_PHASE
-    if (tdbg) {  // reported through the trace pad (ring.stall: waits, busy: barriers, xwait: compute)
-        ring.stall += tw;
-        ring.busy += tb;
-        ring.xwait += tcomp;
-    }
+    // this warp's partial: sub-split c * 8 + warp
     float* part = reinterpret_cast<float*>(op.p[3]);
-    if (warp < nks) {  // o: O^T (d0, h0) (d0, h0+1) (d0+8, h0) (d0+8, h0+1)
-        const int d0 = 16 * warp + g8, h0 = 2 * q4;
+    const int sub = c * 8 + warp;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+        if (mt < nks) {
+            const int d0 = 16 * mt + g8;
+            if (h0 < G) {
+                float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + sub) * (dh + 2);
+                pr[2 + d0] = o[mt][0];
+                pr[10 + d0] = o[mt][2];
+            }
+            if (h0 + 1 < G) {
+                float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + sub) * (dh + 2);
+                pr[2 + d0] = o[mt][1];
+                pr[10 + d0] = o[mt][3];
+            }
+        }
+    }
+    if (g8 == 0) {  // lanes 0..3: (m, l) of heads h0, h0+1
         if (h0 < G) {
-            float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + c) * (dh + 2);
-            pr[2 + d0] = o[0];
-            pr[10 + d0] = o[2];
+            float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + sub) * (dh + 2);
+            pr[0] = m0;
+            pr[1] = l0;
         }
         if (h0 + 1 < G) {
-            float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + c) * (dh + 2);
-            pr[2 + d0] = o[1];
-            pr[10 + d0] = o[3];
+            float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + sub) * (dh + 2);
+            pr[0] = m1;
+            pr[1] = l1;
         }
-    }
-    if (ctid < G) {
-        float* pr = part + ((static_cast<long long>(gi) * G + ctid) * maxs + c) * (dh + 2);
-        pr[0] = st[4 * ctid];
-        pr[1] = st[4 * ctid + 1];
     }
     return true;
 }
@@ -1243,7 +1238,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
 template <bool kQK>
 __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const SlotView& si, float* scratch, int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
-    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = op.i[5];
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = attn_part_stride(op);
     const long long s = P.binding[op.i[4]];
     const int nspl = attn_splits_with_data(op, P.binding);
     const int g = si.coord[0];

@@ -292,9 +292,12 @@ __device__ __forceinline__ void attn_coord(const et_op& op, const int* coord, co
         *c = coord[1];
     }
 }
+// flags bit 9: every split leaves 8 partials (one per consumer warp, tensor-core
+// split body), so the partials buffer holds 8 x i5 per group and the merge folds 8 x splits.
 __device__ __forceinline__ int attn_splits_with_data(const et_op& op, const long long* binding) {
-    return attn_tasks(op, binding);  // empty splits leave a neutral partial (m = -inf, l = 0)
+    return attn_tasks(op, binding) * ((op.flags & 512) ? 8 : 1);  // empty splits leave (m = -inf, l = 0)
 }
+__device__ __forceinline__ int attn_part_stride(const et_op& op) { return op.i[5] * ((op.flags & 512) ? 8 : 1); }
 __device__ __forceinline__ AttnBlocks attn_blocks(const et_op& op, int c, const long long* binding) {
     const int s = static_cast<int>(binding[op.i[4]]), CH = op.i[2];
     const int nb = (s + CH - 1) / CH;

@@ -311,6 +311,8 @@ class MoEDecodeModel:
         from .decode import attn_split_cap
 
         self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
+        if max_batch > 8:  # tensor-core attention: 8 warp partials per split (batch.py)
+            self.max_splits = max(1, self.max_splits // 4)
         self.scheduler = scheduler
         t0 = time.perf_counter()
         from .decode import balanced_tasks
@@ -377,7 +379,8 @@ class MoEDecodeModel:
         self.h = torch.zeros(b, cfg.hidden, dtype=torch.float32, device=dev)
         self.qkv = torch.zeros(b, cfg.q_rows + 2 * cfg.kv_rows, dtype=torch.float32, device=dev)
         self.attn = torch.zeros(b, cfg.q_rows, dtype=torch.bfloat16, device=dev)
-        self.partials = torch.zeros(b * cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        self.partials = torch.zeros(b * cfg.heads, (8 if self.tc else 1) * self.max_splits, cfg.head_dim + 2,
+                                    dtype=torch.float32, device=dev)  # tensor-core variant: a partial per warp
         self.logits_r = torch.zeros(cfg.layers, b, E, dtype=torch.float32, device=dev)   # router logits per layer
         self.xn = torch.zeros(cfg.layers, b, cfg.hidden, dtype=torch.bfloat16, device=dev)
         self.wslot = torch.zeros(cfg.layers, b * K, dtype=torch.float32, device=dev)
@@ -438,7 +441,7 @@ class MoEDecodeModel:
             ops.append(make_op(OP_ATTN_SPLIT,
                                i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
                                   cfg.kv_heads * self.capacity * dh, kp, bs, self.tc_tasks["attn_budget"]],
-                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 128 | 256,
+                               f=[1.0 / math.sqrt(dh), cfg.eps], flags=1 | 2 | 32 | 128 | 256 | 512,
                                p=[ptr(self.qkv), ptr(self.kcache[l]), ptr(self.vcache[l]), ptr(self.partials),
                                   ptr(self.attn_tc), ptr(self.arrive_attn[l]), ptr(L["k_norm"]), ptr(self.inv_freq),
                                   ptr(self.qkv) + 4 * nq, ptr(L["q_norm"])]))
