@@ -191,9 +191,9 @@ class BatchDecodeModel:
                                       ("gateup", I, H, False, 2), ("down", H, I, True, 1),
                                       ("lm", cfg.vocab, H, False, 1)):
             self.tasks[name], self.splits[name] = tc_tasks(n // 128, w, add, nseg, npad, k // kp)
-        # attention splits per (sequence, kv head): a quarter of the batch-1 cap -- every
-        # split already runs 8 warps on separate tiles and leaves 8 partials to merge
-        self.max_splits = max(1, attn_split_cap(cfg, self.samples[-1], self.num_workers) // 4)
+        # attention splits per (sequence, kv head): half the batch-1 cap -- a split runs its
+        # blocks two at a time (warps 0-3 / 4-7), so it should own at least two
+        self.max_splits = max(1, attn_split_cap(cfg, self.samples[-1], self.num_workers) // 2)
         self.scheduler = scheduler
         t0 = time.perf_counter()
         self.attn_budget = attn_budget(cfg, self.num_workers)
@@ -220,8 +220,8 @@ class BatchDecodeModel:
         self.qkv = torch.zeros(B, rows, dtype=torch.float32, device=dev)        # raw projections (split-K adds)
         self.attn = torch.zeros(npad * nq, dtype=torch.bfloat16, device=dev)    # attention out (operand layout)
         self.act = torch.zeros(npad * I, dtype=torch.bfloat16, device=dev)      # silu(gate)*up (operand layout)
-        # 8 partials per split (one per consumer warp: attention flags bit 9)
-        self.partials = torch.zeros(B * cfg.heads, 8 * self.max_splits, cfg.head_dim + 2, dtype=torch.float32,
+        # split stride max(splits, 8): a lone split leaves its 8 warp partials (flags bit 9)
+        self.partials = torch.zeros(B * cfg.heads, max(8, self.max_splits), cfg.head_dim + 2, dtype=torch.float32,
                                     device=dev)
         self.arrive = torch.zeros(cfg.layers, B * cfg.kv_heads, dtype=torch.int32, device=dev)
         self.logits = torch.zeros(B, cfg.vocab, dtype=torch.float32, device=dev)
@@ -272,7 +272,7 @@ class BatchDecodeModel:
             ops.append(tc(rows, H, 1, EPI_ADD, L["wqkv"], None, self.xn, self.qkv, sp["qkv"]))
             # flags: 1 q/k fused mode, 2 fused merge, 32 zero the raw q/k/v after use, 64 RoPE only,
             # 128 flat batch-dependent grid, 256 chunk-swizzled cache rows (cache_swizzle),
-            # 512 one partial per consumer warp
+            # 512 a lone split leaves its 8 warp partials to the merge
             ops.append(make_op(OP_ATTN_SPLIT,
                                i=[dh, G, CH, self.capacity, 0, self.max_splits, cfg.kv_heads, rows,
                                   cfg.kv_heads * self.capacity * dh, kp, bs, self.attn_budget],

@@ -882,8 +882,9 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
 // running max / sum by shuffles over the tile's 16 positions, P^T transposed
 // through a per-warp scratch, then O^T += V^T P^T for every 16-dim tile of the
 // head (V^T by ldmatrix.trans, P split hi + lo).  The four warps of a block meet
-// on a named barrier only to release its two ring stages.  Each warp leaves its own
-// partial (split c, sub-split w: flags bit 9), folded by the group merge.
+// on a named barrier only to release its two ring stages.  At the end the 8 warp
+// partials are folded in shared memory into the split's partial (or, with flags
+// bit 9 and a single split, left as 8 sub-splits for the group merge).
 // G <= 8, dh % 16 == 0, dh <= 128, CH == 64 (checked on the host).
 __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& op, int gi, int c, const AttnBlocks ab,
                                             long long s, const float* qs, int qstride, float* sc, float* st, Ring& ring,
@@ -999,6 +1000,61 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
             ring.release(ck);
             ring.release(cv);
         }
+    }
+    if (!attn_warp_partials(op, P.binding)) {
+        // fold the 8 warps' partials in shared memory: M = max_w m_w, L = sum_w l_w e^(m_w - M),
+        // O = sum_w e^(m_w - M) O_w (red.shared.add), one partial per split
+        bar_sync(1, kConsumers);  // every warp is past its P scratch
+        float* mW = sc;           // [8 warps][8 heads]
+        float* lW = sc + 64;
+        float* oacc = sc + 128;   // [G][dh]
+        if (g8 == 0) {
+            mW[warp * 8 + h0] = m0;
+            mW[warp * 8 + h0 + 1] = m1;
+            lW[warp * 8 + h0] = l0;
+            lW[warp * 8 + h0 + 1] = l1;
+        }
+        for (int i = ctid; i < G * dh; i += kConsumers) oacc[i] = 0.f;
+        bar_sync(1, kConsumers);
+        float M0 = -INFINITY, M1 = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) {
+            M0 = fmaxf(M0, mW[w * 8 + h0]);
+            M1 = fmaxf(M1, mW[w * 8 + h0 + 1]);
+        }
+        const float f0 = m0 == -INFINITY ? 0.f : __expf(m0 - M0), f1 = m1 == -INFINITY ? 0.f : __expf(m1 - M1);
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            if (mt < nks) {
+                const int d0 = 16 * mt + g8;
+                if (h0 < G) {
+                    atomicAdd(&oacc[h0 * dh + d0], o[mt][0] * f0);
+                    atomicAdd(&oacc[h0 * dh + d0 + 8], o[mt][2] * f0);
+                }
+                if (h0 + 1 < G) {
+                    atomicAdd(&oacc[(h0 + 1) * dh + d0], o[mt][1] * f1);
+                    atomicAdd(&oacc[(h0 + 1) * dh + d0 + 8], o[mt][3] * f1);
+                }
+            }
+        }
+        bar_sync(1, kConsumers);
+        float* part = reinterpret_cast<float*>(op.p[3]);
+        for (int i = ctid; i < G * dh; i += kConsumers) {
+            const int h = i / dh, d = i - h * dh;
+            part[((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + 2) + 2 + d] = oacc[i];
+        }
+        if (ctid < G) {
+            float M = -INFINITY, L = 0.f;
+            for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, mW[w * 8 + ctid]);
+            for (int w = 0; w < kConsumerWarps; ++w) {
+                const float mw = mW[w * 8 + ctid];
+                if (mw != -INFINITY) L += lW[w * 8 + ctid] * __expf(mw - M);
+            }
+            float* pr = part + ((static_cast<long long>(gi) * G + ctid) * maxs + c) * (dh + 2);
+            pr[0] = M;
+            pr[1] = L;
+        }
+        return true;
     }
     // this warp's partial: sub-split c * 8 + warp
     float* part = reinterpret_cast<float*>(op.p[3]);

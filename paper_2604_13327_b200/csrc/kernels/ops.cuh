@@ -292,12 +292,19 @@ __device__ __forceinline__ void attn_coord(const et_op& op, const int* coord, co
         *c = coord[1];
     }
 }
-// flags bit 9: every split leaves 8 partials (one per consumer warp, tensor-core
-// split body), so the partials buffer holds 8 x i5 per group and the merge folds 8 x splits.
-__device__ __forceinline__ int attn_splits_with_data(const et_op& op, const long long* binding) {
-    return attn_tasks(op, binding) * ((op.flags & 512) ? 8 : 1);  // empty splits leave (m = -inf, l = 0)
+// flags bit 9 (tensor-core split body): a group with a single split leaves its 8 warp
+// partials unfolded for the merge (which folds up to 8 in registers anyway); with more
+// splits each split folds its warps in shared memory.  The partials' split stride is
+// then max(i5, 8).
+__device__ __forceinline__ bool attn_warp_partials(const et_op& op, const long long* binding) {
+    return (op.flags & 512) && attn_tasks(op, binding) <= 1;
 }
-__device__ __forceinline__ int attn_part_stride(const et_op& op) { return op.i[5] * ((op.flags & 512) ? 8 : 1); }
+__device__ __forceinline__ int attn_splits_with_data(const et_op& op, const long long* binding) {
+    return attn_warp_partials(op, binding) ? 8 : attn_tasks(op, binding);  // empty splits: (m = -inf, l = 0)
+}
+__device__ __forceinline__ int attn_part_stride(const et_op& op) {
+    return (op.flags & 512) && op.i[5] < 8 ? 8 : op.i[5];
+}
 __device__ __forceinline__ AttnBlocks attn_blocks(const et_op& op, int c, const long long* binding) {
     const int s = static_cast<int>(binding[op.i[4]]), CH = op.i[2];
     const int nb = (s + CH - 1) / CH;

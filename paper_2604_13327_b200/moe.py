@@ -311,8 +311,8 @@ class MoEDecodeModel:
         from .decode import attn_split_cap
 
         self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
-        if max_batch > 8:  # tensor-core attention: 8 warp partials per split (batch.py)
-            self.max_splits = max(1, self.max_splits // 4)
+        if max_batch > 8:  # tensor-core attention: a split runs two blocks at a time (batch.py)
+            self.max_splits = max(1, self.max_splits // 2)
         self.scheduler = scheduler
         t0 = time.perf_counter()
         from .decode import balanced_tasks
@@ -379,8 +379,8 @@ class MoEDecodeModel:
         self.h = torch.zeros(b, cfg.hidden, dtype=torch.float32, device=dev)
         self.qkv = torch.zeros(b, cfg.q_rows + 2 * cfg.kv_rows, dtype=torch.float32, device=dev)
         self.attn = torch.zeros(b, cfg.q_rows, dtype=torch.bfloat16, device=dev)
-        self.partials = torch.zeros(b * cfg.heads, (8 if self.tc else 1) * self.max_splits, cfg.head_dim + 2,
-                                    dtype=torch.float32, device=dev)  # tensor-core variant: a partial per warp
+        self.partials = torch.zeros(b * cfg.heads, max(8, self.max_splits) if self.tc else self.max_splits,
+                                    cfg.head_dim + 2, dtype=torch.float32, device=dev)
         self.logits_r = torch.zeros(cfg.layers, b, E, dtype=torch.float32, device=dev)   # router logits per layer
         self.xn = torch.zeros(cfg.layers, b, cfg.hidden, dtype=torch.bfloat16, device=dev)
         self.wslot = torch.zeros(cfg.layers, b * K, dtype=torch.float32, device=dev)
