@@ -75,3 +75,56 @@ def test_qwen3_moe_shape_two_layers(scheduler):
     mg = m.kernel.graph.instantiate({"s": s}, routing=m.realization())
     assert mg.check(m.executor.trace()) == []
     assert m.last_stats["tasks_executed"] == mg.num_tasks
+
+
+@pytest.mark.parametrize("b,s", [(9, 1024), (64, 333)])
+def test_llama8b_shape_batched_tensor_core(b, s):
+    """The tensor-core batch path at the real shapes (2 layers): 128-row blocks of the
+    6144 / 4096 / 2x14336 / 128256-row projections, K = 14336 pieces, split-K adds,
+    flat batch-dependent attention grid; sequences 0 and b-1 against the oracle."""
+    from paper_2604_13327_b200.batch import BatchDecodeModel, cache_swizzle
+
+    cfg = dataclasses.replace(LLAMA3_8B, name="llama3-8b-2L", layers=2)
+    m = BatchDecodeModel(cfg, samples=(1024,), max_batch=64, seed=0, record_trace=True, keep_logical=True)
+    m.fill_cache(s, seed=1)
+    toks = [(101 * i + 7) % cfg.vocab for i in range(b)]
+    m.set_token(toks)
+    kc = [cache_swizzle(k).cpu() for k in m.kcache]
+    vc = [cache_swizzle(v).cpu() for v in m.vcache]
+    logits = m.step(s, b).cpu()
+    Wc = weights_to_cpu(m.W_logical)
+    for t in (0, b - 1):
+        ref, _, _ = decode_step(cfg, Wc, [k[t] for k in kc], [v[t] for v in vc], toks[t], s, m.inv_freq.cpu())
+        _check(logits[t], ref)
+    assert m.graph.instantiate({"s": s, "b": b}).check(m.executor.trace()) == []
+
+
+@pytest.mark.parametrize("scheduler", ["static", "dynamic"])
+def test_qwen3_moe_shape_batch32_tensor_core(scheduler):
+    """Qwen3-MoE shape (2 layers) at batch 32 on the tensor-core variant: per-token
+    routing bit-exact against the CPU top-k of the device logits, two sequences'
+    logits against the oracle."""
+    from paper_2604_13327_b200.batch import cache_swizzle
+
+    cfg = dataclasses.replace(QWEN3_30B_A3B, name="qwen3-moe-2L", layers=2)
+    b, s = 32, 200
+    m = MoEDecodeModel(cfg, samples=(256,), seed=0, scheduler=scheduler, keep_logical=True, max_batch=32,
+                       batch_samples=(32,))
+    m.fill_cache(s, seed=1)
+    toks = [(977 * i + 5) % cfg.vocab for i in range(b)]
+    m.set_token(toks)
+    kc = [cache_swizzle(k).cpu() for k in m.kcache]
+    vc = [cache_swizzle(v).cpu() for v in m.vcache]
+    logits = m.step(s, b).cpu()
+    for l in range(cfg.layers):
+        r = m.routing(l, b)
+        want = []
+        for t in range(b):
+            want += topk_ref(m.logits_r[l, t].cpu().tolist(), cfg.top_k)
+        assert r["topk"] == want
+    Wc = weights_to_cpu(m.W_logical)
+    for t in (0, b - 1):
+        routing = [m.routing(l, b)["topk"][t * cfg.top_k:(t + 1) * cfg.top_k] for l in range(cfg.layers)]
+        ref, _, _ = moe_decode_step(cfg, Wc, [k[t] for k in kc], [v[t] for v in vc], toks[t], s, m.inv_freq.cpu(),
+                                    routing=routing)
+        _check(logits[t], ref)
