@@ -773,15 +773,17 @@ __device__ __noinline__ void qk_norm_rope(float* v, int dh, const float* w, floa
 // use, so a pass costs one L2 round trip.
 // kWide: G * dh <= 1024 (MoE instantiation: 8 q heads per kv head), else G * dh
 // <= 512 -- the register footprint of the dense kernel stays spill-free.
-template <bool kWide>
+// kTcLayout (tensor-core instantiations): operand-layout output (i9) and swizzled cache rows.
+template <bool kWide, bool kTcLayout = false>
 __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op& op, int gi, const float* qs,
                                               int qstride, float* scr, int ctid) {
     constexpr int kPass = kWide ? 8 : 16, kOut = kWide ? 4 : 2;  // splits in registers; outputs per thread
     const int warp = ctid >> 5, lane = ctid & 31;
-    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], maxs = attn_part_stride(op), kvh = op.i[6];
+    const int dh = op.i[0], G = op.i[1], CH = op.i[2], cap = op.i[3], kvh = op.i[6];
+    const int maxs = kTcLayout ? attn_part_stride(op) : op.i[5];
     const int g = gi % kvh, bq = gi / kvh;  // kv head, sequence of the batch
     const long long s = P.binding[op.i[4]];
-    const int nspl = attn_splits_with_data(op, P.binding);
+    const int nspl = kTcLayout ? attn_splits_with_data(op, P.binding) : attn_splits_base(op, P.binding);
     const float scale = op.f[0];
     const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(gi) * G * maxs * (dh + 2);
     const long long cb = static_cast<long long>(bq) * op.i[8];  // this sequence's cache
@@ -789,7 +791,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + cb + (static_cast<long long>(g) * cap + s) * dh;
     // i9 > 0 (tensor-core instantiation): the output goes to the operand layout of the
     // next GEMV (piece length i9, batch from symbol slot i10)
-    const int kxb = kWide ? op.i[9] : 0;
+    const int kxb = kTcLayout ? op.i[9] : 0;
     const int xnp = kxb ? tc_npad(op.i[10] >= 0 ? static_cast<int>(P.binding[op.i[10]]) : 1) : 0;
     uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) +
                     (kxb ? 0 : static_cast<long long>(bq) * kvh * G * dh + static_cast<long long>(g) * G * dh);
@@ -799,7 +801,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     float* kns = hs + G;                // [dh]
     // flags bit 8 (tensor-core instantiations): cache rows hold their 16-byte chunks
     // XOR-swizzled by position % 8, so row-strided tensor-core reads are bank-conflict free
-    const int csw = (kWide && (op.flags & 256)) ? static_cast<int>(s & 7) : 0;
+    const int csw = (kTcLayout && (op.flags & 256)) ? static_cast<int>(s & 7) : 0;
     float ov[kOut][kPass];
     float vv[kOut];
 #pragma unroll
@@ -1282,7 +1284,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         bar_sync(1, kConsumers);
         if (*flag) {
             if ((P.debug & 16) && ctid == 0) ring.stall = globaltimer() - *t_split;  // arrival round trip
-            attn_merge_group<kQK>(P, op, gi, qs, qstride, st + 4 * G + 4, ctid);
+            attn_merge_group<kQK, kMMA>(P, op, gi, qs, qstride, st + 4 * G + 4, ctid);
         }
     }
 }
@@ -1386,7 +1388,7 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
 // eoff and elist for the expert call).  Everything is written before this
 // task's NOTIFY (release), and the dynamic scheduler reveals the counts when
 // the whole writer call has finished (ref simulate.cpp:632-649).
-__device__ __noinline__ void body_moe_route(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
+__device__ __forceinline__ void body_moe_route_impl(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs, float* acc,
                                float* red, Ring& ring, int ctid, uint64_t* t_pro) {
     // flags bit 1: the router logits were accumulated by a tensor-core GEMV (large batch)
     // into p1 (fp32 [b][E], split-K adds): one route task copies them to p4 and zeroes p1
@@ -1552,6 +1554,20 @@ __device__ __noinline__ void body_moe_route(const StaticParams& P, const et_op& 
             }
         }
     }
+}
+
+// Inlined into the MoE kernels (its registers are free there); out of line in the
+// MoE + tensor-core kernels, whose other bodies already fill the register budget.
+template <bool kOutOfLine>
+__device__ __forceinline__ void body_moe_route(const StaticParams& P, const et_op& op, const SlotView& si, uint16_t* xs,
+                                               float* acc, float* red, Ring& ring, int ctid, uint64_t* t_pro) {
+    body_moe_route_impl(P, op, si, xs, acc, red, ring, ctid, t_pro);
+}
+template <>
+__device__ __noinline__ void body_moe_route<true>(const StaticParams& P, const et_op& op, const SlotView& si,
+                                                  uint16_t* xs, float* acc, float* red, Ring& ring, int ctid,
+                                                  uint64_t* t_pro) {
+    body_moe_route_impl(P, op, si, xs, acc, red, ring, ctid, t_pro);
 }
 
 // Routed expert task (see expert_task): gate/up rows of its row split for the
@@ -1788,7 +1804,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_ALLREDUCE: body_allreduce(P, op, v, ctid, worker); break;
                 case ET_OP_MOE_ROUTE:
-                    if constexpr (kMoE) body_moe_route(P, op, v, xs, acc, red, ring, ctid, &t_pro);
+                    if constexpr (kMoE) body_moe_route<kTC>(P, op, v, xs, acc, red, ring, ctid, &t_pro);
                     break;
                 case ET_OP_MOE_EXPERT:
                     if constexpr (kMoE) t_pro = body_moe_expert(P, op, v, xs, acc, ring, ctid);
@@ -2561,7 +2577,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_MOE_ROUTE:
-                    if constexpr (kMoE) body_moe_route(P, op, v, xs, acc, red, ring, ctid, &tp);
+                    if constexpr (kMoE) body_moe_route<kTC>(P, op, v, xs, acc, red, ring, ctid, &tp);
                     break;
                 case ET_OP_MOE_EXPERT:
                     if constexpr (kMoE) tp = body_moe_expert(P, op, v, xs, acc, ring, ctid);

@@ -264,6 +264,13 @@ struct AttnBlocks {
     int nblk;      // blocks (the last one may be partial)
 };
 
+// Splits without a batch budget (the mma.sync instantiations' attention).
+__device__ __forceinline__ int attn_splits_base(const et_op& op, const long long* binding) {
+    const int s = static_cast<int>(binding[op.i[4]]), CH = op.i[2], cap = op.i[5];
+    const int nb = (s + CH - 1) / CH;
+    return nb < cap ? nb : cap;
+}
+
 // Splits of one (sequence, kv head) group: one per CH-position block, at most i5 (the
 // partials' split dimension) and, with a per-step budget i11 > 0, at most
 // max(1, i11 / b) (b from symbol slot i10): large batches get fewer, longer splits.

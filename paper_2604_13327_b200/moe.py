@@ -288,7 +288,7 @@ class MoEDecodeModel:
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
                  scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=True,
                  balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False, qkv_split=True,
-                 max_batch=1, batch_samples=None):
+                 max_batch=1, batch_samples=None, attn_cap=None):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
@@ -310,8 +310,8 @@ class MoEDecodeModel:
         self.capacity = self.samples[-1] + 1
         from .decode import attn_split_cap
 
-        self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
-        if max_batch > 8:  # tensor-core attention: a split runs two blocks at a time (batch.py)
+        self.max_splits = attn_cap or attn_split_cap(cfg, self.samples[-1], self.num_workers)
+        if max_batch > 8 and not attn_cap:  # tensor-core attention: a split runs two blocks at a time (batch.py)
             self.max_splits = max(1, self.max_splits // 2)
         self.scheduler = scheduler
         t0 = time.perf_counter()

@@ -30,13 +30,15 @@ def main():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--schedulers", nargs="+", default=["static", "dynamic", "dynamic-early"])
     ap.add_argument("--batch", type=int, nargs="+", default=[1])
+    ap.add_argument("--attn-cap", type=int, default=None, help="attention splits per (sequence, kv head)")
     args = ap.parse_args()
     if len(args.schedulers) > 1:  # one process per scheduler
         import subprocess
         for sched in args.schedulers:
             subprocess.run([sys.executable, __file__, "--config", args.config, "--steps", str(args.steps), "--warmup",
                             str(args.warmup), "--seq", str(args.seq), "--schedulers", sched, "--batch",
-                            *map(str, args.batch)], check=False)
+                            *map(str, args.batch)] + (["--attn-cap", str(args.attn_cap)] if args.attn_cap else []),
+                           check=False)
         return
     cfg = MOE_CONFIGS[args.config]
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -50,7 +52,8 @@ def main():
         t1 = time.perf_counter()
         m = MoEDecodeModel(cfg, samples=(args.seq,), weights=W, scheduler=sched.split("-")[0],
                            early_push=sched.endswith("early"), max_batch=mb,
-                           batch_samples=tuple(sorted(set(args.batch) | {1, mb})) if mb > 1 else None)
+                           batch_samples=tuple(sorted(set(args.batch) | {1, mb})) if mb > 1 else None,
+                           attn_cap=args.attn_cap)
         m.fill_cache(args.seq, seed=1)
         m.set_token([1 + 7 * i for i in range(mb)])
         stream = torch.cuda.Stream()
