@@ -1105,8 +1105,8 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     const int warp = ctid >> 5, lane = ctid & 31;
     const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5], kvh = op.i[6];
     const long long s = P.binding[op.i[4]];
-    int gi, c;  // gi = sequence * kv_heads + kv head, c = split
-    attn_coord(op, si.coord, P.binding, &gi, &c);
+    int gi = si.coord[0], c = si.coord[1];  // gi = sequence * kv_heads + kv head, c = split
+    if constexpr (kMMA) attn_coord(op, si.coord, P.binding, &gi, &c);  // flat batch-dependent grid
     const int g = gi % kvh, bq = gi / kvh;
     const long long rb = static_cast<long long>(bq) * op.i[7];  // this sequence's q / projection row
     const AttnBlocks ab = attn_blocks(op, c, P.binding);
@@ -1276,7 +1276,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             int* arrive = reinterpret_cast<int*>(op.p[5]) + gi;
             // release: this split's partial (CTA writes ordered by the bar above) before
             // the arrival; acquire: the other splits' partials after it
-            const int ntask = attn_tasks(op, P.binding);  // grid max(splits, 1)
+            const int ntask = kMMA ? attn_tasks(op, P.binding) : attn_splits_base(op, P.binding);  // max(splits, 1)
             const bool last = atom_add_acq_rel(arrive, 1) == (ntask > 0 ? ntask : 1) - 1;
             if (last) *reinterpret_cast<volatile int*>(arrive) = 0;  // every split of this step arrived
             *flag = last ? 1 : 0;
