@@ -24,7 +24,7 @@ def model(request):
                             scheduler=request.param, keep_logical=True, record_trace=True)
 
 
-@pytest.mark.parametrize("b,s", [(1, 16), (5, 40), (17, 96), (64, 7)])
+@pytest.mark.parametrize("b,s", [(1, 16), (5, 40), (17, 96), (64, 7), (1, 0), (33, 96), (48, 1)])
 def test_batch_logits_vs_oracle(model, b, s):
     m, cfg = model, model.cfg
     m.fill_cache(s, seed=b)
