@@ -854,8 +854,18 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
             if (c < nspl) o = fmaf(w[c], ov[j][c], o);
             if (c + 1 < nspl) o2 = fmaf(w[c + 1], ov[j][c + 1], o2);
         }
-        for (int c = kPass; c < nspl; ++c)  // long contexts: the remaining splits
-            o = fmaf(w[c], __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d), o);
+        // long contexts: the remaining splits, their loads batched eight at a time (one L2
+        // round trip per batch instead of per split)
+        for (int c0 = kPass; c0 < nspl; c0 += 8) {
+            float pv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                pv[u] = c0 + u < nspl ? __ldcg(part + (static_cast<long long>(hh) * maxs + c0 + u) * (dh + 2) + 2 + d)
+                                      : 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (c0 + u < nspl) o = fmaf(w[c0 + u], pv[u], o);
+        }
         out[kxb ? xb_offset(bq, g * G * dh + idx, xnp, kxb) : idx] = f2bf(o + o2);
     }
     if constexpr (kWide) {
