@@ -610,15 +610,20 @@ __device__ __noinline__ void tc_issue(uint8_t* smem, uint32_t tmem, unsigned lon
                 }
                 tc_fence_after();
                 const uint64_t a = umma_desc(ring0 + st * kStageBytes);
+                if (elect_one_sync()) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    umma_bf16(d, a + j * 256, xk + j * xstep, idesc, (p != k || ch != 0 || j != 0) ? 1u : 0u);
-                umma_commit(&empty[st]);
+                    for (int j = 0; j < 4; ++j)
+                        umma_bf16(d, a + j * 256, xk + j * xstep, idesc, (p != k || ch != 0 || j != 0) ? 1u : 0u);
+                    umma_commit(&empty[st]);
+                }
+                __syncwarp();
             }
         }
-        umma_commit(&bars[kTcXSlots + xb]);  // the x slot is free once these MMAs complete
+        if (elect_one_sync()) umma_commit(&bars[kTcXSlots + xb]);  // the x slot is free once these MMAs complete
+        __syncwarp();
     }
-    umma_commit(&bars[2 * kTcXSlots]);  // one of the kTcIssuers arrivals on the done barrier
+    if (elect_one_sync()) umma_commit(&bars[2 * kTcXSlots]);  // one of the kTcIssuers arrivals on the done barrier
+    __syncwarp();
 }
 
 __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op& op, const SlotView& si, uint8_t* smem,
@@ -645,7 +650,7 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
     nis = nis < nxs ? nis : nxs;
     nis = nis > 1 ? nis : 1;
     const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
-    if (lane == 0 && warp < kTcIssuers) {  // the rest of each issuer warp parks on the closing barrier
+    if (warp < kTcIssuers) {  // whole issuer warps (converged: uniform operands), one elected lane issues
         unsigned long long xw[2] = {0, 0};  // debug: ns waiting for activation pieces / ring stages
         tc_issue(smem, ts.tmem + static_cast<uint32_t>(warp * cols), ring.seq, ts.xp, warp, nis, warp < nis ? sp.np : 0,
                  nseg * sp.nblk, cpb, npad, kp, ring.dbg ? xw : nullptr, P.status, P.watchdog_ns, ring.worker);

@@ -336,4 +336,12 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
     lo = static_cast<uint32_t>(f2bf(a - bf2f(ha))) | (static_cast<uint32_t>(f2bf(b - bf2f(hb))) << 16);
 }
 
+// One elected lane of a converged warp (the tcgen05 issue idiom: operands stay
+// warp-uniform, so they live in uniform registers).
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, %1;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "+r"(pred) : "r"(0xffffffffu));
+    return pred != 0;
+}
+
 }  // namespace etk
