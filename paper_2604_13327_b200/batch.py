@@ -164,7 +164,8 @@ class BatchDecodeModel:
     largest sample on one lowered artifact; projections on tcgen05 tensor cores."""
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), max_batch=64, batch_samples=None,
-                 num_workers=None, seed=0, weights=None, scheduler="static", record_trace=False, keep_logical=False):
+                 num_workers=None, seed=0, weights=None, scheduler="static", record_trace=False, keep_logical=False,
+                 kp=None):
         if not etsim.gpu_available():
             raise RuntimeError("BatchDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         assert 1 <= max_batch <= 128
@@ -179,7 +180,8 @@ class BatchDecodeModel:
         self.batch_samples = sorted(set(batch_samples or default) | {max_batch})
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
-        self.kp = kp = tc_piece_for(max_batch, (cfg.hidden, cfg.q_rows, cfg.intermediate))
+        # piece length (input columns per activation piece); kp overrides (multiple of 64)
+        self.kp = kp = kp or tc_piece_for(max_batch, (cfg.hidden, cfg.q_rows, cfg.intermediate))
         npad = tc_npad(max_batch)
         H, I, nq, nkv = cfg.hidden, cfg.intermediate, cfg.q_rows, cfg.kv_rows
         rows = nq + 2 * nkv

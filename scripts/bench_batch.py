@@ -29,13 +29,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scheduler", default="static")
+    ap.add_argument("--kp", type=int, default=None, help="activation piece length (default: fill 16 KB)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))["hbm_gbs"]
     mb = args.max_batch or max(args.batch)
     t0 = time.perf_counter()
-    m = BatchDecodeModel(cfg, samples=tuple(sorted(set(args.seq))), max_batch=mb, scheduler=args.scheduler)
+    m = BatchDecodeModel(cfg, samples=tuple(sorted(set(args.seq))), max_batch=mb, scheduler=args.scheduler,
+                         kp=args.kp)
     setup = time.perf_counter() - t0
     stream = torch.cuda.Stream()
     for s in args.seq:
@@ -63,7 +65,7 @@ def main():
             nbytes = cfg.step_bytes(s, b)
             ach = nbytes / (ms * 1e-3) / 1e9
             print(json.dumps({"workload": f"{cfg.name} decode bs={b} seq {s}", "scheduler": args.scheduler,
-                              "path": "tcgen05 GEMV", "batch": b, "seq": s, "max_batch": mb,
+                              "path": "tcgen05 GEMV", "kp": m.kp, "batch": b, "seq": s, "max_batch": mb,
                               "us_per_step": ms * 1e3, "tokens_per_s": b / (ms * 1e-3), "bytes_per_step": nbytes,
                               "achieved_gbs": ach, "frac_of_measured_hbm": ach / peak,
                               "tasks_executed": st["tasks_executed"], "first_step_s": first,
