@@ -95,24 +95,25 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
 
 
-def cpu_reference_step_us(cfg, seq, budget_s=12.0):
-    """The reference's own CPU path for this step, timed on this host.
+def cpu_reference_steps_us(cfg, seq, steps=5, budget_s=12.0):
+    """The reference's own CPU path for this step, timed on this host, `steps` samples.
 
+    Per sample:
     (1) the reference executor (etsim, built from its sources into oracle/_ref)
-        running the static schedule of the same Llama-3-8B decode graph;
+        running the static schedule of the same Llama-3-8B decode graph (one
+        `simulate` call, 1 thread);
     (2) the numerics of the step (the reference has none): the CPU
         fp32 oracle on layer 0, scaled by the layer count, plus lm_head.
-    Returns (us_per_token, detail dict)."""
+    Setup (graph lowering, weight init) happens once; each sample is ~30 ms, so
+    100 samples stay within a few seconds.  Returns (list of us_per_token, detail)."""
     import torch
 
     from paper_2604_13327_b200 import etsim
     from paper_2604_13327_b200.decode import decode_graph_spec
 
-    def etsim_graph_from_spec(spec):
-        return etsim.Graph.from_json(json.dumps(spec))
-
+    steps = max(1, steps)
     detail = {}
-    sim_us = None
+    sims = None
     # The reference module registers pybind types with the same names as this
     # framework's module, so it runs in its own interpreter.
     code = (
@@ -121,21 +122,23 @@ def cpu_reference_step_us(cfg, seq, budget_s=12.0):
         "import etsim\n"
         "g = etsim.Graph.from_json(sys.stdin.read())\n"
         f"k = etsim.lower_static(g, [{{'s': {seq}}}], num_sms=148)\n"
-        "t0 = time.perf_counter(); n = 0\n"
-        f"while time.perf_counter() - t0 < {budget_s * 0.3} or n < 2:\n"
-        f"    etsim.simulate(k, {{'s': {seq}}}); n += 1\n"
-        "print(json.dumps({'us': (time.perf_counter() - t0) / n * 1e6, 'runs': n}))\n"
+        f"etsim.simulate(k, {{'s': {seq}}})\n"
+        "ts = []\n"
+        f"for _ in range({steps}):\n"
+        "    t0 = time.perf_counter()\n"
+        f"    etsim.simulate(k, {{'s': {seq}}})\n"
+        "    ts.append((time.perf_counter() - t0) * 1e6)\n"
+        "print(json.dumps({'us': ts}))\n"
     )
     try:
         # the same decode graph DecodeModel lowers (148 workers)
-        g = etsim_graph_from_spec(decode_graph_spec(cfg, 148, seq)[0])
+        g = etsim.Graph.from_json(json.dumps(decode_graph_spec(cfg, 148, seq)[0]))
         detail["graph_tasks"] = g.instantiate({"s": seq}).num_tasks
         out = subprocess.run([sys.executable, "-c", code], input=g.to_json(),
-                             capture_output=True, text=True, timeout=budget_s * 3 + 60)
-        r = json.loads(out.stdout.strip().splitlines()[-1])
-        sim_us = r["us"]
-        detail["reference_simulate_us"] = sim_us
-        detail["reference_runs"] = r["runs"]
+                             capture_output=True, text=True, timeout=budget_s * 5 + 60)
+        sims = json.loads(out.stdout.strip().splitlines()[-1])["us"]
+        detail["reference_simulate_us"] = statistics.median(sims)
+        detail["reference_runs"] = len(sims)
     except Exception as exc:  # reference build absent on this host
         detail["reference_error"] = (str(exc) + " " + (out.stderr[-200:] if "out" in dir() else ""))[:300]
     # numerics: one layer + lm_head in fp32 on CPU
@@ -144,6 +147,7 @@ def cpu_reference_step_us(cfg, seq, budget_s=12.0):
     q_rows, kv_rows = cfg.q_rows, cfg.kv_rows
     w = lambda *s: (torch.randn(*s) * 0.02)  # noqa: E731
     wqkv, wo, wg, wu, wd = w(q_rows + 2 * kv_rows, H), w(H, q_rows), w(I, H), w(I, H), w(H, I)
+    lm = w(V, H)
     K = torch.randn(cfg.kv_heads, seq, cfg.head_dim)
     Vc = torch.randn(cfg.kv_heads, seq, cfg.head_dim)
     x = torch.randn(H)
@@ -158,23 +162,20 @@ def cpu_reference_step_us(cfg, seq, budget_s=12.0):
         return h + wd @ (torch.nn.functional.silu(wg @ h) * (wu @ h))
 
     layer()
-    t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < budget_s * 0.4 or n < 2:
-        layer()
-        n += 1
-    layer_us = (time.perf_counter() - t0) / n * 1e6
-    del wqkv, wo, wg, wu, wd
-    lm = w(V, H)
     lm @ x
-    t0 = time.perf_counter()
-    for _ in range(3):
+    vals, lay, lms = [], [], []
+    for i in range(steps):
+        t0 = time.perf_counter()
+        layer()
+        t1 = time.perf_counter()
         lm @ x
-    lm_us = (time.perf_counter() - t0) / 3 * 1e6
-    numerics_us = layer_us * cfg.layers + lm_us
-    detail.update({"numerics_layer_us": layer_us, "numerics_lm_head_us": lm_us, "numerics_us": numerics_us})
-    total = numerics_us + (sim_us or 0.0)
-    return total, detail
+        t2 = time.perf_counter()
+        lay.append((t1 - t0) * 1e6)
+        lms.append((t2 - t1) * 1e6)
+        vals.append(lay[-1] * cfg.layers + lms[-1] + (sims[i] if sims else 0.0))
+    detail.update({"numerics_layer_us": statistics.median(lay), "numerics_lm_head_us": statistics.median(lms),
+                   "numerics_us": statistics.median(lay) * cfg.layers + statistics.median(lms)})
+    return vals, detail
 
 
 def run_reference(args):
@@ -188,12 +189,10 @@ def run_reference(args):
         return
     cfg = CONFIGS[args.config]
     threads = torch.get_num_threads()
-    vals = []
-    for _ in range(args.warmup):
-        pass
-    for _ in range(max(1, args.steps)):
-        v, detail = cpu_reference_step_us(cfg, args.seq, budget_s=args.ref_budget)
-        vals.append(v)
+    # W warm-up samples, then K timed samples (each one simulate + one layer + lm_head)
+    vals, detail = cpu_reference_steps_us(cfg, args.seq, steps=args.warmup + max(1, args.steps),
+                                          budget_s=args.ref_budget)
+    vals = vals[args.warmup:]
     value = statistics.median(vals)
     kind = "reference" if "reference_simulate_us" in detail else "port"
     line = {
@@ -318,7 +317,8 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             import torch as _t
 
-            v, detail = cpu_reference_step_us(cfg, args.seq, budget_s=args.ref_budget)
+            vals, detail = cpu_reference_steps_us(cfg, args.seq, steps=8, budget_s=args.ref_budget)
+            v = statistics.median(vals)
             cpu = {"value": v, "unit": UNIT, "cores": _t.get_num_threads(),
                    "kind": "reference" if "reference_simulate_us" in detail else "port",
                    "sample": "reference etsim.simulate of the static Llama-3-8B decode schedule (1 thread) + fp32 "
