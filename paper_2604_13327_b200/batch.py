@@ -116,10 +116,10 @@ def tc_tasks(nblk, workers, splittable, nseg=1, npad=64, pieces=1):
     return groups, 1
 
 
-def attn_budget(cfg, workers):
+def attn_budget(cfg, workers, per_sm=2):
     """Per-step split budget of the batched attention: splits per (sequence, kv head)
-    <= max(1, budget // b), about two attention tasks per SM at any batch."""
-    return max(1, 2 * workers // cfg.kv_heads)
+    <= max(1, budget // b), about `per_sm` attention tasks per SM at any batch."""
+    return max(1, per_sm * workers // cfg.kv_heads)
 
 
 def attn_grid(cfg, attn_cap, budget):
@@ -165,7 +165,7 @@ class BatchDecodeModel:
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), max_batch=64, batch_samples=None,
                  num_workers=None, seed=0, weights=None, scheduler="static", record_trace=False, keep_logical=False,
-                 kp=None):
+                 kp=None, attn_tasks_per_sm=2):
         if not etsim.gpu_available():
             raise RuntimeError("BatchDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         assert 1 <= max_batch <= 128
@@ -198,7 +198,7 @@ class BatchDecodeModel:
         self.max_splits = max(1, attn_split_cap(cfg, self.samples[-1], self.num_workers) // 2)
         self.scheduler = scheduler
         t0 = time.perf_counter()
-        self.attn_budget = attn_budget(cfg, self.num_workers)
+        self.attn_budget = attn_budget(cfg, self.num_workers, attn_tasks_per_sm)
         self.spec = batch_graph_spec(cfg, self.tasks, self.max_splits, self.attn_budget)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.bindings = [{"s": s, "b": b} for s in self.samples for b in self.batch_samples]

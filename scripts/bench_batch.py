@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scheduler", default="static")
     ap.add_argument("--kp", type=int, default=None, help="activation piece length (default: fill 16 KB)")
+    ap.add_argument("--attn-per-sm", type=int, default=2, help="attention split budget: tasks per SM")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -37,7 +38,7 @@ def main():
     mb = args.max_batch or max(args.batch)
     t0 = time.perf_counter()
     m = BatchDecodeModel(cfg, samples=tuple(sorted(set(args.seq))), max_batch=mb, scheduler=args.scheduler,
-                         kp=args.kp)
+                         kp=args.kp, attn_tasks_per_sm=args.attn_per_sm)
     setup = time.perf_counter() - t0
     stream = torch.cuda.Stream()
     for s in args.seq:
