@@ -77,15 +77,16 @@ def test_qwen3_moe_shape_two_layers(scheduler):
     assert m.last_stats["tasks_executed"] == mg.num_tasks
 
 
-@pytest.mark.parametrize("b,s", [(9, 1024), (64, 333)])
-def test_llama8b_shape_batched_tensor_core(b, s):
+@pytest.mark.parametrize("b,s,scheduler", [(9, 1024, "static"), (64, 333, "static"), (24, 700, "dynamic")])
+def test_llama8b_shape_batched_tensor_core(b, s, scheduler):
     """The tensor-core batch path at the real shapes (2 layers): 128-row blocks of the
     6144 / 4096 / 2x14336 / 128256-row projections, K = 14336 pieces, split-K adds,
     flat batch-dependent attention grid; sequences 0 and b-1 against the oracle."""
     from paper_2604_13327_b200.batch import BatchDecodeModel, cache_swizzle
 
     cfg = dataclasses.replace(LLAMA3_8B, name="llama3-8b-2L", layers=2)
-    m = BatchDecodeModel(cfg, samples=(1024,), max_batch=64, seed=0, record_trace=True, keep_logical=True)
+    m = BatchDecodeModel(cfg, samples=(1024,), max_batch=64, seed=0, record_trace=True, keep_logical=True,
+                         scheduler=scheduler)
     m.fill_cache(s, seed=1)
     toks = [(101 * i + 7) % cfg.vocab for i in range(b)]
     m.set_token(toks)
