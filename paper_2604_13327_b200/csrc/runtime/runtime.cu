@@ -485,6 +485,14 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     for (int32_t c = 0; c < num_calls; ++c)
         if (ops[c].kind == ET_OP_MOE_ROUTE || ops[c].kind == ET_OP_MOE_EXPERT) rt->has_moe |= 1;
         else if (ops[c].kind == ET_OP_GEMV_TC || ops[c].kind == ET_OP_NORM) rt->has_moe |= 2;
+    if (rt->has_moe & 2)  // the tensor-core instantiation runs attention on mma.sync tiles (attn_split_mma)
+        for (int32_t c = 0; c < num_calls; ++c)
+            if (ops[c].kind == ET_OP_ATTN_SPLIT) {
+                const int dh = ops[c].i[0], G = ops[c].i[1], CH = ops[c].i[2];
+                if (G > 8 || dh % 16 != 0 || dh > 128 || CH != 64)
+                    return rt->fail(ET_ERR_INVALID, "tensor-core attention needs <= 8 q heads per kv head, head_dim "
+                                                    "a multiple of 16 up to 128 and 64-position blocks");
+            }
     rt->ops_bound = 1;
     return ET_OK;
 }
