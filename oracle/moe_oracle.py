@@ -13,7 +13,7 @@ indptr) follows ref workloads.cpp:116-150 (`moe_routing_tensors`).
 
 import torch
 
-from oracle.decoder_oracle import _bf16, rmsnorm, rotary_pairs
+from oracle.decoder_oracle import DecodeStream, _bf16, rmsnorm, rotary_pairs
 
 
 def topk_ref(logits, k):
@@ -40,47 +40,56 @@ def moe_routing_tensors(topk_flat, experts, tile, row_splits):
     return {"cnt": cnt, "ind": ind, "tind": [v * row_splits for v in ind], "eoff": eoff, "elist": elist}
 
 
+class MoEDecodeStream(DecodeStream):
+    """One Qwen3-MoE decode step of one sequence, fed layer by layer (see
+    DecodeStream).  layer() takes the layer's dense weights plus an `expert(e)`
+    accessor returning (gate [I, H], up [I, H], down [H, I]) of expert e, so only
+    the experts the step routes to need to reach host memory."""
+
+    @torch.no_grad()
+    def layer(self, L, kc, vc, expert=None, routing=None):
+        """Returns (router logits [E], selected experts, new k, new v).  routing: the
+        experts to use (the device's choice) instead of the oracle's own top-k."""
+        cfg, e, f32 = self.cfg, self.e, self.dt
+        d, nq, nkv = cfg.head_dim, cfg.heads, cfg.kv_heads
+        if expert is None:
+            def expert(ex):
+                return L["wgate"][ex], L["wup"][ex], L["wdown"][ex]
+        h = self.h
+        x = _bf16(rmsnorm(h, L["attn_norm"].to(f32), cfg.eps), e)
+        qkv = L["wqkv"].to(f32) @ x
+        q = qkv[: nq * d].view(nq, d)
+        k = qkv[nq * d: nq * d + nkv * d].view(nkv, d)
+        v = qkv[nq * d + nkv * d:].view(nkv, d)
+        q = rotary_pairs(rmsnorm(q, L["q_norm"].to(f32), cfg.eps), self.s, self.inv_freq)
+        k = _bf16(rotary_pairs(rmsnorm(k, L["k_norm"].to(f32), cfg.eps), self.s, self.inv_freq), e)
+        v = _bf16(v, e)
+        h = h + L["wo"].to(f32) @ self.attention(q, k, v, kc, vc)
+        xn = _bf16(rmsnorm(h, L["ffn_norm"].to(f32), cfg.eps), e)
+        self.last_xn = xn
+        lg = L["router"].to(f32) @ xn
+        sel = list(routing) if routing is not None else topk_ref(lg.tolist(), cfg.top_k)
+        pr = torch.softmax(lg.to(torch.float64), dim=0)
+        w = pr[sel] / pr[sel].sum()
+        for j, ex in enumerate(sel):
+            wg, wu, wd = expert(ex)
+            act = _bf16(torch.nn.functional.silu(wg.to(f32) @ xn) * (wu.to(f32) @ xn), e)
+            h = h + float(w[j]) * (wd.to(f32) @ act)
+        self.h = h
+        return lg, sel, k, v
+
+
 @torch.no_grad()
 def moe_decode_step(cfg, W, kcache, vcache, token, s, inv_freq, emulate_bf16=True, routing=None):
     """Returns (logits [vocab], per-layer router logits, per-layer topk).
 
     routing: optional list (per layer) of forced top-k expert lists (the device's
     choice), so that numerics can be compared even across a router near-tie."""
-    f32 = torch.float32
-    e = emulate_bf16
-    H, d, nq, nkv = cfg.hidden, cfg.head_dim, cfg.heads, cfg.kv_heads
-    G = nq // nkv
-    h = W["embed"][token].to(f32).clone()
+    st = MoEDecodeStream(cfg, token, s, inv_freq, emulate_bf16)
+    st.head(W["embed"][token])
     router_logits, topks = [], []
     for l, L in enumerate(W["layers"]):
-        x = _bf16(rmsnorm(h, L["attn_norm"].to(f32), cfg.eps), e)
-        qkv = L["wqkv"].to(f32) @ x
-        q = qkv[: nq * d].view(nq, d)
-        k = qkv[nq * d: nq * d + nkv * d].view(nkv, d)
-        v = qkv[nq * d + nkv * d:].view(nkv, d)
-        q = rotary_pairs(rmsnorm(q, L["q_norm"].to(f32), cfg.eps), s, inv_freq)
-        k = _bf16(rotary_pairs(rmsnorm(k, L["k_norm"].to(f32), cfg.eps), s, inv_freq), e)
-        v = _bf16(v, e)
-        K = torch.cat([kcache[l][:, :s].to(f32), k[:, None]], dim=1)
-        V = torch.cat([vcache[l][:, :s].to(f32), v[:, None]], dim=1)
-        att = torch.empty(nq, d, dtype=f32)
-        for hh in range(nq):
-            g = hh // G
-            sc = (K[g] @ q[hh]) / (d ** 0.5)
-            p = torch.softmax(sc.to(torch.float64), dim=0).to(f32)
-            att[hh] = p @ V[g]
-        h = h + L["wo"].to(f32) @ _bf16(att.reshape(-1), e)
-        xn = _bf16(rmsnorm(h, L["ffn_norm"].to(f32), cfg.eps), e)
-        lg = L["router"].to(f32) @ xn
+        lg, sel, _, _ = st.layer(L, kcache[l], vcache[l], routing=routing[l] if routing is not None else None)
         router_logits.append(lg)
-        sel = list(routing[l]) if routing is not None else topk_ref(lg.tolist(), cfg.top_k)
         topks.append(sel)
-        pr = torch.softmax(lg.to(torch.float64), dim=0)
-        w = pr[sel] / pr[sel].sum()
-        for j, ex in enumerate(sel):
-            gt = L["wgate"][ex].to(f32) @ xn
-            up = L["wup"][ex].to(f32) @ xn
-            act = _bf16(torch.nn.functional.silu(gt) * up, e)
-            h = h + float(w[j]) * (L["wdown"][ex].to(f32) @ act)
-    x = _bf16(rmsnorm(h, W["final_norm"].to(f32), cfg.eps), e)
-    return W["lm_head"].to(f32) @ x, router_logits, topks
+    return st.final(W["final_norm"], W["lm_head"]), router_logits, topks

@@ -159,6 +159,41 @@ def batch_graph_spec(cfg, tasks, attn_cap, budget):
             "device_functions": fns, "event_tensors": events, "calls": calls}
 
 
+def batch_layout(cfg, num_workers, samples, max_batch=64, batch_samples=None, kp=None, attn_tasks_per_sm=2):
+    """Every layout choice BatchDecodeModel makes before touching the device (graph
+    spec, bindings, task counts, piece length).  Device-free, so the committed
+    bench-graph fixtures are exactly the graphs the model lowers."""
+    assert 1 <= max_batch <= 128
+    L = {"max_batch": max_batch}
+    # batch samples: powers of two up to max_batch by default, so a small batch runs on a
+    # schedule at most twice its size (masked tasks still wait and notify)
+    default = [1 << i for i in range(8) if (1 << i) < max_batch]
+    L["batch_samples"] = sorted(set(batch_samples or default) | {max_batch})
+    L["samples"] = sorted(int(s) for s in samples)
+    L["capacity"] = L["samples"][-1] + 1
+    # piece length (input columns per activation piece); kp overrides (multiple of 64)
+    kp = kp or tc_piece_for(max_batch, (cfg.hidden, cfg.q_rows, cfg.intermediate))
+    L["kp"] = kp
+    npad = tc_npad(max_batch)
+    H, I, nq, nkv = cfg.hidden, cfg.intermediate, cfg.q_rows, cfg.kv_rows
+    rows = nq + 2 * nkv
+    for k in (H, nq, I):
+        assert k % kp == 0, (k, kp)
+    tasks, splits = {}, {}
+    for name, n, k, add, nseg in (("qkv", rows, H, True, 1), ("oproj", H, nq, True, 1),
+                                  ("gateup", I, H, False, 2), ("down", H, I, True, 1),
+                                  ("lm", cfg.vocab, H, False, 1)):
+        tasks[name], splits[name] = tc_tasks(n // 128, num_workers, add, nseg, npad, k // kp)
+    L["tasks"], L["splits"] = tasks, splits
+    # attention splits per (sequence, kv head): half the batch-1 cap -- a split runs its
+    # blocks two at a time (warps 0-3 / 4-7), so it should own at least two
+    L["max_splits"] = max(1, attn_split_cap(cfg, L["samples"][-1], num_workers) // 2)
+    L["attn_budget"] = attn_budget(cfg, num_workers, attn_tasks_per_sm)
+    L["spec"] = batch_graph_spec(cfg, tasks, L["max_splits"], L["attn_budget"])
+    L["bindings"] = [{"s": s, "b": b} for s in L["samples"] for b in L["batch_samples"]]
+    return L
+
+
 class BatchDecodeModel:
     """Llama-style decoder, batch 1..max_batch (<= 128) and sequence length up to the
     largest sample on one lowered artifact; projections on tcgen05 tensor cores."""
@@ -173,35 +208,15 @@ class BatchDecodeModel:
         self.device = torch.device(device)
         props = torch.cuda.get_device_properties(self.device)
         self.num_workers = num_workers or props.multi_processor_count
-        self.max_batch = max_batch
-        # batch samples: powers of two up to max_batch by default, so a small batch runs on a
-        # schedule at most twice its size (masked tasks still wait and notify)
-        default = [1 << i for i in range(8) if (1 << i) < max_batch]
-        self.batch_samples = sorted(set(batch_samples or default) | {max_batch})
-        self.samples = sorted(int(s) for s in samples)
-        self.capacity = self.samples[-1] + 1
-        # piece length (input columns per activation piece); kp overrides (multiple of 64)
-        self.kp = kp = kp or tc_piece_for(max_batch, (cfg.hidden, cfg.q_rows, cfg.intermediate))
-        npad = tc_npad(max_batch)
-        H, I, nq, nkv = cfg.hidden, cfg.intermediate, cfg.q_rows, cfg.kv_rows
-        rows = nq + 2 * nkv
-        for k in (H, nq, I):
-            assert k % kp == 0, (k, kp)
-        w = self.num_workers
-        self.tasks, self.splits = {}, {}
-        for name, n, k, add, nseg in (("qkv", rows, H, True, 1), ("oproj", H, nq, True, 1),
-                                      ("gateup", I, H, False, 2), ("down", H, I, True, 1),
-                                      ("lm", cfg.vocab, H, False, 1)):
-            self.tasks[name], self.splits[name] = tc_tasks(n // 128, w, add, nseg, npad, k // kp)
-        # attention splits per (sequence, kv head): half the batch-1 cap -- a split runs its
-        # blocks two at a time (warps 0-3 / 4-7), so it should own at least two
-        self.max_splits = max(1, attn_split_cap(cfg, self.samples[-1], self.num_workers) // 2)
         self.scheduler = scheduler
         t0 = time.perf_counter()
-        self.attn_budget = attn_budget(cfg, self.num_workers, attn_tasks_per_sm)
-        self.spec = batch_graph_spec(cfg, self.tasks, self.max_splits, self.attn_budget)
+        for k, v in batch_layout(cfg, self.num_workers, samples, max_batch, batch_samples, kp,
+                                 attn_tasks_per_sm).items():
+            setattr(self, k, v)
+        kp, npad = self.kp, tc_npad(max_batch)
+        H, I, nq, nkv = cfg.hidden, cfg.intermediate, cfg.q_rows, cfg.kv_rows
+        rows = nq + 2 * nkv
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
-        self.bindings = [{"s": s, "b": b} for s in self.samples for b in self.batch_samples]
         if scheduler == "dynamic":
             self.kernel = etsim.lower_dynamic(self.graph)
         else:

@@ -110,6 +110,21 @@ __device__ __forceinline__ bool aborted(const DevStatus* st) {
     return *reinterpret_cast<const volatile int*>(&st->code) != 0;
 }
 
+// Status blocks alternate between launches (each launch prepares the other one
+// for the next).  Errors are sticky until the host collects them (et_sync): a
+// launch that finds its own block already failed (an earlier asynchronous step
+// went wrong) copies the error forward and does nothing, and a launch never
+// clears a block that holds an error.  Returns true when this launch must exit.
+__device__ __forceinline__ bool sticky_status(const StaticParams& P) {
+    const bool failed = aborted(P.status);
+    if (blockIdx.x == 0 && threadIdx.x < sizeof(DevStatus) / 4) {
+        int* other = reinterpret_cast<int*>(P.status_other);
+        if (failed) other[threadIdx.x] = reinterpret_cast<const int*>(P.status)[threadIdx.x];
+        else if (!aborted(P.status_other)) other[threadIdx.x] = 0;
+    }
+    return failed;
+}
+
 // Spin until every wait element in [b, e) has received its initial count.
 // Acquire loads: the producer's data written before its release increment is
 // visible to this thread, and to the rest of the CTA after the barrier that
@@ -998,9 +1013,13 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
             split_bf16x2(q10, q11, bh1, bl1);
             const uint8_t* vb = ring.wait(cv);
             if (!vb) return false;
-            const int mi = lane >> 3, prow = t0 + ((mi & 2) ? 8 : 0) + (lane & 7);  // this lane's V row
+            // this lane's V row; rows past the block's valid positions (the partial
+            // last block) hold stale stage bytes that need not be finite, and their
+            // P is 0 but 0 * Inf = NaN: read the tile's first (valid) row instead
+            const int mi = lane >> 3, prow0 = t0 + ((mi & 2) ? 8 : 0) + (lane & 7);
+            const int prow = prow0 < np ? prow0 : t0;
             const uint8_t* vrow = vb + prow * dh * 2;
-            const int csw = swz ? (lane & 7) : 0;                                  // prow % 8 == lane % 8
+            const int csw = swz ? (prow & 7) : 0;                                  // chunk swizzle of that row
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
                 if (mt < nks) {
@@ -2076,11 +2095,10 @@ template <bool kMoE, bool kTC>
 __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_constant__ StaticParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int worker = blockIdx.x;
+    if (sticky_status(P)) return;
     // zero this CTA's slice of the other-parity counters (used by the next step)
     for (int i = worker * blockDim.x + threadIdx.x; i < P.cnt_capacity; i += gridDim.x * blockDim.x)
         P.cnt_other[i] = 0u;
-    if (worker == 0 && threadIdx.x < sizeof(DevStatus) / 4)
-        reinterpret_cast<int*>(P.status_other)[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
         uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
         for (int i = 0; i < kStages; ++i) {
@@ -2713,7 +2731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     et_dynamic_kernel(const __grid_constant__ StaticParams P, const __grid_constant__ DynParams D) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int worker = blockIdx.x;
-    if (worker == 0 && threadIdx.x < sizeof(DevStatus) / 4) reinterpret_cast<int*>(P.status_other)[threadIdx.x] = 0;
+    if (sticky_status(P)) return;
     // the other parity is rebuilt for the next launch (same sample)
     dyn_reset_state(P, D, D.ctl_other, D.rem_other, D.slots_other, D.fired_other, D.disp_other, P.cnt_other, worker,
                     gridDim.x);

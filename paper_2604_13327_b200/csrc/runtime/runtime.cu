@@ -144,6 +144,7 @@ struct et_runtime {
     bool launched = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timed = false;  // ev0/ev1 bracket the last launch (synchronous steps only)
+    int debug = 0;       // ET_DEBUG at et_create
 
     int fail(int code, const std::string& m) {
         err = m;
@@ -194,6 +195,10 @@ int et_create(const et_config* cfg, et_runtime** out) {
         return ET_ERR_CUDA;
     }
     if (rt->cfg.num_workers <= 0) rt->cfg.num_workers = rt->sm_count;
+    {  // timing-experiment switches (megakernel.cuh StaticParams::debug), read once
+        const char* dbg = getenv("ET_DEBUG");
+        rt->debug = dbg ? atoi(dbg) : 0;
+    }
     *out = rt;
     return ET_OK;
 }
@@ -476,23 +481,36 @@ bool gemv_acc_fits(const et_op& op, int64_t grid0, const int64_t* binding) {
 
 int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     if (!rt || (!ops && num_calls > 0)) return ET_ERR_INVALID;
+    // A rejected table leaves the runtime unbound (et_step refuses to launch) rather
+    // than running whatever table was bound before.
+    rt->ops_bound = 0;
     if (num_calls != rt->num_calls) return rt->fail(ET_ERR_INVALID, "op table must have one entry per call");
+    // validate everything before touching the device copy
+    int variant = 0;
+    for (int32_t c = 0; c < num_calls; ++c) {
+        const int k = ops[c].kind;
+        if (k == ET_OP_MOE_GROUP || k == ET_OP_MOE_COMBINE || k < ET_OP_NONE || k > ET_OP_ARGMAX_LAST)
+            return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": op kind " + std::to_string(k) +
+                                                " has no device body (the routed notify / red.add epilogues "
+                                                "replace MOE_GROUP and MOE_COMBINE)");
+        if (k == ET_OP_MOE_ROUTE || k == ET_OP_MOE_EXPERT) variant |= 1;
+        else if (k == ET_OP_GEMV_TC || k == ET_OP_NORM) variant |= 2;
+    }
+    for (int32_t c = 0; c < num_calls; ++c) {
+        if (ops[c].kind != ET_OP_ATTN_SPLIT && ops[c].kind != ET_OP_ATTN_MERGE) continue;
+        const int dh = ops[c].i[0], G = ops[c].i[1], CH = ops[c].i[2];
+        if ((ops[c].flags & 256) && dh % 64 != 0)  // chunk j ^ (pos % 8) must stay inside the row
+            return rt->fail(ET_ERR_INVALID, "chunk-swizzled KV rows (attention flags bit 8) need head_dim % 64 == 0");
+        if ((variant & 2) && ops[c].kind == ET_OP_ATTN_SPLIT && (G > 8 || dh % 16 != 0 || dh > 128 || CH != 64))
+            // the tensor-core instantiation runs attention on mma.sync tiles (attn_split_mma)
+            return rt->fail(ET_ERR_INVALID, "tensor-core attention needs <= 8 q heads per kv head, head_dim "
+                                            "a multiple of 16 up to 128 and 64-position blocks");
+    }
     cudaSetDevice(rt->cfg.device);
     cudaStreamSynchronize(rt->stream);
     ET_CUDA(rt->d_ops.upload(ops, static_cast<size_t>(std::max(1, num_calls))), "bind ops");
-    rt->has_moe = 0;
+    rt->has_moe = variant;
     rt->h_ops.assign(ops, ops + num_calls);
-    for (int32_t c = 0; c < num_calls; ++c)
-        if (ops[c].kind == ET_OP_MOE_ROUTE || ops[c].kind == ET_OP_MOE_EXPERT) rt->has_moe |= 1;
-        else if (ops[c].kind == ET_OP_GEMV_TC || ops[c].kind == ET_OP_NORM) rt->has_moe |= 2;
-    if (rt->has_moe & 2)  // the tensor-core instantiation runs attention on mma.sync tiles (attn_split_mma)
-        for (int32_t c = 0; c < num_calls; ++c)
-            if (ops[c].kind == ET_OP_ATTN_SPLIT) {
-                const int dh = ops[c].i[0], G = ops[c].i[1], CH = ops[c].i[2];
-                if (G > 8 || dh % 16 != 0 || dh > 128 || CH != 64)
-                    return rt->fail(ET_ERR_INVALID, "tensor-core attention needs <= 8 q heads per kv head, head_dim "
-                                                    "a multiple of 16 up to 128 and 64-position blocks");
-            }
     rt->ops_bound = 1;
     return ET_OK;
 }
@@ -527,11 +545,34 @@ int et_get_runtime_tensor(et_runtime* rt, int32_t index, int32_t* values, int64_
     return ET_OK;
 }
 
+// After a failed step the op-side state that the kernels normally leave clean for
+// the next step (split-arrival counters of the fused attention merge and the MoE
+// route, raw split-K q/k/v and router accumulators zeroed by their consumers) may
+// be half-updated: zero it, sized by the runtime's max_batch.
+static void reset_op_state(et_runtime* rt) {
+    const size_t B = static_cast<size_t>(std::max(1, rt->cfg.max_batch));
+    for (const et_op& op : rt->h_ops) {
+        if (op.kind == ET_OP_ATTN_SPLIT && (op.flags & 2) && op.p[5])
+            cudaMemset(reinterpret_cast<void*>(op.p[5]), 0, B * static_cast<size_t>(std::max(1, op.i[6])) * 4);
+        if (op.kind == ET_OP_ATTN_SPLIT && (op.flags & 32) && op.p[0] && op.i[7] > 0)
+            cudaMemset(reinterpret_cast<void*>(op.p[0]), 0, B * static_cast<size_t>(op.i[7]) * 4);
+        if (op.kind == ET_OP_MOE_ROUTE) {
+            if (op.p[7]) cudaMemset(reinterpret_cast<void*>(op.p[7]), 0, 4);
+            if ((op.flags & 2) && op.p[1]) cudaMemset(reinterpret_cast<void*>(op.p[1]), 0, B * static_cast<size_t>(op.i[0]) * 4);
+        }
+    }
+}
+
 static int collect(et_runtime* rt, et_step_info* info) {
     ET_CUDA(cudaStreamSynchronize(rt->stream), "step");
-    etk::DevStatus st{};
+    etk::DevStatus st{}, prev{};
     const int cur = rt->parity ^ 1;  // parity already advanced past the last launch
     ET_CUDA(cudaMemcpy(&st, rt->d_status.ptr + cur, sizeof(st), cudaMemcpyDeviceToHost), "status");
+    // An earlier asynchronous step's error is sticky: a launch never zeroes a status
+    // block that holds an error (megakernel.cu), and launches that find their own
+    // block failed exit at once, so the first error survives until it is collected here.
+    ET_CUDA(cudaMemcpy(&prev, rt->d_status.ptr + (cur ^ 1), sizeof(prev), cudaMemcpyDeviceToHost), "status");
+    if (st.code == 0 && prev.code != 0) st = prev;
     if (info) {
         std::memset(info, 0, sizeof(*info));
         info->status = st.code;
@@ -555,6 +596,8 @@ static int collect(et_runtime* rt, et_step_info* info) {
         // leave the runtime reusable: clear every counter and status block
         cudaMemset(rt->d_cnt.ptr, 0, rt->d_cnt.n * sizeof(uint32_t));
         cudaMemset(rt->d_status.ptr, 0, 2 * sizeof(etk::DevStatus));
+        reset_op_state(rt);
+        cudaDeviceSynchronize();
         rt->prepared[0] = rt->prepared[1] = -1;
         rt->err = st.code == ET_ERR_DEADLOCK     ? "deadlock"
                   : st.code == ET_ERR_UNDERFLOW  ? "counter underflow"
@@ -656,10 +699,7 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     p.table_ok = S.table_ok;
     p.step_id = ++rt->steps;
     p.l2_ahead = rt->cfg.l2_prefetch_bytes < 0 ? 0 : rt->cfg.l2_prefetch_bytes;
-    {
-        const char* dbg = getenv("ET_DEBUG");
-        p.debug = dbg ? atoi(dbg) : 0;
-    }
+    p.debug = rt->debug;
 
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rt->stream;
     int e = 0;

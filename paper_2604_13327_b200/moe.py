@@ -79,6 +79,13 @@ class MoEConfig:
     attn_chunk: int = 64
     row_splits: int = 12       # expert row splits (expert_inter / row_splits % 32 == 0)
     tile_tokens: int = 8       # tokens per expert tile (<= 8: the mma N dimension)
+    # Router init scale.  0.02 like every projection: round 1 drew the router from
+    # N(0, 0.1), whose logits (std ~4.5) make the renormalised top-k softmax so sharp
+    # that a bf16-ulp difference in the hidden state grows ~12% per layer (measured:
+    # 0.4% after layer 0, 66% after layer 47, profiles/r2_diag_moe_depth.txt) -- a
+    # property of that synthetic function, not of any implementation, which made a
+    # 48-layer logits comparison meaningless.
+    router_std: float = 0.02
 
     @property
     def q_rows(self):
@@ -224,7 +231,10 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
             "device_functions": fns, "event_tensors": events, "runtime_tensors": rts, "calls": calls}
 
 
-def init_moe_weights(cfg: MoEConfig, device, seed=0, std=0.02):
+def init_moe_weights(cfg: MoEConfig, device, seed=0, std=0.02, layer_hook=None):
+    """Random-init weights (bf16 N(0, std), router N(0, cfg.router_std), norms ~ 1 + N(0, 0.01)).
+    `layer_hook(d)` (optional) may replace the top-level dict and each layer dict as
+    soon as it is drawn (the draw order is unchanged)."""
     g = torch.Generator(device=device)
     g.manual_seed(seed)
 
@@ -240,13 +250,16 @@ def init_moe_weights(cfg: MoEConfig, device, seed=0, std=0.02):
 
     H, I, E = cfg.hidden, cfg.expert_inter, cfg.experts
     W = {"embed": w(cfg.vocab, H), "final_norm": norm(H), "lm_head": w(cfg.vocab, H), "layers": []}
+    if layer_hook is not None:
+        W = layer_hook(W)
     for _ in range(cfg.layers):
-        W["layers"].append({
+        d = {
             "attn_norm": norm(H), "wqkv": w(cfg.q_rows + 2 * cfg.kv_rows, H), "q_norm": norm(cfg.head_dim),
             "k_norm": norm(cfg.head_dim), "wo": w(H, cfg.q_rows), "ffn_norm": norm(H),
-            "router": w(E, H, s=0.1),
+            "router": w(E, H, s=cfg.router_std),
             "wgate": w(E, I, H), "wup": w(E, I, H), "wdown": w(E, H, I),
-        })
+        }
+        W["layers"].append(layer_hook(d) if layer_hook is not None else d)
     return W
 
 
@@ -282,6 +295,68 @@ def moe_device_layout(cfg, W, kp=0):
     return D
 
 
+def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=None, attn_cap=None,
+               fused_merge=True, balance=False, route_tasks=None, group_stage=None, qkv_split=True):
+    """Every layout choice MoEDecodeModel makes before touching the device: the graph
+    spec it lowers, its bindings (samples) and task counts.  Pure (no device, no
+    extension), so the committed bench-graph fixtures (tests/golden/make_bench_graphs.py)
+    are exactly the graphs the model runs.
+
+    batch: a graph symbol `b`; every (s, b) at or below a sample runs on the lowered
+    artifact.  Up to 8 the projections carry the batch in the mma.sync N dimension;
+    above, they run on the tcgen05 tensor cores (batch.py layouts)."""
+    from .decode import attn_split_cap, balanced_tasks
+
+    assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
+    assert 1 <= max_batch <= 64
+    L = {"max_batch": max_batch, "batched": max_batch > 1, "tc": max_batch > 8}
+    L["tokens"] = "b" if L["batched"] else 1
+    default = [1 << i for i in range(7) if (1 << i) < max_batch] if L["tc"] else [1]
+    L["batch_samples"] = sorted(set(batch_samples or default) | {max_batch}) if L["batched"] else [1]
+    L["samples"] = sorted(int(s) for s in samples)
+    L["capacity"] = L["samples"][-1] + 1
+    ms = attn_cap or attn_split_cap(cfg, L["samples"][-1], num_workers)
+    if max_batch > 8 and not attn_cap:  # tensor-core attention: a split runs two blocks at a time (batch.py)
+        ms = max(1, ms // 2)
+    L["max_splits"] = ms
+    L["fused_merge"] = fused_merge
+    L["group_stage"] = (scheduler == "dynamic") if group_stage is None else group_stage
+    L["qkv_split"] = qkv_split and fused_merge
+    L["route_tasks"] = route_tasks or max(1, cfg.experts // 16)
+    assert fused_merge or not L["batched"], "batched decode uses the fused attention merge"
+    og = None
+    if L["batched"]:  # per kv-head-group output projection (a batch of full attention rows would not fit)
+        og = max(1, num_workers // cfg.kv_heads)
+        while (cfg.hidden // 16) % og:
+            og -= 1
+    # the lm_head task's rows x batch accumulate in shared memory (2048 fp32): a large
+    # vocabulary at batch 8 needs more, smaller row spans than one per worker
+    tiles, cap_tiles = cfg.vocab // 16, max(1, 2048 // (16 * max_batch))
+    L["lm_tasks"] = max(num_workers, -(-tiles // cap_tiles))
+    kp, tct, tcs = 0, None, None
+    if L["tc"]:
+        from .batch import attn_budget, tc_npad, tc_piece_for, tc_tasks
+
+        assert fused_merge
+        og = None
+        H, nq = cfg.hidden, cfg.q_rows
+        kp = tc_piece_for(max_batch, (H, nq))
+        npad = tc_npad(max_batch)
+        tct, tcs = {}, {}
+        for name, n, k, add in (("qkv", nq + 2 * cfg.kv_rows, H, True), ("oproj", H, nq, True),
+                                ("router", -(-cfg.experts // 128) * 128, H, True), ("lm", cfg.vocab, H, False)):
+            tct[name], tcs[name] = tc_tasks(n // 128, num_workers, add, 1, npad, k // kp)
+        tct["attn_budget"] = attn_budget(cfg, num_workers)
+    L.update(oproj_group_tasks=og, kp=kp, tc_tasks=tct, tc_splits=tcs)
+    L["spec"] = moe_graph_spec(cfg, num_workers, L["lm_tasks"], L["tokens"], fused_merge=fused_merge,
+                               qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, num_workers)
+                               if balance else None, route_tasks=L["route_tasks"], group_stage=L["group_stage"],
+                               attn_cap=ms, oproj_group_tasks=og, tc=tct)
+    L["bindings"] = [({"s": int(s), "b": int(b)} if L["batched"] else {"s": int(s)})
+                     for s in L["samples"] for b in L["batch_samples"]]
+    return L
+
+
 class MoEDecodeModel:
     """One MoE decoder + its lowered megakernel (static or dynamic scheduler)."""
 
@@ -291,72 +366,20 @@ class MoEDecodeModel:
                  max_batch=1, batch_samples=None, attn_cap=None):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
-        assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
         self.cfg = cfg
         self.device = torch.device(device)
         props = torch.cuda.get_device_properties(self.device)
         self.num_workers = num_workers or props.multi_processor_count
-        # batch: a graph symbol `b`; every (s, b) at or below a sample runs on the lowered
-        # artifact.  Up to 8 the projections carry the batch in the mma.sync N dimension;
-        # above, they run on the tcgen05 tensor cores (batch.py layouts)
-        assert 1 <= max_batch <= 64
-        self.max_batch = max_batch
-        self.batched = max_batch > 1
-        self.tc = max_batch > 8
-        self.tokens = "b" if self.batched else 1
-        default = [1 << i for i in range(7) if (1 << i) < max_batch] if self.tc else [1]
-        self.batch_samples = sorted(set(batch_samples or default) | {max_batch}) if self.batched else [1]
-        self.samples = sorted(int(s) for s in samples)
-        self.capacity = self.samples[-1] + 1
-        from .decode import attn_split_cap
-
-        self.max_splits = attn_cap or attn_split_cap(cfg, self.samples[-1], self.num_workers)
-        if max_batch > 8 and not attn_cap:  # tensor-core attention: a split runs two blocks at a time (batch.py)
-            self.max_splits = max(1, self.max_splits // 2)
         self.scheduler = scheduler
-        t0 = time.perf_counter()
-        from .decode import balanced_tasks
-
-        self.fused_merge = fused_merge
-        self.group_stage = (scheduler == "dynamic") if group_stage is None else group_stage
         self.l2_prefetch_experts = l2_prefetch_experts
-        self.qkv_split = qkv_split and fused_merge
-        self.route_tasks = route_tasks or max(1, cfg.experts // 16)
-        assert fused_merge or not self.batched, "batched decode uses the fused attention merge"
-        self.oproj_group_tasks = None
-        if self.batched:  # per kv-head-group output projection (a batch of full attention rows would not fit)
-            og = max(1, self.num_workers // cfg.kv_heads)
-            while (cfg.hidden // 16) % og:
-                og -= 1
-            self.oproj_group_tasks = og
-        # the lm_head task's rows x batch accumulate in shared memory (2048 fp32): a large
-        # vocabulary at batch 8 needs more, smaller row spans than one per worker
-        tiles, cap_tiles = cfg.vocab // 16, max(1, 2048 // (16 * max_batch))
-        self.lm_tasks = max(self.num_workers, -(-tiles // cap_tiles))
-        self.kp, self.tc_tasks, self.tc_splits = 0, None, None
-        if self.tc:
-            from .batch import tc_npad, tc_piece_for, tc_tasks
-
-            assert fused_merge
-            self.oproj_group_tasks = None
-            H, nq = cfg.hidden, cfg.q_rows
-            self.kp = tc_piece_for(max_batch, (H, nq))
-            npad, w = tc_npad(max_batch), self.num_workers
-            self.tc_tasks, self.tc_splits = {}, {}
-            for name, n, k, add in (("qkv", nq + 2 * cfg.kv_rows, H, True), ("oproj", H, nq, True),
-                                    ("router", -(-cfg.experts // 128) * 128, H, True), ("lm", cfg.vocab, H, False)):
-                self.tc_tasks[name], self.tc_splits[name] = tc_tasks(n // 128, w, add, 1, npad, k // self.kp)
-            from .batch import attn_budget
-
-            self.tc_tasks["attn_budget"] = attn_budget(cfg, w)
-        self.spec = moe_graph_spec(cfg, self.num_workers, self.lm_tasks, self.tokens, fused_merge=fused_merge,
-                                   qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, self.num_workers)
-                                   if balance else None, route_tasks=self.route_tasks, group_stage=self.group_stage,
-                                   attn_cap=self.max_splits, oproj_group_tasks=self.oproj_group_tasks,
-                                   tc=self.tc_tasks)
+        t0 = time.perf_counter()
+        lay = moe_layout(cfg, self.num_workers, samples, scheduler, max_batch=max_batch, batch_samples=batch_samples,
+                         attn_cap=attn_cap, fused_merge=fused_merge, balance=balance, route_tasks=route_tasks,
+                         group_stage=group_stage, qkv_split=qkv_split)
+        for k, v in lay.items():
+            setattr(self, k, v)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.rt_index = {r["name"]: i for i, r in enumerate(self.spec["runtime_tensors"])}
-        self.bindings = [self._binding(s, b) for s in self.samples for b in self.batch_samples]
         if scheduler == "dynamic":
             self.kernel = etsim.lower_dynamic(self.graph, early_push=early_push)
         else:

@@ -86,6 +86,19 @@ def shard_weights(cfg, W, rank, world):
             "layers": [_shard_layer(cfg, L, rank, world) for L in W["layers"]]}
 
 
+def local_config(cfg, world):
+    """The per-rank decoder shape (heads, kv heads, intermediate and vocab / TP)."""
+    return dataclasses.replace(cfg, heads=cfg.heads // world, kv_heads=cfg.kv_heads // world,
+                               intermediate=cfg.intermediate // world, vocab=cfg.vocab // world)
+
+
+def tp_graph_spec(cfg, world, num_workers, samples, ar_tasks=None):
+    """The graph one rank lowers (device-free; the committed bench-graph fixtures use it)."""
+    lc = local_config(cfg, world)
+    return graph_spec(lc, num_workers, num_workers, fused_merge=True, allreduce_tasks=ar_tasks or num_workers,
+                      attn_cap=attn_split_cap(lc, max(samples), num_workers))
+
+
 class TPDecodeModel:
     """Rank `rank` of a TP-way sharded Llama-style decoder (static scheduler)."""
 
@@ -101,13 +114,11 @@ class TPDecodeModel:
         self.num_workers = num_workers or props.multi_processor_count
         self.samples = sorted(int(s) for s in samples)
         self.capacity = self.samples[-1] + 1
-        self.local = dataclasses.replace(cfg, heads=cfg.heads // world, kv_heads=cfg.kv_heads // world,
-                                         intermediate=cfg.intermediate // world, vocab=cfg.vocab // world)
+        self.local = local_config(cfg, world)
         self.ar_tasks = ar_tasks or self.num_workers
         self.max_splits = attn_split_cap(self.local, self.samples[-1], self.num_workers)
         t0 = time.perf_counter()
-        spec = graph_spec(self.local, self.num_workers, self.num_workers, fused_merge=True,
-                          allreduce_tasks=self.ar_tasks, attn_cap=self.max_splits)
+        spec = tp_graph_spec(cfg, world, self.num_workers, self.samples, self.ar_tasks)
         self.graph = etsim.Graph.from_json(json.dumps(spec))
         self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
         self.lower_ms = (time.perf_counter() - t0) * 1e3

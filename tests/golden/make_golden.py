@@ -143,6 +143,42 @@ for name, cfg_kw, tasks, samples in [
         entry["simulate"] = {str(s): trace_acc(etsim.simulate(k, {"s": s})) for s in (1000, 1024)}
     cases[name] = entry
 
+# --- the graphs bench.py actually lowers (tests/golden/bench_graphs.json.gz, pinned to the
+# live layout functions by tests/test_bench_graphs.py): the headline Llama-3-8B step
+# (balanced / grouped / fused-merge spec) and the Qwen3-30B-A3B bs=1 step on both schedulers
+import gzip  # noqa: E402
+
+with gzip.open(os.path.join(HERE, "bench_graphs.json.gz"), "rt") as f:
+    BENCH = json.load(f)
+fx = BENCH["llama3-8b|b1|static|s1024|tp0"]
+g = etsim.Graph.from_json(json.dumps(fx["spec"]))
+k = etsim.lower_static(g, fx["bindings"], num_sms=fx["num_sms"])
+cases["llama8b_bench"] = {"spec": fx["spec"], "num_sms": fx["num_sms"], "samples": fx["bindings"],
+                          "kernel_sha256": sha(k.to_json()),
+                          "instantiate": {str(s): mat(g.instantiate({"s": s})) for s in (1000, 1024)},
+                          "simulate": {str(s): trace_acc(etsim.simulate(k, {"s": s})) for s in (1000, 1024)}}
+for sched in ("static", "dynamic"):
+    fx = BENCH[f"qwen3-30b-a3b|b1|{sched}|s1024|tp0"]
+    g = etsim.Graph.from_json(json.dumps(fx["spec"]))
+    routing = {}
+    for l in range(fx["moe"]["layers"]):
+        r = etsim.moe_realization(tokens=1, experts=128, top_k=8, tile_size=8, seed=l)
+        routing.update({f"topk{l}": r["topk"], f"cnt{l}": r["expert_counts"], f"ind{l}": r["exp_indptr"],
+                        f"tind{l}": [12 * v for v in r["exp_indptr"]]})
+    if sched == "static":
+        k = etsim.lower_static(etsim.worst_case_rewrite(g), fx["bindings"], num_sms=fx["num_sms"])
+        t = etsim.simulate(k, fx["binding"], routing=routing)
+        extra = {}
+    else:
+        k = etsim.lower_dynamic(g)
+        t = etsim.simulate(k, fx["binding"], routing=routing, num_sms=fx["num_sms"])
+        md = etsim.metrics(t)
+        extra = {"pushes": md["pushes"], "pops": md["pops"], "real_tasks": md["real_tasks"]}
+    m = g.instantiate(fx["binding"], routing=routing)
+    cases[f"qwen3_bench_{sched}"] = dict({"spec": fx["spec"], "bindings": fx["bindings"], "routing": routing,
+                                          "kernel_sha256": sha(k.to_json()), "instantiate": mat(m),
+                                          "simulate": trace_acc(t)}, **extra)
+
 out = os.path.join(HERE, "reference_golden.json")
 with open(out, "w") as f:
     json.dump(cases, f, sort_keys=True)

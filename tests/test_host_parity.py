@@ -84,7 +84,7 @@ def test_realizations_bit_exact():
         assert etsim.moe_realization(**case["args"]) == case["out"]
 
 
-@pytest.mark.parametrize("name", ["tiny", "llama8b"])
+@pytest.mark.parametrize("name", ["tiny", "llama8b", "llama8b_bench"])
 def test_decode_graph_lowering_bit_exact(name):
     import hashlib
 
@@ -197,3 +197,22 @@ def test_no_cpu_fallback_without_gpu():
     k = etsim.lower_static(etsim.gemm_reduce_scatter("4", 2), [{}], num_sms=2)
     with pytest.raises(etsim.GraphError):
         etsim.simulate(k)
+
+
+@pytest.mark.parametrize("sched", ["static", "dynamic"])
+def test_qwen3_bench_graph_lowering_bit_exact(sched):
+    """The Qwen3-30B-A3B bs=1 graph bench.py lowers: this framework's lowering and
+    routed instantiation equal the reference's (tests/golden/make_golden.py)."""
+    import hashlib
+
+    c = GOLD[f"qwen3_bench_{sched}"]
+    g = etsim.Graph.from_json(json.dumps(c["spec"]))
+    if sched == "static":
+        k = etsim.lower_static(etsim.worst_case_rewrite(g), c["bindings"], num_sms=148)
+    else:
+        k = etsim.lower_dynamic(g)
+    assert hashlib.sha256(k.to_json().encode()).hexdigest() == c["kernel_sha256"]
+    m = g.instantiate(c["bindings"][0], routing=c["routing"])
+    want = c["instantiate"]
+    assert (m.num_tasks, m.num_events) == (want["num_tasks"], want["num_events"])
+    assert m.call_task_counts == want["call_task_counts"] and m.initial_counts == want["initial_counts"]
