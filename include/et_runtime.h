@@ -239,6 +239,10 @@ int et_get_runtime_tensor(et_runtime* rt, int32_t index, int32_t* values, int64_
 int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* stream, int32_t synchronous,
             et_step_info* info);
 int et_sync(et_runtime* rt, et_step_info* info);
+/* Diagnostics only (timing experiments, scripts/diag_*.py): the megakernel's
+ * debug bits (StaticParams::debug in csrc/kernels/megakernel.cuh; 0 = normal).
+ * Initialised from the ET_DEBUG environment variable at et_create. */
+int et_set_debug(et_runtime* rt, int32_t bits);
 
 /* Event Tensor counters of the last step in the reference's representation
  * (initial count minus notifies received; all zero after a clean step). */

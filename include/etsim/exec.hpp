@@ -65,6 +65,7 @@ public:
     bool dynamic() const;
     int num_workers() const;
     double upload_ms() const;
+    void set_debug(int bits);  // diagnostics: megakernel debug bits (et_set_debug)
 
 private:
     struct Impl;

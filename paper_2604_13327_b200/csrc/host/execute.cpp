@@ -807,6 +807,7 @@ const StaticMegakernel& Executor::kernel() const { return impl_->k; }
 bool Executor::dynamic() const { return impl_->dyn; }
 int Executor::num_workers() const { return impl_->workers; }
 double Executor::upload_ms() const { return impl_->upload_ms; }
+void Executor::set_debug(int bits) { et_set_debug(impl_->rt, bits); }
 
 // ---------------------------------------------------------------------------
 // Reference-named entry points.

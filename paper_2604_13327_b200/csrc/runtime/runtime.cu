@@ -749,6 +749,12 @@ int et_sync(et_runtime* rt, et_step_info* info) {
     return collect(rt, info);
 }
 
+int et_set_debug(et_runtime* rt, int32_t bits) {
+    if (!rt) return ET_ERR_INVALID;
+    rt->debug = bits;
+    return ET_OK;
+}
+
 int et_read_counters(et_runtime* rt, int64_t* out, int64_t n) {
     if (!rt || rt->last_sample < 0) return ET_ERR_INVALID;
     cudaSetDevice(rt->cfg.device);

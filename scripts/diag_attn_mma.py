@@ -18,7 +18,7 @@ calls = m.graph.call_functions
 ca = [c for c in range(len(calls)) if calls[c] == "L1.attn"][0]
 for dbg, name in (("4098", "ring waits"), ("4104", "barriers"), ("4608", "compute"),
                   ("37376", "compute (no MMA)")):
-    os.environ["ET_DEBUG"] = dbg
+    m.executor.set_debug(int(dbg))
     for _ in range(2):
         m.executor.run({"s": s, "b": b})
     raw = m.executor.raw_trace()

@@ -26,9 +26,9 @@ def timed(n=4):
 
 
 for dbg in ("0", "1", "4", "64", "68", "324"):
-    os.environ["ET_DEBUG"] = dbg
+    m.executor.set_debug(int(dbg))
     print("ET_DEBUG", dbg, "ms", round(timed(), 3), flush=True)
-os.environ["ET_DEBUG"] = os.environ.get("TL_DEBUG", "0")  # timeline under this ET_DEBUG
+m.executor.set_debug(int(os.environ.get("TL_DEBUG", "0")))  # timeline under this ET_DEBUG
 timed(2)
 t = m.executor.trace()
 calls = m.graph.call_functions
@@ -47,7 +47,7 @@ for c in l1:
 
 recs_of = {}
 for dbg in ("2", "8", "514", "6"):
-    os.environ["ET_DEBUG"] = dbg
+    m.executor.set_debug(int(dbg))
     timed(2)
     recs_of[dbg] = m.executor.raw_trace()
 t = m.executor.trace()
@@ -60,7 +60,7 @@ for c in l1:
     print(row + " us")
 
 # attention task phases (normal run): wait-end -> split work done (t_prologue stamp) -> exec end
-os.environ["ET_DEBUG"] = "0"
+m.executor.set_debug(0)
 timed(2)
 raw = m.executor.raw_trace()
 t = m.executor.trace()

@@ -24,21 +24,21 @@ def timed(n=5):
     return statistics.median(ts[1:])
 
 
-os.environ["ET_DEBUG"] = "0"
+m.executor.set_debug(int("0"))
 print("normal  ms", timed())
-os.environ["ET_DEBUG"] = "1"
+m.executor.set_debug(int("1"))
 print("nowait  ms", timed())
-os.environ["ET_DEBUG"] = "4"
+m.executor.set_debug(int("4"))
 print("nohbm   ms", timed())
-os.environ["ET_DEBUG"] = "5"
+m.executor.set_debug(int("5"))
 print("nohbm+nowait ms", timed())
 for f in ("16", "32", "48", "20", "36", "52"):
-    os.environ["ET_DEBUG"] = f
+    m.executor.set_debug(int(f))
     print("flags", f, "ms", timed())
-os.environ["ET_DEBUG"] = "12"
+m.executor.set_debug(int("12"))
 print("nohbm+busy ms", timed())
 recs_nohbm = m.executor.raw_trace()
-os.environ["ET_DEBUG"] = "2"
+m.executor.set_debug(int("2"))
 print("stall   ms", timed())
 recs = m.executor.raw_trace()
 calls = m.graph.call_functions
@@ -60,7 +60,7 @@ for c in list(range(1, 8)) + [len(calls) - 1]:
           f"{statistics.median(pro) if pro else 0:6.0f}")
 
 # stage timeline of layer 1 (normal run, trace on)
-os.environ["ET_DEBUG"] = "0"
+m.executor.set_debug(int("0"))
 timed(3)
 t = m.executor.trace()
 by = collections.defaultdict(list)
