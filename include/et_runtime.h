@@ -243,6 +243,9 @@ int et_sync(et_runtime* rt, et_step_info* info);
  * debug bits (StaticParams::debug in csrc/kernels/megakernel.cuh; 0 = normal).
  * Initialised from the ET_DEBUG environment variable at et_create. */
 int et_set_debug(et_runtime* rt, int32_t bits);
+/* Per-worker L2 run-ahead of the weight producer in bytes (et_config.l2_prefetch_bytes;
+ * negative = off), changeable between steps. */
+int et_set_l2_prefetch(et_runtime* rt, int64_t bytes);
 
 /* Event Tensor counters of the last step in the reference's representation
  * (initial count minus notifies received; all zero after a clean step). */

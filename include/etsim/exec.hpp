@@ -66,6 +66,7 @@ public:
     int num_workers() const;
     double upload_ms() const;
     void set_debug(int bits);  // diagnostics: megakernel debug bits (et_set_debug)
+    void set_l2_prefetch(Int bytes);  // producer L2 run-ahead per worker (et_set_l2_prefetch)
 
 private:
     struct Impl;

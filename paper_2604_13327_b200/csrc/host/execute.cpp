@@ -808,6 +808,7 @@ bool Executor::dynamic() const { return impl_->dyn; }
 int Executor::num_workers() const { return impl_->workers; }
 double Executor::upload_ms() const { return impl_->upload_ms; }
 void Executor::set_debug(int bits) { et_set_debug(impl_->rt, bits); }
+void Executor::set_l2_prefetch(Int bytes) { et_set_l2_prefetch(impl_->rt, bytes); }
 
 // ---------------------------------------------------------------------------
 // Reference-named entry points.

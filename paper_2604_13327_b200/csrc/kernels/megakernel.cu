@@ -390,6 +390,94 @@ __device__ __forceinline__ void gemv_stream(Ring& ring, int warp, int lane, int 
     ring.seq = c;
 }
 
+// Attention-merge prologue of a GEMV (x mode 2, b = 1): activation slice g is the
+// merge of kv group g's attention splits, whose unnormalised partials (m, l, o)
+// per q head the splits left in p2 (fp32 [heads][i10][dh + 2]; ATTN_SPLIT flags
+// bit 10):  x = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c  (M = max_c m_c),
+// so the attention needs no merge task and its consumer no second hop.
+// i6 = position slot, i8 = head_dim, i10 = split stride, i11 = CH, i12 = split cap.
+// Out of line: its 32 loads in flight would otherwise crowd the GEMV loop's registers.
+__device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et_op& op, int gsel, uint16_t* xs,
+                                                 float* acc, int ctid) {
+    const int warp = ctid >> 5, lane = ctid & 31;
+    const int K = op.i[1];
+
+    const int dh = op.i[8], G = K / dh, maxs = op.i[10], CH = op.i[11];
+    const long long s = P.binding[op.i[6]];
+    long long nsl = (s + CH - 1) / CH;
+    if (nsl > op.i[12]) nsl = op.i[12];
+    const int ns = nsl > 0 ? static_cast<int>(nsl) : 1;
+    const float* part = reinterpret_cast<const float*>(op.p[2]) +
+                        static_cast<long long>(gsel) * G * maxs * (dh + 2);
+    float* ml = acc;              // [G][ns][2] (acc is zeroed after the prologue)
+    float* wts = acc + 2 * G * ns;  // [G][ns]
+    constexpr int kPass = 16, kOut = 2;  // splits per register batch; outputs per thread (K <= 512)
+    float ov[kOut][kPass];
+#pragma unroll
+    for (int j = 0; j < kOut; ++j) {
+        const int idx = ctid + j * kConsumers;
+        const int hh = idx / dh, d = idx - hh * dh;
+#pragma unroll
+        for (int c = 0; c < kPass; ++c)
+            ov[j][c] = (idx < K && c < ns) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d)
+                                           : 0.f;
+    }
+    for (int i = ctid; i < G * ns; i += kConsumers) {
+        const float* pr = part + (static_cast<long long>(i / ns) * maxs + i % ns) * (dh + 2);
+        ml[2 * i] = __ldcg(pr);
+        ml[2 * i + 1] = __ldcg(pr + 1);
+    }
+    bar_sync(1, kConsumers);
+    for (int hh = warp; hh < G; hh += kConsumerWarps) {
+        float M = -INFINITY;
+        for (int c = lane; c < ns; c += 32) M = fmaxf(M, ml[2 * (hh * ns + c)]);
+        M = warp_max(M);
+        float L = 0.f;
+        for (int c = lane; c < ns; c += 32) {
+            const float e = __expf(ml[2 * (hh * ns + c)] - M);
+            wts[hh * ns + c] = e;
+            L += e * ml[2 * (hh * ns + c) + 1];
+        }
+        const float inv = 1.f / warp_sum(L);
+        __syncwarp();
+        for (int c = lane; c < ns; c += 32) wts[hh * ns + c] *= inv;
+    }
+    bar_sync(1, kConsumers);
+#pragma unroll
+    for (int j = 0; j < kOut; ++j) {
+        const int idx = ctid + j * kConsumers;
+        if (idx < K) {
+            const int hh = idx / dh, d = idx - hh * dh;
+            const float* w = wts + hh * ns;
+            float o = 0.f, o2 = 0.f;
+#pragma unroll
+            for (int c = 0; c < kPass; c += 2) {
+                if (c < ns) o = fmaf(w[c], ov[j][c], o);
+                if (c + 1 < ns) o2 = fmaf(w[c + 1], ov[j][c + 1], o2);
+            }
+            for (int c0 = kPass; c0 < ns; c0 += kPass) {  // further splits, one batch of loads at a time
+                float pv[kPass];
+#pragma unroll
+                for (int u = 0; u < kPass; ++u)
+                    pv[u] = c0 + u < ns ? __ldcg(part + (static_cast<long long>(hh) * maxs + c0 + u) * (dh + 2) + 2 + d)
+                                        : 0.f;
+#pragma unroll
+                for (int u = 0; u < kPass; ++u)
+                    if (c0 + u < ns) o = fmaf(w[c0 + u], pv[u], o);
+            }
+            xs[idx] = f2bf(o + o2);
+        }
+    }
+    for (int idx = ctid + kOut * kConsumers; idx < K; idx += kConsumers) {  // K > 512
+        const int hh = idx / dh, d = idx - hh * dh;
+        float o = 0.f;
+        for (int c = 0; c < ns; ++c)
+            o = fmaf(wts[hh * ns + c], __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d), o);
+        xs[idx] = f2bf(o);
+    }
+    bar_sync(1, kConsumers);  // ml / wts live in acc, zeroed by the caller
+}
+
 // Row-range GEMV y[b][r] = sum_k W[r][k] x[b][k] for rows [r0, r1) (multiples
 // of 16) of a bf16 weight in mma-fragment tile order (K % 32 == 0).  The
 // weight tiles stream through the shared-memory ring; activations are staged
@@ -406,6 +494,8 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
     // flags bit 4: grouped GEMV -- coord 0 selects the group's weight matrix and
     // activation slice, coord 1 the row span among i9 tasks per group
     const bool grouped = (op.flags & 16) != 0;
+    uint64_t t_probe = 0;  // debug bits 0x1000 / 0x2000 / 0x4000 / 0x8000: prologue probe points
+    if ((P.debug & 0x8000) && ctid == 0) t_probe = globaltimer();  // body entry
     const GemvSpan sp = gemv_span(op, grouped ? si.coord[1] : si.coord[0], grouped ? op.i[13] : si.ext0);
     const int r0 = sp.row0, R = sp.rows;
 
@@ -418,6 +508,8 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
             const int bi = v / k8, kk = v - bi * k8;
             reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x + static_cast<long long>(bi) * xstride) + kk);
         }
+    } else if (op.i[3] == 2) {
+        gemv_merge_prologue(P, op, grouped ? si.coord[0] : 0, xs, acc, ctid);
     } else {
         // RMSNorm prologue: one pass over the fp32 residual stream held in
         // registers (K <= 8192), sum of squares reduced across the CTA
@@ -438,6 +530,10 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
             for (int j = 0; j < kMaxPer; ++j)
                 if ((ctid + j * kConsumers) * 4 < K)
                     ss += hv[j].x * hv[j].x + hv[j].y * hv[j].y + hv[j].z * hv[j].z + hv[j].w * hv[j].w;
+            if ((P.debug & 0x1000) && ctid == 0) {
+                const float4 z = hv[0];
+                t_probe = globaltimer() + (z.x == 12345.f ? 1 : 0);  // after the loads land
+            }
             ss = warp_sum(ss);
             if (lane == 0) red[warp] = ss;
             bar_sync(1, kConsumers);
@@ -445,6 +541,7 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
 #pragma unroll
             for (int w = 0; w < kConsumerWarps; ++w) t += red[w];
             const float scale = rsqrtf(t / static_cast<float>(K) + op.f[0]);
+            if ((P.debug & 0x2000) && ctid == 0) t_probe = globaltimer();  // after the reduction
 #pragma unroll
             for (int j = 0; j < kMaxPer; ++j) {
                 const int k = (ctid + j * kConsumers) * 4;
@@ -458,12 +555,13 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
                     *reinterpret_cast<uint2*>(xs + bi * K + k) = o;
                 }
             }
+            if ((P.debug & 0x4000) && ctid == 0) t_probe = globaltimer();  // after the bf16 stores
             if (bi + 1 < nb) bar_sync(1, kConsumers);  // red[] is reused
         }
     }
     for (int i = ctid; i < nseg * R * nb; i += kConsumers) acc[i] = 0.f;
     bar_sync(1, kConsumers);
-    const uint64_t t_pro = ctid == 0 ? globaltimer() : 0;
+    const uint64_t t_pro = ctid == 0 ? (t_probe ? t_probe : globaltimer()) : 0;
 
     gemv_stream(ring, warp, lane, nseg, static_cast<int>(sp.u1 - sp.u0),
                 static_cast<int>(sp.u0 - static_cast<long long>(r0 / 16) * (K / 16)), K, nb, xs,
@@ -1152,6 +1250,22 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     float* st = sc + G * CH;             // [G][4]: running max, running sum, block rescale
     const float* q = reinterpret_cast<const float*>(op.p[0]) + rb + static_cast<long long>(g) * G * dh;
     for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
+    // flags bit 10 (no merge task): the group's last split also folds in the new token
+    // -- cache row s, appended by the q/k/v projection this task waited on -- so the
+    // partials alone make the attention output and the group's consumer (the output
+    // projection's prologue, gemv_merge_prologue) merges them.  Its k/v rows load with q.
+    const int nsl = attn_splits_base(op, P.binding);
+    const bool fold = !kMMA && (op.flags & 1024) && c == (nsl > 0 ? nsl : 1) - 1;
+    float* kv_new = st + 4 * G + 8;  // [2][dh] new k, v
+    if (fold) {
+        const long long row = static_cast<long long>(bq) * op.i[8] + (static_cast<long long>(g) * op.i[3] + s) * dh;
+        const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + row;
+        const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + row;
+        for (int d = ctid; d < dh; d += kConsumers) {
+            kv_new[d] = bf2f(__ldcg(kn + d));
+            kv_new[dh + d] = bf2f(__ldcg(vn + d));
+        }
+    }
     if (ctid < G) {
         st[4 * ctid] = -INFINITY;
         st[4 * ctid + 1] = 0.f;
@@ -1193,6 +1307,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         }
     }
     bar_sync(1, kConsumers);
+    if ((P.debug & 0x1000) && t_split && ctid == 0) *t_split = globaltimer();  // probe: q staged
     if constexpr (kMMA) {
         if (!attn_split_mma(P, op, gi, c, ab, s, qs, qstride, sc, st, ring, ctid)) return;
     } else {
@@ -1231,6 +1346,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
                 sc[h * CH + p] = (a0 + a1) * scale;
             }
             bar_sync(1, kConsumers);
+            if ((P.debug & 0x2000) && blk == 0 && t_split && ctid == 0) *t_split = globaltimer();  // probe: scores
             if (ctid == Ring::owner(ck) * 32) ring.release(ck);
             // online softmax statistics per head (warp h), probabilities in place
             for (int h = warp; h < G; h += kConsumerWarps) {
@@ -1286,6 +1402,37 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             bar_sync(1, kConsumers);  // sc / st are reused by the next block
             if (ctid == Ring::owner(cv) * 32) ring.release(cv);
         }
+        // flags bit 10 (no merge task): the group's last split also folds in the new
+        // token -- cache row s, appended by the q/k/v projection this task waited on --
+        // so the partials alone make the attention output and the consumer of the
+        // group (the output projection's prologue) merges them
+        const int nsl = attn_splits_base(op, P.binding);
+        if ((P.debug & 0x4000) && t_split && ctid == 0) *t_split = globaltimer();  // probe: blocks done
+        if (fold) {
+            for (int h = warp; h < G; h += kConsumerWarps) {
+                float dot = 0.f;
+                for (int d = lane; d < dh; d += 32) dot += qs[h * qstride + d] * kv_new[d];
+                const float snew = warp_sum(dot) * scale;
+                if (lane == 0) {
+                    const float mo = st[4 * h], mn = fmaxf(mo, snew);
+                    const float alpha = __expf(mo - mn), en = __expf(snew - mn);
+                    st[4 * h] = mn;
+                    st[4 * h + 1] = st[4 * h + 1] * alpha + en;
+                    st[4 * h + 2] = alpha;
+                    st[4 * h + 3] = en;
+                }
+            }
+            bar_sync(1, kConsumers);
+    #pragma unroll
+            for (int j = 0; j < kOutMax; ++j) {
+                const int idx = ctid + j * kConsumers;
+                if (idx >= G * half) break;
+                const int h = idx / half, dp = idx - h * half;
+                const float alpha = st[4 * h + 2], en = st[4 * h + 3];
+                o0[j] = fmaf(en, kv_new[dh + 2 * dp], o0[j] * alpha);
+                o1[j] = fmaf(en, kv_new[dh + 2 * dp + 1], o1[j] * alpha);
+            }
+        }
         // the unnormalised partial (m, l, o) of every q head of the group
         float* part = reinterpret_cast<float*>(op.p[3]);
     #pragma unroll
@@ -1302,7 +1449,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             }
         }
     }
-    if (t_split && ctid == 0) *t_split = globaltimer();  // split work done (trace: prologue stamp)
+    if ((P.debug & 0x7000) == 0 && t_split && ctid == 0) *t_split = globaltimer();  // split work done (trace: prologue stamp)
     if (op.flags & 2) {  // fused merge: the split of group g that arrives last merges it
         volatile int* flag = reinterpret_cast<volatile int*>(st + 4 * G);
         bar_sync(1, kConsumers);
@@ -1788,6 +1935,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         int first_notify = -1;
         if (ctid == 0) {
             if (v.ne > v.nb) first_notify = __ldg(P.notifies + v.nb);
+            misc[12] = s;  // the wait episode (L2 run-ahead)
             misc[2] = 1;  // consumers blocked on an Event Tensor: HBM idles, the producer may fill L2
             bool ok = (P.debug & 1) ? true : wait_range(P, v.wb, v.we, s, worker);
             misc[2] = 0;
@@ -1872,6 +2020,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         }
     }
     if (ctid == 0) {
+        misc[11] = 1;  // queue done: the L2 run-ahead warp exits
         if (P.step_limit <= 0) atomicAdd(&P.status->executed, executed);
         atomicAdd(&P.status->noops, noops);
     }
@@ -1976,6 +2125,63 @@ __device__ __noinline__ bool tc_produce(const StaticParams& P, uint8_t* smem, co
     return true;
 }
 
+// L2 run-ahead of the producer (static scheduler).  While the consumers sit in
+// an Event Tensor wait (misc[2]) the ring fills within a few microseconds and
+// HBM would idle for the rest of the hop; the producer then walks a second
+// cursor ahead of the ring and prefetches the next slots' bytes into L2
+// (cp.async.bulk.prefetch.L2), at most P.l2_ahead bytes beyond the ring, so the
+// ring refills from L2 once the wait ends.  Only during waits: in steady
+// streaming the same bytes would cross L2 twice for nothing.  Data-dependent
+// (lazy) slots are skipped -- their extents exist only after their waits -- so
+// a producer held at a routed expert slot keeps prefetching the later
+// non-routed work (the next layer's projections).
+struct L2Cursor {
+    int slot;        // slot of the next chunk to prefetch
+    int chunk;       // its chunk index in `plan`
+    int n;           // chunks of `plan` (-1: plan of `slot` not made yet)
+    long long ahead; // bytes prefetched beyond the ring cursor
+    StreamPlan plan;
+};
+
+__device__ __noinline__ bool l2_step(const StaticParams& P, const SlotTable& T, int qb, int qe, L2Cursor& L) {
+    while (L.slot < qe) {
+        if (L.n < 0) {
+            const SlotView v = view_slot(P, T, L.slot, qb);
+            const et_op& op = P.ops[v.call];
+            if (v.masked || v.lazy || !op_streams(op.kind)) {
+                ++L.slot;
+                L.chunk = 0;
+                continue;
+            }
+            L.plan = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
+            L.n = L.plan.tc_np ? 0 : L.plan.total_chunks();
+        }
+        if (L.chunk < L.n) {
+            const Chunk ch = L.plan.chunk(L.chunk++);
+            bulk_prefetch_l2(ch.src, ch.bytes);
+            L.ahead += ch.bytes;
+            return true;
+        }
+        ++L.slot;
+        L.chunk = 0;
+        L.n = -1;
+    }
+    return false;
+}
+
+// The ring issues chunk c of slot s: bytes the cursor prefetched stop counting
+// as run-ahead; a cursor at or behind the ring jumps to the chunk after it.
+__device__ __forceinline__ void l2_passed(L2Cursor& L, int s, int c, uint32_t bytes) {
+    if (L.slot > s || (L.slot == s && L.chunk > c)) {
+        L.ahead = L.ahead > bytes ? L.ahead - bytes : 0;
+    } else {
+        if (L.slot != s) L.n = -1;
+        L.slot = s;
+        L.chunk = c + 1;
+        L.ahead = 0;
+    }
+}
+
 __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     if ((threadIdx.x & 31) != 0) return;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -1985,6 +2191,19 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
     unsigned long long cseq = 0;  // chunks issued to the ring
     unsigned int xq = 0;          // activation pieces issued to the tensor-core x buffers
+    long long pcum = 0;           // bytes of non-lazy chunks issued (the prefetch warp's reference)
+    const bool l2_lsu = (P.debug & 128) == 0;  // run-ahead by the prefetch warp (default) or by TMA here
+    const long long l2win = (P.prefetch && !l2_lsu) ? P.l2_ahead : 0;
+    const bool l2_ungated = (P.debug & 64) != 0;  // timing experiment: run ahead whenever the ring is full
+    L2Cursor L;
+    L.slot = qb;
+    L.chunk = 0;
+    L.n = -1;
+    L.ahead = 0;
+    // one prefetch when the run-ahead is allowed now; false: spin as before
+    auto l2_try = [&]() -> bool {
+        return l2win > 0 && L.ahead < l2win && (l2_ungated || misc[2] != 0) && l2_step(P, T, qb, qe, L);
+    };
     for (int s = qb; s < qe; ++s) {
         SlotView v = view_slot(P, T, s, qb);
         if (v.masked) continue;
@@ -1994,6 +2213,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             // data-dependent extents are known only once the slot's waits pass
             while (misc[1] <= s) {
                 if (aborted(P.status)) return;
+                l2_try();
             }
             if (v.lazy && extent_masked(P, v.call, v.coord)) continue;
         }
@@ -2009,6 +2229,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             uint32_t spins = 0;
             uint64_t t0 = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
+                if (l2_try()) continue;
                 if ((++spins & 1023u) == 0) {
                     if (aborted(P.status)) return;
                     if (t0 == 0) t0 = globaltimer();
@@ -2019,12 +2240,81 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 }
             }
             const Chunk ch = pl.chunk(c);
+            if (l2win > 0 && !l2_lsu) l2_passed(L, s, c, ch.bytes);
+            misc[9] = s;
+            misc[10] = c;
+            if (!v.lazy) {
+                pcum += ch.bytes;
+                reinterpret_cast<volatile long long*>(misc)[7] = pcum;
+            }
             if (P.debug & 4) {  // timing experiment: stages "fill" instantly (no HBM traffic)
                 mbar_arrive(&full[stage]);
             } else {
                 mbar_arrive_expect_tx(&full[stage], ch.bytes);
                 bulk_g2s(smem + kSmemRing + stage * kStageBytes, ch.src, ch.bytes, &full[stage], pol);
             }
+        }
+    }
+}
+
+// L2 run-ahead by warp 9 (static scheduler, workers without a DMA queue).  While
+// the consumers sit in an Event Tensor wait (misc[2]) the prefetch warp walks
+// the slots ahead of the producer and prefetches their bytes into L2 with
+// prefetch.global.L2 (one 128-byte line per lane per instruction), keeping at
+// most P.l2_ahead bytes in front of the producer's ring position.  Positions
+// are compared as cumulative bytes of the non-lazy streaming chunks: the
+// producer publishes its count (misc64[7]) and its (slot, chunk) (misc[9],
+// misc[10]); a prefetch cursor that fell behind jumps to the producer.  The
+// LSU path keeps the prefetches out of the TMA unit, so the ring's own bulk
+// copies never queue behind them.  Data-dependent (lazy) slots are skipped
+// (debug bit 32: the walk stops at them instead).
+__device__ void l2_ahead_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
+    volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
+    volatile long long* pbytes = reinterpret_cast<volatile long long*>(smem + kSmemMisc) + 7;
+    const int lane = threadIdx.x & 31;
+    const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
+    const bool stop_lazy = (P.debug & 32) != 0;
+    int slot = qb, chunk = 0, n = -1;
+    long long fbytes = 0;  // cumulative bytes up to the cursor
+    StreamPlan pl;
+    while (misc[11] == 0 && slot < qe) {
+        if (aborted(P.status)) return;
+        const long long pb = *pbytes;
+        if (pb > fbytes) {  // behind the producer: continue from its position
+            const int ps = misc[9], pc = misc[10];
+            if (ps != slot) n = -1;
+            slot = ps < qb ? qb : ps;
+            chunk = pc + 1;
+            fbytes = pb;
+        }
+        if (misc[2] == 0 || fbytes - pb >= P.l2_ahead) {
+            __nanosleep(64);
+            continue;
+        }
+        if (n < 0) {
+            const SlotView v = view_slot(P, T, slot, qb);
+            const et_op& op = P.ops[v.call];
+            if (v.lazy && stop_lazy) {
+                __nanosleep(64);
+                continue;
+            }
+            if (v.masked || v.lazy || !op_streams(op.kind)) {
+                ++slot;
+                chunk = 0;
+                continue;
+            }
+            pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
+            n = pl.tc_np ? 0 : pl.total_chunks();
+        }
+        if (chunk < n) {
+            const Chunk ch = pl.chunk(chunk++);
+            for (uint32_t off = lane * 128u; off < ch.bytes; off += 32u * 128u)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ch.src + off));
+            fbytes += ch.bytes;
+        } else {
+            ++slot;
+            chunk = 0;
+            n = -1;
         }
     }
 }
@@ -2110,6 +2400,11 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
         misc[0] = 0;
         misc[1] = 0;
         misc[2] = 0;
+        misc[9] = -1;
+        misc[10] = 0;
+        misc[11] = 0;
+        misc[12] = -1;
+        reinterpret_cast<volatile long long*>(misc)[7] = 0;
     }
     // slot table for this CTA's queue
     SlotTable T;
@@ -2148,6 +2443,8 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
         producer_loop(P, worker, smem, T);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
         dma_loop(P);
+    } else if (warp == kDmaWarp && P.prefetch && P.l2_ahead > 0 && (P.debug & 128) == 0) {
+        l2_ahead_loop(P, worker, smem, T);
     }
 }
 

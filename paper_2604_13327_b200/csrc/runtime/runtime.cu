@@ -497,6 +497,19 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
         else if (k == ET_OP_GEMV_TC || k == ET_OP_NORM) variant |= 2;
     }
     for (int32_t c = 0; c < num_calls; ++c) {
+        const et_op& o = ops[c];
+        if (o.kind == ET_OP_GEMV && o.i[3] == 2) {  // attention-merge prologue (megakernel.cu body_gemv)
+            if (o.i[5] >= 0 || o.i[8] <= 0 || o.i[1] % o.i[8] || o.i[11] <= 0 || o.i[12] <= 0 ||
+                3LL * (o.i[1] / o.i[8]) * o.i[12] > etk::kAccFloats || !o.p[2])
+                return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": GEMV x mode 2 (attention merge) "
+                                "needs b = 1, K a multiple of head_dim, and 3 * heads * split cap <= " +
+                                std::to_string(etk::kAccFloats));
+        }
+        if (o.kind == ET_OP_ATTN_SPLIT && (o.flags & 1024) && (variant & 2))
+            return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": attention flags bit 10 (new token "
+                            "folded by the last split) is implemented by the mma.sync instantiations only");
+    }
+    for (int32_t c = 0; c < num_calls; ++c) {
         if (ops[c].kind != ET_OP_ATTN_SPLIT && ops[c].kind != ET_OP_ATTN_MERGE) continue;
         const int dh = ops[c].i[0], G = ops[c].i[1], CH = ops[c].i[2];
         if ((ops[c].flags & 256) && dh % 64 != 0)  // chunk j ^ (pos % 8) must stay inside the row
@@ -752,6 +765,12 @@ int et_sync(et_runtime* rt, et_step_info* info) {
 int et_set_debug(et_runtime* rt, int32_t bits) {
     if (!rt) return ET_ERR_INVALID;
     rt->debug = bits;
+    return ET_OK;
+}
+
+int et_set_l2_prefetch(et_runtime* rt, int64_t bytes) {
+    if (!rt) return ET_ERR_INVALID;
+    rt->cfg.l2_prefetch_bytes = bytes;
     return ET_OK;
 }
 

@@ -248,7 +248,7 @@ class DecodeModel:
 
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
-                 l2_prefetch=-1, residual="split", fused_merge=True, balance=True, grouped=True,
+                 l2_prefetch=512 << 10, residual="split", fused_merge=True, balance=True, grouped=True,
                  scheduler="static", early_push=False):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
@@ -325,7 +325,11 @@ class DecodeModel:
                                                ptr(kc), ptr(vc), ptr(self.inv_freq)]))
             attn_i = [dh, G, CH, self.capacity, s_slot, self.max_splits, cfg.kv_heads]
             attn_p = [ptr(self.q), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(self.arrive[l])]
-            if self.fused_merge:  # flags bit 1: the last split of a kv head merges it
+            if self.grouped:
+                # flags bit 10: the last split folds in the new token; the output projection's
+                # prologue merges each group's partials (no merge task, one hop less)
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p, flags=1024))
+            elif self.fused_merge:  # flags bit 1: the last split of a kv head merges it
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p, flags=2))
             else:
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p))
@@ -333,9 +337,10 @@ class DecodeModel:
             if self.grouped:
                 # per kv-head group: h += Wo[:, group cols] a_group (red.global.add), each
                 # group's tasks released by its own merge
-                ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 0, EPI_ADD, -1, 0, 16, 0, cfg.q_rows, 0, 0, 0,
-                                               self.oproj_group_tasks],
-                                   flags=16, p=[ptr(L["wo"]), 0, ptr(self.attn), 0, ptr(self.h_a)]))
+                # x mode 2: the activations are the merge of the group's attention partials
+                ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 2, EPI_ADD, -1, s_slot, 16, dh, 0, self.max_splits, CH,
+                                               self.max_splits, self.oproj_group_tasks],
+                                   flags=16, p=[ptr(L["wo"]), 0, ptr(self.partials), 0, ptr(self.h_a)]))
             elif self.residual == "split":
                 # row-parallel products add into the residual stream in place: split-K
                 # spans (every task streams the same bytes), red.global.add epilogue
