@@ -238,7 +238,7 @@ class BatchDecodeModel:
         self.attn = torch.zeros(npad * nq, dtype=torch.bfloat16, device=dev)    # attention out (operand layout)
         self.act = torch.zeros(npad * I, dtype=torch.bfloat16, device=dev)      # silu(gate)*up (operand layout)
         # split stride max(splits, 8): a lone split leaves its 8 warp partials (flags bit 9)
-        self.partials = torch.zeros(B * cfg.heads, max(8, self.max_splits), cfg.head_dim + 2, dtype=torch.float32,
+        self.partials = torch.zeros(B * cfg.heads, max(8, self.max_splits), cfg.head_dim + 4, dtype=torch.float32,
                                     device=dev)
         self.arrive = torch.zeros(cfg.layers, B * cfg.kv_heads, dtype=torch.int32, device=dev)
         self.logits = torch.zeros(B, cfg.vocab, dtype=torch.float32, device=dev)

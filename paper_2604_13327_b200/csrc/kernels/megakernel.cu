@@ -129,15 +129,18 @@ __device__ __forceinline__ bool sticky_status(const StaticParams& P) {
 // Acquire loads: the producer's data written before its release increment is
 // visible to this thread, and to the rest of the CTA after the barrier that
 // follows (PTX causality order through bar.sync).
+// Acquire polls (debug bit 0x10000: relaxed polls and one acquire fence at the
+// end -- measured slower: the fence's MEMBAR sits on the critical path).
 __device__ bool wait_range(const StaticParams& P, int b, int e, int s, int worker) {
+    const bool relaxed = (P.debug & 0x10000) != 0;
     for (int w = b; w < e; ++w) {
         const int el = __ldg(P.waits + w);
         const uint32_t need = static_cast<uint32_t>(__ldg(P.initial_counts + el));
-        uint32_t v = ld_acquire(P.cnt + el);
+        uint32_t v = relaxed ? ld_relaxed(P.cnt + el) : ld_acquire(P.cnt + el);
         if (v >= need) continue;
         const uint64_t t0 = globaltimer();
         uint32_t it = 0;
-        while ((v = ld_acquire(P.cnt + el)) < need) {
+        while ((v = relaxed ? ld_relaxed(P.cnt + el) : ld_acquire(P.cnt + el)) < need) {
             if ((++it & 255u) == 0) {
                 if (aborted(P.status)) return false;
                 if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
@@ -147,6 +150,7 @@ __device__ bool wait_range(const StaticParams& P, int b, int e, int s, int worke
             }
         }
     }
+    if (relaxed && e > b) fence_acquire_gpu();
     return true;
 }
 
@@ -390,17 +394,40 @@ __device__ __forceinline__ void gemv_stream(Ring& ring, int warp, int lane, int 
     ring.seq = c;
 }
 
+// Shared-memory mbarrier of the attention-merge prologue's bulk loads (behind the
+// tensor-core barriers in the misc area); its phase count is misc[13].
+__device__ __forceinline__ uint64_t* merge_bar(uint8_t* smem) {
+    return reinterpret_cast<uint64_t*>(smem + kSmemMisc + 464);
+}
+constexpr int kMergeBulkOff = 2048;                      // partials staged at xs + 2 KB ...
+constexpr int kMergeBulkMax = kXBytes + kAccFloats * 4 - kMergeBulkOff - 2048;  // ... up to acc's last 2 KB
+
 // Attention-merge prologue of a GEMV (x mode 2, b = 1): activation slice g is the
 // merge of kv group g's attention splits, whose unnormalised partials (m, l, o)
-// per q head the splits left in p2 (fp32 [heads][i10][dh + 2]; ATTN_SPLIT flags
+// per q head the splits left in p2 (fp32 [heads][i10][kPartHead + dh]; ATTN_SPLIT flags
 // bit 10):  x = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c  (M = max_c m_c),
 // so the attention needs no merge task and its consumer no second hop.
 // i6 = position slot, i8 = head_dim, i10 = split stride, i11 = CH, i12 = split cap.
-// Out of line: its 32 loads in flight would otherwise crowd the GEMV loop's registers.
-__device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et_op& op, int gsel, uint16_t* xs,
-                                                 float* acc, int ctid) {
+// p5 (optional): the group's raw split-K q/k/v accumulators (fp32: q [i9 * G * dh],
+// k, v [i9 * dh]; i9 = kv heads), consumed by now -- task t of the group's i13
+// zeroes its share for the next step (the splits that read them all arrived).
+// kOut outputs per thread (K <= 256 * kOut), kPass splits per batch of loads.
+// Out of line: its loads in flight would otherwise crowd the GEMV loop's registers.
+template <int kOut, int kPass>
+__device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et_op& op, int gsel, int tsel,
+                                                 uint16_t* xs, float* acc, int ctid, uint64_t* t_probe) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int K = op.i[1];
+    if (op.p[5]) {
+        const int dh = op.i[8], G = K / dh, nkv = op.i[9] * dh, nq = op.i[9] * G * dh;
+        const int n = G * dh + 2 * dh, per = (n + op.i[13] - 1) / op.i[13];
+        float* raw = reinterpret_cast<float*>(op.p[5]);
+        for (int i = tsel * per + ctid; i < (tsel + 1) * per && i < n; i += kConsumers) {
+            const int off = i < G * dh ? gsel * G * dh + i
+                            : i < G * dh + dh ? nq + gsel * dh + (i - G * dh) : nq + nkv + gsel * dh + (i - G * dh - dh);
+            raw[off] = 0.f;
+        }
+    }
 
     const int dh = op.i[8], G = K / dh, maxs = op.i[10], CH = op.i[11];
     const long long s = P.binding[op.i[6]];
@@ -408,10 +435,68 @@ __device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et
     if (nsl > op.i[12]) nsl = op.i[12];
     const int ns = nsl > 0 ? static_cast<int>(nsl) : 1;
     const float* part = reinterpret_cast<const float*>(op.p[2]) +
-                        static_cast<long long>(gsel) * G * maxs * (dh + 2);
+                        static_cast<long long>(gsel) * G * maxs * (dh + kPartHead);
+    const int row = dh + kPartHead;
+    const uint32_t hbytes = static_cast<uint32_t>(ns) * row * 4;  // one head's used splits, contiguous
+    if (G * hbytes <= static_cast<uint32_t>(kMergeBulkMax) && 3 * G * ns <= 512) {
+        // Bulk path: the group's partials reach shared memory by G bulk copies (the TMA
+        // engine keeps far more bytes in flight than 256 threads' loads: 33 KB take one
+        // L2 round trip instead of ~3 us of load-slot-limited requests).
+        float* ps = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xs) + kMergeBulkOff);  // [G][ns][row]
+        float* ml = acc + kAccFloats - 512;  // [G][ns][2]
+        float* wts = ml + 2 * G * ns;        // [G][ns]
+        volatile int* misc = reinterpret_cast<volatile int*>(reinterpret_cast<uint8_t*>(xs) - kSmemX + kSmemMisc);
+        uint64_t* bar = merge_bar(reinterpret_cast<uint8_t*>(xs) - kSmemX);
+        const uint32_t par = static_cast<uint32_t>(misc[13]) & 1u;
+        if (ctid == 0) {
+            fence_proxy_async_global();  // partials: generic stores of other CTAs, acquired by the wait
+            fence_proxy_async();         // xs was last written through the generic proxy
+            mbar_arrive_expect_tx(bar, G * hbytes);
+            for (int h = 0; h < G; ++h)
+                bulk_g2s_keep(ps + h * ns * row, part + static_cast<long long>(h) * maxs * row, hbytes, bar);
+        }
+        mbar_wait(bar, par);
+        if ((P.debug & 0x1000) && ctid == 0) *t_probe = globaltimer();  // partials staged
+        for (int i = ctid; i < G * ns; i += kConsumers) {
+            ml[2 * i] = ps[i * row];
+            ml[2 * i + 1] = ps[i * row + 1];
+        }
+        bar_sync(1, kConsumers);
+        for (int hh = warp; hh < G; hh += kConsumerWarps) {
+            float M = -INFINITY;
+            for (int c = lane; c < ns; c += 32) M = fmaxf(M, ml[2 * (hh * ns + c)]);
+            M = warp_max(M);
+            float L = 0.f;
+            for (int c = lane; c < ns; c += 32) {
+                const float e = __expf(ml[2 * (hh * ns + c)] - M);
+                wts[hh * ns + c] = e;
+                L += e * ml[2 * (hh * ns + c) + 1];
+            }
+            const float inv = 1.f / warp_sum(L);
+            __syncwarp();
+            for (int c = lane; c < ns; c += 32) wts[hh * ns + c] *= inv;
+        }
+        bar_sync(1, kConsumers);
+        if ((P.debug & 0x4000) && ctid == 0) *t_probe = globaltimer();  // weights
+        for (int idx = ctid; idx < K; idx += kConsumers) {
+            const int hh = idx / dh, d = idx - hh * dh;
+            const float* w = wts + hh * ns;
+            const float* pc = ps + hh * ns * row + kPartHead + d;
+            float o = 0.f, o2 = 0.f;
+            int c = 0;
+            for (; c + 1 < ns; c += 2) {
+                o = fmaf(w[c], pc[c * row], o);
+                o2 = fmaf(w[c + 1], pc[(c + 1) * row], o2);
+            }
+            if (c < ns) o = fmaf(w[c], pc[c * row], o);
+            xs[idx] = f2bf(o + o2);
+        }
+        bar_sync(1, kConsumers);  // ps / ml / wts are done with (acc is zeroed by the caller)
+        if (ctid == 0) misc[13] = misc[13] + 1;
+        return;
+    }
     float* ml = acc;              // [G][ns][2] (acc is zeroed after the prologue)
     float* wts = acc + 2 * G * ns;  // [G][ns]
-    constexpr int kPass = 16, kOut = 2;  // splits per register batch; outputs per thread (K <= 512)
     float ov[kOut][kPass];
 #pragma unroll
     for (int j = 0; j < kOut; ++j) {
@@ -419,15 +504,17 @@ __device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et
         const int hh = idx / dh, d = idx - hh * dh;
 #pragma unroll
         for (int c = 0; c < kPass; ++c)
-            ov[j][c] = (idx < K && c < ns) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d)
+            ov[j][c] = (idx < K && c < ns) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + kPartHead) + kPartHead + d)
                                            : 0.f;
     }
     for (int i = ctid; i < G * ns; i += kConsumers) {
-        const float* pr = part + (static_cast<long long>(i / ns) * maxs + i % ns) * (dh + 2);
+        const float* pr = part + (static_cast<long long>(i / ns) * maxs + i % ns) * (dh + kPartHead);
         ml[2 * i] = __ldcg(pr);
         ml[2 * i + 1] = __ldcg(pr + 1);
     }
+    if ((P.debug & 0x1000) && ctid == 0) *t_probe = globaltimer() + (ov[0][0] == 1234.5f ? 1 : 0);  // loads landed
     bar_sync(1, kConsumers);
+    if ((P.debug & 0x2000) && ctid == 0) *t_probe = globaltimer();  // every thread's loads landed
     for (int hh = warp; hh < G; hh += kConsumerWarps) {
         float M = -INFINITY;
         for (int c = lane; c < ns; c += 32) M = fmaxf(M, ml[2 * (hh * ns + c)]);
@@ -443,6 +530,7 @@ __device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et
         for (int c = lane; c < ns; c += 32) wts[hh * ns + c] *= inv;
     }
     bar_sync(1, kConsumers);
+    if ((P.debug & 0x4000) && ctid == 0) *t_probe = globaltimer();  // weights
 #pragma unroll
     for (int j = 0; j < kOut; ++j) {
         const int idx = ctid + j * kConsumers;
@@ -459,7 +547,7 @@ __device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et
                 float pv[kPass];
 #pragma unroll
                 for (int u = 0; u < kPass; ++u)
-                    pv[u] = c0 + u < ns ? __ldcg(part + (static_cast<long long>(hh) * maxs + c0 + u) * (dh + 2) + 2 + d)
+                    pv[u] = c0 + u < ns ? __ldcg(part + (static_cast<long long>(hh) * maxs + c0 + u) * (dh + kPartHead) + kPartHead + d)
                                         : 0.f;
 #pragma unroll
                 for (int u = 0; u < kPass; ++u)
@@ -468,11 +556,11 @@ __device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et
             xs[idx] = f2bf(o + o2);
         }
     }
-    for (int idx = ctid + kOut * kConsumers; idx < K; idx += kConsumers) {  // K > 512
+    for (int idx = ctid + kOut * kConsumers; idx < K; idx += kConsumers) {  // K > 256 * kOut
         const int hh = idx / dh, d = idx - hh * dh;
         float o = 0.f;
         for (int c = 0; c < ns; ++c)
-            o = fmaf(wts[hh * ns + c], __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d), o);
+            o = fmaf(wts[hh * ns + c], __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + kPartHead) + kPartHead + d), o);
         xs[idx] = f2bf(o);
     }
     bar_sync(1, kConsumers);  // ml / wts live in acc, zeroed by the caller
@@ -509,7 +597,8 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
             reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x + static_cast<long long>(bi) * xstride) + kk);
         }
     } else if (op.i[3] == 2) {
-        gemv_merge_prologue(P, op, grouped ? si.coord[0] : 0, xs, acc, ctid);
+        if (K <= 2 * kConsumers) gemv_merge_prologue<2, 16>(P, op, grouped ? si.coord[0] : 0, grouped ? si.coord[1] : 0, xs, acc, ctid, &t_probe);
+        else gemv_merge_prologue<4, 8>(P, op, grouped ? si.coord[0] : 0, grouped ? si.coord[1] : 0, xs, acc, ctid, &t_probe);
     } else {
         // RMSNorm prologue: one pass over the fp32 residual stream held in
         // registers (K <= 8192), sum of squares reduced across the CTA
@@ -873,9 +962,9 @@ __device__ __noinline__ void qk_norm_rope(float* v, int dh, const float* w, floa
         sc = rsqrtf(ss / static_cast<float>(dh) + eps);
     }
     for (int j = lane; j < dh / 2; j += 32) {
-        const float a = v[2 * j] * sc * (w ? __ldg(w + 2 * j) : 1.f), b = v[2 * j + 1] * sc * (w ? __ldg(w + 2 * j + 1) : 1.f);
+        const float a = v[2 * j] * sc * (w ? w[2 * j] : 1.f), b = v[2 * j + 1] * sc * (w ? w[2 * j + 1] : 1.f);
         float sn, cs;
-        sincosf(static_cast<float>(pos) * __ldg(invf + j), &sn, &cs);
+        sincosf(static_cast<float>(pos) * invf[j], &sn, &cs);
         v[2 * j] = a * cs - b * sn;
         v[2 * j + 1] = a * sn + b * cs;
     }
@@ -903,7 +992,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     const long long s = P.binding[op.i[4]];
     const int nspl = kTcLayout ? attn_splits_with_data(op, P.binding) : attn_splits_base(op, P.binding);
     const float scale = op.f[0];
-    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(gi) * G * maxs * (dh + 2);
+    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(gi) * G * maxs * (dh + kPartHead);
     const long long cb = static_cast<long long>(bq) * op.i[8];  // this sequence's cache
     const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + cb + (static_cast<long long>(g) * cap + s) * dh;
     const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + cb + (static_cast<long long>(g) * cap + s) * dh;
@@ -929,11 +1018,11 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
         vv[j] = idx < G * dh ? bf2f(__ldcg(vn + ((((d >> 3) ^ csw)) << 3) + (d & 7))) : 0.f;
 #pragma unroll
         for (int c = 0; c < kPass; ++c)
-            ov[j][c] = (idx < G * dh && c < nspl) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + 2) + 2 + d)
+            ov[j][c] = (idx < G * dh && c < nspl) ? __ldcg(part + (static_cast<long long>(hh) * maxs + c) * (dh + kPartHead) + kPartHead + d)
                                                  : 0.f;
     }
     for (int i = ctid; i < G * nspl; i += kConsumers) {
-        const float* pr = part + (static_cast<long long>(i / nspl) * maxs + i % nspl) * (dh + 2);
+        const float* pr = part + (static_cast<long long>(i / nspl) * maxs + i % nspl) * (dh + kPartHead);
         ml[2 * i] = __ldcg(pr);
         ml[2 * i + 1] = __ldcg(pr + 1);
     }
@@ -978,7 +1067,7 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
             float pv[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                pv[u] = c0 + u < nspl ? __ldcg(part + (static_cast<long long>(hh) * maxs + c0 + u) * (dh + 2) + 2 + d)
+                pv[u] = c0 + u < nspl ? __ldcg(part + (static_cast<long long>(hh) * maxs + c0 + u) * (dh + kPartHead) + kPartHead + d)
                                       : 0.f;
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -1175,7 +1264,7 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
         float* part = reinterpret_cast<float*>(op.p[3]);
         for (int i = ctid; i < G * dh; i += kConsumers) {
             const int h = i / dh, d = i - h * dh;
-            part[((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + 2) + 2 + d] = oacc[i];
+            part[((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + kPartHead) + kPartHead + d] = oacc[i];
         }
         if (ctid < G) {
             float M = -INFINITY, L = 0.f;
@@ -1184,7 +1273,7 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
                 const float mw = mW[w * 8 + ctid];
                 if (mw != -INFINITY) L += lW[w * 8 + ctid] * __expf(mw - M);
             }
-            float* pr = part + ((static_cast<long long>(gi) * G + ctid) * maxs + c) * (dh + 2);
+            float* pr = part + ((static_cast<long long>(gi) * G + ctid) * maxs + c) * (dh + kPartHead);
             pr[0] = M;
             pr[1] = L;
         }
@@ -1198,25 +1287,25 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
         if (mt < nks) {
             const int d0 = 16 * mt + g8;
             if (h0 < G) {
-                float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + sub) * (dh + 2);
-                pr[2 + d0] = o[mt][0];
-                pr[10 + d0] = o[mt][2];
+                float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + sub) * (dh + kPartHead);
+                pr[kPartHead + d0] = o[mt][0];
+                pr[kPartHead + 8 + d0] = o[mt][2];
             }
             if (h0 + 1 < G) {
-                float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + sub) * (dh + 2);
-                pr[2 + d0] = o[mt][1];
-                pr[10 + d0] = o[mt][3];
+                float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + sub) * (dh + kPartHead);
+                pr[kPartHead + d0] = o[mt][1];
+                pr[kPartHead + 8 + d0] = o[mt][3];
             }
         }
     }
     if (g8 == 0) {  // lanes 0..3: (m, l) of heads h0, h0+1
         if (h0 < G) {
-            float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + sub) * (dh + 2);
+            float* pr = part + ((static_cast<long long>(gi) * G + h0) * maxs + sub) * (dh + kPartHead);
             pr[0] = m0;
             pr[1] = l0;
         }
         if (h0 + 1 < G) {
-            float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + sub) * (dh + 2);
+            float* pr = part + ((static_cast<long long>(gi) * G + h0 + 1) * maxs + sub) * (dh + kPartHead);
             pr[0] = m1;
             pr[1] = l1;
         }
@@ -1257,7 +1346,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     const int nsl = attn_splits_base(op, P.binding);
     const bool fold = !kMMA && (op.flags & 1024) && c == (nsl > 0 ? nsl : 1) - 1;
     float* kv_new = st + 4 * G + 8;  // [2][dh] new k, v
-    if (fold) {
+    if (fold && !(kQK && (op.flags & 1))) {  // (q/k-norm mode: normalised from the raw projection below)
         const long long row = static_cast<long long>(bq) * op.i[8] + (static_cast<long long>(g) * op.i[3] + s) * dh;
         const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + row;
         const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + row;
@@ -1272,11 +1361,28 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     }
     if constexpr (kQK) {
         if (op.flags & 1) {  // q-norm + RoPE applied here (q is the raw projection)
+            // the q / k norm weights and the RoPE frequencies load with q (one L2 round
+            // trip; the wait's acquire left L1 cold)
+            float* wqs = kv_new + 2 * dh;  // [dh] q-norm, [dh] k-norm, [dh/2] inverse frequencies
+            {
+                const bool nw = (op.flags & 64) == 0;
+                const float* wq = reinterpret_cast<const float*>(op.p[(op.flags & 2) ? 9 : 5]);
+                const float* wk = reinterpret_cast<const float*>(op.p[6]);
+                const float* fr = reinterpret_cast<const float*>(op.p[7]);
+                for (int d = ctid; d < dh; d += kConsumers) {
+                    if (nw) {
+                        wqs[d] = __ldg(wq + d);
+                        wqs[dh + d] = __ldg(wk + d);
+                    }
+                    if (d < dh / 2) wqs[2 * dh + d] = __ldg(fr + d);
+                }
+            }
             // fused merge: split 0 also normalises + rotates the new k and appends the
             // new k/v (bf16) to the cache row s before it arrives, so the merger reads
             // them like any cached row
-            const bool knew = (op.flags & 2) && c == 0;
-            float* kv = sc;  // [2][dh] scratch before the blocks use sc
+            // no merge task (flags bit 10): the last split does it and keeps them for its fold
+            const bool knew = ((op.flags & 2) && c == 0) || fold;
+            float* kv = fold ? kv_new : sc;  // [2][dh] (sc: scratch before the blocks use it)
             if (knew) {
                 const float* kr = reinterpret_cast<const float*>(op.p[8]) + rb + static_cast<long long>(g) * dh;
                 const float* vr = kr + static_cast<long long>(kvh) * dh;
@@ -1287,11 +1393,8 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             }
             bar_sync(1, kConsumers);
             for (int h = warp; h < G + (knew ? 1 : 0); h += kConsumerWarps)
-                qk_norm_rope(h < G ? qs + h * qstride : kv, dh,
-                             (op.flags & 64) ? nullptr
-                                             : reinterpret_cast<const float*>(op.p[h < G ? ((op.flags & 2) ? 9 : 5) : 6]),
-                             op.f[1],
-                             reinterpret_cast<const float*>(op.p[7]), s, lane);
+                qk_norm_rope(h < G ? qs + h * qstride : kv, dh, (op.flags & 64) ? nullptr : wqs + (h < G ? 0 : dh),
+                             op.f[1], wqs + 2 * dh, s, lane);
             if (knew) {
                 bar_sync(1, kConsumers);
                 const long long cb = static_cast<long long>(bq) * op.i[8];
@@ -1300,8 +1403,11 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
                 const int sw = (op.flags & 256) ? static_cast<int>(s & 7) : 0;  // cache row chunk swizzle
                 for (int d = ctid; d < dh; d += kConsumers) {
                     const int dp = ((((d >> 3) ^ sw)) << 3) | (d & 7);
-                    kc[dp] = f2bf(kv[d]);
-                    vc[dp] = f2bf(kv[dh + d]);
+                    const uint16_t kb = f2bf(kv[d]), vb = f2bf(kv[dh + d]);
+                    kc[dp] = kb;
+                    vc[dp] = vb;
+                    kv[d] = bf2f(kb);  // the fold uses the cached (bf16) row, like every later step
+                    kv[dh + d] = bf2f(vb);
                 }
             }
         }
@@ -1440,9 +1546,9 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             const int idx = ctid + j * kConsumers;
             if (idx >= G * half) break;
             const int h = idx / half, dp = idx - h * half;
-            float* pr = part + ((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + 2);
-            pr[2 + 2 * dp] = o0[j];
-            pr[3 + 2 * dp] = o1[j];
+            float* pr = part + ((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + kPartHead);
+            pr[kPartHead + 2 * dp] = o0[j];
+            pr[kPartHead + 1 + 2 * dp] = o1[j];
             if (dp == 0) {
                 pr[0] = st[4 * h];
                 pr[1] = st[4 * h + 1];
@@ -1482,7 +1588,7 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
     const int nspl = attn_splits_with_data(op, P.binding);
     const int g = si.coord[0];
     const float scale = op.f[0];
-    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + 2);
+    const float* part = reinterpret_cast<const float*>(op.p[3]) + static_cast<long long>(g) * G * maxs * (dh + kPartHead);
     const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + (static_cast<long long>(g) * cap + s) * dh;
     const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + (static_cast<long long>(g) * cap + s) * dh;
     uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]) + static_cast<long long>(g) * G * dh;
@@ -1490,7 +1596,7 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
     float* wts = ml + 2 * G * nspl;     // [G][nspl]
     float* hs = wts + G * nspl;         // [G]: s_new, then e^(s_new-M)/L
     for (int idx = ctid; idx < G * nspl; idx += kConsumers) {
-        const float* pr = part + (static_cast<long long>(idx / nspl) * maxs + idx % nspl) * (dh + 2);
+        const float* pr = part + (static_cast<long long>(idx / nspl) * maxs + idx % nspl) * (dh + kPartHead);
         ml[2 * idx] = __ldcg(pr);
         ml[2 * idx + 1] = __ldcg(pr + 1);
     }
@@ -1552,11 +1658,11 @@ __device__ void body_attn_merge(const StaticParams& P, const et_op& op, const Sl
     bar_sync(1, kConsumers);
     for (int idx = ctid; idx < G * dh; idx += kConsumers) {
         const int hh = idx / dh, d = idx % dh;
-        const float* ph = part + static_cast<long long>(hh) * maxs * (dh + 2) + 2 + d;
+        const float* ph = part + static_cast<long long>(hh) * maxs * (dh + kPartHead) + kPartHead + d;
         const float* w = wts + hh * nspl;
         float o = hs[hh] * bf2f(__ldcg(vn + d));
 #pragma unroll 8
-        for (int c = 0; c < nspl; ++c) o = fmaf(w[c], __ldcg(ph + static_cast<long long>(c) * (dh + 2)), o);
+        for (int c = 0; c < nspl; ++c) o = fmaf(w[c], __ldcg(ph + static_cast<long long>(c) * (dh + kPartHead)), o);
         out[idx] = f2bf(o);
     }
 }
@@ -1846,7 +1952,7 @@ __device__ void body_allreduce(const StaticParams& P, const et_op& op, const Slo
         const uint32_t* f = flags + slot * TP + ctid;
         const uint64_t t0 = globaltimer();
         uint32_t it = 0;
-        while (static_cast<int>(ld_acquire_sys(f) - epoch) < 0) {
+        while (static_cast<int>(ld_relaxed_sys(f) - epoch) < 0) {
             if ((++it & 255u) == 0) {
                 if (aborted(P.status)) break;
                 if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
@@ -1855,6 +1961,7 @@ __device__ void body_allreduce(const StaticParams& P, const et_op& op, const Slo
                 }
             }
         }
+        fence_acquire_sys();
     }
     bar_sync(1, kConsumers);
     const int T = si.ext0, t = si.coord[0];
@@ -2092,9 +2199,8 @@ __device__ __noinline__ bool tc_produce(const StaticParams& P, uint8_t* smem, co
             if (half) break;
             // X(p)
             if (!fenced) {
-                while (dep == 0 ? misc[1] <= key : misc[6] != key) {
-                    if (aborted(P.status)) return false;
-                }
+                for (uint32_t it = 0; dep == 0 ? misc[1] <= key : misc[6] != key;)
+                    if ((++it & 1023u) == 0 && aborted(P.status)) return false;
                 __threadfence();             // the pieces were written by other CTAs before the waits passed
                 fence_proxy_async_global();  // ... with generic stores; the bulk copy reads through the async proxy
                 fenced = true;
@@ -2211,8 +2317,8 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         if (!op_streams(op.kind)) continue;
         if (!P.prefetch || v.lazy) {
             // data-dependent extents are known only once the slot's waits pass
-            while (misc[1] <= s) {
-                if (aborted(P.status)) return;
+            for (uint32_t it = 0; misc[1] <= s;) {
+                if ((++it & 1023u) == 0 && aborted(P.status)) return;  // (a global load: not every spin)
                 l2_try();
             }
             if (v.lazy && extent_masked(P, v.call, v.coord)) continue;
@@ -2277,8 +2383,8 @@ __device__ void l2_ahead_loop(const StaticParams& P, int worker, uint8_t* smem, 
     int slot = qb, chunk = 0, n = -1;
     long long fbytes = 0;  // cumulative bytes up to the cursor
     StreamPlan pl;
-    while (misc[11] == 0 && slot < qe) {
-        if (aborted(P.status)) return;
+    for (uint32_t it = 0; misc[11] == 0 && slot < qe;) {
+        if ((++it & 1023u) == 0 && aborted(P.status)) return;
         const long long pb = *pbytes;
         if (pb > fbytes) {  // behind the producer: continue from its position
             const int ps = misc[9], pc = misc[10];
@@ -2395,6 +2501,7 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
             mbar_init(&full[i], 1);
             mbar_init(&full[kStages + i], 1);
         }
+        mbar_init(merge_bar(smem), 1);
         fence_mbar_init();
         volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
         misc[0] = 0;
@@ -2404,6 +2511,7 @@ __global__ void __launch_bounds__(kThreads, 1) et_static_kernel(const __grid_con
         misc[10] = 0;
         misc[11] = 0;
         misc[12] = -1;
+        misc[13] = 0;
         reinterpret_cast<volatile long long*>(misc)[7] = 0;
     }
     // slot table for this CTA's queue
@@ -2473,7 +2581,10 @@ __device__ __forceinline__ uint32_t dyn_init(const StaticParams& P, const DynPar
 
 __device__ __forceinline__ bool dyn_visible(const DynParams& D, int el) {
     const int t = __ldg(D.el_dd + el);
-    return t < 0 || ld_acquire(reinterpret_cast<const uint32_t*>(&D.ctl->revealed[t])) != 0u;
+    if (t < 0) return true;
+    if (ld_relaxed(reinterpret_cast<const uint32_t*>(&D.ctl->revealed[t])) == 0u) return false;
+    fence_acquire_gpu();  // the revealed counts / indptr are read next
+    return true;
 }
 
 __device__ void dyn_push(const StaticParams& P, const DynParams& D, int task) {
@@ -2684,16 +2795,27 @@ __device__ void dyn_count_warp(const StaticParams& P, const DynParams& D, unsign
 __device__ bool dyn_wait_el(const StaticParams& P, const DynParams& D, int el, int worker, int task) {
     const uint64_t t0 = globaltimer();
     uint32_t it = 0;
-    while (!(dyn_visible(D, el) && ld_acquire(P.cnt + el) >= dyn_init(P, D, el))) {
+    while (!dyn_visible(D, el)) {  // data-dependent element: its count exists once revealed
         if ((++it & 255u) == 0) {
             if (aborted(P.status)) return false;
             if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
-                report(P.status, ET_ERR_DEADLOCK, worker, task, el,
-                       static_cast<int>(dyn_init(P, D, el) - ld_acquire(P.cnt + el)));
+                report(P.status, ET_ERR_DEADLOCK, worker, task, el, -1);
                 return false;
             }
         }
     }
+    const uint32_t need = dyn_init(P, D, el);
+    while (ld_relaxed(P.cnt + el) < need) {
+        if ((++it & 255u) == 0) {
+            if (aborted(P.status)) return false;
+            if (globaltimer() - t0 > static_cast<uint64_t>(P.watchdog_ns)) {
+                report(P.status, ET_ERR_DEADLOCK, worker, task, el,
+                       static_cast<int>(dyn_init(P, D, el) - ld_relaxed(P.cnt + el)));
+                return false;
+            }
+        }
+    }
+    fence_acquire_gpu();
     return true;
 }
 
@@ -2705,8 +2827,9 @@ __device__ int dyn_pop(const StaticParams& P, const DynParams& D, int cls, int w
     uint32_t it = 0;
     for (;;) {
         if (static_cast<int>(i) < D.num_tasks) {
-            const uint32_t v = ld_acquire(slot);
+            const uint32_t v = ld_relaxed(slot);
             if (v) {
+                fence_acquire_gpu();
                 atomicAdd(&P.status->pops, 1ull);
                 return static_cast<int>(v) - 1;
             }
@@ -2942,9 +3065,8 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
     unsigned int xq = 0;
     int gen = 0;
     for (;;) {
-        while (misc[5] == gen) {
-            if (aborted(P.status)) return;
-        }
+        for (uint32_t it = 0; misc[5] == gen;)
+            if ((++it & 1023u) == 0 && aborted(P.status)) return;
         gen = misc[5];
         const int task = misc[4];
         if (task < 0) return;
@@ -3038,11 +3160,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full[i], 1);
             mbar_init(&full[kStages + i], 1);
         }
+        mbar_init(merge_bar(smem), 1);
         fence_mbar_init();
         volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
         misc[0] = misc[1] = misc[2] = 0;
         misc[3] = misc[4] = misc[5] = 0;
         misc[6] = -1;
+        misc[13] = 0;
         if (worker == 0) atomicAdd(&P.status->pushes, static_cast<unsigned long long>(D.num_ready[0] + D.num_ready[1]));
     }
     if (P.num_calls <= kMaxCallExt) {  // grid extents of every call at this binding (masking)

@@ -26,6 +26,9 @@ constexpr int kAccFloats = 2048;
 constexpr int kMaxSymbols = 8;
 constexpr int kMaxRuntime = 512;  // runtime tensors per graph (6 per MoE layer)
 constexpr int kMaxRank = 4;
+// Attention partial row per (q head, split): m, l, 2 pad floats, then o[dh] -- 16-byte
+// aligned rows, so a group's partials move with bulk copies.
+constexpr int kPartHead = 4;
 constexpr int kMaxBatch = 8;   // GEMV batch rows carried in the mma M dimension
 constexpr int kMaxBatchTc = 128;  // tensor-core GEMV: batch = MMA N (Npad * kp * 2 <= 16 KB)
 

@@ -33,7 +33,7 @@
 //   flags bit 7: one flat grid dimension [b * kv * splits] instead, with i11 = per-step split
 //   budget (splits <= max(1, i11 / b)) and i10 = batch symbol slot (attn_tasks, attn_coord);
 //   p0 = q (fp32 [q_heads*head_dim], RoPE applied), p1/p2 = K/V cache, p3 = partials
-//   (fp32 [q_heads][max_splits][head_dim+2]); f0 = softmax scale
+//   (fp32 [q_heads][max_splits][4 + head_dim]: m, l, pad, pad, o); f0 = softmax scale
 // ET_OP_ATTN_MERGE      task (g): merges the splits and the new token at position s
 //   (K/V row s of the cache) for the group's q heads; same i/p as ATTN_SPLIT plus
 //   p4 = out (bf16 [q_heads*head_dim])

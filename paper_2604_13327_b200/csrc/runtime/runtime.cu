@@ -499,10 +499,10 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     for (int32_t c = 0; c < num_calls; ++c) {
         const et_op& o = ops[c];
         if (o.kind == ET_OP_GEMV && o.i[3] == 2) {  // attention-merge prologue (megakernel.cu body_gemv)
-            if (o.i[5] >= 0 || o.i[8] <= 0 || o.i[1] % o.i[8] || o.i[11] <= 0 || o.i[12] <= 0 ||
-                3LL * (o.i[1] / o.i[8]) * o.i[12] > etk::kAccFloats || !o.p[2])
+            if (o.i[5] >= 0 || o.i[8] <= 0 || o.i[1] % o.i[8] || o.i[11] <= 0 || o.i[12] <= 0 || o.i[1] > 4 * etk::kConsumers ||
+                3LL * (o.i[1] / o.i[8]) * o.i[12] > etk::kAccFloats || !o.p[2] || (o.p[5] && (o.i[9] <= 0 || o.i[13] <= 0)))
                 return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": GEMV x mode 2 (attention merge) "
-                                "needs b = 1, K a multiple of head_dim, and 3 * heads * split cap <= " +
+                                "needs b = 1, K a multiple of head_dim up to 1024, and 3 * heads * split cap <= " +
                                 std::to_string(etk::kAccFloats));
         }
         if (o.kind == ET_OP_ATTN_SPLIT && (o.flags & 1024) && (variant & 2))

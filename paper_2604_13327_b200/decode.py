@@ -295,7 +295,7 @@ class DecodeModel:
         self.act = torch.zeros(cfg.intermediate, dtype=torch.bfloat16, device=dev)
         self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=dev)
         self.h_b = torch.zeros_like(self.h_a) if residual == "double" else self.h_a
-        self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 4, dtype=torch.float32, device=dev)
         self.arrive = torch.zeros(cfg.layers, cfg.kv_heads, dtype=torch.int32, device=dev)  # split arrivals (fused merge)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
 

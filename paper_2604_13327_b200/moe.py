@@ -296,7 +296,8 @@ def moe_device_layout(cfg, W, kp=0):
 
 
 def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=None, attn_cap=None,
-               fused_merge=True, balance=False, route_tasks=None, group_stage=None, qkv_split=True):
+               fused_merge=True, balance=False, route_tasks=None, group_stage=None, qkv_split=True,
+               oproj_merge=True):
     """Every layout choice MoEDecodeModel makes before touching the device: the graph
     spec it lowers, its bindings (samples) and task counts.  Pure (no device, no
     extension), so the committed bench-graph fixtures (tests/golden/make_bench_graphs.py)
@@ -316,6 +317,10 @@ def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=
     L["samples"] = sorted(int(s) for s in samples)
     L["capacity"] = L["samples"][-1] + 1
     ms = attn_cap or attn_split_cap(cfg, L["samples"][-1], num_workers)
+    if not attn_cap and max_batch == 1 and oproj_merge and fused_merge:
+        # the output projection stages each group's partials in shared memory with bulk
+        # copies (G * splits * (dh + 4) * 4 bytes <= ~35 KB): at most 8 splits of 8 heads
+        ms = min(ms, max(1, (35 * 1024) // ((cfg.heads // cfg.kv_heads) * (cfg.head_dim + 4) * 4)))
     if max_batch > 8 and not attn_cap:  # tensor-core attention: a split runs two blocks at a time (batch.py)
         ms = max(1, ms // 2)
     L["max_splits"] = ms
@@ -325,7 +330,10 @@ def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=
     L["route_tasks"] = route_tasks or max(1, cfg.experts // 16)
     assert fused_merge or not L["batched"], "batched decode uses the fused attention merge"
     og = None
-    if L["batched"]:  # per kv-head-group output projection (a batch of full attention rows would not fit)
+    # one sequence: the attention splits leave partials and the per-group output
+    # projection merges them in its prologue (no merge task; GEMV x mode 2)
+    L["oproj_merge"] = bool(oproj_merge and not L["batched"] and fused_merge)
+    if L["batched"] or L["oproj_merge"]:  # per kv-head-group output projection (a batch of full attention rows would not fit)
         og = max(1, num_workers // cfg.kv_heads)
         while (cfg.hidden // 16) % og:
             og -= 1
@@ -363,7 +371,7 @@ class MoEDecodeModel:
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
                  scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=True,
                  balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False, qkv_split=True,
-                 max_batch=1, batch_samples=None, attn_cap=None):
+                 max_batch=1, batch_samples=None, attn_cap=None, oproj_merge=True):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -375,7 +383,7 @@ class MoEDecodeModel:
         t0 = time.perf_counter()
         lay = moe_layout(cfg, self.num_workers, samples, scheduler, max_batch=max_batch, batch_samples=batch_samples,
                          attn_cap=attn_cap, fused_merge=fused_merge, balance=balance, route_tasks=route_tasks,
-                         group_stage=group_stage, qkv_split=qkv_split)
+                         group_stage=group_stage, qkv_split=qkv_split, oproj_merge=oproj_merge)
         for k, v in lay.items():
             setattr(self, k, v)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
@@ -403,7 +411,7 @@ class MoEDecodeModel:
         self.qkv = torch.zeros(b, cfg.q_rows + 2 * cfg.kv_rows, dtype=torch.float32, device=dev)
         self.attn = torch.zeros(b, cfg.q_rows, dtype=torch.bfloat16, device=dev)
         self.partials = torch.zeros(b * cfg.heads, max(8, self.max_splits) if self.tc else self.max_splits,
-                                    cfg.head_dim + 2, dtype=torch.float32, device=dev)
+                                    cfg.head_dim + 4, dtype=torch.float32, device=dev)
         self.logits_r = torch.zeros(cfg.layers, b, E, dtype=torch.float32, device=dev)   # router logits per layer
         self.xn = torch.zeros(cfg.layers, b, cfg.hidden, dtype=torch.bfloat16, device=dev)
         self.wslot = torch.zeros(cfg.layers, b * K, dtype=torch.float32, device=dev)
@@ -513,7 +521,9 @@ class MoEDecodeModel:
                       cfg.kv_heads * self.capacity * dh]
             attn_p = [ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(L["q_norm"]),
                       ptr(L["k_norm"]), ptr(self.inv_freq), ptr(self.qkv) + 4 * nq]
-            if self.fused_merge:  # flags: 1 = q/k-norm mode, 2 = the last split merges; p5 of the split
+            if self.oproj_merge:  # flags: 1 = q/k-norm mode, 1024 = the last split folds the new token
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], flags=1 | 1024, p=attn_p))
+            elif self.fused_merge:  # flags: 1 = q/k-norm mode, 2 = the last split merges; p5 of the split
                 # op carries the arrival counters, so the norm weights move to the merge-compatible slots
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], flags=3 | (32 if self.qkv_split else 0),
                                    p=[ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn),
@@ -522,7 +532,13 @@ class MoEDecodeModel:
             else:
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
                 ops.append(make_op(OP_ATTN_MERGE, i=attn_i, f=[scale, cfg.eps], p=attn_p, flags=1))
-            if self.oproj_group_tasks:  # per kv-head group, activation rows nq apart
+            if self.oproj_merge:  # per kv-head group; x mode 2: merge the group's attention partials,
+                # then zero its raw split-K q/k/v accumulators
+                ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 2, EPI_ADD, -1, 0, 16, dh, cfg.kv_heads, self.max_splits,
+                                               CH, self.max_splits, self.oproj_group_tasks], flags=16,
+                                   p=[ptr(L["wo_grouped"]), 0, ptr(self.partials), 0, ptr(self.h),
+                                      ptr(self.qkv) if self.qkv_split else 0]))
+            elif self.oproj_group_tasks:  # per kv-head group, activation rows nq apart
                 ops.append(make_op(OP_GEMV, i=[H, G * dh, 1, 0, EPI_ADD, bs, 0, 16, 0, nq, 0, 0, 0,
                                                self.oproj_group_tasks], flags=16,
                                    p=[ptr(L["wo_grouped"]), 0, ptr(self.attn), 0, ptr(self.h)]))

@@ -133,7 +133,7 @@ class TPDecodeModel:
         self.q = torch.zeros(lc.q_rows, dtype=torch.float32, device=dev)
         self.attn = torch.zeros(lc.q_rows, dtype=torch.bfloat16, device=dev)
         self.act = torch.zeros(lc.intermediate, dtype=torch.bfloat16, device=dev)
-        self.partials = torch.zeros(lc.heads, self.max_splits, cfg.head_dim + 2, dtype=torch.float32, device=dev)
+        self.partials = torch.zeros(lc.heads, self.max_splits, cfg.head_dim + 4, dtype=torch.float32, device=dev)
         self.arrive = torch.zeros(cfg.layers, lc.kv_heads, dtype=torch.int32, device=dev)
         self.logits = torch.zeros(1, lc.vocab, dtype=torch.float32, device=dev)   # this rank's vocab slice
         slots = 2 * cfg.layers
