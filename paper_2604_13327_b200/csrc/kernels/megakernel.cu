@@ -358,40 +358,44 @@ __device__ __forceinline__ void gemv_stream(Ring& ring, int warp, int lane, int 
     const int g = lane >> 2, q = lane & 3;
     const bool xlane = g < nb;
     const uint16_t* xrow = xs + (xlane ? g : 0) * K + 8 * q;
-    unsigned long long c = ring.seq;
-    for (int seg = 0; seg < nseg; ++seg) {
-        const int nch = (seg_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
-        for (int ch = 0; ch < nch; ++ch, ++c) {
-            if (Ring::owner(c) != warp) continue;
-            const uint8_t* buf = ring.wait(c);
-            if (!buf) continue;  // aborted: the step reports an error
-            const int t0 = ch * kTilesPerChunk;
-            const int nt = seg_tiles - t0 < kTilesPerChunk ? seg_tiles - t0 : kTilesPerChunk;
-            int done = 0;
-            while (done < nt) {
-                const int tt = u0 + t0 + done;  // unit index relative to the span's first tile
-                const int rtile = tt / kst, j = tt - rtile * kst;
-                const int len = (kst - j < nt - done) ? kst - j : nt - done;
-                float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-                const uint4* ap = reinterpret_cast<const uint4*>(buf + done * 512) + lane;
-                const uint16_t* xp = xrow + j * 16;
+    const int nch = (seg_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
+    const int total = nseg * nch;
+    const unsigned long long c0 = ring.seq;
+    // this warp's chunks only (c % 8 == warp): no walk over the other warps' chunks
+    for (int idx = (warp - static_cast<int>(c0 % kConsumerWarps) + kConsumerWarps) % kConsumerWarps; idx < total;
+         idx += kConsumerWarps) {
+        const unsigned long long c = c0 + idx;
+        const int seg = idx / nch, ch = idx - seg * nch;
+        const uint8_t* buf = ring.wait(c);
+        if (!buf) continue;  // aborted: the step reports an error
+        const int t0 = ch * kTilesPerChunk;
+        const int nt = seg_tiles - t0 < kTilesPerChunk ? seg_tiles - t0 : kTilesPerChunk;
+        const int tt0 = u0 + t0;  // unit index relative to the span's first tile
+        int rtile = tt0 / kst, j = tt0 - rtile * kst;
+        int done = 0;
+        while (done < nt) {
+            const int len = (kst - j < nt - done) ? kst - j : nt - done;
+            float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint4* ap = reinterpret_cast<const uint4*>(buf + done * 512) + lane;
+            const uint16_t* xp = xrow + j * 16;
 #pragma unroll 4
-                for (int i = 0; i < len; i += 2) {
-                    const uint4 a0 = lds128(ap + i * 32);
-                    const uint4 a1 = lds128(ap + (i + 1) * 32);
-                    const uint4 xv = xlane ? lds128(xp + i * 16) : make_uint4(0u, 0u, 0u, 0u);
-                    mma_bf16_16816(d0, a0, xv.x, xv.y);
-                    mma_bf16_16816(d1, a1, xv.z, xv.w);
-                }
-                const float d[4] = {d0[0] + d1[0], d0[1] + d1[1], d0[2] + d1[2], d0[3] + d1[3]};
-                flush(seg, rtile, g, q, d);
-                done += len;
+            for (int i = 0; i < len; i += 2) {
+                const uint4 a0 = lds128(ap + i * 32);
+                const uint4 a1 = lds128(ap + (i + 1) * 32);
+                const uint4 xv = xlane ? lds128(xp + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+                mma_bf16_16816(d0, a0, xv.x, xv.y);
+                mma_bf16_16816(d1, a1, xv.z, xv.w);
             }
-            __syncwarp();
-            if (lane == 0) ring.release(c);
+            const float d[4] = {d0[0] + d1[0], d0[1] + d1[1], d0[2] + d1[2], d0[3] + d1[3]};
+            flush(seg, rtile, g, q, d);
+            done += len;
+            ++rtile;  // the next unit (if any) starts the next row tile
+            j = 0;
         }
+        __syncwarp();
+        if (lane == 0) ring.release(c);
     }
-    ring.seq = c;
+    ring.seq = c0 + total;
 }
 
 // Shared-memory mbarrier of the attention-merge prologue's bulk loads (behind the
@@ -399,6 +403,32 @@ __device__ __forceinline__ void gemv_stream(Ring& ring, int warp, int lane, int 
 __device__ __forceinline__ uint64_t* merge_bar(uint8_t* smem) {
     return reinterpret_cast<uint64_t*>(smem + kSmemMisc + 464);
 }
+// Stage `bytes` (16-byte multiple and alignment) of data produced by other CTAs
+// (acquired by this task's wait) at smem dst with one bulk copy; every consumer
+// thread returns once it landed.  dst must not be read or written by anyone
+// else meanwhile (the caller's previous generic accesses are ordered by its last
+// consumer barrier).
+// The barrier's phase count misc[13] advances once per use, after a consumer
+// barrier; the next use is a later task's prologue (further barriers apart).
+__device__ __forceinline__ uint8_t* smem_cta_base() {
+    extern __shared__ __align__(1024) uint8_t smem_all[];
+    return smem_all;
+}
+__device__ __forceinline__ void stage_bulk(const StaticParams&, void* dst, const void* src, uint32_t bytes, int ctid) {
+    uint64_t* bar = merge_bar(smem_cta_base());
+    volatile int* misc = reinterpret_cast<volatile int*>(smem_cta_base() + kSmemMisc);
+    const uint32_t par = static_cast<uint32_t>(misc[13]) & 1u;
+    if (ctid == 0) {
+        fence_proxy_async_global();
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bar, bytes);
+        bulk_g2s_keep(dst, src, bytes, bar);
+    }
+    mbar_wait(bar, par);
+    bar_sync(1, kConsumers);  // everyone saw this phase before it is reused
+    if (ctid == 0) misc[13] = misc[13] + 1;
+}
+
 constexpr int kMergeBulkOff = 2048;                      // partials staged at xs + 2 KB ...
 constexpr int kMergeBulkMax = kXBytes + kAccFloats * 4 - kMergeBulkOff - 2048;  // ... up to acc's last 2 KB
 
@@ -592,9 +622,15 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
         // activation rows are i9 elements apart (0: packed [nb][K]); a grouped GEMV reads slice g
         const uint16_t* x = reinterpret_cast<const uint16_t*>(op.p[2]) + (grouped ? static_cast<long long>(si.coord[0]) * K : 0);
         const int xstride = op.i[9] > 0 ? op.i[9] : K, k8 = K / 8;
-        for (int v = ctid; v < nb * k8; v += kConsumers) {
-            const int bi = v / k8, kk = v - bi * k8;
-            reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x + static_cast<long long>(bi) * xstride) + kk);
+        if ((nb == 1 || xstride == K) && (P.debug & 0x20000) == 0) {
+            // one bulk copy (the TMA engine keeps the whole row in flight; 256 threads'
+            // 16-byte loads are limited by the SM's outstanding-miss slots)
+            stage_bulk(P, xs, x, static_cast<uint32_t>(nb) * K * 2, ctid);
+        } else {
+            for (int v = ctid; v < nb * k8; v += kConsumers) {
+                const int bi = v / k8, kk = v - bi * k8;
+                reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(x + static_cast<long long>(bi) * xstride) + kk);
+            }
         }
     } else if (op.i[3] == 2) {
         if (K <= 2 * kConsumers) gemv_merge_prologue<2, 16>(P, op, grouped ? si.coord[0] : 0, grouped ? si.coord[1] : 0, xs, acc, ctid, &t_probe);
@@ -607,6 +643,8 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
                                                              : reinterpret_cast<const float*>(op.p[3]);
         const int stride = op.i[9];
         constexpr int kMaxPer = 8;  // float4 per thread: K <= 8192
+        // (a bulk copy of the fp32 row, as x mode 0 does, measured slower here: the
+        // register loads overlap the reduction's first shuffles)
         for (int bi = 0; bi < nb; ++bi) {
             float4 hv[kMaxPer];
             float ss = 0.f;
