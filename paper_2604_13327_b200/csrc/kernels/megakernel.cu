@@ -27,6 +27,10 @@
 
 namespace etk {
 
+__device__ __forceinline__ uint8_t* smem_cta_base() {
+    extern __shared__ __align__(1024) uint8_t smem_all[];
+    return smem_all;
+}
 struct SlotInfo {
     int call;
     int rank;
@@ -410,10 +414,6 @@ __device__ __forceinline__ uint64_t* merge_bar(uint8_t* smem) {
 // consumer barrier).
 // The barrier's phase count misc[13] advances once per use, after a consumer
 // barrier; the next use is a later task's prologue (further barriers apart).
-__device__ __forceinline__ uint8_t* smem_cta_base() {
-    extern __shared__ __align__(1024) uint8_t smem_all[];
-    return smem_all;
-}
 __device__ __forceinline__ void stage_bulk(const StaticParams&, void* dst, const void* src, uint32_t bytes, int ctid) {
     uint64_t* bar = merge_bar(smem_cta_base());
     volatile int* misc = reinterpret_cast<volatile int*>(smem_cta_base() + kSmemMisc);
@@ -2625,20 +2625,36 @@ __device__ __forceinline__ bool dyn_visible(const DynParams& D, int el) {
     return true;
 }
 
-__device__ void dyn_push(const StaticParams& P, const DynParams& D, int task) {
+// Ready-queue slot word: (call << 21) | (task + 1) -- the popper starts loading the
+// call's op record in the same round trip as the task's own records.  Call 511 =
+// not encoded (more than 511 calls): the popper reads it from task_desc.
+constexpr int kSlotTaskBits = 21;
+constexpr uint32_t kSlotNoCall = 511u;
+__device__ __forceinline__ uint32_t slot_word(int task, int call) {
+    const uint32_t c = (call >= 0 && call < static_cast<int>(kSlotNoCall)) ? static_cast<uint32_t>(call) : kSlotNoCall;
+    return (c << kSlotTaskBits) | static_cast<uint32_t>(task + 1);
+}
+// consumers[] entries: task in bits 0..20, its call in 21..29 (511: unknown), bit 30 =
+// DMA class, bit 31 = this element is the consumer's only pending wait
+__device__ __forceinline__ int cons_task(int e) { return e & ((1 << kSlotTaskBits) - 1); }
+__device__ __forceinline__ int cons_call(int e) {
+    const int c = (e >> kSlotTaskBits) & 511;
+    return c == static_cast<int>(kSlotNoCall) ? -1 : c;
+}
+
+__device__ void dyn_push(const StaticParams& P, const DynParams& D, int task, int call = -1) {
     const int cls = __ldg(D.task_class + task);
     const unsigned int i = atomicAdd(&D.ctl->tail[cls], 1u);
     if (P.record) D.push_time[task] = globaltimer();
-    st_release(reinterpret_cast<uint32_t*>(D.slots + static_cast<long long>(cls) * D.num_tasks + i),
-               static_cast<uint32_t>(task + 1));
+    st_release(reinterpret_cast<uint32_t*>(D.slots + static_cast<long long>(cls) * D.num_tasks + i), slot_word(task, call));
     atomicAdd(&P.status->pushes, 1ull);
 }
 
 __device__ void dyn_fire(const StaticParams& P, const DynParams& D, int el) {
     if (atomicExch(&D.fired[el], 1u) != 0u) return;
     for (int k = __ldg(D.consumer_off + el), e = __ldg(D.consumer_off + el + 1); k < e; ++k) {
-        const int ce = __ldg(D.consumers + k), c = ce & 0x7fffffff;
-        if (ce < 0 || atomicSub(&D.rem[c], 1) == 1) dyn_push(P, D, c);
+        const int ce = __ldg(D.consumers + k), c = cons_task(ce);
+        if (ce < 0 || atomicSub(&D.rem[c], 1) == 1) dyn_push(P, D, c, cons_call(ce));
     }
     const int t = __ldg(D.el_dd + el);
     if (t >= 0 && D.dd_range_call[t] >= 0) {
@@ -2647,7 +2663,7 @@ __device__ void dyn_fire(const StaticParams& P, const DynParams& D, int el) {
         const int g = el - D.dd_base[t];
         const int first = __ldg(D.call_first_task + call);
         for (int f = __ldcg(ip + g), hi = __ldcg(ip + g + 1); f < hi; ++f)
-            if (atomicSub(&D.rem[first + f], 1) == 1) dyn_push(P, D, first + f);
+            if (atomicSub(&D.rem[first + f], 1) == 1) dyn_push(P, D, first + f, call);
     }
 }
 
@@ -2693,10 +2709,11 @@ __device__ void dyn_count(const StaticParams& P, const DynParams& D, unsigned in
 // completes an element releases its consumers lane-strided over the warp and
 // pushes the ready ones with one tail reservation per warp (a 148-way fan-out
 // costs ~5 serial atomics instead of ~300).  Lane 0 owns the counter atomics.
-__device__ __forceinline__ void dyn_push_warp(const StaticParams& P, const DynParams& D, int task, bool ready, int lane) {
+__device__ __forceinline__ void dyn_push_warp(const StaticParams& P, const DynParams& D, int task, bool ready, int lane,
+                                              int known_cls = -1, int call = -1) {
     const unsigned any = __ballot_sync(0xffffffffu, ready);
     if (!any) return;
-    const int cls = ready ? __ldg(D.task_class + task) : 0;
+    const int cls = !ready ? 0 : known_cls >= 0 ? known_cls : __ldg(D.task_class + task);
     for (int c = 0; c < 2; ++c) {
         const unsigned m = __ballot_sync(0xffffffffu, ready && cls == c);
         if (!m) continue;
@@ -2708,14 +2725,17 @@ __device__ __forceinline__ void dyn_push_warp(const StaticParams& P, const DynPa
             const unsigned int i = base + __popc(m & ((1u << lane) - 1u));
             if (P.record) D.push_time[task] = globaltimer();
             st_release(reinterpret_cast<uint32_t*>(D.slots + static_cast<long long>(c) * D.num_tasks + i),
-                       static_cast<uint32_t>(task + 1));
+                       slot_word(task, call));
         }
     }
     if (lane == 0) atomicAdd(&P.status->pushes, static_cast<unsigned long long>(__popc(any)));
 }
 
-__device__ __noinline__ void dyn_fire_warp(const StaticParams& P, const DynParams& D, int el, int lane) {
-    const int4 info = __ldg(D.el_info + el);  // (consumers begin, end, dd tensor, initial count)
+// info: the element's record when the caller has it; e_first: this lane's entry of
+// its first 32 consumers, preloaded by the caller (or pass have_first = false).
+__device__ __noinline__ void dyn_fire_warp(const StaticParams& P, const DynParams& D, int el, int lane,
+                                           const int4* pinfo = nullptr, int e_first = 0, bool have_first = false) {
+    const int4 info = pinfo ? *pinfo : __ldg(D.el_info + el);  // (consumers begin, end, dd tensor, initial count)
     if (info.z >= 0) {  // a data-dependent element can be fired by its count and by the reveal
         int first = 0;
         if (lane == 0) first = atomicExch(&D.fired[el], 1u) == 0u;
@@ -2724,11 +2744,11 @@ __device__ __noinline__ void dyn_fire_warp(const StaticParams& P, const DynParam
     const int cb = info.x, ce = info.y;
     for (int k0 = cb; k0 < ce; k0 += 32) {
         const int k = k0 + lane;
-        const int e = k < ce ? __ldg(D.consumers + k) : 0;
-        const int c = e & 0x7fffffff;
-        // bit 31: this element is the consumer's only pending wait -> ready now
+        const int e = k < ce ? ((k0 == cb && have_first) ? e_first : __ldg(D.consumers + k)) : 0;
+        const int c = cons_task(e);
+        // bit 31: this element is the consumer's only pending wait -> ready now; bit 30: DMA class
         const bool ready = k < ce && (e < 0 || atomicSub(&D.rem[c], 1) == 1);
-        dyn_push_warp(P, D, c, ready, lane);
+        dyn_push_warp(P, D, c, ready, lane, (e >> 30) & 1, cons_call(e));
     }
     const int t = info.z;
     if (t >= 0 && D.dd_range_call[t] >= 0) {
@@ -2740,7 +2760,7 @@ __device__ __noinline__ void dyn_fire_warp(const StaticParams& P, const DynParam
         for (int f0 = lo; f0 < hi; f0 += 32) {
             const int f = f0 + lane;
             const bool ready = f < hi && atomicSub(&D.rem[first_task + f], 1) == 1;
-            dyn_push_warp(P, D, first_task + f, ready, lane);
+            dyn_push_warp(P, D, first_task + f, ready, lane, -1, call);
         }
     }
 }
@@ -2764,29 +2784,39 @@ __device__ void dyn_reveal_warp(const StaticParams& P, const DynParams& D, int t
         }
     }
     __syncwarp();
-    for (int e0 = D.dd_base[t], e1 = D.dd_base[t] + D.dd_count[t]; e0 < e1; e0 += 32) {
-        const int el = e0 + lane;
-        bool f = false;
-        if (el < e1) {
-            const uint32_t need = dyn_init(P, D, el);
-            // an element that releases nothing (no static consumers, empty range) never needs to fire
-            bool releases = __ldg(D.consumer_off + el + 1) > __ldg(D.consumer_off + el);
-            const int rc = D.dd_range_call[t];
-            if (!releases && rc >= 0) {
-                const int* ip = P.rt[__ldg(D.call_range_rt + rc)];
-                const int g = el - D.dd_base[t];
-                releases = __ldcg(ip + g + 1) > __ldcg(ip + g);
-            }
-            if (releases) {
-                const uint32_t have = D.early_push ? ld_acquire(D.disp + el) : ld_acquire(P.cnt + el);
-                f = have >= need;
-            }
+    // Every element of the tensor, 4 per lane with all their loads in flight at once
+    // (one pass of L2 round trips for up to 128 elements instead of one per 32).
+    const int rcw = D.dd_range_call[t];
+    const int* ipw = rcw >= 0 ? P.rt[__ldg(D.call_range_rt + rcw)] : nullptr;
+    const int* cntw = P.rt[D.dd_counts_rt[t]];
+    const unsigned int* havew = D.early_push ? D.disp : P.cnt;
+    for (int e0 = D.dd_base[t], e1 = D.dd_base[t] + D.dd_count[t]; e0 < e1; e0 += 128) {
+        int4 info[4];
+        uint32_t need[4], have[4];
+        int r0[4], r1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int el = e0 + lane + 32 * u;
+            const bool in = el < e1;
+            info[u] = in ? __ldg(D.el_info + el) : make_int4(0, 0, -1, 0);
+            need[u] = in ? static_cast<uint32_t>(__ldcg(cntw + (el - D.dd_base[t]))) : 0u;
+            r0[u] = in && ipw ? __ldcg(ipw + (el - D.dd_base[t])) : 0;
+            r1[u] = in && ipw ? __ldcg(ipw + (el - D.dd_base[t]) + 1) : 0;
+            have[u] = in ? ld_relaxed(havew + el) : 0u;
         }
-        unsigned m = __ballot_sync(0xffffffffu, f);
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            dyn_fire_warp(P, D, e0 + b, lane);
+        fence_acquire_gpu();  // the counts above were written before the notifies they count
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int el = e0 + lane + 32 * u;
+            // an element that releases nothing (no static consumers, empty range) never needs to fire
+            const bool releases = info[u].y > info[u].x || r1[u] > r0[u];
+            const bool f = el < e1 && releases && have[u] >= need[u];
+            unsigned m = __ballot_sync(0xffffffffu, f);
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                dyn_fire_warp(P, D, e0 + b + 32 * u, lane);
+            }
         }
     }
     // Range-call tasks at or beyond indptr[last] never exist (extent_from): the
@@ -2814,12 +2844,14 @@ __device__ void dyn_reveal_warp(const StaticParams& P, const DynParams& D, int t
 __device__ void dyn_count_warp(const StaticParams& P, const DynParams& D, unsigned int* ctr, int el, bool may_fire,
                                int worker, int task, int lane) {
     int fire = 0;
+    int4 info = make_int4(0, 0, 0, 0);
     if (lane == 0) {
+        info = __ldg(D.el_info + el);  // in flight together with the atomic
         const uint32_t old = atom_add_release(ctr + el, 1u);
-        const uint32_t need = dyn_init(P, D, el);
+        const uint32_t need = info.z < 0 ? static_cast<uint32_t>(info.w) : dyn_init(P, D, el);
         if (ctr == P.cnt && old >= need) report(P.status, ET_ERR_UNDERFLOW, worker, task, el, -1);
         if (may_fire && old + 1 == need) {
-            if (__ldg(D.el_dd + el) < 0) {
+            if (info.z < 0) {
                 fire = 1;  // static element: only this notify can complete it
             } else {
                 fence_sc_gpu();  // ordered against the reveal of the data-dependent tensor
@@ -2827,7 +2859,13 @@ __device__ void dyn_count_warp(const StaticParams& P, const DynParams& D, unsign
             }
         }
     }
-    if (__shfl_sync(0xffffffffu, fire, 0)) dyn_fire_warp(P, D, el, lane);
+    if (__shfl_sync(0xffffffffu, fire, 0)) {
+        info.x = __shfl_sync(0xffffffffu, info.x, 0);
+        info.y = __shfl_sync(0xffffffffu, info.y, 0);
+        info.z = __shfl_sync(0xffffffffu, info.z, 0);
+        info.w = __shfl_sync(0xffffffffu, info.w, 0);
+        dyn_fire_warp(P, D, el, lane, &info);
+    }
 }
 
 __device__ bool dyn_wait_el(const StaticParams& P, const DynParams& D, int el, int worker, int task) {
@@ -2869,7 +2907,7 @@ __device__ int dyn_pop(const StaticParams& P, const DynParams& D, int cls, int w
             if (v) {
                 fence_acquire_gpu();
                 atomicAdd(&P.status->pops, 1ull);
-                return static_cast<int>(v) - 1;
+                return static_cast<int>(v);  // slot_word: the caller decodes task and call
             }
         }
         if (static_cast<int>(i) >= *reinterpret_cast<volatile int*>(&D.ctl->total[cls])) return -1;
@@ -2886,7 +2924,7 @@ __device__ int dyn_pop(const StaticParams& P, const DynParams& D, int cls, int w
 // A task's slot view from its packed records; masking compares the coordinates
 // with the call's grid extents at this launch's binding (shared-memory table
 // filled at kernel start when the graph has <= kMaxCallExt calls of rank <= 2).
-__device__ SlotView dyn_view(const StaticParams& P, const DynParams& D, int task, const int2* cext = nullptr) {
+__device__ SlotView dyn_view(const StaticParams& P, const DynParams& D, int task, const int4* cext = nullptr) {
     SlotView v;
     const int4 d = __ldg(D.task_desc + task);
     const int4 r = __ldg(D.task_rng + task);
@@ -2896,7 +2934,7 @@ __device__ SlotView dyn_view(const StaticParams& P, const DynParams& D, int task
     v.coord[2] = v.coord[3] = 0;
     v.ext0 = d.w;
     if (cext) {
-        const int2 e = cext[v.call];
+        const int4 e = cext[v.call];
         v.masked = v.coord[0] >= e.x || v.coord[1] >= e.y;
     } else {
         const int rank = __ldg(P.call_rank + v.call);
@@ -2923,7 +2961,17 @@ __device__ bool dyn_prepare(const StaticParams& P, const DynParams& D, const Slo
         const int* ip = P.rt[rr];
         const int flat = __ldg(D.task_flat + task);
         int g = 0;
-        while (__ldcg(ip + g + 1) <= flat) ++g;
+        for (bool found = false; !found; g += 8) {  // 8 loads in flight per probe round
+            int v8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v8[u] = __ldcg(ip + g + u + 1);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (!found && v8[u] > flat) {
+                    found = true;
+                    g += u - 8;
+                }
+        }
         if (!dyn_wait_el(P, D, __ldg(D.call_range_base + v.call) + g, worker, task)) return false;
     }
     if (D.early_push && dispatch) {
@@ -2954,15 +3002,41 @@ __device__ void dyn_dispatch_warp(const StaticParams& P, const DynParams& D, con
 }
 
 __device__ void dyn_finish_warp(const StaticParams& P, const DynParams& D, const SlotView& v, int task, int worker,
-                                int lane) {
-    for (int t = 0; t < D.num_dd; ++t) {
+                                int lane, int4 note = make_int4(-1, 0, 0, 0), const int4* cext = nullptr) {
+    if ((P.debug & 0x100000) && lane == 0) D.push_time[task] = globaltimer();  // probe: finish entry
+    // data-dependent tensors this call writes: from the shared-memory call table (an
+    // indexed walk over the kernel parameters costs ~4 us of constant-cache misses)
+    const int t_lo = cext ? cext[v.call].z : 0, t_hi = cext ? (cext[v.call].z < 0 ? 0 : cext[v.call].z + cext[v.call].w)
+                                                       : D.num_dd;
+    for (int t = t_lo < 0 ? 0 : t_lo; t < t_hi; ++t) {
         if (D.dd_writer_call[t] != v.call) continue;
         int last = 0;
         if (lane == 0) last = atomicSub(&D.ctl->writer_rem[t], 1) == 1;
         if (__shfl_sync(0xffffffffu, last, 0)) dyn_reveal_warp(P, D, t, lane);
     }
+    if ((P.debug & 0x200000) && lane == 0) D.push_time[task] = globaltimer();  // probe: after the writer loop
     const bool fire = !D.early_push;
-    for (int n = v.nb; n < v.ne; ++n) dyn_count_warp(P, D, P.cnt, __ldg(D.task_notifies + n), fire, worker, task, lane);
+    int n0 = v.nb;
+    if (note.x >= 0 && v.ne > v.nb) {
+        // the first notify's element record came with the task (task_note): its consumer
+        // entries load together with the count's atomic -- one round trip, then the push
+        const int k = note.y + lane;
+        const int e = k < note.z ? __ldg(D.consumers + k) : 0;
+        int go = 0;
+        if (lane == 0) {
+            const uint32_t old = atom_add_release(P.cnt + note.x, 1u);
+            if (old >= static_cast<uint32_t>(note.w)) report(P.status, ET_ERR_UNDERFLOW, worker, task, note.x, -1);
+            go = fire && old + 1 == static_cast<uint32_t>(note.w);
+        }
+        if ((P.debug & 0x40000) && lane == 0) D.push_time[task] = globaltimer();  // probe: count returned
+        if (__shfl_sync(0xffffffffu, go, 0)) {
+            const int4 info = make_int4(note.y, note.z, -1, note.w);
+            dyn_fire_warp(P, D, note.x, lane, &info, e, true);
+        }
+        if ((P.debug & 0x80000) && lane == 0) D.push_time[task] = globaltimer();  // probe: fired
+        n0 = v.nb + 1;
+    }
+    for (int n = n0; n < v.ne; ++n) dyn_count_warp(P, D, P.cnt, __ldg(D.task_notifies + n), fire, worker, task, lane);
     const int rel = v.masked ? -1 : dyn_routed_el(P, D, v.call, __ldg(D.task_flat + task));  // masked: no routing
     if (rel >= 0) dyn_count_warp(P, D, P.cnt, rel, fire, worker, task, lane);
 }
@@ -2988,7 +3062,7 @@ template <bool kMoE, bool kTC>
 __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
     const int ctid = threadIdx.x;
     TcState ts{kTC ? reinterpret_cast<volatile uint32_t*>(smem + kSmemMisc)[8] : 0u, 0u, 0u};
-    const int2* cext = P.num_calls <= kMaxCallExt ? reinterpret_cast<const int2*>(smem + kSmemCallExt) : nullptr;
+    const int4* cext = P.num_calls <= kMaxCallExt ? reinterpret_cast<const int4*>(smem + kSmemCallExt) : nullptr;
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kSmemX);
     float* acc = reinterpret_cast<float*>(smem + kSmemAcc);
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
@@ -2999,9 +3073,12 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
     for (;;) {
         uint64_t tb = 0, tw = 0, tp = 0, te = 0;
         if (ctid == 0) {
-            const int task = dyn_pop(P, D, 0, worker);
+            const int word = dyn_pop(P, D, 0, worker);
             tb = globaltimer();
+            const int task = word < 0 ? -1 : (word & ((1 << kSlotTaskBits) - 1)) - 1;
+            const uint32_t wc = word < 0 ? kSlotNoCall : static_cast<uint32_t>(word) >> kSlotTaskBits;
             misc[3] = task;
+            misc[7] = wc == kSlotNoCall ? -1 : static_cast<int>(wc);
             misc[4] = task;  // hand the task to the producer warp (streams during the waits)
             __threadfence_block();
             misc[5] = misc[5] + 1;
@@ -3009,15 +3086,30 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
         bar_sync(1, kConsumers);
         const int task = misc[3];
         if (task < 0) break;
+        const int wcall = misc[7];  // the call, when the slot word carried it
+        // the op record's copy starts with the task's own records (same round trip)
+        const et_op* opp = wcall >= 0 ? P.ops + wcall : nullptr;
+        int opw = 0;
+        if (opp && ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
+            opw = reinterpret_cast<const int*>(opp)[ctid - 32];
+        int4 note = make_int4(-1, 0, 0, 0);
+        if (ctid < 32) note = __ldg(D.task_note + task);  // used by warp 0 at the task's end
         SlotView v = dyn_view(P, D, task, cext);
+        if (opp) {
+            if (ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
+                reinterpret_cast<int*>(smem + kSmemOp)[ctid - 32] = opw;
+        }
         const et_op& opg = P.ops[v.call];  // shared-memory copy, as in the static loop
-        if (ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
+        if (!opp && ctid >= 32 && ctid < 32 + static_cast<int>(sizeof(et_op) / 4))
             reinterpret_cast<int*>(smem + kSmemOp)[ctid - 32] = reinterpret_cast<const int*>(&opg)[ctid - 32];
         const et_op& op = *reinterpret_cast<const et_op*>(smem + kSmemOp);
         if (ctid < 32) {
             int ok = 1;
             if (ctid == 0) {
-                ok = dyn_prepare(P, D, v, task, worker, false);
+                // Without early push a task is pushed only once every wait element (armed or
+                // not, range trigger included) has fired, so its armed waits hold already: no
+                // device round trips to re-check them (early push: dispatched tasks wait here).
+                ok = D.early_push ? dyn_prepare(P, D, v, task, worker, false) : true;
                 if (ok && P.step_limit > 0 &&
                     atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
                     report(P.status, ET_ERR_STEP_LIMIT, worker, task, -1, 0);
@@ -3079,7 +3171,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
         bar_sync(1, kConsumers);
         if (ctid < 32) {
             if (ctid == 0) te = globaltimer();
-            dyn_finish_warp(P, D, v, task, worker, ctid);
+            dyn_finish_warp(P, D, v, task, worker, ctid, note, cext);
             if (ctid == 0) dyn_record(P, D, task, worker, v.masked, tb, tw, tp, te);
         }
     }
@@ -3094,7 +3186,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
 
 __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int worker, uint8_t* smem) {
     if ((threadIdx.x & 31) != 0) return;
-    const int2* cext = P.num_calls <= kMaxCallExt ? reinterpret_cast<const int2*>(smem + kSmemCallExt) : nullptr;
+    const int4* cext = P.num_calls <= kMaxCallExt ? reinterpret_cast<const int4*>(smem + kSmemCallExt) : nullptr;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
     uint64_t* empty = full + kStages;
     volatile int* misc = reinterpret_cast<volatile int*>(smem + kSmemMisc);
@@ -3133,12 +3225,13 @@ __device__ void dyn_producer_loop(const StaticParams& P, const DynParams& D, int
 }
 
 // DMA-class tasks: popped from their own queue by worker 0's DMA warp.
-__device__ void dyn_dma_loop(const StaticParams& P, const DynParams& D, const int2* cext) {
+__device__ void dyn_dma_loop(const StaticParams& P, const DynParams& D, const int4* cext) {
     if ((threadIdx.x & 31) != 0) return;
     const int worker = P.num_queues;
     for (;;) {
-        const int task = dyn_pop(P, D, 1, worker);
-        if (task < 0) return;
+        const int word = dyn_pop(P, D, 1, worker);
+        if (word < 0) return;
+        const int task = (word & ((1 << kSlotTaskBits) - 1)) - 1;
         const uint64_t tb = globaltimer();
         const SlotView v = dyn_view(P, D, task, cext);
         if (!dyn_prepare(P, D, v, task, worker)) return;
@@ -3162,8 +3255,18 @@ __device__ void dyn_reset_state(const StaticParams& P, const DynParams& D, DynCt
     for (int i = tid; i < D.num_tasks; i += stride) {
         rem[i] = __ldg(D.task_rem_init + i);
         // the ready seeds occupy the first slots of each class queue (id order)
-        slots[i] = i < D.num_ready[0] ? __ldg(D.ready + i) + 1 : 0;
-        slots[D.num_tasks + i] = i < D.num_ready[1] ? __ldg(D.ready + D.num_ready[0] + i) + 1 : 0;
+        if (i < D.num_ready[0]) {
+            const int t = __ldg(D.ready + i);
+            slots[i] = static_cast<int>(slot_word(t, __ldg(D.task_call + t)));
+        } else {
+            slots[i] = 0;
+        }
+        if (i < D.num_ready[1]) {
+            const int t = __ldg(D.ready + D.num_ready[0] + i);
+            slots[D.num_tasks + i] = static_cast<int>(slot_word(t, __ldg(D.task_call + t)));
+        } else {
+            slots[D.num_tasks + i] = 0;
+        }
     }
     for (int i = tid; i < P.cnt_capacity; i += stride) {
         fired[i] = 0u;
@@ -3208,11 +3311,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (worker == 0) atomicAdd(&P.status->pushes, static_cast<unsigned long long>(D.num_ready[0] + D.num_ready[1]));
     }
     if (P.num_calls <= kMaxCallExt) {  // grid extents of every call at this binding (masking)
-        int2* cext = reinterpret_cast<int2*>(smem + kSmemCallExt);
+        // (.z: first data-dependent tensor the call writes, -1 = none; .w: how many, consecutive)
+        int4* cext = reinterpret_cast<int4*>(smem + kSmemCallExt);
         for (int c = threadIdx.x; c < P.num_calls; c += blockDim.x) {
             const int rank = __ldg(P.call_rank + c);
-            cext[c] = make_int2(rank > 0 ? static_cast<int>(eval_code(P, c, 0)) : 1,
-                                rank > 1 ? static_cast<int>(eval_code(P, c, 1)) : 1);
+            const int dd = __ldg(D.call_dd + c);
+            cext[c] = make_int4(rank > 0 ? static_cast<int>(eval_code(P, c, 0)) : 1,
+                                rank > 1 ? static_cast<int>(eval_code(P, c, 1)) : 1, dd < 0 ? -1 : (dd & 0xffff),
+                                dd < 0 ? 0 : (dd >> 16));
         }
     }
     if constexpr (kTC) tc_setup(smem);
@@ -3225,7 +3331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == kProducerWarp) {
         dyn_producer_loop(P, D, worker, smem);
     } else if (warp == kDmaWarp && worker == 0 && P.has_dma) {
-        dyn_dma_loop(P, D, P.num_calls <= kMaxCallExt ? reinterpret_cast<const int2*>(smem + kSmemCallExt) : nullptr);
+        dyn_dma_loop(P, D, P.num_calls <= kMaxCallExt ? reinterpret_cast<const int4*>(smem + kSmemCallExt) : nullptr);
     }
 }
 

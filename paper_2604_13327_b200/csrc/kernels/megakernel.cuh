@@ -167,12 +167,16 @@ struct DynParams {
     const int4* task_desc;       // (call, coord0, coord1, ext0 of the call at the sample)
     const int4* task_rng;        // (wait_off, wait_end, notify_off, notify_end)
     const int4* el_info;         // (consumer_off, consumer_end, dd tensor or -1, initial count)
+    const int* call_dd;          // per call: first data-dependent tensor it writes | count << 16, or -1
+    const int4* task_note;       // first notify of the task when static: (element, consumer_off,
+                                 // consumer_end, initial count), else element = -1
     // consumers[] entries carry bit 31 when that consumer has exactly one pending
     // wait (it is ready the moment the element fires: no rem[] decrement needed)
 };
 
-constexpr int kSmemCallExt = kSmemTable;       // dynamic kernel: per-call grid extents at the binding (int2)
-constexpr int kMaxCallExt = (kSmemBar - kSmemTable) / 8;
+constexpr int kSmemCallExt = kSmemTable;       // dynamic kernel: per-call grid extents at the binding and
+                                               // the data-dependent tensors it writes (int4)
+constexpr int kMaxCallExt = (kSmemBar - kSmemTable) / 16;
 
 }  // namespace etk
 

@@ -65,7 +65,8 @@ struct Sample {
     DevArray<int32_t> d_task_call, d_task_flat, d_task_duration, d_task_wait_off, d_task_waits, d_task_notify_off,
         d_task_notifies, d_task_rem_init, d_task_class, d_consumer_off, d_consumers, d_call_first_task, d_call_routed_rt,
         d_call_routed_base, d_call_range_rt, d_call_range_base, d_el_dd, d_ready;
-    DevArray<int4> d_task_desc, d_task_rng, d_el_info;
+    DevArray<int4> d_task_desc, d_task_rng, d_el_info, d_task_note;
+    DevArray<int32_t> d_call_dd;
     DevArray<uint8_t> d_task_wait_armed, d_call_range_armed;
 };
 
@@ -318,6 +319,8 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
         const et_dynamic_desc& d = dyn[i];
         Sample& S = rt->samples[static_cast<size_t>(i)];
         if (d.num_dd > etk::kMaxDd) return rt->fail(ET_ERR_INVALID, "too many data-dependent event tensors");
+        if (d.num_tasks >= (1 << 21) - 1)  // ready-queue slot words carry task + 1 in 21 bits
+            return rt->fail(ET_ERR_INVALID, "the dynamic scheduler supports fewer than 2^21 - 1 tasks per sample");
         const size_t nt = static_cast<size_t>(std::max(1, d.num_tasks));
         const size_t nw = static_cast<size_t>(std::max(1, d.task_wait_off[d.num_tasks]));
         const size_t nn = static_cast<size_t>(std::max(1, d.task_notify_off[d.num_tasks]));
@@ -378,9 +381,36 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
             for (int el = 0; el < S.num_counters; ++el)
                 info[static_cast<size_t>(el)] = make_int4(d.consumer_off[el], d.consumer_off[el + 1], d.el_dd[el],
                                                           s[i].initial_counts[el]);
+            std::vector<int4> note(nt, make_int4(-1, 0, 0, 0));
+            for (int t = 0; t < d.num_tasks; ++t) {
+                if (d.task_notify_off[t + 1] <= d.task_notify_off[t]) continue;
+                const int el = d.task_notifies[d.task_notify_off[t]];
+                if (d.el_dd[el] < 0) note[static_cast<size_t>(t)] = info[static_cast<size_t>(el)], note[static_cast<size_t>(t)].x = el,
+                                     note[static_cast<size_t>(t)].y = d.consumer_off[el],
+                                     note[static_cast<size_t>(t)].z = d.consumer_off[el + 1];
+            }
+            ET_CUDA(S.d_task_note.upload(note.data(), nt), "upload dynamic");
+            // per call: the data-dependent tensors it writes (consecutive indices), first | count << 16
+            std::vector<int32_t> cdd(static_cast<size_t>(std::max(1, rt->num_calls)), -1);
+            for (int t = 0; t < d.num_dd; ++t) {
+                const int c = d.dd_writer_call[t];
+                if (c < 0 || c >= rt->num_calls) continue;
+                int32_t& e = cdd[static_cast<size_t>(c)];
+                if (e < 0) e = t | (1 << 16);
+                else if ((e & 0xffff) + (e >> 16) == t) e += 1 << 16;
+                else return rt->fail(ET_ERR_INVALID, "a call's data-dependent tensors must be consecutive");
+            }
+            ET_CUDA(S.d_call_dd.upload(cdd.data(), cdd.size()), "upload dynamic");
             std::vector<int32_t> cons(d.consumers, d.consumers + d.consumer_off[S.num_counters]);
-            for (auto& c : cons)
-                if (d.task_rem_init[c] == 1 && d.call_range_rt[d.task_call[c]] < 0) c |= static_cast<int32_t>(0x80000000u);
+            // task (bits 0..20), its call (21..29; 511 = more calls than fit), bit 30: DMA class,
+            // bit 31: single pending wait (ready when this fires) -- megakernel.cu cons_task
+            for (auto& c : cons) {
+                const int t = c;
+                const int call = d.task_call[t] < 511 ? d.task_call[t] : 511;
+                c = t | (call << 21);
+                if (cls[static_cast<size_t>(t)] == 1) c |= 0x40000000;
+                if (d.task_rem_init[t] == 1 && d.call_range_rt[d.task_call[t]] < 0) c |= static_cast<int32_t>(0x80000000u);
+            }
             ET_CUDA(S.d_consumers.upload(cons.empty() ? nullptr : cons.data(), nc), "upload dynamic");
             ET_CUDA(S.d_task_desc.upload(desc.data(), nt), "upload dynamic");
             ET_CUDA(S.d_task_rng.upload(rng.data(), nt), "upload dynamic");
@@ -427,6 +457,8 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
         P.task_desc = S.d_task_desc.ptr;
         P.task_rng = S.d_task_rng.ptr;
         P.el_info = S.d_el_info.ptr;
+        P.task_note = S.d_task_note.ptr;
+        P.call_dd = S.d_call_dd.ptr;
         P.num_ready[0] = static_cast<int>(ready0.size());
         P.num_ready[1] = static_cast<int>(ready1.size());
         P.class_total[0] = totals[0];

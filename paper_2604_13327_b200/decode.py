@@ -249,7 +249,7 @@ class DecodeModel:
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
                  l2_prefetch=512 << 10, residual="split", fused_merge=True, balance=True, grouped=True,
-                 scheduler="static", early_push=False):
+                 scheduler="static", early_push=False, stage_barriers=False):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -272,6 +272,9 @@ class DecodeModel:
         self.call_tasks = self.layout["call_tasks"]
         self.grouped = self.layout["grouped"]
         self.oproj_group_tasks = self.layout["oproj_group_tasks"]
+        if stage_barriers:  # ablation: every call waits for the whole previous call (graphs.add_stage_barriers)
+            from .graphs import add_stage_barriers
+            spec = add_stage_barriers(spec)
         self.graph = etsim.Graph.from_json(json.dumps(spec))
         self.scheduler = scheduler
         if scheduler == "dynamic":  # on-GPU ready queues (Algorithm 2) instead of per-SM queues

@@ -88,3 +88,19 @@ def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allred
     }
 
 
+def add_stage_barriers(spec):
+    """The "unfused" ablation of a graph spec (the rewrite of ref simulate.cpp:682-794,
+    `simulate_barrier_baseline`): one single-element barrier Event Tensor between
+    every pair of consecutive calls, so each call starts only once the whole
+    previous call finished -- the stage-by-stage execution of one kernel per
+    operator, kept inside the persistent launch."""
+    import copy
+
+    spec = copy.deepcopy(spec)
+    calls = spec["calls"]
+    for i in range(len(calls) - 1):
+        name = f"__stage{i}"
+        spec["event_tensors"].append({"name": name, "shape": ["1"]})
+        calls[i].setdefault("out", []).append({"event": name, "map": ["0"]})
+        calls[i + 1].setdefault("in", []).append({"event": name, "map": ["0"]})
+    return spec

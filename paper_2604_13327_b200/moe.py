@@ -371,7 +371,7 @@ class MoEDecodeModel:
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
                  scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=True,
                  balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False, qkv_split=True,
-                 max_batch=1, batch_samples=None, attn_cap=None, oproj_merge=True):
+                 max_batch=1, batch_samples=None, attn_cap=None, oproj_merge=True, stage_barriers=False):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -386,6 +386,9 @@ class MoEDecodeModel:
                          group_stage=group_stage, qkv_split=qkv_split, oproj_merge=oproj_merge)
         for k, v in lay.items():
             setattr(self, k, v)
+        if stage_barriers:  # ablation: every call waits for the whole previous call (graphs.add_stage_barriers)
+            from .graphs import add_stage_barriers
+            self.spec = add_stage_barriers(self.spec)
         self.graph = etsim.Graph.from_json(json.dumps(self.spec))
         self.rt_index = {r["name"]: i for i, r in enumerate(self.spec["runtime_tensors"])}
         if scheduler == "dynamic":

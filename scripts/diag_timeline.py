@@ -27,7 +27,8 @@ def main():
     else:
         from paper_2604_13327_b200.moe import MOE_CONFIGS, MoEDecodeModel
         sched = sys.argv[1].split("-")[1] if "-" in which else "static"
-        m = MoEDecodeModel(MOE_CONFIGS["qwen3-30b-a3b"], samples=(1024,), scheduler=sched, record_trace=True)
+        m = MoEDecodeModel(MOE_CONFIGS["qwen3-30b-a3b"], samples=(1024,), scheduler=sched.replace("early", "dynamic"),
+                           early_push=sched == "early", record_trace=True)
         m.fill_cache(1024, seed=1)
         m.set_token([1])
         binding = m._binding(1024, 1)
