@@ -526,6 +526,10 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
                                                 " has no device body (the routed notify / red.add epilogues "
                                                 "replace MOE_GROUP and MOE_COMBINE)");
         if (k == ET_OP_MOE_ROUTE || k == ET_OP_MOE_EXPERT) variant |= 1;
+        // attention groups wider than 512 (head, dim) outputs (e.g. Llama-3-70B: 8 q heads per kv
+        // head) need the wide split / merge bodies, compiled into the kMoE instantiations
+        if ((k == ET_OP_ATTN_SPLIT || k == ET_OP_ATTN_MERGE) && ops[c].i[0] * ops[c].i[1] > 2 * etk::kConsumers)
+            variant |= 1;
         else if (k == ET_OP_GEMV_TC || k == ET_OP_NORM) variant |= 2;
     }
     for (int32_t c = 0; c < num_calls; ++c) {
@@ -544,6 +548,8 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     for (int32_t c = 0; c < num_calls; ++c) {
         if (ops[c].kind != ET_OP_ATTN_SPLIT && ops[c].kind != ET_OP_ATTN_MERGE) continue;
         const int dh = ops[c].i[0], G = ops[c].i[1], CH = ops[c].i[2];
+        if (G * dh > 4 * etk::kConsumers)  // the wide bodies hold 4 (head, dim) outputs per thread
+            return rt->fail(ET_ERR_INVALID, "attention groups need q heads per kv head x head_dim <= 1024");
         if ((ops[c].flags & 256) && dh % 64 != 0)  // chunk j ^ (pos % 8) must stay inside the row
             return rt->fail(ET_ERR_INVALID, "chunk-swizzled KV rows (attention flags bit 8) need head_dim % 64 == 0");
         if ((variant & 2) && ops[c].kind == ET_OP_ATTN_SPLIT && (G > 8 || dh % 16 != 0 || dh > 128 || CH != 64))

@@ -226,3 +226,71 @@ def exchange_peers(local_ptrs, rank, world, group=None, get_handle=None, opener=
     handles = [None] * world
     dist.all_gather_object(handles, mine, group=group)
     return [tuple(local_ptrs) if p == rank else tuple(opener(h) for h in handles[p]) for p in range(world)]
+
+
+class LocalTPGroup:
+    """All TP ranks of a sharded decoder in ONE process on ONE GPU (a single-GPU
+    pool): each rank is its own persistent kernel on its own stream over
+    num_workers // world SMs, peers mapped by plain device pointers.  The ranks
+    share one token buffer and write their vocab slices into one logits row, so
+    the group looks like one model to a caller (launch / executor.sync / logits).
+    The cross-rank Event Tensor elements and the peer reads are exactly the
+    multi-GPU ones; only NVLink is replaced by the GPU's own memory."""
+
+    class _Sync:
+        def __init__(self, ranks):
+            self.ranks = ranks
+
+        def sync(self):
+            out = {}
+            for m in self.ranks:  # per-rank counts summed over the group
+                for k, v in m.executor.sync().items():
+                    out[k] = out.get(k, 0) + v if isinstance(v, (int, float)) and k != "kernel_ms" else v
+            return out
+
+    def __init__(self, cfg, world, device="cuda:0", samples=(1024,), seed=0, weights=None, record_trace=False):
+        dev = torch.device(device)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.cfg, self.world, self.device = cfg, world, dev
+        self.ranks = [TPDecodeModel(cfg, r, world, device=dev, samples=samples, num_workers=sms // world, seed=seed,
+                                    weights=weights, record_trace=record_trace) for r in range(world)]
+        self.tokens = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=dev)
+        V = cfg.vocab // world
+        for r, m in enumerate(self.ranks):
+            m.tokens = self.tokens
+            m.logits = self.logits[:, r * V:(r + 1) * V]
+        peers = [m.local_buffers() for m in self.ranks]
+        for m in self.ranks:
+            m.connect(peers)
+        self.streams = [torch.cuda.Stream(device=dev) for _ in self.ranks]
+        self.executor = LocalTPGroup._Sync(self.ranks)
+        self.local = self.ranks[0].local
+        self.lower_ms = sum(m.lower_ms for m in self.ranks)
+        self.upload_ms = sum(m.upload_ms for m in self.ranks)
+
+    def fill_cache(self, s, seed=1):
+        for m in self.ranks:
+            m.fill_cache(s, seed=seed)
+
+    def set_token(self, token):
+        self.tokens.fill_(int(token))
+
+    def launch(self, s, stream=0):
+        """Every rank's step, ordered after the work already on `stream`, which then
+        waits for all of them (events time the whole TP step on `stream`)."""
+        main = torch.cuda.ExternalStream(stream, device=self.device) if stream else torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        done = []
+        for m, st in zip(self.ranks, self.streams):
+            st.wait_event(start)
+            m.launch(s, st.cuda_stream)
+            e = torch.cuda.Event()
+            e.record(st)
+            done.append(e)
+        for e in done:
+            main.wait_event(e)
+
+    def step_bytes(self, s):
+        return self.world * self.local.step_bytes(s)

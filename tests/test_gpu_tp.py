@@ -49,3 +49,35 @@ def test_tp2_logits_match_full_model_oracle(s, token):
         t = m.executor.trace()
         assert m.graph.instantiate({"s": s}).check(t) == []
         assert all(c == 0 for c in m.executor.final_counters())
+
+
+def test_tp2_llama70b_shape_two_layers_on_one_gpu():
+    """Llama-3-70B-shaped layers (hidden 8192, 64 q / 8 kv heads, intermediate 28672,
+    vocab 128256), 2 of the 80, TP=2 as two concurrent persistent kernels on one GPU
+    (74 SMs each, tp.LocalTPGroup): the gathered logits against the full-model CPU
+    oracle at the full-depth tolerance (oracle/parity.py), appended K/V per layer."""
+    import dataclasses
+
+    from oracle.parity import dense_parity
+    from paper_2604_13327_b200.decode import LLAMA3_70B
+    from paper_2604_13327_b200.tp import LocalTPGroup
+
+    cfg, s, token = dataclasses.replace(LLAMA3_70B, layers=2), 300, 11
+    dev = torch.device("cuda:0")
+    g = LocalTPGroup(cfg, 2, device=dev, samples=(512,), seed=0)
+    try:
+        g.fill_cache(s, seed=1)
+        g.set_token(token)
+        g.launch(s)
+        torch.cuda.synchronize()
+        g.executor.sync()
+        full_k = [torch.cat([m.kcache[l] for m in g.ranks]) for l in range(cfg.layers)]
+        full_v = [torch.cat([m.vcache[l] for m in g.ranks]) for l in range(cfg.layers)]
+        rep = dense_parity(cfg, 0, dev, [token], s, g.ranks[0].inv_freq, full_k, full_v, g.logits)
+        print("llama3-70b 2L TP=2 on one GPU", rep)
+        assert rep["pass"], rep
+        for m in g.ranks:
+            assert all(c == 0 for c in m.executor.final_counters())
+    finally:
+        del g
+        torch.cuda.empty_cache()
