@@ -61,11 +61,11 @@ enum et_op_kind {
     ET_OP_ALLREDUCE = 8,      /* NVLink peer-memory allreduce (tensor parallel)    */
     ET_OP_MOE_GROUP = 9,      /* scatter routed (token, k) slots into expert lists */
     ET_OP_MOE_COMBINE = 10,   /* weighted combine of expert outputs + residual     */
-    ET_OP_ARGMAX = 11,        /* greedy token from logits                          */
+    ET_OP_ARGMAX = 11,        /* greedy token from the lm_head's argmax words      */
     ET_OP_EMBED = 12,         /* embedding rows of the step's tokens -> fp32 stream */
     ET_OP_GEMV_TC = 13,       /* large-batch GEMV on tcgen05 tensor cores (TMEM)   */
     ET_OP_NORM = 14,          /* RMSNorm of the stream -> bf16 tensor-core operand */
-    ET_OP_ARGMAX_LAST = 14    /* (highest kind with a device body; et_bind_ops rejects
+    ET_OP_KIND_LAST = 14      /* (highest kind with a device body; et_bind_ops rejects
                                  the rest, and ET_OP_MOE_GROUP / ET_OP_MOE_COMBINE,
                                  whose work the routed notify and the expert tiles'
                                  red.add epilogue absorb) */

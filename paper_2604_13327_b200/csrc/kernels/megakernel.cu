@@ -596,6 +596,15 @@ __device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et
     bar_sync(1, kConsumers);  // ml / wts live in acc, zeroed by the caller
 }
 
+// Greedy-decoding argmax word: float bits made unsigned-ordered, row complemented
+// so that atomicMax prefers the lower row among equal values.
+__device__ __forceinline__ unsigned long long argmax_key(float v, int row) {
+    uint32_t b = __float_as_uint(v);
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return (static_cast<unsigned long long>(b) << 32) | static_cast<uint32_t>(~row);
+}
+__device__ __forceinline__ int argmax_row(unsigned long long key) { return static_cast<int>(~static_cast<uint32_t>(key)); }
+
 // Row-range GEMV y[b][r] = sum_k W[r][k] x[b][k] for rows [r0, r1) (multiples
 // of 16) of a bf16 weight in mma-fragment tile order (K % 32 == 0).  The
 // weight tiles stream through the shared-memory ring; activations are staged
@@ -762,6 +771,21 @@ __device__ uint64_t body_gemv(const StaticParams& P, const et_op& op, const Slot
                 const float sv = v / (1.f + __expf(-v));
                 reinterpret_cast<uint16_t*>(op.p[4])[o] = f2bf(sv * u);
             }
+        }
+        if ((op.flags & 32) && epi == EPI_F32 && nb == 1) {
+            // flags bit 5 (greedy decoding): fold this task's rows into the step's argmax,
+            // one packed 64-bit word (ordered float bits << 32 | ~row: atomicMax keeps the
+            // largest logit, the lowest row on ties) at p6, zeroed by the step's embed
+            unsigned long long best = 0ull;
+            for (int i = ctid; i < R; i += kConsumers) {
+                const unsigned long long key = argmax_key(acc[i], r0 + i);
+                best = key > best ? key : best;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+                best = x > best ? x : best;
+            }
+            if ((ctid & 31) == 0 && best) atomicMax(reinterpret_cast<unsigned long long*>(op.p[6]), best);
         }
     }
     return t_pro;
@@ -2022,12 +2046,29 @@ __device__ void body_allreduce(const StaticParams& P, const et_op& op, const Slo
 __device__ void body_embed(const StaticParams& P, const et_op& op, int ctid) {
     const int H = op.i[0];
     const int nb = op.i[1] >= 0 ? static_cast<int>(P.binding[op.i[1]]) : 1;
+    // flags bit 0: this step's greedy-argmax words (p3, one per sequence) start at 0; every
+    // lm_head task waits on this task through the layer chain
+    if ((op.flags & 1) && ctid < nb) reinterpret_cast<unsigned long long*>(op.p[3])[ctid] = 0ull;
     const uint16_t* table = reinterpret_cast<const uint16_t*>(op.p[0]);
     const int* tok = reinterpret_cast<const int*>(op.p[1]);
     float* out = reinterpret_cast<float*>(op.p[2]);
     for (int bi = 0; bi < nb; ++bi) {
         const long long row = __ldcg(tok + bi);
         for (int k = ctid; k < H; k += kConsumers) out[static_cast<long long>(bi) * H + k] = bf2f(table[row * H + k]);
+    }
+}
+
+// ET_OP_ARGMAX: task (0): the greedy token of each sequence from the argmax words the
+// lm_head epilogue (GEMV flags bit 5) left at p0 -> int32 p1[b] (and, when p2 is set,
+// the next step's token input), words re-zeroed.  i0 = batch symbol slot (-1: 1).
+__device__ void body_argmax(const StaticParams& P, const et_op& op, int ctid) {
+    const int nb = op.i[0] >= 0 ? static_cast<int>(P.binding[op.i[0]]) : 1;
+    if (ctid < nb) {
+        unsigned long long* w = reinterpret_cast<unsigned long long*>(op.p[0]);
+        const int tok = argmax_row(__ldcg(w + ctid));
+        reinterpret_cast<int*>(op.p[1])[ctid] = tok;
+        if (op.p[2]) reinterpret_cast<int*>(op.p[2])[ctid] = tok;
+        w[ctid] = 0ull;
     }
 }
 
@@ -2129,6 +2170,7 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                     if constexpr (kTC) body_norm(P, op, v, red, ctid);
                     break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
+                case ET_OP_ARGMAX: body_argmax(P, op, ctid); break;
                 case ET_OP_ALLREDUCE: body_allreduce(P, op, v, ctid, worker); break;
                 case ET_OP_MOE_ROUTE:
                     if constexpr (kMoE) body_moe_route<kTC>(P, op, v, xs, acc, red, ring, ctid, &t_pro);
@@ -3159,6 +3201,7 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     if constexpr (kTC) body_norm(P, op, v, red, ctid);
                     break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
+                case ET_OP_ARGMAX: body_argmax(P, op, ctid); break;
                 case ET_OP_MOE_ROUTE:
                     if constexpr (kMoE) body_moe_route<kTC>(P, op, v, xs, acc, red, ring, ctid, &tp);
                     break;

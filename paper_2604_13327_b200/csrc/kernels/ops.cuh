@@ -74,7 +74,12 @@
 //   p3 = peer table (uint64 [TP][2]: rank p's part buffer base (fp32 [slots][H]), its flags)
 // ET_OP_EMBED           task (0): h[b][:] = float(table[tokens[b]][:]) for every batch row
 //   i0 = hidden, i1 = batch symbol slot (-1: 1); p0 = table (bf16 [vocab][hidden]),
-//   p1 = token ids (int32 [b]), p2 = out (fp32 [b][hidden])
+//   p1 = token ids (int32 [b]), p2 = out (fp32 [b][hidden]); flags bit 0: zero the step's
+//   greedy argmax words at p3 (u64 [b])
+// GEMV flags bit 5 (EPI_F32, b = 1): greedy decoding -- the task's rows fold into the argmax
+//   word at p6 (u64: ordered float bits << 32 | ~row, atomicMax)
+// ET_OP_ARGMAX          task (0): token[b] = row of the argmax word p0[b] -> p1 (int32 [b]) and,
+//   if set, p2 (the next step's token input); words re-zeroed; i0 = batch symbol slot (-1: 1)
 // ET_OP_GEMV_TC         large-batch GEMV on the tcgen05 tensor cores: task t of T = G * i3 takes
 //   row blocks [g*nblk/G, (g+1)*nblk/G) (128 rows each, nblk = N/128) and k pieces
 //   [r*np/i3, (r+1)*np/i3) (np = K/kp) with g = t / i3, r = t % i3; per piece the activation

@@ -521,7 +521,7 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     int variant = 0;
     for (int32_t c = 0; c < num_calls; ++c) {
         const int k = ops[c].kind;
-        if (k == ET_OP_MOE_GROUP || k == ET_OP_MOE_COMBINE || k < ET_OP_NONE || k > ET_OP_ARGMAX_LAST)
+        if (k == ET_OP_MOE_GROUP || k == ET_OP_MOE_COMBINE || k < ET_OP_NONE || k > ET_OP_KIND_LAST)
             return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": op kind " + std::to_string(k) +
                                                 " has no device body (the routed notify / red.add epilogues "
                                                 "replace MOE_GROUP and MOE_COMBINE)");

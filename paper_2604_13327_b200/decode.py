@@ -41,6 +41,7 @@ from .ops import (
     EPI_ADD,
     EPI_RESID,
     EPI_SILU_MUL,
+    GEMV_ARGMAX,
     OP_ATTN_MERGE,
     OP_ATTN_SPLIT,
     OP_EMBED,
@@ -297,6 +298,9 @@ class DecodeModel:
         self.attn = torch.zeros(cfg.q_rows, dtype=torch.bfloat16, device=dev)
         self.act = torch.zeros(cfg.intermediate, dtype=torch.bfloat16, device=dev)
         self.logits = torch.zeros(1, cfg.vocab, dtype=torch.float32, device=dev)
+        # greedy decoding on the device: the lm_head tasks fold their rows into one argmax
+        # word per step (zeroed by the step's embed); 8 bytes to read instead of the logits
+        self.best = torch.zeros(1, dtype=torch.int64, device=dev)
         self.h_b = torch.zeros_like(self.h_a) if residual == "double" else self.h_a
         self.partials = torch.zeros(cfg.heads, self.max_splits, cfg.head_dim + 4, dtype=torch.float32, device=dev)
         self.arrive = torch.zeros(cfg.layers, cfg.kv_heads, dtype=torch.int32, device=dev)  # split arrivals (fused merge)
@@ -316,7 +320,8 @@ class DecodeModel:
     def _ops(self):
         cfg, W = self.cfg, self.W
         H, dh, CH = cfg.hidden, cfg.head_dim, cfg.attn_chunk
-        ops = [make_op(OP_EMBED, i=[H, -1], p=[ptr(W["embed"]), ptr(self.tokens), ptr(self.h_a)])]
+        ops = [make_op(OP_EMBED, i=[H, -1], p=[ptr(W["embed"]), ptr(self.tokens), ptr(self.h_a), ptr(self.best)],
+                       flags=1)]
         s_slot = 0
         scale = 1.0 / math.sqrt(dh)
         G = cfg.heads // cfg.kv_heads
@@ -361,9 +366,15 @@ class DecodeModel:
             else:
                 ops.append(make_op(OP_GEMV, i=[H, cfg.intermediate, 1, 0, EPI_RESID, -1, 0, 16],
                                    p=[ptr(L["wdown"]), 0, ptr(self.act), 0, ptr(self.h_a), ptr(self.h_b)]))
-        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps],
-                           p=[ptr(W["lm_head"]), 0, ptr(self.h_a), ptr(W["final_norm"]), ptr(self.logits)]))
+        ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, -1, 0, 16, 0, H], f=[cfg.eps], flags=GEMV_ARGMAX,
+                           p=[ptr(W["lm_head"]), 0, ptr(self.h_a), ptr(W["final_norm"]), ptr(self.logits), 0,
+                              ptr(self.best)]))
         return ops
+
+    def greedy_token(self):
+        """The last step's greedy token, computed on the device (reads 8 bytes)."""
+        from .ops import argmax_token
+        return argmax_token(self.best.item())
 
     def fill_cache(self, s, seed=1):
         """Synthetic prefilled KV cache: N(0, 1) bf16 for positions [0, s)."""

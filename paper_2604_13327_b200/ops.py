@@ -28,6 +28,13 @@ OP_NORM = 14
 
 EPI_F32, EPI_BF16, EPI_RESID, EPI_SILU_MUL, EPI_QKV_ROPE, EPI_ADD = range(6)
 
+GEMV_ARGMAX = 32  # GEMV flags bit 5: the lm_head folds its rows into the step's greedy argmax word
+
+
+def argmax_token(word):
+    """Token id of a greedy argmax word (ordered float bits << 32 | ~row, megakernel.cu argmax_key)."""
+    return (~int(word)) & 0xFFFFFFFF
+
 
 class EtOp(ctypes.Structure):
     _fields_ = [

@@ -51,6 +51,22 @@ def test_tiny_logits_match_oracle(tiny, s):
     assert mg.check(t) == []
     assert all(c == 0 for c in m.executor.final_counters())
     assert m.last_stats["tasks_executed"] == mg.num_tasks
+    # greedy token decided on the device (lm_head argmax words) == argmax of the logits
+    assert m.greedy_token() == int(logits.argmax())
+
+
+def test_greedy_token_on_device_across_steps(tiny):
+    """The argmax word restarts every step (the embed zeroes it) and ET_OP_ARGMAX-style
+    decoding follows the logits step after step (tokens fed back by the host)."""
+    m = tiny
+    m.fill_cache(20, seed=3)
+    tok = 5
+    for step in range(4):
+        m.set_token(tok)
+        logits = m.step(20 + step)[0]
+        got = m.greedy_token()
+        assert got == int(logits.argmax()), (step, got)
+        tok = got
 
 
 @pytest.fixture(scope="module")
