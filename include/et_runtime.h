@@ -222,6 +222,17 @@ int et_upload_static(et_runtime* rt, const et_sample_desc* samples, int32_t num_
 int et_upload_dynamic(et_runtime* rt, const et_sample_desc* samples, const et_dynamic_desc* dyn,
                       int32_t num_samples);
 int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls);
+/* Ahead-of-time program image (replaces ref json_io.cpp:294-376 / 455-494, the
+ * reference's kernel_to_json / kernel_from_json "compile once, run many" form):
+ * et_save_program writes the graph and static samples exactly as uploaded (flat
+ * arrays, length-prefixed) plus an opaque metadata blob (the Python Executor stores
+ * the symbol / runtime-tensor / call names there); et_load_program uploads a saved
+ * image into a fresh runtime -- no lowering, no flattening -- and returns the
+ * metadata (*meta_len in: capacity of meta_out, out: its size; meta_out may be
+ * NULL to query).  Op tables hold this process's device pointers and are bound
+ * again after a load (et_bind_ops).  Dynamic programs have no image. */
+int et_save_program(et_runtime* rt, const char* path, const void* meta, int64_t meta_len);
+int et_load_program(et_runtime* rt, const char* path, void* meta_out, int64_t* meta_len);
 
 /* Copies host values into a runtime tensor (a routing realization supplied by
  * the host).  Tensors not written this way are produced on the device by their

@@ -43,6 +43,11 @@ public:
     // binding runs on the next-larger sample with masked no-ops); data-dependent
     // routing is resolved on the device.
     Executor(const DynamicMegakernel& k, const std::vector<ShapeBinding>& samples, const ExecConfig& cfg);
+    // Ahead-of-time program image (et_save_program / et_load_program): a static
+    // executor saved once loads without lowering or flattening; the graph rides
+    // along as the image's metadata (reference JSON), so traces keep working.
+    static std::unique_ptr<Executor> load_program(const std::string& path, const ExecConfig& cfg);
+    void save_program(const std::string& path) const;
     ~Executor();
     Executor(const Executor&) = delete;
     Executor& operator=(const Executor&) = delete;
@@ -69,6 +74,7 @@ public:
     void set_l2_prefetch(Int bytes);  // producer L2 run-ahead per worker (et_set_l2_prefetch)
 
 private:
+    Executor();
     struct Impl;
     std::unique_ptr<Impl> impl_;
 };

@@ -2,6 +2,7 @@
 // program arrays, the Executor, and the reference-named simulate() entry
 // points (ref simulate.hpp:23-36), which here run on the device.
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 
 #include "etsim/exec.hpp"
@@ -566,6 +567,115 @@ Executor::Executor(const StaticMegakernel& k, const ExecConfig& cfg) : impl_(new
 }
 
 Executor::~Executor() = default;
+Executor::Executor() : impl_(new Impl) {}
+
+void Executor::save_program(const std::string& path) const {
+    const Impl& I = *impl_;
+    if (I.dyn) throw Error("program images hold static schedules only");
+    const std::string meta = graph_to_json(I.k.graph, -1);
+    I.check(et_save_program(I.rt, path.c_str(), meta.data(), static_cast<int64_t>(meta.size())), "save program");
+}
+
+namespace {
+// Reads back the flat arrays of a program image (format: runtime.cu et_save_program)
+// into HostSamples (trace reconstruction and error messages need them host-side).
+struct ImageReader {
+    std::vector<uint8_t> buf;
+    size_t pos = 0;
+    int64_t i64() {
+        int64_t v = 0;
+        if (pos + 8 > buf.size()) throw Error("truncated program image");
+        std::memcpy(&v, buf.data() + pos, 8);
+        pos += 8;
+        return v;
+    }
+    template <typename T>
+    std::vector<T> arr() {
+        const int64_t n = i64();
+        std::vector<T> v(static_cast<size_t>(n > 0 ? n : 0));
+        const size_t bytes = v.size() * sizeof(T);
+        if (pos + bytes > buf.size()) throw Error("truncated program image");
+        if (bytes) std::memcpy(v.data(), buf.data() + pos, bytes);
+        pos += bytes;
+        return v;
+    }
+};
+}  // namespace
+
+std::unique_ptr<Executor> Executor::load_program(const std::string& path, const ExecConfig& cfg) {
+    const auto t0 = std::chrono::steady_clock::now();
+    ImageReader r;
+    {
+        FILE* f = std::fopen(path.c_str(), "rb");
+        if (!f) throw Error("cannot read " + path);
+        uint8_t tmp[1 << 16];
+        size_t n;
+        while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) r.buf.insert(r.buf.end(), tmp, tmp + n);
+        std::fclose(f);
+    }
+    r.pos = 8;  // magic (checked by et_load_program)
+    r.i64();    // abi
+    const int workers = static_cast<int>(r.i64());
+    const auto meta = r.arr<char>();
+    r.i64();
+    r.i64();
+    std::unique_ptr<Executor> ex(new Executor());
+    Impl& I = *ex->impl_;
+    I.cfg = cfg;
+    I.workers = workers;
+    I.k.graph = graph_from_json(std::string(meta.begin(), meta.end()));
+    I.k.num_sms = workers;
+    for (const auto& t : I.k.graph.runtime_tensors) I.rt_names.push_back(t.name);
+    // graph section (the order of et_upload_graph): num_symbols; call_rank, call_extent_from,
+    // grid_code_off, code_op (int32); code_arg, runtime_capacity (int64); runtime_len_off (int32)
+    r.i64();
+    for (int j = 0; j < 4; ++j) r.arr<int32_t>();
+    r.arr<int64_t>();
+    r.arr<int64_t>();
+    r.arr<int32_t>();
+    const int64_t ns = r.i64();
+    for (int64_t i = 0; i < ns; ++i) {
+        HostSample h;
+        h.num_queues = static_cast<int>(r.i64());
+        h.has_dma = static_cast<int>(r.i64());
+        r.i64();  // slots
+        r.i64();  // counters
+        h.binding = r.arr<int64_t>();
+        h.call_extents = r.arr<int32_t>();
+        h.queue_off = r.arr<int32_t>();
+        h.slot_task = r.arr<int32_t>();
+        h.slot_call = r.arr<int32_t>();
+        h.slot_flat = r.arr<int32_t>();
+        h.slot_duration = r.arr<int32_t>();
+        h.wait_off = r.arr<int32_t>();
+        h.waits = r.arr<int32_t>();
+        h.notify_off = r.arr<int32_t>();
+        h.notifies = r.arr<int32_t>();
+        h.initial_counts = r.arr<int32_t>();
+        for (int q = 0; q + 1 < static_cast<int>(h.queue_off.size()); ++q)
+            for (int s = h.queue_off[static_cast<size_t>(q)]; s < h.queue_off[static_cast<size_t>(q) + 1]; ++s)
+                h.slot_queue.push_back(q);
+        I.hs.push_back(std::move(h));
+    }
+    et_config ec{};
+    ec.device = cfg.device;
+    ec.num_workers = workers;
+    ec.record_trace = cfg.record_trace ? 1 : 0;
+    ec.enable_prefetch = cfg.enable_prefetch ? 1 : 0;
+    ec.watchdog_ns = cfg.watchdog_ns;
+    ec.tick_ns = cfg.tick_ns;
+    ec.step_limit = cfg.step_limit;
+    ec.max_batch = cfg.max_batch;
+    ec.l2_prefetch_bytes = cfg.l2_prefetch_bytes;
+    const int rc = et_create(&ec, &I.rt);
+    if (rc != ET_OK) raise_status(rc, "cannot create the GPU runtime");
+    I.check(et_load_program(I.rt, path.c_str(), nullptr, nullptr), "load program");
+    std::vector<et_op> none(I.k.graph.calls.size());
+    std::memset(none.data(), 0, none.size() * sizeof(et_op));
+    I.check(et_bind_ops(I.rt, none.data(), static_cast<int32_t>(none.size())), "bind ops");
+    I.upload_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return ex;
+}
 
 void Executor::bind_ops(const std::vector<et_op>& ops) {
     Impl& I = *impl_;

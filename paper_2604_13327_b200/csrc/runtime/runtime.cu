@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -146,6 +147,9 @@ struct et_runtime {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timed = false;  // ev0/ev1 bracket the last launch (synchronous steps only)
     int debug = 0;       // ET_DEBUG at et_create
+    // program image (et_save_program): the graph and static samples as uploaded
+    std::vector<uint8_t> img_graph, img_samples;
+    bool img_static = false;
 
     int fail(int code, const std::string& m) {
         err = m;
@@ -162,6 +166,48 @@ struct et_runtime {
         cudaError_t e__ = (call);                             \
         if (e__ != cudaSuccess) return rt->cuda_fail(e__, what); \
     } while (0)
+
+namespace {
+// Program image: length-prefixed little-endian arrays, in the field order of the
+// descriptors (include/et_runtime.h), so a load needs no lowering.
+struct ImgOut {
+    std::vector<uint8_t>& b;
+    void raw(const void* p, size_t n) {
+        const uint8_t* c = static_cast<const uint8_t*>(p);
+        b.insert(b.end(), c, c + n);
+    }
+    void i64(int64_t v) { raw(&v, 8); }
+    template <typename T>
+    void arr(const T* p, int64_t n) {
+        i64(p ? n : -1);
+        if (p && n > 0) raw(p, static_cast<size_t>(n) * sizeof(T));
+    }
+};
+struct ImgIn {
+    const uint8_t* p;
+    const uint8_t* e;
+    bool ok = true;
+    int64_t i64() {
+        int64_t v = 0;
+        if (e - p < 8) { ok = false; return 0; }
+        std::memcpy(&v, p, 8);
+        p += 8;
+        return v;
+    }
+    template <typename T>
+    std::vector<T> arr(bool* present = nullptr) {
+        const int64_t n = i64();
+        if (present) *present = n >= 0;
+        std::vector<T> v(static_cast<size_t>(n > 0 ? n : 0));
+        const size_t bytes = v.size() * sizeof(T);
+        if (static_cast<size_t>(e - p) < bytes) { ok = false; return {}; }
+        if (bytes) std::memcpy(v.data(), p, bytes);
+        p += bytes;
+        return v;
+    }
+};
+constexpr char kImgMagic[8] = {'E', 'T', 'P', 'R', 'O', 'G', '0', '1'};
+}  // namespace
 
 extern "C" {
 
@@ -249,6 +295,18 @@ int et_upload_graph(et_runtime* rt, const et_graph_desc* g) {
     ET_CUDA(rt->d_rt_table.upload(table.data(), table.size()), "runtime tensors");
     rt->samples.clear();
     rt->last_sample = -1;
+    rt->img_graph.clear();
+    rt->img_samples.clear();
+    rt->img_static = false;
+    ImgOut o{rt->img_graph};
+    o.i64(g->num_symbols);
+    o.arr(g->call_rank, g->num_calls);
+    o.arr(g->call_extent_from, g->num_calls);
+    o.arr(g->grid_code_off, g->num_calls * 4 + 1);
+    o.arr(g->code_op, g->code_len);
+    o.arr(g->code_arg, g->code_len);
+    o.arr(g->runtime_capacity, g->num_runtime_tensors);
+    o.arr(g->runtime_len_off, g->num_runtime_tensors + 1);
     return ET_OK;
 }
 
@@ -303,7 +361,133 @@ int et_upload_static(et_runtime* rt, const et_sample_desc* s, int32_t num_sample
     rt->last_sample = -1;
     rt->launched = false;
     rt->mode = ET_MODE_STATIC;
+    rt->img_samples.clear();
+    ImgOut o{rt->img_samples};
+    o.i64(num_samples);
+    for (int i = 0; i < num_samples; ++i) {
+        const et_sample_desc& d = s[i];
+        const int64_t nq = d.num_queues + d.has_dma + 1;
+        o.i64(d.num_queues);
+        o.i64(d.has_dma);
+        o.i64(d.num_slots);
+        o.i64(d.num_counters);
+        o.arr(d.binding, rt->num_symbols);
+        o.arr(d.call_extents, rt->num_calls * 4);
+        o.arr(d.queue_off, nq);
+        o.arr(d.slot_task, d.num_slots);
+        o.arr(d.slot_call, d.num_slots);
+        o.arr(d.slot_flat, d.num_slots);
+        o.arr(d.slot_duration, d.num_slots);
+        o.arr(d.wait_off, d.num_slots + 1);
+        o.arr(d.waits, d.wait_off[d.num_slots]);
+        o.arr(d.notify_off, d.num_slots + 1);
+        o.arr(d.notifies, d.notify_off[d.num_slots]);
+        o.arr(d.initial_counts, d.num_counters);
+    }
+    rt->img_static = true;
     return ET_OK;
+}
+
+int et_save_program(et_runtime* rt, const char* path, const void* meta, int64_t meta_len) {
+    if (!rt || !path || meta_len < 0 || (meta_len > 0 && !meta)) return ET_ERR_INVALID;
+    if (!rt->img_static) return rt->fail(ET_ERR_INVALID, "no static program uploaded (dynamic programs have no image)");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return rt->fail(ET_ERR_INVALID, std::string("cannot write ") + path);
+    std::vector<uint8_t> head;
+    ImgOut o{head};
+    o.raw(kImgMagic, 8);
+    o.i64(ET_ABI_VERSION);
+    o.i64(rt->cfg.num_workers);
+    o.arr(static_cast<const uint8_t*>(meta), meta_len);
+    o.i64(static_cast<int64_t>(rt->img_graph.size()));
+    o.i64(static_cast<int64_t>(rt->img_samples.size()));
+    bool ok = std::fwrite(head.data(), 1, head.size(), f) == head.size();
+    ok = ok && std::fwrite(rt->img_graph.data(), 1, rt->img_graph.size(), f) == rt->img_graph.size();
+    ok = ok && std::fwrite(rt->img_samples.data(), 1, rt->img_samples.size(), f) == rt->img_samples.size();
+    ok = std::fclose(f) == 0 && ok;
+    return ok ? ET_OK : rt->fail(ET_ERR_INVALID, std::string("short write to ") + path);
+}
+
+int et_load_program(et_runtime* rt, const char* path, void* meta_out, int64_t* meta_len) {
+    if (!rt || !path) return ET_ERR_INVALID;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return rt->fail(ET_ERR_INVALID, std::string("cannot read ") + path);
+    std::vector<uint8_t> buf;
+    uint8_t tmp[1 << 16];
+    size_t n;
+    while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
+    std::fclose(f);
+    if (buf.size() < 8 || std::memcmp(buf.data(), kImgMagic, 8) != 0)
+        return rt->fail(ET_ERR_INVALID, std::string(path) + " is not a program image");
+    ImgIn in{buf.data() + 8, buf.data() + buf.size()};
+    if (in.i64() != ET_ABI_VERSION) return rt->fail(ET_ERR_INVALID, "program image from another ABI version");
+    const int64_t workers = in.i64();
+    if (workers != rt->cfg.num_workers)
+        return rt->fail(ET_ERR_INVALID, "program image was lowered for " + std::to_string(workers) + " workers");
+    const std::vector<uint8_t> meta = in.arr<uint8_t>();
+    if (meta_len) {
+        const int64_t cap = *meta_len;
+        *meta_len = static_cast<int64_t>(meta.size());
+        if (meta_out && cap >= static_cast<int64_t>(meta.size()) && !meta.empty())
+            std::memcpy(meta_out, meta.data(), meta.size());
+    }
+    in.i64();
+    in.i64();
+    // graph
+    et_graph_desc g{};
+    g.num_symbols = static_cast<int32_t>(in.i64());
+    const auto call_rank = in.arr<int32_t>(), call_ef = in.arr<int32_t>(), grid_off = in.arr<int32_t>(),
+               code_op = in.arr<int32_t>();
+    const auto code_arg = in.arr<int64_t>(), rt_cap = in.arr<int64_t>();
+    const auto rt_len_off = in.arr<int32_t>();
+    if (!in.ok) return rt->fail(ET_ERR_INVALID, "truncated program image (graph)");
+    g.num_calls = static_cast<int32_t>(call_rank.size());
+    g.call_rank = call_rank.data();
+    g.call_extent_from = call_ef.data();
+    g.grid_code_off = grid_off.data();
+    g.code_op = code_op.data();
+    g.code_arg = code_arg.data();
+    g.code_len = static_cast<int32_t>(code_op.size());
+    g.num_runtime_tensors = static_cast<int32_t>(rt_cap.size());
+    g.runtime_capacity = rt_cap.data();
+    g.runtime_len_off = rt_len_off.data();
+    int rc = et_upload_graph(rt, &g);
+    if (rc != ET_OK) return rc;
+    // samples
+    const int64_t ns = in.i64();
+    if (!in.ok || ns < 0 || ns > (1 << 20)) return rt->fail(ET_ERR_INVALID, "corrupt program image (samples)");
+    struct S {
+        std::vector<int64_t> binding;
+        std::vector<int32_t> a[11];
+        bool has_dur = false;
+    };
+    std::vector<S> keep(static_cast<size_t>(ns));
+    std::vector<et_sample_desc> descs(static_cast<size_t>(ns));
+    for (int64_t i = 0; i < ns; ++i) {
+        S& k = keep[static_cast<size_t>(i)];
+        et_sample_desc& d = descs[static_cast<size_t>(i)];
+        d.num_queues = static_cast<int32_t>(in.i64());
+        d.has_dma = static_cast<int32_t>(in.i64());
+        d.num_slots = static_cast<int32_t>(in.i64());
+        d.num_counters = static_cast<int32_t>(in.i64());
+        k.binding = in.arr<int64_t>();
+        for (int j = 0; j < 11; ++j) k.a[j] = in.arr<int32_t>(j == 5 ? &k.has_dur : nullptr);
+        if (!in.ok) return rt->fail(ET_ERR_INVALID, "truncated program image (sample)");
+        d.binding = k.binding.data();
+        d.call_extents = k.a[0].data();
+        d.queue_off = k.a[1].data();
+        d.slot_task = k.a[2].data();
+        d.slot_call = k.a[3].data();
+        d.slot_flat = k.a[4].data();
+        d.slot_duration = k.has_dur ? k.a[5].data() : nullptr;
+        d.wait_off = k.a[6].data();
+        d.waits = k.a[7].data();
+        d.notify_off = k.a[8].data();
+        d.notifies = k.a[9].data();
+        d.initial_counts = k.a[10].data();
+        d.counter_dd = nullptr;
+    }
+    return et_upload_static(rt, descs.data(), static_cast<int32_t>(ns));
 }
 
 int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_desc* dyn, int32_t num_samples) {
@@ -311,6 +495,7 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
     int rc = et_upload_static(rt, s, num_samples);  // sample bindings, extents, counters, status
     if (rc != ET_OK) return rc;
     rt->mode = ET_MODE_DYNAMIC;
+    rt->img_static = false;  // program images hold static schedules only
     for (int c = 0; c < rt->num_calls; ++c)
         if (rt->call_rank[static_cast<size_t>(c)] > 2)
             return rt->fail(ET_ERR_INVALID, "the dynamic scheduler supports grids of rank <= 2");

@@ -250,7 +250,7 @@ class DecodeModel:
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
                  l2_prefetch=512 << 10, residual="split", fused_merge=True, balance=True, grouped=True,
-                 scheduler="static", early_push=False, stage_barriers=False):
+                 scheduler="static", early_push=False, stage_barriers=False, program=None):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -278,7 +278,13 @@ class DecodeModel:
             spec = add_stage_barriers(spec)
         self.graph = etsim.Graph.from_json(json.dumps(spec))
         self.scheduler = scheduler
-        if scheduler == "dynamic":  # on-GPU ready queues (Algorithm 2) instead of per-SM queues
+        # program: path of an ahead-of-time program image (Executor.save_program): loaded
+        # when it exists (no lowering), else written after lowering
+        import os
+        self.program_loaded = bool(program) and scheduler == "static" and os.path.exists(program)
+        if self.program_loaded:
+            self.kernel = None
+        elif scheduler == "dynamic":  # on-GPU ready queues (Algorithm 2) instead of per-SM queues
             self.kernel = etsim.lower_dynamic(self.graph, early_push=early_push)
         else:
             self.kernel = etsim.lower_static(self.graph, [{"s": s} for s in self.samples], num_sms=self.num_workers)
@@ -310,9 +316,15 @@ class DecodeModel:
         if scheduler == "dynamic":
             self.executor = etsim.Executor(self.kernel, [{"s": s} for s in self.samples], device=self.device.index or 0,
                                            num_workers=self.num_workers, record_trace=record_trace, prefetch=prefetch)
+        elif self.program_loaded:
+            self.executor = etsim.Executor.load_program(program, device=self.device.index or 0,
+                                                        record_trace=record_trace, prefetch=prefetch,
+                                                        l2_prefetch=l2_prefetch)
         else:
             self.executor = etsim.Executor(self.kernel, device=self.device.index or 0, num_workers=self.num_workers,
                                            record_trace=record_trace, prefetch=prefetch, l2_prefetch=l2_prefetch)
+            if program and scheduler == "static":
+                self.executor.save_program(program)
         self.executor.bind_ops(pack(self._ops()))
         self.upload_ms = (time.perf_counter() - t1) * 1e3
 

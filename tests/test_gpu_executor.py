@@ -169,3 +169,26 @@ def test_dynamic_shapes_and_random_dags():
         g = etsim.random_dag(5 + seed % 16, 8 + seed % 20, seed)
         t = etsim.simulate(etsim.lower_dynamic(g, early_push=seed % 2 == 1), {}, num_sms=1 + seed % 4, seed=seed)
         assert g.instantiate({}, seed=seed).check(t) == []
+
+
+def test_program_image_loads_without_lowering(tmp_path):
+    """f1 (ref json_io.cpp:294-376 / 455-494, kernel_to_json / kernel_from_json): a lowered
+    static program saved as a binary image (et_save_program) loads into a fresh runtime
+    without lowering; same logits, counters, task counts and a checkable trace."""
+    from paper_2604_13327_b200.decode import TINY, DecodeModel
+
+    path = str(tmp_path / "tiny.etprog")
+    a = DecodeModel(TINY, samples=(16, 64), num_workers=16, seed=0, program=path)
+    assert not a.program_loaded
+    b = DecodeModel(TINY, samples=(16, 64), num_workers=16, seed=0, program=path)
+    assert b.program_loaded and b.kernel is None
+    for m in (a, b):
+        m.fill_cache(40, seed=1)
+        m.set_token(7)
+    la, lb = a.step(40).clone(), b.step(40).clone()
+    # the same program and weights: equal up to the order of the fp32 atomics (split-K)
+    assert (la - lb).abs().max().item() <= 1e-3 * la.abs().max().item()
+    assert a.greedy_token() == b.greedy_token()
+    assert a.last_stats["tasks_executed"] == b.last_stats["tasks_executed"]
+    assert all(c == 0 for c in b.executor.final_counters())
+    assert b.graph.instantiate({"s": 40}).check(b.executor.trace()) == []
