@@ -2311,63 +2311,6 @@ __device__ __noinline__ bool tc_produce(const StaticParams& P, uint8_t* smem, co
     return true;
 }
 
-// L2 run-ahead of the producer (static scheduler).  While the consumers sit in
-// an Event Tensor wait (misc[2]) the ring fills within a few microseconds and
-// HBM would idle for the rest of the hop; the producer then walks a second
-// cursor ahead of the ring and prefetches the next slots' bytes into L2
-// (cp.async.bulk.prefetch.L2), at most P.l2_ahead bytes beyond the ring, so the
-// ring refills from L2 once the wait ends.  Only during waits: in steady
-// streaming the same bytes would cross L2 twice for nothing.  Data-dependent
-// (lazy) slots are skipped -- their extents exist only after their waits -- so
-// a producer held at a routed expert slot keeps prefetching the later
-// non-routed work (the next layer's projections).
-struct L2Cursor {
-    int slot;        // slot of the next chunk to prefetch
-    int chunk;       // its chunk index in `plan`
-    int n;           // chunks of `plan` (-1: plan of `slot` not made yet)
-    long long ahead; // bytes prefetched beyond the ring cursor
-    StreamPlan plan;
-};
-
-__device__ __noinline__ bool l2_step(const StaticParams& P, const SlotTable& T, int qb, int qe, L2Cursor& L) {
-    while (L.slot < qe) {
-        if (L.n < 0) {
-            const SlotView v = view_slot(P, T, L.slot, qb);
-            const et_op& op = P.ops[v.call];
-            if (v.masked || v.lazy || !op_streams(op.kind)) {
-                ++L.slot;
-                L.chunk = 0;
-                continue;
-            }
-            L.plan = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
-            L.n = L.plan.tc_np ? 0 : L.plan.total_chunks();
-        }
-        if (L.chunk < L.n) {
-            const Chunk ch = L.plan.chunk(L.chunk++);
-            bulk_prefetch_l2(ch.src, ch.bytes);
-            L.ahead += ch.bytes;
-            return true;
-        }
-        ++L.slot;
-        L.chunk = 0;
-        L.n = -1;
-    }
-    return false;
-}
-
-// The ring issues chunk c of slot s: bytes the cursor prefetched stop counting
-// as run-ahead; a cursor at or behind the ring jumps to the chunk after it.
-__device__ __forceinline__ void l2_passed(L2Cursor& L, int s, int c, uint32_t bytes) {
-    if (L.slot > s || (L.slot == s && L.chunk > c)) {
-        L.ahead = L.ahead > bytes ? L.ahead - bytes : 0;
-    } else {
-        if (L.slot != s) L.n = -1;
-        L.slot = s;
-        L.chunk = c + 1;
-        L.ahead = 0;
-    }
-}
-
 __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, const SlotTable& T) {
     if ((threadIdx.x & 31) != 0) return;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -2377,19 +2320,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
     const int qb = __ldg(P.queue_off + worker), qe = __ldg(P.queue_off + worker + 1);
     unsigned long long cseq = 0;  // chunks issued to the ring
     unsigned int xq = 0;          // activation pieces issued to the tensor-core x buffers
-    long long pcum = 0;           // bytes of non-lazy chunks issued (the prefetch warp's reference)
-    const bool l2_lsu = (P.debug & 128) == 0;  // run-ahead by the prefetch warp (default) or by TMA here
-    const long long l2win = (P.prefetch && !l2_lsu) ? P.l2_ahead : 0;
-    const bool l2_ungated = (P.debug & 64) != 0;  // timing experiment: run ahead whenever the ring is full
-    L2Cursor L;
-    L.slot = qb;
-    L.chunk = 0;
-    L.n = -1;
-    L.ahead = 0;
-    // one prefetch when the run-ahead is allowed now; false: spin as before
-    auto l2_try = [&]() -> bool {
-        return l2win > 0 && L.ahead < l2win && (l2_ungated || misc[2] != 0) && l2_step(P, T, qb, qe, L);
-    };
+    long long pcum = 0;           // bytes of non-lazy chunks issued (the L2 run-ahead warp's reference)
     for (int s = qb; s < qe; ++s) {
         SlotView v = view_slot(P, T, s, qb);
         if (v.masked) continue;
@@ -2399,7 +2330,7 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             // data-dependent extents are known only once the slot's waits pass
             for (uint32_t it = 0; misc[1] <= s;) {
                 if ((++it & 1023u) == 0 && aborted(P.status)) return;  // (a global load: not every spin)
-                l2_try();
+                __nanosleep(32);  // routed slots wait microseconds: leave the issue slots to the consumers
             }
             if (v.lazy && extent_masked(P, v.call, v.coord)) continue;
         }
@@ -2415,7 +2346,6 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
             uint32_t spins = 0;
             uint64_t t0 = 0;
             while (!mbar_try_wait(&empty[stage], phase ^ 1u)) {
-                if (l2_try()) continue;
                 if ((++spins & 1023u) == 0) {
                     if (aborted(P.status)) return;
                     if (t0 == 0) t0 = globaltimer();
@@ -2426,7 +2356,6 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                 }
             }
             const Chunk ch = pl.chunk(c);
-            if (l2win > 0 && !l2_lsu) l2_passed(L, s, c, ch.bytes);
             misc[9] = s;
             misc[10] = c;
             if (!v.lazy) {
