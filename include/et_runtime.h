@@ -65,7 +65,9 @@ enum et_op_kind {
     ET_OP_EMBED = 12,         /* embedding rows of the step's tokens -> fp32 stream */
     ET_OP_GEMV_TC = 13,       /* large-batch GEMV on tcgen05 tensor cores (TMEM)   */
     ET_OP_NORM = 14,          /* RMSNorm of the stream -> bf16 tensor-core operand */
-    ET_OP_KIND_LAST = 14      /* (highest kind with a device body; et_bind_ops rejects
+    ET_OP_REDUCE = 15,        /* sum of k-split partial tiles (GEMM + reduce-scatter) */
+    ET_OP_COPY = 16,          /* chunk copy (all-gather + GEMM, DMA queue)         */
+    ET_OP_KIND_LAST = 16      /* (highest kind with a device body; et_bind_ops rejects
                                  the rest, and ET_OP_MOE_GROUP / ET_OP_MOE_COMBINE,
                                  whose work the routed notify and the expert tiles'
                                  red.add epilogue absorb) */

@@ -894,8 +894,11 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
                                  Ring& ring, TcState& ts, int ctid) {
     const int warp = ctid >> 5, lane = ctid & 31;
     const int N = op.i[0], nseg = op.i[2], kp = op.i[6];
-    const int nb = batch_of(op, P), npad = tc_npad(nb);
-    const TcSpan sp = tc_span(op, si.coord[0], si.ext0);
+    const int nb = tc_batch(op, P.binding), npad = tc_npad(nb);
+    const bool tiled = tc_tiled(op);  // f4 GEMM tile: (token block, GEMV task) from the coordinates
+    int tj = 0, tt = 0;
+    if (tiled) tc_tile(op, si.coord, &tj, &tt);
+    const TcSpan sp = tiled ? tc_span(op, tt, op.i[12]) : tc_span(op, si.coord[0], si.ext0);
     if (sp.nblk <= 0 || sp.np <= 0) return 0;
     uint64_t* bars = tc_bars(smem);
     const int cpb = kp / 64;                       // 16 KB weight chunks per (piece, block)
@@ -939,6 +942,10 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
     const int epi = op.i[4];
     const int ostride = op.i[8] > 0 ? op.i[8] : N;  // output rows (a padded block's tail rows are dropped)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    // tiled GEMM: token rows start at block j; EPI_F32 goes to the k-split's partial buffer
+    const long long obase = tiled ? static_cast<long long>(tt % (op.i[3] > 0 ? op.i[3] : 1)) * op.i[11] +
+                                        static_cast<long long>(tj) * op.i[10] * ostride
+                                  : 0;
     for (int it = half; it < nitems; it += 2) {
         const int blk = it / nchunk, n0 = (it - blk * nchunk) * 16;
         float v[16], u[16];
@@ -950,7 +957,7 @@ __device__ __noinline__ uint64_t body_gemv_tc(const StaticParams& P, const et_op
         for (int j = 0; j < 16; ++j) {
             const int n = n0 + j;
             if (n < nb && row < ostride) {
-                const long long o = static_cast<long long>(n) * ostride + row;
+                const long long o = obase + static_cast<long long>(n) * ostride + row;
                 if (epi == EPI_F32) {
                     reinterpret_cast<float*>(op.p[4])[o] = v[j];
                 } else if (epi == EPI_ADD) {
@@ -2072,6 +2079,68 @@ __device__ void body_argmax(const StaticParams& P, const et_op& op, int ctid) {
     }
 }
 
+// ET_OP_REDUCE (f4, GEMM + reduce-scatter): output tile (token block j, row group g) =
+// the sum of the k-split partial buffers, once every split's GEMM tile of it notified.
+__device__ void body_reduce(const StaticParams&, const et_op& op, const int* coord, int ctid) {
+    const int N = op.i[0], TB = op.i[1], parts = op.i[2], RG = op.i[4];
+    const long long pstride = static_cast<long long>(op.i[3]);
+    const int j = coord[0], g = coord[1];
+    const float* part = reinterpret_cast<const float*>(op.p[0]);
+    const int per_row = RG / 4;  // float4 per token row of the tile
+    for (int v = ctid; v < TB * per_row; v += kConsumers) {
+        const int n = v / per_row, c4 = v - n * per_row;
+        const long long o = (static_cast<long long>(j) * TB + n) * N + static_cast<long long>(g) * RG + c4 * 4;
+        float4 acc = ldcg_f4(part + o);
+        for (int r = 1; r < parts; ++r) {
+            const float4 x = ldcg_f4(part + r * pstride + o);
+            acc.x += x.x;
+            acc.y += x.y;
+            acc.z += x.z;
+            acc.w += x.w;
+        }
+        if (op.i[5] == 1) {
+            uint2 b;
+            b.x = static_cast<uint32_t>(f2bf(acc.x)) | (static_cast<uint32_t>(f2bf(acc.y)) << 16);
+            b.y = static_cast<uint32_t>(f2bf(acc.z)) | (static_cast<uint32_t>(f2bf(acc.w)) << 16);
+            *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(op.p[1]) + o) = b;
+        } else {
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(op.p[1]) + o) = acc;
+        }
+    }
+}
+
+// ET_OP_COPY (f4, all-gather + GEMM; DMA-class tasks, one warp): chunk t of i0 bytes
+// (16-byte multiple) from p0 + t * i0 to p1 + t * i0 (flags bit 0: source chunk t at p2[t],
+// a table of per-rank source addresses -- the peers' buffers).
+// flags bit 1 (pull-based all-gather): no copy -- the consumers' TMA loads read the chunk
+// in place (over NVLink on a TP node); this task only pulls it into L2 ahead of them
+// (bulk L2 prefetches, 1 MB each) and releases its arrival element.
+__device__ void body_copy(const et_op& op, int t, int lane) {
+    const long long bytes = op.i[0];
+    if (op.flags & 2) {
+        const uint8_t* src = (op.flags & 1)
+                                 ? reinterpret_cast<const uint8_t*>(reinterpret_cast<const unsigned long long*>(op.p[2])[t])
+                                 : reinterpret_cast<const uint8_t*>(op.p[0]) + t * bytes;
+        for (long long off = static_cast<long long>(lane) << 20; off < bytes; off += 32ll << 20)
+            bulk_prefetch_l2(src + off, static_cast<uint32_t>(bytes - off < (1 << 20) ? bytes - off : (1 << 20)));
+        return;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(
+        (op.flags & 1) ? reinterpret_cast<const uint8_t*>(reinterpret_cast<const unsigned long long*>(op.p[2])[t])
+                       : reinterpret_cast<const uint8_t*>(op.p[0]) + t * bytes);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(op.p[1]) + t * bytes);
+    const long long n = bytes / 16;
+    long long i = lane;
+    for (; i + 96 < n; i += 128) {  // four 16-byte loads in flight per lane
+        const uint4 a = __ldcg(src + i), b = __ldcg(src + i + 32), c = __ldcg(src + i + 64), d = __ldcg(src + i + 96);
+        dst[i] = a;
+        dst[i + 32] = b;
+        dst[i + 64] = c;
+        dst[i + 96] = d;
+    }
+    for (; i < n; i += 32) dst[i] = __ldcg(src + i);
+}
+
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ bool op_streams(int kind) {
@@ -2171,6 +2240,10 @@ __device__ void consumer_loop(const StaticParams& P, int worker, uint8_t* smem, 
                     break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_ARGMAX: body_argmax(P, op, ctid); break;
+                case ET_OP_REDUCE: body_reduce(P, op, v.coord, ctid); break;
+                case ET_OP_COPY:  // copies are DMA-class tasks (dma_loop)
+                    if (ctid == 0) report(P.status, ET_ERR_INVALID, worker, -1, -7, op.kind);
+                    break;
                 case ET_OP_ALLREDUCE: body_allreduce(P, op, v, ctid, worker); break;
                 case ET_OP_MOE_ROUTE:
                     if constexpr (kMoE) body_moe_route<kTC>(P, op, v, xs, acc, red, ring, ctid, &t_pro);
@@ -2336,7 +2409,10 @@ __device__ void producer_loop(const StaticParams& P, int worker, uint8_t* smem, 
         }
         const StreamPlan pl = make_plan(op, v.coord, v.ext0, P.binding, P.rt);
         if (pl.tc_np) {  // tensor-core GEMV: weight chunks + activation pieces (gated on the waits)
-            if (!tc_produce(P, smem, pl, misc, 0, s, cseq, xq, worker, pol)) return;
+            // tiled GEMM (f4): every token block re-reads the weights -- keep them in L2
+            // (evict_last) instead of streaming them through it (debug bit 0x400000: evict_first)
+            const uint64_t wpol = (tc_tiled(op) && !(P.debug & 0x400000)) ? policy_evict_last() : pol;
+            if (!tc_produce(P, smem, pl, misc, 0, s, cseq, xq, worker, wpol)) return;
             continue;
         }
         const int n = pl.total_chunks();
@@ -2436,25 +2512,35 @@ __device__ void l2_ahead_loop(const StaticParams& P, int worker, uint8_t* smem, 
 
 // DMA-class queue: synthetic bodies only (copies are modelled by duration).
 __device__ void dma_loop(const StaticParams& P) {
-    if ((threadIdx.x & 31) != 0) return;
+    // the whole warp walks the DMA queue: lane 0 waits / notifies, every lane copies
+    const int lane = threadIdx.x & 31;
     const int q = P.num_queues;
     const int qb = __ldg(P.queue_off + q), qe = __ldg(P.queue_off + q + 1);
     for (int s = qb; s < qe; ++s) {
         const SlotInfo si = slot_info(P, s);
         const uint64_t t_begin = globaltimer();
-        if (!wait_slot(P, s, q)) return;
-        if (P.step_limit > 0 &&
-            atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
-            report(P.status, ET_ERR_STEP_LIMIT, q, s, -1, 0);
-            return;
+        int ok = 1;
+        if (lane == 0) {
+            ok = wait_slot(P, s, q);
+            if (ok && P.step_limit > 0 &&
+                atomicAdd(&P.status->executed, 1ull) >= static_cast<unsigned long long>(P.step_limit)) {
+                report(P.status, ET_ERR_STEP_LIMIT, q, s, -1, 0);
+                ok = 0;
+            }
         }
+        if (!__shfl_sync(0xffffffffu, ok, 0)) return;
         const uint64_t t_wait = globaltimer();
         const bool masked = si.masked || (si.lazy && extent_masked(P, si.call, si.coord));
-        if (!masked && P.tick_ns > 0 && P.slot_duration) {
+        const et_op& op = P.ops[si.call];
+        if (!masked && op.kind == ET_OP_COPY) {
+            body_copy(op, si.coord[0], lane);
+            __syncwarp();  // every lane's stores precede lane 0's release notify
+        } else if (!masked && lane == 0 && P.tick_ns > 0 && P.slot_duration) {
             const uint64_t until = t_wait + static_cast<uint64_t>(__ldg(P.slot_duration + s)) * P.tick_ns;
             while (globaltimer() < until) {
             }
         }
+        if (lane != 0) continue;
         const uint64_t t_exec = globaltimer();
         notify_slot(P, s, q);
         if (P.step_limit <= 0 && !masked) atomicAdd(&P.status->executed, 1ull);
@@ -3131,6 +3217,10 @@ __device__ void dyn_consumer_loop(const StaticParams& P, const DynParams& D, int
                     break;
                 case ET_OP_EMBED: body_embed(P, op, ctid); break;
                 case ET_OP_ARGMAX: body_argmax(P, op, ctid); break;
+                case ET_OP_REDUCE: body_reduce(P, op, v.coord, ctid); break;
+                case ET_OP_COPY:  // copies are DMA-class tasks (dma_loop)
+                    if (ctid == 0) report(P.status, ET_ERR_INVALID, worker, -1, -7, op.kind);
+                    break;
                 case ET_OP_MOE_ROUTE:
                     if constexpr (kMoE) body_moe_route<kTC>(P, op, v, xs, acc, red, ring, ctid, &tp);
                     break;

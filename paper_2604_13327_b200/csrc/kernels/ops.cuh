@@ -94,6 +94,16 @@
 //   of the row-major epilogues (0 = N; rows of a zero-padded last block beyond it are dropped);
 //   p0/p1 = weights in the tensor-core layout of segment 0/1 (tc_weight_offset), p2 = x in the
 //   operand layout (xb_offset), p4 = out, p5 = residual in (fp32, EPI_RESID)
+//   flags bit 6 (tiled GEMM, f4 workloads): grid [token blocks, i12]; task (j, t) is GEMV task t of
+//   i12 on token block j (i10 tokens, the MMA N; activations at p2 + j * K * Npad, operand
+//   layout); EPI_F32 writes Y[j*i10 + n][row] into the k-split's own partial buffer
+//   p4 + r * i11 (r = t % i3, i11 elements apart): the reduce-scatter tasks sum them
+// ET_OP_REDUCE          task (j, g): out[tokens of block j][rows of group g] = sum over i2 partial
+//   buffers (i3 elements apart) at p0; i0 = N (row stride), i1 = tokens per block, i4 = rows per
+//   group, i5 = out dtype (0 fp32, 1 bf16); p1 = out
+// ET_OP_COPY            DMA-class task t (one warp): i0 bytes from p0 + t * i0 (flags bit 0: from the
+//   address p2[t]) to p1 + t * i0; flags bit 1: pull-based all-gather -- no copy, the chunk is
+//   prefetched into L2 and its consumers read it in place
 // ET_OP_NORM            task n (< b): out[n] = bf16(h[n] * rsqrt(mean(h[n]^2) + eps) * gamma) in
 //   the tensor-core operand layout; i0 = K, i5 = batch symbol slot, i6 = kp; p0 = h (fp32
 //   [b][K]), p1 = gamma (fp32 [K]), p2 = out, p3 = optional row-major copy (bf16 [b][K]); f0 = eps
@@ -133,6 +143,28 @@ __host__ __device__ __forceinline__ long long xb_offset(int n, int k, int npad, 
     const int piece = k / kp, kk = k - piece * kp;
     return static_cast<long long>(piece) * npad * kp + (kk >> 4) * (npad * 16) + (n >> 3) * 128 + ((kk >> 3) & 1) * 64 +
            (n & 7) * 8 + (k & 7);
+}
+
+// Tiled GEMM mode (GEMV_TC flags bit 6, the f4 workloads): grid [token blocks, i12 tasks per
+// block]; coordinate 1 is the GEMV task (row-block group, k split), coordinate 0 the block
+// of i10 tokens.  Batch (MMA N) = i10; otherwise the batch symbol's value.
+__host__ __device__ __forceinline__ bool tc_tiled(const et_op& op) { return (op.flags & 64) != 0; }
+__host__ __device__ __forceinline__ int tc_batch(const et_op& op, const long long* binding) {
+    if (tc_tiled(op)) return op.i[10];
+    return op.i[5] >= 0 ? static_cast<int>(binding[op.i[5]]) : 1;
+}
+
+// (token block, GEMV task) of a tiled-GEMM task.  flags bit 7 (the reference's
+// all_gather_gemm grid [chunks, tiles per chunk]): coordinate 1 also walks the i13
+// token blocks of chunk coord 0 -- block = coord0 * i13 + coord1 / i12, task = coord1 % i12.
+__host__ __device__ __forceinline__ void tc_tile(const et_op& op, const int* coord, int* j, int* t) {
+    if (op.flags & 128) {
+        *j = coord[0] * op.i[13] + coord[1] / op.i[12];
+        *t = coord[1] % op.i[12];
+    } else {
+        *j = coord[0];
+        *t = coord[1];
+    }
 }
 
 struct TcSpan {
@@ -340,12 +372,15 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
     pl.cbytes = kStageBytes;
     pl.interleave = false;
     if (op.kind == ET_OP_GEMV_TC) {
-        const TcSpan sp = tc_span(op, coord[0], T);
+        const bool tiled = tc_tiled(op);
+        int tj = 0, tt = 0;
+        if (tiled) tc_tile(op, coord, &tj, &tt);
+        const TcSpan sp = tiled ? tc_span(op, tt, op.i[12]) : tc_span(op, coord[0], T);
         if (sp.nblk <= 0 || sp.np <= 0) {  // idle task: nothing streams
             pl.finish();
             return pl;
         }
-        const int nb = op.i[5] >= 0 ? static_cast<int>(binding[op.i[5]]) : 1;
+        const int nb = tc_batch(op, binding);
         const long long kp = op.i[6], blk_bytes = kp * 256;  // one 128-row block of one piece
         pl.tc_pstride = static_cast<long long>(op.i[0] / 128) * blk_bytes;
         pl.nseg = op.i[2];
@@ -357,6 +392,8 @@ __device__ __forceinline__ StreamPlan make_plan(const et_op& op, const int* coor
         pl.tc_pre = pl.tc_w < kStages ? pl.tc_w : kStages;
         pl.tc_xbytes = static_cast<uint32_t>(tc_npad(nb) * kp * 2);
         pl.tc_x = reinterpret_cast<const uint8_t*>(op.p[2]) + static_cast<long long>(sp.p0) * pl.tc_xbytes;
+        if (tiled)  // this token block's operand-layout activations (all K pieces of the block)
+            pl.tc_x += static_cast<long long>(tj) * (op.i[1] / op.i[6]) * pl.tc_xbytes;
         return pl;
     }
     if (op.kind == ET_OP_GEMV) {

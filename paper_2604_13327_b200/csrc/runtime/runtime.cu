@@ -669,13 +669,16 @@ namespace {
 // bound the rows of the widest task from the span arithmetic of ops.cuh gemv_span.
 bool gemv_acc_fits(const et_op& op, int64_t grid0, const int64_t* binding) {
     if (op.kind == ET_OP_GEMV_TC) {  // TMEM columns, operand shapes and piece buffers
-        const int64_t nb = op.i[5] >= 0 ? binding[op.i[5]] : 1;
+        const bool tiled = etk::tc_tiled(op);  // f4 GEMM tiles: i12 tasks per token block, batch i10
+        const int64_t nb = tiled ? op.i[10] : op.i[5] >= 0 ? binding[op.i[5]] : 1;
         const int npad = etk::tc_npad(static_cast<int>(nb));
         const int kp = op.i[6], splits = op.i[3] > 0 ? op.i[3] : 1;
+        const int64_t tasks = tiled ? op.i[12] : grid0;
         if (nb > etk::kMaxBatchTc || kp <= 0 || kp % 64 || op.i[1] % kp || op.i[0] % 128) return false;
-        if (static_cast<int64_t>(npad) * kp * 2 > etk::kTcXBuf || grid0 % splits) return false;
-        if (splits > 1 && op.i[4] != etk::EPI_ADD) return false;
-        const int64_t G = grid0 / splits, nblk = op.i[0] / 128;
+        if (static_cast<int64_t>(npad) * kp * 2 > etk::kTcXBuf || tasks % splits) return false;
+        if (splits > 1 && op.i[4] != etk::EPI_ADD && !(tiled && op.i[4] == etk::EPI_F32 && op.i[11] > 0)) return false;
+        if (tiled && (nb % 16 || op.i[4] != etk::EPI_F32)) return false;
+        const int64_t G = tasks / splits, nblk = op.i[0] / 128;
         return op.i[2] * ((nblk + G - 1) / G) * npad <= etk::kTmemCols;
     }
     if (op.kind != ET_OP_GEMV) return true;
@@ -716,6 +719,11 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
         if ((k == ET_OP_ATTN_SPLIT || k == ET_OP_ATTN_MERGE) && ops[c].i[0] * ops[c].i[1] > 2 * etk::kConsumers)
             variant |= 1;
         else if (k == ET_OP_GEMV_TC || k == ET_OP_NORM) variant |= 2;
+        if (k == ET_OP_COPY && (rt->mode != ET_MODE_STATIC || ops[c].i[0] <= 0 || ops[c].i[0] % 16))
+            return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": copies run on the static scheduler's "
+                                            "DMA queue, in 16-byte multiples");
+        if (k == ET_OP_REDUCE && (ops[c].i[4] % 4 || ops[c].i[0] % 4 || ops[c].i[2] < 1))
+            return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": reduce tiles need rows % 4 == 0");
     }
     for (int32_t c = 0; c < num_calls; ++c) {
         const et_op& o = ops[c];

@@ -25,6 +25,8 @@ OP_ARGMAX = 11
 OP_EMBED = 12
 OP_GEMV_TC = 13
 OP_NORM = 14
+OP_REDUCE = 15
+OP_COPY = 16
 
 EPI_F32, EPI_BF16, EPI_RESID, EPI_SILU_MUL, EPI_QKV_ROPE, EPI_ADD = range(6)
 
