@@ -1791,6 +1791,8 @@ __device__ __forceinline__ void body_moe_route_impl(const StaticParams& P, const
     int4* tinfo = reinterpret_cast<int4*>(op.p[8]);   // [tiles] (expert, first slot, tokens)
     int* scnt = reinterpret_cast<int*>(acc + (single ? E * nb : 0));  // [E] counts (single: logits in acc[0, E*nb))
     int* stop = scnt + 256;                           // [nb*K] experts per slot
+    float* sw = reinterpret_cast<float*>(stop + 256);  // [nb*K] routing weight per slot
+    int* tfirst = reinterpret_cast<int*>(sw + 256);    // [E] first tile of a one-token expert, else -1
     for (int e = ctid; e < E; e += kConsumers) scnt[e] = 0;
     bar_sync(1, kConsumers);
     // one warp per token: softmax over E (<= 256), top-K by repeated warp argmax
@@ -1850,6 +1852,7 @@ __device__ __forceinline__ void body_moe_route_impl(const StaticParams& P, const
             const int slot = t * K + lane;
             if (!(op.flags & 1)) topk[slot] = ej;
             wslot[slot] = wj / wsum;
+            sw[slot] = wj / wsum;
             atomicAdd(&scnt[ej], 1);
         }
     }
@@ -1880,6 +1883,7 @@ __device__ __forceinline__ void body_moe_route_impl(const StaticParams& P, const
                 ind[e] = tp;
                 tind[e] = tp * RS;
                 eoff[e] = op_;
+                tfirst[e] = c8[u] == 1 ? tp : -1;
                 scnt[e] = op_;  // cursor for elist
                 for (int i = 0; i * TS < c8[u]; ++i)  // direct tile table for the expert tasks
                     tinfo[tp + i] = make_int4(e, op_ + i * TS, c8[u] - i * TS < TS ? c8[u] - i * TS : TS, 0);
@@ -1895,7 +1899,13 @@ __device__ __forceinline__ void body_moe_route_impl(const StaticParams& P, const
     }
     bar_sync(1, kConsumers);
     if (ctid == 0)  // slots grouped by expert, stable in slot order
-        for (int sl = 0; sl < nb * K; ++sl) elist[scnt[stop[sl]]++] = sl;
+        for (int sl = 0; sl < nb * K; ++sl) {
+            const int e = stop[sl];
+            elist[scnt[e]++] = sl;
+            // a one-token tile carries its slot's routing weight (int4 .w, float bits): its
+            // expert tasks skip the elist / weight lookups (one L2 round trip instead of three)
+            if (tfirst[e] >= 0) tinfo[tfirst[e]].w = __float_as_int(sw[sl]);
+        }
     // The selected experts' weights cannot be streamed before this point (their ids
     // exist only now); start pulling them into L2 while the expert tasks get
     // released.  (Plain writes above are published by the task's NOTIFY release.)
@@ -1937,20 +1947,34 @@ __device__ uint64_t body_moe_expert(const StaticParams& P, const et_op& op, cons
     int* stok = reinterpret_cast<int*>(acc + kAccFloats - 16);     // [8] token of each tile row
     float* swt = acc + kAccFloats - 8;                             // [8] its routing weight
     int nb;
-    {
-        const ExpertTask t = expert_task(op, si.coord[0], P.rt);
-        nb = t.ntok;
-        if (ctid < nb) {
-            stok[ctid] = t.slot[ctid] / K;
-            swt[ctid] = __ldcg(reinterpret_cast<const float*>(op.p[4]) + t.slot[ctid]);
-        }
-    }
-    bar_sync(1, kConsumers);
     const uint16_t* xn = reinterpret_cast<const uint16_t*>(op.p[3]);
-    for (int v = ctid; v < nb * H / 8; v += kConsumers) {
-        const int j = v / (H / 8), k8 = v - j * (H / 8);
-        reinterpret_cast<uint4*>(xs)[v] =
-            __ldcg(reinterpret_cast<const uint4*>(xn + static_cast<long long>(stok[j]) * H) + k8);
+    if (op.i[9] < 0) {
+        // one sequence (i9 = -1): every tile is token 0 with one slot, whose routing weight the
+        // route task left in the tile record -- the record and the activations load together
+        const int4 info = __ldcg(reinterpret_cast<const int4*>(op.p[6]) + si.coord[0] / op.i[2]);
+        for (int v = ctid; v < H / 8; v += kConsumers)
+            reinterpret_cast<uint4*>(xs)[v] = __ldcg(reinterpret_cast<const uint4*>(xn) + v);
+        nb = 1;
+        if (ctid == 0) {
+            stok[0] = 0;
+            swt[0] = __int_as_float(info.w);
+        }
+        bar_sync(1, kConsumers);
+    } else {
+        {
+            const ExpertTask t = expert_task(op, si.coord[0], P.rt);
+            nb = t.ntok;
+            if (ctid < nb) {
+                stok[ctid] = t.slot[ctid] / K;
+                swt[ctid] = __ldcg(reinterpret_cast<const float*>(op.p[4]) + t.slot[ctid]);
+            }
+        }
+        bar_sync(1, kConsumers);
+        for (int v = ctid; v < nb * H / 8; v += kConsumers) {
+            const int j = v / (H / 8), k8 = v - j * (H / 8);
+            reinterpret_cast<uint4*>(xs)[v] =
+                __ldcg(reinterpret_cast<const uint4*>(xn + static_cast<long long>(stok[j]) * H) + k8);
+        }
     }
     for (int i = ctid; i < 2 * IR * nb; i += kConsumers) acc[i] = 0.f;
     bar_sync(1, kConsumers);

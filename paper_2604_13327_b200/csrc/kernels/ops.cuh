@@ -57,13 +57,16 @@
 //   counts, exp_indptr, task_indptr, elist, eoff), i12 = RS, i13 = TS; p0 = router weight (frag16
 //   [E][H]), p2 = h (fp32 [b][H]), p3 = gamma, p4 = logits (fp32 [b][E]), p5 = xn out
 //   (bf16 [b][H]), p6 = slot weights out (fp32 [b*top_k]), p7 = arrival counter (int32);
+//   The tile table (p8, int4 per tile) holds (expert, first elist index, tokens, routing weight
+//   bits of a one-token tile).
 //   flags bit 1 (large batch): no GEMV -- one task reads the logits a tensor-core GEMV
 //   accumulated at p1 (fp32 [b][E]), copies them to p4 and zeroes p1
 // ET_OP_MOE_EXPERT      task flat = tile * RS + r (range-triggered on task_indptr, extent_from):
 //   for the tile's tokens x = xn[token]: act = silu(Wg_e x) * (Wu_e x) on rows [r*IR, r*IR+IR)
 //   (IR = I / RS), then h[token] += w_slot * Wd_e[:, rows] act (red.global.add).
 //   i0 = I, i1 = H, i2 = RS, i3 = TS (<= 8), i4..i7 = rt exp_indptr, counts, elist, eoff,
-//   i8 = top_k, i10 = E; p0/p1 = Wgate/Wup (frag16 [E][I][H]), p2 = Wdown blocks (frag16
+//   i8 = top_k, i9 = batch symbol slot (-1: one sequence -- every tile is token 0 with one slot and
+//   the route left its weight in the tile record's .w), i10 = E; p0/p1 = Wgate/Wup (frag16 [E][I][H]), p2 = Wdown blocks (frag16
 //   [E][RS][H][IR]), p3 = xn (bf16 [b][H]), p4 = slot weights, p5 = h (fp32 [b][H]),
 //   p6 = tile table (from ET_OP_MOE_ROUTE)
 // ET_OP_ALLREDUCE       task t of T (static scheduler): h[r0:r1] += sum over TP ranks of their

@@ -559,8 +559,10 @@ class MoEDecodeModel:
                                flags=1 if self.injected else 0))
             if self.group_stage:
                 ops.append(make_op(OP_NONE))  # group: the routed notify is the Event Tensor edge itself
+            # i9: the batch symbol slot, -1 = one sequence (tiles of token 0: the expert tasks read
+            # the slot weight from the tile record)
             ops.append(make_op(OP_MOE_EXPERT,
-                               i=[cfg.expert_inter, H, RS, TS, ri["ind"], ri["cnt"], ri["elist"], ri["eoff"], K, 0, E],
+                               i=[cfg.expert_inter, H, RS, TS, ri["ind"], ri["cnt"], ri["elist"], ri["eoff"], K, bs, E],
                                p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(L["wdown"]), ptr(self.xn[l]), ptr(self.wslot[l]),
                                   ptr(self.h), ptr(self.tiles[l])]))
         ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, bs, 0, 16, 0, H], f=[cfg.eps],
