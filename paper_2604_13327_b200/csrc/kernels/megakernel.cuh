@@ -145,6 +145,7 @@ struct DynParams {
     int dd_counts_rt[kMaxDd];
     int dd_writer_call[kMaxDd];
     int dd_range_call[kMaxDd];   // call range-triggered by this tensor, or -1
+    int dd_range_uniform_el[kMaxDd];  // the one element all its tasks notify, or -1
     const int* el_dd;
     int num_ready[2];
     int class_total[2];          // tasks per resource class (before extent_from shrink)

@@ -633,6 +633,20 @@ int et_upload_dynamic(et_runtime* rt, const et_sample_desc* s, const et_dynamic_
             P.dd_range_call[t] = -1;
             for (int c = 0; c < rt->num_calls; ++c)
                 if (d.call_range_rt[c] >= 0 && d.call_range_base[c] == d.dd_base[t]) P.dd_range_call[t] = c;
+            // the element every task of the range call notifies, when there is exactly one (one
+            // notify per task, the same element): the never-instantiated tail tasks are then
+            // credited with a single add at reveal time instead of one atomic per task
+            P.dd_range_uniform_el[t] = -1;
+            if (P.dd_range_call[t] >= 0) {
+                int el = -2;
+                for (int task = 0; task < d.num_tasks && el != -1; ++task) {
+                    if (d.task_call[task] != P.dd_range_call[t]) continue;
+                    const int n0 = d.task_notify_off[task], n1 = d.task_notify_off[task + 1];
+                    if (n1 - n0 != 1 || (el >= 0 && d.task_notifies[n0] != el)) el = -1;
+                    else el = d.task_notifies[n0];
+                }
+                P.dd_range_uniform_el[t] = el >= 0 ? el : -1;
+            }
             int wt = 1;
             for (int k = 0; k < rt->call_rank[static_cast<size_t>(d.dd_writer_call[t])]; ++k)
                 wt *= S.call_extents[static_cast<size_t>(d.dd_writer_call[t] * 4 + k)];

@@ -27,11 +27,12 @@ def main():
     else:
         from paper_2604_13327_b200.moe import MOE_CONFIGS, MoEDecodeModel
         sched = sys.argv[1].split("-")[1] if "-" in which else "static"
+        mb = int(os.environ.get("MB", "1"))  # batch (MB > 8: the tensor-core instantiation)
         m = MoEDecodeModel(MOE_CONFIGS["qwen3-30b-a3b"], samples=(1024,), scheduler=sched.replace("early", "dynamic"),
-                           early_push=sched == "early", record_trace=True)
+                           early_push=sched == "early", record_trace=True, max_batch=mb)
         m.fill_cache(1024, seed=1)
-        m.set_token([1])
-        binding = m._binding(1024, 1)
+        m.set_token([1 + 7 * i for i in range(mb)])
+        binding = m._binding(1024, mb)
     ex = m.executor
     if os.environ.get("DIAG_DEBUG"):
         ex.set_debug(int(os.environ["DIAG_DEBUG"], 0))
