@@ -525,6 +525,85 @@ __device__ __noinline__ void gemv_merge_prologue(const StaticParams& P, const et
         if (ctid == 0) misc[13] = misc[13] + 1;
         return;
     }
+    // more splits than the staging area holds: the same, in rounds of nsr splits
+    const int nsr = static_cast<int>(kMergeBulkMax / (static_cast<uint32_t>(G) * row * 4));  // splits per round
+    if (nsr >= 1 && 3 * G * ns <= 512) {
+        // (m, l) of every split load directly while round 0 lands
+        float* ps = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xs) + kMergeBulkOff);  // [G][round][row]
+        float* ml = acc + kAccFloats - 512;  // [G][ns][2]
+        float* wts = ml + 2 * G * ns;        // [G][ns]
+        volatile int* misc = reinterpret_cast<volatile int*>(reinterpret_cast<uint8_t*>(xs) - kSmemX + kSmemMisc);
+        uint64_t* bar = merge_bar(reinterpret_cast<uint8_t*>(xs) - kSmemX);
+        const uint32_t ph0 = static_cast<uint32_t>(misc[13]);
+        const int rounds = (ns + nsr - 1) / nsr;
+        auto issue = [&](int c0) {  // thread 0: splits [c0, c0 + cnt) of every head
+            const int cnt = ns - c0 < nsr ? ns - c0 : nsr;
+            const uint32_t rb = static_cast<uint32_t>(cnt) * row * 4;
+            mbar_arrive_expect_tx(bar, G * rb);
+            for (int h = 0; h < G; ++h)
+                bulk_g2s_keep(ps + h * cnt * row, part + (static_cast<long long>(h) * maxs + c0) * row, rb, bar);
+        };
+        if (ctid == 0) {
+            fence_proxy_async_global();  // partials: generic stores of other CTAs, acquired by the wait
+            fence_proxy_async();         // xs was last written through the generic proxy
+            issue(0);
+        }
+        for (int i = ctid; i < G * ns; i += kConsumers) {
+            const float* pr = part + (static_cast<long long>(i / ns) * maxs + i % ns) * row;
+            ml[2 * i] = __ldcg(pr);
+            ml[2 * i + 1] = __ldcg(pr + 1);
+        }
+        bar_sync(1, kConsumers);
+        for (int hh = warp; hh < G; hh += kConsumerWarps) {
+            float M = -INFINITY;
+            for (int c = lane; c < ns; c += 32) M = fmaxf(M, ml[2 * (hh * ns + c)]);
+            M = warp_max(M);
+            float L = 0.f;
+            for (int c = lane; c < ns; c += 32) {
+                const float e = __expf(ml[2 * (hh * ns + c)] - M);
+                wts[hh * ns + c] = e;
+                L += e * ml[2 * (hh * ns + c) + 1];
+            }
+            const float inv = 1.f / warp_sum(L);
+            __syncwarp();
+            for (int c = lane; c < ns; c += 32) wts[hh * ns + c] *= inv;
+        }
+        bar_sync(1, kConsumers);
+        if ((P.debug & 0x4000) && ctid == 0) *t_probe = globaltimer();  // weights
+        float o[kOut], o2[kOut];
+#pragma unroll
+        for (int j = 0; j < kOut; ++j) o[j] = o2[j] = 0.f;
+        for (int r = 0; r < rounds; ++r) {
+            const int c0 = r * nsr, cnt = ns - c0 < nsr ? ns - c0 : nsr;
+            if (r > 0 && ctid == 0) issue(c0);  // the previous round's readers passed the barrier below
+            mbar_wait(bar, (ph0 + static_cast<uint32_t>(r)) & 1u);
+            if (r == 0 && (P.debug & 0x1000) && ctid == 0) *t_probe = globaltimer();  // partials staged
+#pragma unroll
+            for (int j = 0; j < kOut; ++j) {
+                const int idx = ctid + j * kConsumers;
+                if (idx < K) {
+                    const int hh = idx / dh, d = idx - hh * dh;
+                    const float* w = wts + hh * ns + c0;
+                    const float* pc = ps + hh * cnt * row + kPartHead + d;
+                    int c = 0;
+                    for (; c + 1 < cnt; c += 2) {
+                        o[j] = fmaf(w[c], pc[c * row], o[j]);
+                        o2[j] = fmaf(w[c + 1], pc[(c + 1) * row], o2[j]);
+                    }
+                    if (c < cnt) o[j] = fmaf(w[c], pc[c * row], o[j]);
+                }
+            }
+            bar_sync(1, kConsumers);  // ps is free for the next round (and ml / wts after the last)
+        }
+#pragma unroll
+        for (int j = 0; j < kOut; ++j) {
+            const int idx = ctid + j * kConsumers;
+            if (idx < K) xs[idx] = f2bf(o[j] + o2[j]);
+        }
+        if (ctid == 0) misc[13] = static_cast<int>(ph0) + rounds;
+        bar_sync(1, kConsumers);  // xs complete (acc is zeroed by the caller)
+        return;
+    }
     float* ml = acc;              // [G][ns][2] (acc is zeroed after the prologue)
     float* wts = acc + 2 * G * ns;  // [G][ns]
     float ov[kOut][kPass];
