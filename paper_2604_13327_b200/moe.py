@@ -49,6 +49,7 @@ from .decode import frag16, rope_inv_freq
 from .ops import (
     EPI_ADD,
     EPI_F32,
+    GEMV_ARGMAX,
     OP_ATTN_MERGE,
     OP_ATTN_SPLIT,
     OP_EMBED,
@@ -431,6 +432,7 @@ class MoEDecodeModel:
             self.logits_acc = torch.zeros(b, E, dtype=torch.float32, device=dev)
         self.inv_freq = rope_inv_freq(cfg).to(dev)
         self.injected = False
+        self.best = torch.zeros(1, dtype=torch.int64, device=dev)  # greedy argmax word (one sequence)
 
         t1 = time.perf_counter()
         if scheduler == "dynamic":
@@ -510,7 +512,9 @@ class MoEDecodeModel:
         scale = 1.0 / math.sqrt(dh)
         nq = cfg.q_rows
         bs = 1 if self.batched else -1  # binding slot of the batch symbol (-1: one sequence)
-        ops = [make_op(OP_EMBED, i=[H, bs], p=[ptr(W["embed"]), ptr(self.tok), ptr(self.h)])]
+        greedy = not self.batched  # one sequence: the greedy token is decided on the device
+        ops = [make_op(OP_EMBED, i=[H, bs], p=[ptr(W["embed"]), ptr(self.tok), ptr(self.h), ptr(self.best)],
+                       flags=1 if greedy else 0)]
         for l, L in enumerate(W["layers"]):
             ri = {n: self.rt_index[f"{n}{l}"] for n in RT_PER_LAYER}
             kc, vc = self.kcache[l], self.vcache[l]
@@ -566,8 +570,15 @@ class MoEDecodeModel:
                                p=[ptr(L["wgate"]), ptr(L["wup"]), ptr(L["wdown"]), ptr(self.xn[l]), ptr(self.wslot[l]),
                                   ptr(self.h), ptr(self.tiles[l])]))
         ops.append(make_op(OP_GEMV, i=[cfg.vocab, H, 1, 1, EPI_F32, bs, 0, 16, 0, H], f=[cfg.eps],
-                           p=[ptr(W["lm_head"]), 0, ptr(self.h), ptr(W["final_norm"]), ptr(self.logits)]))
+                           flags=GEMV_ARGMAX if greedy else 0,
+                           p=[ptr(W["lm_head"]), 0, ptr(self.h), ptr(W["final_norm"]), ptr(self.logits), 0,
+                              ptr(self.best)]))
         return ops
+
+    def greedy_token(self):
+        """The last step's greedy token (one sequence), decided on the device (8-byte word)."""
+        from .ops import argmax_token
+        return argmax_token(self.best.item())
 
     # ------------------------------------------------------------------
     def inject_routing(self, topk_per_layer):

@@ -67,6 +67,8 @@ def test_moe_logits_and_routing(model, s, token):
     assert mg.check(t) == [], mg.check(t)[:3]
     assert all(c == 0 for c in m.executor.final_counters())
     assert m.last_stats["tasks_executed"] == mg.num_tasks
+    if not m.batched:  # the greedy token decided on the device
+        assert m.greedy_token() == int(logits.argmax())
 
 
 def test_moe_injected_routing_matches_reference_realization():
