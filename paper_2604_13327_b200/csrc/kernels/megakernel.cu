@@ -1240,6 +1240,65 @@ __device__ __noinline__ void attn_merge_group(const StaticParams& P, const et_op
     }
 }
 
+// Single-split group (fused merge, one split per (sequence, kv head): large batches)
+// finished in shared memory: the split's folded (M, L, O) per q head (sc: mW [8 warps][8],
+// lW, oacc [G][dh]) plus the new token (its k / v, appended by this task, at
+// sc + kAttnSoloKv) give the attention output directly, written in the next GEMV's
+// operand layout -- no partials round trip through L2, no arrival atomic, no merge.
+// The raw q/k/v accumulators of the group are zeroed for the next step (flags 33), as
+// attn_merge_group does.
+__device__ __noinline__ void attn_solo_finish(const StaticParams& P, const et_op& op, int gi, const float* qs,
+                                              int qstride, float* sc, int ctid) {
+    const int warp = ctid >> 5, lane = ctid & 31;
+    const int dh = op.i[0], G = op.i[1], kvh = op.i[6];
+    const int g = gi % kvh, bq = gi / kvh;
+    const float* mW = sc;
+    const float* lW = sc + 64;
+    const float* oacc = sc + 128;
+    const float* kv = sc + kAttnSoloKv;  // [2][dh] new k, v (bf16-rounded, as cached)
+    float* hw = sc + kAttnSoloKv + 2 * dh;  // [G][2]: weight of the folded O, weight of v_new
+    for (int h = warp; h < G; h += kConsumerWarps) {
+        float dot = 0.f;
+        for (int d = lane; d < dh; d += 32) dot += qs[h * qstride + d] * kv[d];
+        const float snew = warp_sum(dot) * op.f[0];
+        if (lane == 0) {
+            float M = -INFINITY;
+            for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, mW[w * 8 + h]);
+            float L = 0.f;
+            if (M != -INFINITY)
+                for (int w = 0; w < kConsumerWarps; ++w) {
+                    const float mw = mW[w * 8 + h];
+                    if (mw != -INFINITY) L += lW[w * 8 + h] * __expf(mw - M);
+                }
+            const float Mn = fmaxf(M, snew);
+            const float a = M == -INFINITY ? 0.f : __expf(M - Mn), en = __expf(snew - Mn);
+            const float inv = 1.f / (L * a + en);
+            hw[2 * h] = a * inv;
+            hw[2 * h + 1] = en * inv;
+        }
+    }
+    bar_sync(1, kConsumers);
+    const int kxb = op.i[9];
+    const int xnp = tc_npad(op.i[10] >= 0 ? static_cast<int>(P.binding[op.i[10]]) : 1);
+    uint16_t* out = reinterpret_cast<uint16_t*>(op.p[4]);
+    for (int idx = ctid; idx < G * dh; idx += kConsumers) {
+        const int h = idx / dh, d = idx - h * dh;
+        const float o = oacc[idx] * hw[2 * h] + kv[dh + d] * hw[2 * h + 1];
+        out[xb_offset(bq, g * G * dh + idx, xnp, kxb)] = f2bf(o);
+    }
+    if ((op.flags & 33) == 33) {  // the split-K q/k/v accumulators of this group: consumed
+        const long long rb = static_cast<long long>(bq) * op.i[7];
+        float* q = reinterpret_cast<float*>(op.p[0]) + rb + static_cast<long long>(g) * G * dh;
+        float* kr = reinterpret_cast<float*>(op.p[8]) + rb + static_cast<long long>(g) * dh;
+        float* vr = kr + static_cast<long long>(kvh) * dh;
+        for (int i = ctid; i < G * dh; i += kConsumers) q[i] = 0.f;
+        for (int i = ctid; i < dh; i += kConsumers) {
+            kr[i] = 0.f;
+            vr[i] = 0.f;
+        }
+    }
+}
+
 // Tensor-core form of a split's block loop (tensor-core instantiations: the batch
 // path), split along positions: warp w owns the 16-position tile (w % 4) of every
 // block of parity (w / 4) -- warps 0-3 take blocks 0, 2, 4, ..., warps 4-7 blocks
@@ -1288,18 +1347,20 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
         const int t0 = 16 * tile;                // the tile's first position in the block
         if (t0 < np) {
             float d[4] = {0.f, 0.f, 0.f, 0.f}, e[4] = {0.f, 0.f, 0.f, 0.f};
-            const int sw = swz ? g8 : 0;
-            const uint8_t* r0 = kb + (t0 + g8) * dh * 2 + 4 * q4;
-            const uint8_t* r1 = r0 + 8 * dh * 2;
+            // K tile as the A operand by ldmatrix: lane l addresses row (l & 7) of matrix
+            // l >> 3 = (rows +8 if odd, k chunk +1 if >= 2); row r's chunks are swizzled by r % 8
+            // chunk (2 ks + hi) ^ sw = (2 ks ^ (sw & 6)) | ((hi ^ sw) & 1): the k step's byte
+            // offset is (ks << 5) ^ ((sw & 6) << 4) past the row's odd-chunk bit (two
+            // registers instead of eight precomputed offsets)
+            const int km = lane >> 3, kr = lane & 7;
+            const int ksw = swz ? kr : 0;
+            const uint32_t kaddr = smem_u32(kb + (t0 + ((km & 1) << 3) + kr) * dh * 2) +
+                                   static_cast<uint32_t>((((km >> 1) ^ ksw) & 1) << 4);
+            const uint32_t kx = static_cast<uint32_t>((ksw & 6) << 4);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 if (ks < nks) {
-                    const int c0 = ((2 * ks) ^ sw) * 16, c1 = ((2 * ks + 1) ^ sw) * 16;
-                    uint4 a;
-                    a.x = *reinterpret_cast<const uint32_t*>(r0 + c0);
-                    a.y = *reinterpret_cast<const uint32_t*>(r1 + c0);
-                    a.z = *reinterpret_cast<const uint32_t*>(r0 + c1);
-                    a.w = *reinterpret_cast<const uint32_t*>(r1 + c1);
+                    const uint4 a = ldsm_x4_addr(kaddr + (static_cast<uint32_t>(ks << 5) ^ kx));
                     mma_bf16_16816(d, a, qh[ks][0], qh[ks][1]);
                     mma_bf16_16816(e, a, ql[ks][0], ql[ks][1]);
                 }
@@ -1366,13 +1427,24 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
         } else {
             if (!ring.wait(cv)) return false;
         }
-        bar_sync(2 + half, 128);  // the block's four warps are done with its K and V stages
-        if ((ctid & 127) == 0) {
-            ring.release(ck);
-            ring.release(cv);
+        // the block's four warps are done with its K and V stages: the first warp of the
+        // four waits for the others and releases them; the other three only arrive and go
+        // on to their next block.  A warp runs at most one group step ahead of the slowest
+        // (step i + 2 reuses step i's stages, released after step i's barrier), so two
+        // barrier ids per group, alternating by step, keep the phases apart.
+        const int bid = 2 + half + (((blk >> 1) & 1) << 1);
+        if ((ctid & 127) < 32) {
+            bar_sync(bid, 128);
+            if ((ctid & 127) == 0) {
+                ring.release(ck);
+                ring.release(cv);
+            }
+        } else {
+            bar_arrive(bid, 128);
         }
     }
-    if (!attn_warp_partials(op, P.binding)) {
+    const bool solo = attn_solo(op, P.binding);
+    if (solo || !attn_warp_partials(op, P.binding)) {
         // fold the 8 warps' partials in shared memory: M = max_w m_w, L = sum_w l_w e^(m_w - M),
         // O = sum_w e^(m_w - M) O_w (red.shared.add), one partial per split
         bar_sync(1, kConsumers);  // every warp is past its P scratch
@@ -1409,6 +1481,10 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
             }
         }
         bar_sync(1, kConsumers);
+        if (solo) {
+            attn_solo_finish(P, op, gi, qs, qstride, sc, ctid);
+            return true;
+        }
         float* part = reinterpret_cast<float*>(op.p[3]);
         for (int i = ctid; i < G * dh; i += kConsumers) {
             const int h = i / dh, d = i - h * dh;
@@ -1530,7 +1606,9 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             // them like any cached row
             // no merge task (flags bit 10): the last split does it and keeps them for its fold
             const bool knew = ((op.flags & 2) && c == 0) || fold;
-            float* kv = fold ? kv_new : sc;  // [2][dh] (sc: scratch before the blocks use it)
+            // [2][dh]: sc is scratch before the blocks use it; the tensor-core split keeps them
+            // past its per-warp P scratch (attn_solo_finish reads them after the blocks)
+            float* kv = fold ? kv_new : kMMA ? sc + kAttnSoloKv : sc;
             if (knew) {
                 const float* kr = reinterpret_cast<const float*>(op.p[8]) + rb + static_cast<long long>(g) * dh;
                 const float* vr = kr + static_cast<long long>(kvh) * dh;
@@ -1704,7 +1782,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
         }
     }
     if ((P.debug & 0x7000) == 0 && t_split && ctid == 0) *t_split = globaltimer();  // split work done (trace: prologue stamp)
-    if (op.flags & 2) {  // fused merge: the split of group g that arrives last merges it
+    if ((op.flags & 2) && !(kMMA && attn_solo(op, P.binding))) {  // fused merge: the split of group g that arrives last merges it
         volatile int* flag = reinterpret_cast<volatile int*>(st + 4 * G);
         bar_sync(1, kConsumers);
         if (ctid == 0) {

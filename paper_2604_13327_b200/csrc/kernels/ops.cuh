@@ -346,6 +346,14 @@ __device__ __forceinline__ void attn_coord(const et_op& op, const int* coord, co
 __device__ __forceinline__ bool attn_warp_partials(const et_op& op, const long long* binding) {
     return (op.flags & 512) && attn_tasks(op, binding) <= 1;
 }
+// Tensor-core split body, fused merge (flags bit 1), q/k fused mode (bit 0: this task
+// appends the new k/v) and one split per group: the task finishes the group itself
+// (attn_solo_finish) -- no partials, no arrival.  Its new k/v stay in shared memory at
+// scratch float kAttnSoloKv (past the eight warps' P transposes, [8][16][9]).
+constexpr int kAttnSoloKv = 8 * 16 * 9;
+__device__ __forceinline__ bool attn_solo(const et_op& op, const long long* binding) {
+    return (op.flags & 3) == 3 && attn_tasks(op, binding) <= 1;
+}
 __device__ __forceinline__ int attn_splits_with_data(const et_op& op, const long long* binding) {
     return attn_warp_partials(op, binding) ? 8 : attn_tasks(op, binding);  // empty splits: (m = -inf, l = 0)
 }
