@@ -107,14 +107,20 @@ def tc_tasks(nblk, workers, splittable, nseg=1, npad=64, pieces=1):
     """(tasks, k splits) of a projection: one 128-row block per group and enough
     k splits to cover the workers when the epilogue adds (split-K: at most one
     wave -- 32 blocks x 5 splits = 160 tasks on 148 SMs put a second task on 12
-    of them and doubled the stage's tail); otherwise
-    groups of blocks small enough that two MMA issuers fit their accumulators
-    in TMEM (ops.cuh kTcIssuers)."""
+    of them and doubled the stage's tail; two blocks per task with twice the
+    splits, halving the activation re-reads, measured slower: more tasks and
+    red.add traffic); otherwise groups of blocks small enough that two MMA
+    issuers fit their accumulators in TMEM (ops.cuh kTcIssuers)."""
     if splittable:
         splits = max(1, min(pieces, workers // nblk))
         return nblk * splits, splits
     per = max(1, TMEM_COLS // (2 * nseg * npad))  # blocks per task that leave TMEM for 2 MMA issuers
     groups = max(min(workers, nblk), -(-nblk // per))
+    if groups > workers:
+        # more than one wave (lm_head: 1002 blocks): one wave of larger tasks with one MMA
+        # issuer each (TMEM holds up to 512 / (nseg * npad) blocks) -- a streaming issuer
+        # keeps up with the SM's share of HBM, a second wave doubles the stage
+        groups = max(workers, -(-nblk // max(1, TMEM_COLS // (nseg * npad))))
     return groups, 1
 
 
