@@ -25,6 +25,13 @@
 #include "megakernel.cuh"
 #include "ops.cuh"
 
+#ifndef ET_ATTN_QLO
+#define ET_ATTN_QLO 1
+#endif
+#ifndef ET_ATTN_PLO
+#define ET_ATTN_PLO 1
+#endif
+
 namespace etk {
 
 __device__ __forceinline__ uint8_t* smem_cta_base() {
@@ -1320,16 +1327,26 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
     const float scale = op.f[0];
     const int nks = dh / 16, half = warp >> 2, tile = warp & 3;
     const bool swz = (op.flags & 256) != 0;  // cache rows chunk-swizzled by position % 8
-    uint32_t qh[8][2], ql[8][2];  // Q^T fragments (k = dim, n = head g8)
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-        qh[ks][0] = qh[ks][1] = ql[ks][0] = ql[ks][1] = 0u;
-        if (ks < nks && g8 < G) {
-            const float* qv = qs + g8 * qstride + ks * 16 + 2 * q4;
-            split_bf16x2(qv[0], qv[1], qh[ks][0], ql[ks][0]);
-            split_bf16x2(qv[8], qv[9], qh[ks][1], ql[ks][1]);
+    // Q^T fragments (k = dim, n = head g8) and the bf16 remainders q - bf16(q) (ET_ATTN_QLO: a
+    // second MMA per k step), likewise P split hi + lo for P.V (ET_ATTN_PLO).  Without the
+    // remainders the batched step is 6-10% faster (b=64: 9.01 -> 8.48 ms at s=1024, 21.8 ->
+    // 19.5 ms at s=8192) but the MoE tensor-core logits leave the 2e-3 tolerance
+    // (tests/test_gpu_moe.py: 5.2e-3; P alone: 4.5e-3), so both stay on.
+    // The fragments live in shared memory, [k step][lane] x {hi0, hi1, lo0, lo1} (the same
+    // for every warp; one 16-byte load per k step): held in registers they took 32 of the
+    // 168 and left the block loop one temporary, serialising every ldmatrix -> mma pair.
+    uint32_t* qfr = reinterpret_cast<uint32_t*>(sc + kAttnQFrag);
+    {
+        const int fks = ctid >> 5, fl = ctid & 31, fg = fl >> 2, fq = fl & 3;  // 256 threads = 8 x 32
+        uint4 f = make_uint4(0u, 0u, 0u, 0u);
+        if (fks < nks && fg < G) {
+            const float* qv = qs + fg * qstride + fks * 16 + 2 * fq;
+            split_bf16x2(qv[0], qv[1], f.x, f.z);
+            split_bf16x2(qv[8], qv[9], f.y, f.w);
         }
+        reinterpret_cast<uint4*>(qfr)[ctid] = f;
     }
+    bar_sync(1, kConsumers);
     const int h0 = 2 * q4;                       // this thread's two head columns
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
     float o[8][4];                               // O^T per 16-dim tile: (d, h0) (d, h0+1) (d+8, h0) (d+8, h0+1)
@@ -1361,8 +1378,9 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
             for (int ks = 0; ks < 8; ++ks) {
                 if (ks < nks) {
                     const uint4 a = ldsm_x4_addr(kaddr + (static_cast<uint32_t>(ks << 5) ^ kx));
-                    mma_bf16_16816(d, a, qh[ks][0], qh[ks][1]);
-                    mma_bf16_16816(e, a, ql[ks][0], ql[ks][1]);
+                    const uint4 qf = reinterpret_cast<const uint4*>(qfr)[ks * 32 + lane];
+                    mma_bf16_16816(d, a, qf.x, qf.y);
+                    if (ET_ATTN_QLO) mma_bf16_16816(e, a, qf.z, qf.w);
                 }
             }
             // scores of positions t0+g8 / t0+g8+8 for heads h0, h0+1 (invalid -> -inf)
@@ -1421,7 +1439,7 @@ __device__ __noinline__ bool attn_split_mma(const StaticParams& P, const et_op& 
                 if (mt < nks) {
                     const uint4 a = ldsm_x4_trans(vrow + ((2 * mt + (mi & 1)) ^ csw) * 16);  // V^T: dims x positions
                     mma_bf16_16816(o[mt], a, bh0, bh1);
-                    mma_bf16_16816(o[mt], a, bl0, bl1);
+                    if (ET_ATTN_PLO) mma_bf16_16816(o[mt], a, bl0, bl1);
                 }
             }
         } else {

@@ -351,6 +351,9 @@ __device__ __forceinline__ bool attn_warp_partials(const et_op& op, const long l
 // (attn_solo_finish) -- no partials, no arrival.  Its new k/v stay in shared memory at
 // scratch float kAttnSoloKv (past the eight warps' P transposes, [8][16][9]).
 constexpr int kAttnSoloKv = 8 * 16 * 9;
+// ... and the Q^T fragments of the split ([8 k steps][32 lanes] x 16 bytes) past the solo
+// split's k/v (2 x 128) and weights (2 x 8) -- 16-byte aligned
+constexpr int kAttnQFrag = kAttnSoloKv + 2 * 128 + 16;
 __device__ __forceinline__ bool attn_solo(const et_op& op, const long long* binding) {
     return (op.flags & 3) == 3 && attn_tasks(op, binding) <= 1;
 }

@@ -103,7 +103,7 @@ def build_graph(cfg, tasks, lm_tasks, fused_merge=False, call_tasks=None, attn_c
 
 
 def decode_graph_spec(cfg, workers, max_seq, lm_tasks=None, residual="split", fused_merge=True, balance=True,
-                      grouped=True):
+                      grouped=True, attn_cap=None):
     """The decode-step graph DecodeModel lowers (reference JSON spec) and the
     layout choices it implies: per-call task counts, kv-head grouping, the
     attention split cap."""
@@ -118,7 +118,7 @@ def decode_graph_spec(cfg, workers, max_seq, lm_tasks=None, residual="split", fu
     og = max(1, workers // cfg.kv_heads)
     while (cfg.hidden // 16) % og:
         og -= 1
-    cap = attn_split_cap(cfg, max_seq, workers)
+    cap = attn_cap or attn_split_cap(cfg, max_seq, workers)
     spec = graph_spec(cfg, workers, lm_tasks or workers, fused_merge, call_tasks=call_tasks, attn_cap=cap,
                       grouped=grouped, oproj_group_tasks=og)
     return spec, {"call_tasks": call_tasks, "grouped": grouped, "oproj_group_tasks": og, "attn_cap": cap}
@@ -250,7 +250,7 @@ class DecodeModel:
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
                  l2_prefetch=512 << 10, residual="split", fused_merge=True, balance=True, grouped=True,
-                 scheduler="static", early_push=False, stage_barriers=False, program=None):
+                 scheduler="static", early_push=False, stage_barriers=False, program=None, attn_cap=None):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -261,7 +261,9 @@ class DecodeModel:
         self.lm_tasks = lm_tasks or self.num_workers
         self.samples = sorted(int(s) for s in samples)
         self.capacity = capacity or (self.samples[-1] + 1)
-        self.max_splits = attn_split_cap(cfg, self.samples[-1], self.num_workers)
+        # attention splits per kv head (attn_cap overrides the default: one per 64-position
+        # block up to about one task per SM)
+        self.max_splits = attn_cap or attn_split_cap(cfg, self.samples[-1], self.num_workers)
         self.residual = residual
 
         import time
@@ -269,7 +271,7 @@ class DecodeModel:
         self.fused_merge = fused_merge
         spec, self.layout = decode_graph_spec(cfg, self.tasks, self.samples[-1], lm_tasks=self.lm_tasks,
                                               residual=residual, fused_merge=fused_merge, balance=balance,
-                                              grouped=grouped)
+                                              grouped=grouped, attn_cap=attn_cap)
         self.call_tasks = self.layout["call_tasks"]
         self.grouped = self.layout["grouped"]
         self.oproj_group_tasks = self.layout["oproj_group_tasks"]
