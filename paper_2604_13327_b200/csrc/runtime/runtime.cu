@@ -126,6 +126,12 @@ struct et_runtime {
     DevArray<et_op> d_ops;
     int has_moe = 0;  // kernel variant: bit 0 MoE bodies, bit 1 tensor-core GEMV bodies (bound ops)
     int ops_bound = 0;
+    // per-step host work memoised by binding: the covering sample and the runtime tensor
+    // lengths of the last binding (a serving loop repeats shapes); reset by every upload
+    // and op-table bind
+    std::vector<int64_t> memo_binding;
+    int memo_pick = -1;
+    std::vector<int> memo_rt_len;
     std::vector<et_op> h_ops;  // host copy of the bound op table (launch-time capacity checks)
 
     int mode = ET_MODE_STATIC;
@@ -294,6 +300,7 @@ int et_upload_graph(et_runtime* rt, const et_graph_desc* g) {
     }
     ET_CUDA(rt->d_rt_table.upload(table.data(), table.size()), "runtime tensors");
     rt->samples.clear();
+    rt->memo_pick = -1;
     rt->last_sample = -1;
     rt->img_graph.clear();
     rt->img_samples.clear();
@@ -315,6 +322,7 @@ int et_upload_static(et_runtime* rt, const et_sample_desc* s, int32_t num_sample
     cudaSetDevice(rt->cfg.device);
     cudaStreamSynchronize(rt->stream);
     rt->samples.clear();
+    rt->memo_pick = -1;
     rt->samples.resize(static_cast<size_t>(num_samples));
     int max_counters = 1, max_slots = 1;
     for (int i = 0; i < num_samples; ++i) {
@@ -770,6 +778,7 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     rt->has_moe = variant;
     rt->h_ops.assign(ops, ops + num_calls);
     rt->ops_bound = 1;
+    rt->memo_pick = -1;
     return ET_OK;
 }
 
@@ -874,41 +883,45 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     if (rt->samples.empty()) return rt->fail(ET_ERR_INVALID, "no program uploaded");
     if (!rt->ops_bound) return rt->fail(ET_ERR_INVALID, "ops not bound");
     cudaSetDevice(rt->cfg.device);
-    // next-larger covering sample (samples are uploaded in selection order)
-    // actual grid extents at this binding
-    std::vector<int64_t> ext(static_cast<size_t>(rt->num_calls) * 4, 0);
-    for (int c = 0; c < rt->num_calls; ++c)
-        for (int d = 0; d < rt->call_rank[static_cast<size_t>(c)]; ++d) {
-            bool ok = true;
-            const int64_t a = eval_host(rt->code_op, rt->code_arg, rt->grid_code_off[static_cast<size_t>(c * 4 + d)],
-                                        rt->grid_code_off[static_cast<size_t>(c * 4 + d + 1)], binding, &ok);
-            if (!ok) return rt->fail(ET_ERR_INVALID, "grid of call " + std::to_string(c) + " is invalid at the binding");
-            ext[static_cast<size_t>(c * 4 + d)] = a;
-            if (d == 0 && !gemv_acc_fits(rt->h_ops[static_cast<size_t>(c)], a, binding))
-                return rt->fail(ET_ERR_INVALID, "GEMV call " + std::to_string(c) +
-                                                    ": rows per task x batch exceed the accumulators (shared memory / "
-                                                    "tensor memory) or the operand shape is invalid");
+    const bool memo = rt->memo_pick >= 0 && rt->memo_binding.size() == static_cast<size_t>(num_symbols) &&
+                      std::equal(rt->memo_binding.begin(), rt->memo_binding.end(), binding);
+    int pick = memo ? rt->memo_pick : -1;
+    if (!memo) {
+        // next-larger covering sample (samples are uploaded in selection order)
+        // actual grid extents at this binding
+        std::vector<int64_t> ext(static_cast<size_t>(rt->num_calls) * 4, 0);
+        for (int c = 0; c < rt->num_calls; ++c)
+            for (int d = 0; d < rt->call_rank[static_cast<size_t>(c)]; ++d) {
+                bool ok = true;
+                const int64_t a = eval_host(rt->code_op, rt->code_arg, rt->grid_code_off[static_cast<size_t>(c * 4 + d)],
+                                            rt->grid_code_off[static_cast<size_t>(c * 4 + d + 1)], binding, &ok);
+                if (!ok) return rt->fail(ET_ERR_INVALID, "grid of call " + std::to_string(c) + " is invalid at the binding");
+                ext[static_cast<size_t>(c * 4 + d)] = a;
+                if (d == 0 && !gemv_acc_fits(rt->h_ops[static_cast<size_t>(c)], a, binding))
+                    return rt->fail(ET_ERR_INVALID, "GEMV call " + std::to_string(c) +
+                                                        ": rows per task x batch exceed the accumulators (shared memory / "
+                                                        "tensor memory) or the operand shape is invalid");
+            }
+        // next-larger sample covering the binding (ref sched_static.cpp:111-175) whose grids
+        // also cover the actual ones (ref sched_static.cpp:153-156); a grid that is not
+        // monotone in the symbols (e.g. splits shrinking with the batch) falls through to
+        // the next covering sample instead of failing
+        int first = -1;
+        for (size_t i = 0; i < rt->samples.size() && pick < 0; ++i) {
+            bool covers = true;
+            for (int k = 0; k < num_symbols; ++k) covers &= rt->samples[i].binding[static_cast<size_t>(k)] >= binding[k];
+            if (!covers) continue;
+            if (first < 0) first = static_cast<int>(i);
+            bool grids = true;
+            for (int c = 0; c < rt->num_calls && grids; ++c)
+                for (int d = 0; d < rt->call_rank[static_cast<size_t>(c)]; ++d)
+                    grids &= ext[static_cast<size_t>(c * 4 + d)] <= rt->samples[i].call_extents[static_cast<size_t>(c * 4 + d)];
+            if (grids) pick = static_cast<int>(i);
         }
-    // next-larger sample covering the binding (ref sched_static.cpp:111-175) whose grids
-    // also cover the actual ones (ref sched_static.cpp:153-156); a grid that is not
-    // monotone in the symbols (e.g. splits shrinking with the batch) falls through to
-    // the next covering sample instead of failing
-    int pick = -1, first = -1;
-    for (size_t i = 0; i < rt->samples.size() && pick < 0; ++i) {
-        bool covers = true;
-        for (int k = 0; k < num_symbols; ++k) covers &= rt->samples[i].binding[static_cast<size_t>(k)] >= binding[k];
-        if (!covers) continue;
-        if (first < 0) first = static_cast<int>(i);
-        bool grids = true;
-        for (int c = 0; c < rt->num_calls && grids; ++c)
-            for (int d = 0; d < rt->call_rank[static_cast<size_t>(c)]; ++d)
-                grids &= ext[static_cast<size_t>(c * 4 + d)] <= rt->samples[i].call_extents[static_cast<size_t>(c * 4 + d)];
-        if (grids) pick = static_cast<int>(i);
+        if (first < 0) return rt->fail(ET_ERR_INVALID, "binding exceeds every sampled shape");
+        if (pick < 0) return rt->fail(ET_ERR_INVALID, "sampled shape does not cover the actual grid of a call");
     }
-    if (first < 0) return rt->fail(ET_ERR_INVALID, "binding exceeds every sampled shape");
-    if (pick < 0) return rt->fail(ET_ERR_INVALID, "sampled shape does not cover the actual grid of a call");
     const Sample& S = rt->samples[static_cast<size_t>(pick)];
-    (void)S;
 
     etk::StaticParams p{};
     p.num_symbols = rt->num_symbols;
@@ -937,12 +950,19 @@ int et_step(et_runtime* rt, const int64_t* binding, int32_t num_symbols, void* s
     p.cnt_capacity = rt->cnt_capacity;
     p.rt = rt->d_rt_table.ptr;
     p.num_rt = static_cast<int>(rt->d_rt.size());
-    for (int i = 0; i < p.num_rt; ++i) {
-        bool ok = true;
-        p.rt_len[i] = (int)eval_host(rt->code_op, rt->code_arg, rt->rt_len_off[static_cast<size_t>(i)],
-                                rt->rt_len_off[static_cast<size_t>(i) + 1], binding, &ok);
-        if (!ok || p.rt_len[i] > rt->rt_capacity[static_cast<size_t>(i)])
-            return rt->fail(ET_ERR_INVALID, "runtime tensor shape invalid at the binding");
+    if (memo) {
+        for (int i = 0; i < p.num_rt; ++i) p.rt_len[i] = rt->memo_rt_len[static_cast<size_t>(i)];
+    } else {
+        for (int i = 0; i < p.num_rt; ++i) {
+            bool ok = true;
+            p.rt_len[i] = (int)eval_host(rt->code_op, rt->code_arg, rt->rt_len_off[static_cast<size_t>(i)],
+                                    rt->rt_len_off[static_cast<size_t>(i) + 1], binding, &ok);
+            if (!ok || p.rt_len[i] > rt->rt_capacity[static_cast<size_t>(i)])
+                return rt->fail(ET_ERR_INVALID, "runtime tensor shape invalid at the binding");
+        }
+        rt->memo_binding.assign(binding, binding + num_symbols);
+        rt->memo_rt_len.assign(p.rt_len, p.rt_len + p.num_rt);
+        rt->memo_pick = pick;
     }
     p.ops = rt->d_ops.ptr;
     p.trace = rt->d_trace.ptr;
