@@ -1073,16 +1073,21 @@ __device__ __noinline__ void body_norm(const StaticParams& P, const et_op& op, c
     const float* gam = reinterpret_cast<const float*>(op.p[1]);
     uint16_t* out = reinterpret_cast<uint16_t*>(op.p[2]);
     constexpr int kMaxPer = 8;  // K <= 8192
-    float4 hv[kMaxPer];
+    float4 hv[kMaxPer], gv[kMaxPer];
     float ss = 0.f;
+    // gamma loads with the row (one L2 round trip: the wait's acquire left L1 cold)
 #pragma unroll
     for (int j = 0; j < kMaxPer; ++j) {
         const int k = (ctid + j * kConsumers) * 4;
         if (k < K) {
             hv[j] = ldcg_f4(h + k);
-            ss += hv[j].x * hv[j].x + hv[j].y * hv[j].y + hv[j].z * hv[j].z + hv[j].w * hv[j].w;
+            gv[j] = __ldg(reinterpret_cast<const float4*>(gam + k));
         }
     }
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j)
+        if ((ctid + j * kConsumers) * 4 < K)
+            ss += hv[j].x * hv[j].x + hv[j].y * hv[j].y + hv[j].z * hv[j].z + hv[j].w * hv[j].w;
     ss = warp_sum(ss);
     if (lane == 0) red[warp] = ss;
     bar_sync(1, kConsumers);
@@ -1094,7 +1099,7 @@ __device__ __noinline__ void body_norm(const StaticParams& P, const et_op& op, c
     for (int j = 0; j < kMaxPer; ++j) {
         const int k = (ctid + j * kConsumers) * 4;
         if (k < K) {
-            const float4 g = __ldg(reinterpret_cast<const float4*>(gam + k));
+            const float4 g = gv[j];
             uint2 o;
             o.x = static_cast<uint32_t>(f2bf(hv[j].x * scale * g.x)) | (static_cast<uint32_t>(f2bf(hv[j].y * scale * g.y)) << 16);
             o.y = static_cast<uint32_t>(f2bf(hv[j].z * scale * g.z)) | (static_cast<uint32_t>(f2bf(hv[j].w * scale * g.w)) << 16);
