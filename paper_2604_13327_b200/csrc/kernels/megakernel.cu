@@ -1997,6 +1997,8 @@ __device__ __forceinline__ void body_moe_route_impl(const StaticParams& P, const
             if (op.flags & 1) {  // injected routing (host-written topk)
                 e = __ldcg(topk + t * K + j);
             } else {  // selection on the raw logits: larger wins, the lower expert index on ties
+                // each lane's best remaining candidate, then two warp reductions (redux.sync):
+                // the largest order-preserving key, and the lowest expert index holding it
                 float bv = -INFINITY;
                 int bi = 1 << 30;
 #pragma unroll
@@ -2005,27 +2007,28 @@ __device__ __forceinline__ void body_moe_route_impl(const StaticParams& P, const
                         bv = lg[u];
                         bi = lane + 32 * u;
                     }
-                for (int o = 16; o > 0; o >>= 1) {
-                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                    if (ov > bv || (ov == bv && oi < bi)) {
-                        bv = ov;
-                        bi = oi;
-                    }
-                }
-                e = bi;
+                uint32_t key = __float_as_uint(bv + 0.f);  // -0 -> +0: equal logits tie on the index
+                key = (key & 0x80000000u) ? ~key : (key | 0x80000000u);
+                const uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
+                e = static_cast<int>(__reduce_min_sync(0xffffffffu, key == kmax ? static_cast<uint32_t>(bi) : 0xffffffffu));
                 if ((e & 31) == lane) {  // taken: drop it from the candidates
 #pragma unroll
                     for (int u = 0; u < kPer; ++u)
                         if (u == (e >> 5)) lg[u] = -INFINITY;
                 }
+                // the selected logit (sw holds it until the slot's weight replaces it below)
+                if (lane == 0) sw[t * K + j] = __uint_as_float((kmax & 0x80000000u) ? (kmax & 0x7fffffffu) : ~kmax);
             }
             if (lane == 0) stop[t * K + j] = e;
         }
         __syncwarp();
-        // weights p_e / sum of the selected p, recomputed from the logits
+        // weights p_e / sum of the selected p, from the selected logits (injected routing:
+        // loaded)
         const int ej = lane < K ? stop[t * K + lane] : 0;
-        const float lj = lane < K ? (single ? acc[ej * nb + t] : __ldcg(logits + static_cast<long long>(t) * E + ej)) : 0.f;
+        const float lj = lane >= K              ? 0.f
+                         : !(op.flags & 1)      ? sw[t * K + lane]
+                         : single               ? acc[ej * nb + t]
+                                                : __ldcg(logits + static_cast<long long>(t) * E + ej);
         const float wj = lane < K ? __expf(lj - m) / z : 0.f;
         const float wsum = warp_sum(wj);
         if (lane < K) {
