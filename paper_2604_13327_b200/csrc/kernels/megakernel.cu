@@ -1571,9 +1571,15 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     // per q head goes to the partials buffer; the merge combines the splits.
     constexpr int kOutMax = kQK ? 2 : 1;  // (head, dim pair) outputs per thread: G * dh / 2 <= 256 * kOutMax
     const int warp = ctid >> 5, lane = ctid & 31;
-    const int dh = op.i[0], G = op.i[1], CH = op.i[2], maxs = op.i[5], kvh = op.i[6];
+    // i13 = HS > 1 (scalar split with the output projection's merge, flags bit 10): the q heads
+    // of a kv head are shared by HS tasks per split (dim 0 of the grid = group * HS + part),
+    // each scoring its G / HS heads against the same K/V blocks -- wide groups (Qwen3: 8 q
+    // heads per kv head) get HS times the tasks at 1/HS the arithmetic each
+    const int HS = (!kMMA && op.i[13] > 1) ? op.i[13] : 1;
+    const int dh = op.i[0], Gf = op.i[1], G = Gf / HS, CH = op.i[2], maxs = op.i[5], kvh = op.i[6];
     const long long s = P.binding[op.i[4]];
-    int gi = si.coord[0], c = si.coord[1];  // gi = sequence * kv_heads + kv head, c = split
+    int gi = si.coord[0] / HS, c = si.coord[1];  // gi = sequence * kv_heads + kv head, c = split
+    const int hb = (si.coord[0] - gi * HS) * G;  // first q head (within the group) of this task
     if constexpr (kMMA) attn_coord(op, si.coord, P.binding, &gi, &c);  // flat batch-dependent grid
     const int g = gi % kvh, bq = gi / kvh;
     const long long rb = static_cast<long long>(bq) * op.i[7];  // this sequence's q / projection row
@@ -1584,7 +1590,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     float* qs = scratch;                 // [G][dh+4]
     float* sc = scratch + G * qstride;   // [G][CH]
     float* st = sc + G * CH;             // [G][4]: running max, running sum, block rescale
-    const float* q = reinterpret_cast<const float*>(op.p[0]) + rb + static_cast<long long>(g) * G * dh;
+    const float* q = reinterpret_cast<const float*>(op.p[0]) + rb + static_cast<long long>(g * Gf + hb) * dh;
     for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
     // flags bit 10 (no merge task): the group's last split also folds in the new token
     // -- cache row s, appended by the q/k/v projection this task waited on -- so the
@@ -1795,7 +1801,7 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
             const int idx = ctid + j * kConsumers;
             if (idx >= G * half) break;
             const int h = idx / half, dp = idx - h * half;
-            float* pr = part + ((static_cast<long long>(gi) * G + h) * maxs + c) * (dh + kPartHead);
+            float* pr = part + ((static_cast<long long>(gi) * Gf + hb + h) * maxs + c) * (dh + kPartHead);
             pr[kPartHead + 2 * dp] = o0[j];
             pr[kPartHead + 1 + 2 * dp] = o1[j];
             if (dp == 0) {

@@ -334,8 +334,8 @@ __device__ __forceinline__ void attn_coord(const et_op& op, const int* coord, co
         const int ns0 = attn_tasks(op, binding), ns = ns0 > 1 ? ns0 : 1;
         *gi = coord[0] / ns;
         *c = coord[0] - *gi * ns;
-    } else {
-        *gi = coord[0];
+    } else {  // i13 > 1: dim 0 = group * i13 + q-head part (body_attn_split)
+        *gi = op.i[13] > 1 ? coord[0] / op.i[13] : coord[0];
         *c = coord[1];
     }
 }

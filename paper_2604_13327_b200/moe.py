@@ -121,7 +121,7 @@ RT_PER_LAYER = ("topk", "cnt", "ind", "tind", "elist", "eoff")
 
 
 def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=None, route_tasks=1,
-                   group_stage=True, attn_cap=None, oproj_group_tasks=None, tc=None):
+                   group_stage=True, attn_cap=None, oproj_group_tasks=None, tc=None, head_split=1):
     """Reference-format graph spec (ref json_io.cpp:115-230) of one MoE decode step.
 
     tokens: an int (fixed batch) or "b" -- the batch is then a graph symbol next
@@ -181,6 +181,10 @@ def moe_graph_spec(cfg, tasks, lm_tasks, tokens=1, fused_merge=False, qkv_tasks=
 
             calls.append({"fn": fn(f"L{l}.attn", [attn_grid(cfg, attn_cap, tc["attn_budget"])]),
                           "in": [{"event": qkv, "map": ["0"]}], "out": [{"event": m, "map": ["0"]}]})
+        elif fused_merge and head_split > 1:  # q heads of a group shared by head_split tasks per split
+            calls.append({"fn": fn(f"L{l}.attn", [f"{tokens} * {kv} * {head_split}", f"max({nsplit}, 1)"]),
+                          "in": [{"event": qkv, "map": ["0"]}],
+                          "out": [{"event": m, "map": [f"(t0 // {head_split}) % {kv}"]}]})
         elif fused_merge:  # the last split of each (sequence, kv head) merges the group
             calls.append({"fn": fn(f"L{l}.attn", [f"{tokens} * {kv}", f"max({nsplit}, 1)"]),
                           "in": [{"event": qkv, "map": ["0"]}],
@@ -298,7 +302,7 @@ def moe_device_layout(cfg, W, kp=0):
 
 def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=None, attn_cap=None,
                fused_merge=True, balance=False, route_tasks=None, group_stage=None, qkv_split=True,
-               oproj_merge=True):
+               oproj_merge=True, head_split=None):
     """Every layout choice MoEDecodeModel makes before touching the device: the graph
     spec it lowers, its bindings (samples) and task counts.  Pure (no device, no
     extension), so the committed bench-graph fixtures (tests/golden/make_bench_graphs.py)
@@ -326,6 +330,14 @@ def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=
         ms = max(1, ms // 2)
     L["max_splits"] = ms
     L["fused_merge"] = fused_merge
+    # q-head split of the scalar attention (one sequence, output projection merge only): by
+    # default 4 tasks per (kv head, split) for groups of >= 8 q heads (Qwen3-30B-A3B bs=1:
+    # 3.80 -> 3.57 ms static, 5.37 -> 5.21 ms dynamic; 2: 3.59 ms, 8: 4.09 ms)
+    G = cfg.heads // cfg.kv_heads
+    if head_split is None:
+        head_split = 4 if G >= 8 else 1
+    L["head_split"] = head_split if (max_batch == 1 and oproj_merge and fused_merge) else 1
+    assert (cfg.heads // cfg.kv_heads) % L["head_split"] == 0
     L["group_stage"] = (scheduler == "dynamic") if group_stage is None else group_stage
     L["qkv_split"] = qkv_split and fused_merge
     L["route_tasks"] = route_tasks or max(1, cfg.experts // 16)
@@ -360,7 +372,7 @@ def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=
     L["spec"] = moe_graph_spec(cfg, num_workers, L["lm_tasks"], L["tokens"], fused_merge=fused_merge,
                                qkv_tasks=balanced_tasks(cfg.q_rows + 2 * cfg.kv_rows, num_workers)
                                if balance else None, route_tasks=L["route_tasks"], group_stage=L["group_stage"],
-                               attn_cap=ms, oproj_group_tasks=og, tc=tct)
+                               attn_cap=ms, oproj_group_tasks=og, tc=tct, head_split=L["head_split"])
     L["bindings"] = [({"s": int(s), "b": int(b)} if L["batched"] else {"s": int(s)})
                      for s in L["samples"] for b in L["batch_samples"]]
     return L
@@ -372,7 +384,8 @@ class MoEDecodeModel:
     def __init__(self, cfg: MoEConfig, device="cuda:0", samples=(1024,), num_workers=None, seed=0, weights=None,
                  scheduler="dynamic", record_trace=False, keep_logical=False, early_push=False, fused_merge=True,
                  balance=False, route_tasks=None, group_stage=None, l2_prefetch_experts=False, qkv_split=True,
-                 max_batch=1, batch_samples=None, attn_cap=None, oproj_merge=True, stage_barriers=False):
+                 max_batch=1, batch_samples=None, attn_cap=None, oproj_merge=True, stage_barriers=False,
+                 head_split=None):
         if not etsim.gpu_available():
             raise RuntimeError("MoEDecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -384,7 +397,8 @@ class MoEDecodeModel:
         t0 = time.perf_counter()
         lay = moe_layout(cfg, self.num_workers, samples, scheduler, max_batch=max_batch, batch_samples=batch_samples,
                          attn_cap=attn_cap, fused_merge=fused_merge, balance=balance, route_tasks=route_tasks,
-                         group_stage=group_stage, qkv_split=qkv_split, oproj_merge=oproj_merge)
+                         group_stage=group_stage, qkv_split=qkv_split, oproj_merge=oproj_merge,
+                         head_split=head_split)
         for k, v in lay.items():
             setattr(self, k, v)
         if stage_barriers:  # ablation: every call waits for the whole previous call (graphs.add_stage_barriers)
@@ -529,7 +543,8 @@ class MoEDecodeModel:
             attn_p = [ptr(self.qkv), ptr(kc), ptr(vc), ptr(self.partials), ptr(self.attn), ptr(L["q_norm"]),
                       ptr(L["k_norm"]), ptr(self.inv_freq), ptr(self.qkv) + 4 * nq]
             if self.oproj_merge:  # flags: 1 = q/k-norm mode, 1024 = the last split folds the new token
-                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], flags=1 | 1024, p=attn_p))
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i + [0] * 4 + [self.head_split], f=[scale, cfg.eps],
+                                   flags=1 | 1024, p=attn_p))
             elif self.fused_merge:  # flags: 1 = q/k-norm mode, 2 = the last split merges; p5 of the split
                 # op carries the arrival counters, so the norm weights move to the merge-compatible slots
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale, cfg.eps], flags=3 | (32 if self.qkv_split else 0),

@@ -138,3 +138,23 @@ def test_moe_batched_decode_no_recompile(scheduler, max_batch, cases):
         assert mg.check(m.executor.trace()) == []
         assert m.last_stats["tasks_executed"] == mg.num_tasks
         assert all(c == 0 for c in m.executor.final_counters())
+
+
+@pytest.mark.parametrize("scheduler", ["static", "dynamic"])
+def test_moe_attention_head_split(scheduler):
+    """head_split=2: each (kv head, split) runs as two tasks over half the q heads each
+    (scalar split, output-projection merge); logits and routing as in the unsplit case."""
+    m = MoEDecodeModel(TINY_MOE, samples=(16, 64), num_workers=16, seed=0, scheduler=scheduler,
+                       keep_logical=True, head_split=2)
+    assert m.head_split == 2
+    for s, token in ((40, 11), (1, 5)):
+        m.fill_cache(s, seed=2)
+        m.set_token(token)
+        ck, cv = _cpu_cache(m)
+        logits = m.step(s)[0].cpu()
+        dev_topk = [m.routing(l)["topk"] for l in range(m.cfg.layers)]
+        ref, _, _ = moe_decode_step(m.cfg, weights_to_cpu(m.W_logical), ck, cv, token, s, m.inv_freq.cpu(),
+                                    routing=dev_topk)
+        err = (logits - ref).abs().max().item()
+        scale = ref.abs().max().item()
+        assert err <= 2e-3 * scale + 2e-3, (s, err, scale)
