@@ -103,7 +103,7 @@ def build_graph(cfg, tasks, lm_tasks, fused_merge=False, call_tasks=None, attn_c
 
 
 def decode_graph_spec(cfg, workers, max_seq, lm_tasks=None, residual="split", fused_merge=True, balance=True,
-                      grouped=True, attn_cap=None):
+                      grouped=True, attn_cap=None, head_split=1):
     """The decode-step graph DecodeModel lowers (reference JSON spec) and the
     layout choices it implies: per-call task counts, kv-head grouping, the
     attention split cap."""
@@ -119,9 +119,11 @@ def decode_graph_spec(cfg, workers, max_seq, lm_tasks=None, residual="split", fu
     while (cfg.hidden // 16) % og:
         og -= 1
     cap = attn_cap or attn_split_cap(cfg, max_seq, workers)
+    head_split = head_split if grouped else 1
     spec = graph_spec(cfg, workers, lm_tasks or workers, fused_merge, call_tasks=call_tasks, attn_cap=cap,
-                      grouped=grouped, oproj_group_tasks=og)
-    return spec, {"call_tasks": call_tasks, "grouped": grouped, "oproj_group_tasks": og, "attn_cap": cap}
+                      grouped=grouped, oproj_group_tasks=og, head_split=head_split)
+    return spec, {"call_tasks": call_tasks, "grouped": grouped, "oproj_group_tasks": og, "attn_cap": cap,
+                  "head_split": head_split}
 
 
 def attn_split_cap(cfg, max_seq, workers):
@@ -250,7 +252,8 @@ class DecodeModel:
     def __init__(self, cfg: DecoderConfig, device="cuda:0", samples=(1024,), num_workers=None, capacity=None,
                  seed=0, weights=None, record_trace=False, prefetch=True, lm_tasks=None, keep_logical=False,
                  l2_prefetch=512 << 10, residual="split", fused_merge=True, balance=True, grouped=True,
-                 scheduler="static", early_push=False, stage_barriers=False, program=None, attn_cap=None):
+                 scheduler="static", early_push=False, stage_barriers=False, program=None, attn_cap=None,
+                 head_split=1):
         if not etsim.gpu_available():
             raise RuntimeError("DecodeModel needs a CUDA device (the executor has no CPU fallback)")
         self.cfg = cfg
@@ -271,7 +274,7 @@ class DecodeModel:
         self.fused_merge = fused_merge
         spec, self.layout = decode_graph_spec(cfg, self.tasks, self.samples[-1], lm_tasks=self.lm_tasks,
                                               residual=residual, fused_merge=fused_merge, balance=balance,
-                                              grouped=grouped, attn_cap=attn_cap)
+                                              grouped=grouped, attn_cap=attn_cap, head_split=head_split)
         self.call_tasks = self.layout["call_tasks"]
         self.grouped = self.layout["grouped"]
         self.oproj_group_tasks = self.layout["oproj_group_tasks"]
@@ -350,7 +353,9 @@ class DecodeModel:
             if self.grouped:
                 # flags bit 10: the last split folds in the new token; the output projection's
                 # prologue merges each group's partials (no merge task, one hop less)
-                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p, flags=1024))
+                # i13: q-head split (graphs.graph_spec head_split)
+                ops.append(make_op(OP_ATTN_SPLIT, i=attn_i + [0] * 6 + [self.layout.get("head_split", 1)], f=[scale],
+                                   p=attn_p, flags=1024))
             elif self.fused_merge:  # flags bit 1: the last split of a kv head merges it
                 ops.append(make_op(OP_ATTN_SPLIT, i=attn_i, f=[scale], p=attn_p, flags=2))
             else:

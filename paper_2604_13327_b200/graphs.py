@@ -5,7 +5,7 @@ fixture generator can build the same graphs for the reference implementation.
 
 
 def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allreduce_tasks: int = 0,
-               call_tasks=None, attn_cap=None, grouped=False, oproj_group_tasks=16):
+               call_tasks=None, attn_cap=None, grouped=False, oproj_group_tasks=16, head_split=1):
     """Reference-format graph spec of one decode step (symbol `s`)."""
     CH = cfg.attn_chunk
     fns, events, calls = [], [], []
@@ -48,7 +48,11 @@ def graph_spec(cfg, tasks: int, lm_tasks: int, fused_merge: bool = False, allred
             nsplit = f"(s + {CH - 1}) // {CH}"
             if attn_cap:
                 nsplit = f"min({nsplit}, {attn_cap})"
-            call(fn(f"L{l}.attn", [kv, f"max({nsplit}, 1)"]), ins=[(qkv, ["t0"])], outs=[(m, ["t0"])])
+            if head_split > 1:  # the q heads of a group shared by head_split tasks per split
+                call(fn(f"L{l}.attn", [f"{kv} * {head_split}", f"max({nsplit}, 1)"]),
+                     ins=[(qkv, [f"t0 // {head_split}"])], outs=[(m, [f"t0 // {head_split}"])])
+            else:
+                call(fn(f"L{l}.attn", [kv, f"max({nsplit}, 1)"]), ins=[(qkv, ["t0"])], outs=[(m, ["t0"])])
             call(fn(f"L{l}.oproj", [kv, str(oproj_group_tasks)]), ins=[(m, ["t0"])], outs=[(o, ["0"])])
             call(fn(f"L{l}.gateup", [ct.get("gateup", T)]), ins=[(o, ["0"])], outs=[(g, ["0"])])
             call(fn(f"L{l}.down", [ct.get("down", T)]), ins=[(g, ["0"])], outs=[(d, ["0"])])
