@@ -756,6 +756,15 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
                                 "needs b = 1, K a multiple of head_dim up to 1024, and 3 * heads * split cap <= " +
                                 std::to_string(etk::kAccFloats));
         }
+        if (o.kind == ET_OP_MOE_EXPERT) {
+            // body_moe_expert keeps gate / up accumulators for up to 8 tokens [2][IR][8] fp32, the
+            // activations [8][IR] bf16 and 16 words of tile state in the accumulator area
+            const int rs = o.i[2], ir = rs > 0 ? o.i[0] / rs : 0;
+            if (rs <= 0 || o.i[0] % rs || ir % 32 || 2LL * ir * 8 + ir * 4 + 16 > etk::kAccFloats)
+                return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": MoE expert row splits need "
+                                "(expert_inter / row_splits) a multiple of 32 with 20 * rows + 16 <= " +
+                                std::to_string(etk::kAccFloats) + " (at most 96 rows)");
+        }
         if (o.kind == ET_OP_ATTN_SPLIT && (o.flags & 1024) && (variant & 2))
             return rt->fail(ET_ERR_INVALID, "call " + std::to_string(c) + ": attention flags bit 10 (new token "
                             "folded by the last split) is implemented by the mma.sync instantiations only");

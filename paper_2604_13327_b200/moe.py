@@ -314,6 +314,8 @@ def moe_layout(cfg, num_workers, samples, scheduler, max_batch=1, batch_samples=
     from .decode import attn_split_cap, balanced_tasks
 
     assert cfg.expert_inter % cfg.row_splits == 0 and (cfg.expert_inter // cfg.row_splits) % 32 == 0
+    # the expert body's accumulators (gate / up for 8 tokens + activations) fit 2048 floats
+    assert cfg.expert_inter // cfg.row_splits <= 96, "expert row split wider than 96 rows"
     assert 1 <= max_batch <= 64
     L = {"max_batch": max_batch, "batched": max_batch > 1, "tc": max_batch > 8}
     L["tokens"] = "b" if L["batched"] else 1

@@ -119,3 +119,17 @@ def test_batched_attention_grid_is_covered_by_power_of_two_samples():
         for b in range(1, 65):
             samples = [1 << i for i in range(7) if (1 << i) >= b]
             assert any(tasks(b, s) <= tasks(x, s) for x in samples), (b, s)
+
+
+def test_moe_layout_rejects_expert_row_splits_wider_than_the_accumulators():
+    """body_moe_expert holds gate / up accumulators for 8 tokens plus the activations in
+    2048 floats: at most 96 rows per expert row split (the runtime rejects wider ones at
+    bind time too; row_splits=6 at Qwen3's 768 rows had overrun it)."""
+    import dataclasses
+
+    from paper_2604_13327_b200.moe import QWEN3_30B_A3B, moe_layout
+
+    moe_layout(QWEN3_30B_A3B, 148, (1024,), "static")  # 64 rows per split
+    moe_layout(dataclasses.replace(QWEN3_30B_A3B, row_splits=8), 148, (1024,), "static")  # 96
+    with pytest.raises(AssertionError):
+        moe_layout(dataclasses.replace(QWEN3_30B_A3B, row_splits=6), 148, (1024,), "static")  # 128
