@@ -1591,7 +1591,12 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     float* sc = scratch + G * qstride;   // [G][CH]
     float* st = sc + G * CH;             // [G][4]: running max, running sum, block rescale
     const float* q = reinterpret_cast<const float*>(op.p[0]) + rb + static_cast<long long>(g * Gf + hb) * dh;
-    for (int i = ctid; i < G * dh; i += kConsumers) qs[(i / dh) * qstride + i % dh] = __ldcg(q + i);
+    for (int i0 = ctid; i0 < G * dh; i0 += 2 * kConsumers) {  // both loads ahead of the stores
+        const int i1 = i0 + kConsumers;
+        const float a = __ldcg(q + i0), b = i1 < G * dh ? __ldcg(q + i1) : 0.f;
+        qs[(i0 / dh) * qstride + i0 % dh] = a;
+        if (i1 < G * dh) qs[(i1 / dh) * qstride + i1 % dh] = b;
+    }
     // flags bit 10 (no merge task): the group's last split also folds in the new token
     // -- cache row s, appended by the q/k/v projection this task waited on -- so the
     // partials alone make the attention output and the group's consumer (the output
