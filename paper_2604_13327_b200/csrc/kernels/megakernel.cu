@@ -1591,28 +1591,37 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     float* sc = scratch + G * qstride;   // [G][CH]
     float* st = sc + G * CH;             // [G][4]: running max, running sum, block rescale
     const float* q = reinterpret_cast<const float*>(op.p[0]) + rb + static_cast<long long>(g * Gf + hb) * dh;
+    // flags bit 10 (no merge task): the group's last split also folds in the new token
+    // -- cache row s, appended by the q/k/v projection this task waited on -- so the
+    // partials alone make the attention output and the group's consumer (the output
+    // projection's prologue, gemv_merge_prologue) merges them.  Its k/v rows load with q:
+    // every load of the prologue is issued before its shared-memory stores (a store
+    // through a generic pointer could alias them as far as the compiler knows, and each
+    // load would then wait for the previous store -- one L2 round trip apiece).
+    const int nsl = attn_splits_base(op, P.binding);
+    const bool fold = !kMMA && (op.flags & 1024) && c == (nsl > 0 ? nsl : 1) - 1;
+    float* kv_new = st + 4 * G + 8;  // [2][dh] new k, v
+    const bool fold_kv = fold && !(kQK && (op.flags & 1));  // (q/k-norm mode: normalised from the raw projection below)
+    const long long krow = static_cast<long long>(bq) * op.i[8] + (static_cast<long long>(g) * op.i[3] + s) * dh;
+    const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + krow;
+    const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + krow;
+    const bool kv1 = fold_kv && ctid < dh;  // dh <= kConsumers: one new k / v element per thread
+    const float kn0 = kv1 ? bf2f(__ldcg(kn + ctid)) : 0.f, vn0 = kv1 ? bf2f(__ldcg(vn + ctid)) : 0.f;
     for (int i0 = ctid; i0 < G * dh; i0 += 2 * kConsumers) {  // both loads ahead of the stores
         const int i1 = i0 + kConsumers;
         const float a = __ldcg(q + i0), b = i1 < G * dh ? __ldcg(q + i1) : 0.f;
         qs[(i0 / dh) * qstride + i0 % dh] = a;
         if (i1 < G * dh) qs[(i1 / dh) * qstride + i1 % dh] = b;
     }
-    // flags bit 10 (no merge task): the group's last split also folds in the new token
-    // -- cache row s, appended by the q/k/v projection this task waited on -- so the
-    // partials alone make the attention output and the group's consumer (the output
-    // projection's prologue, gemv_merge_prologue) merges them.  Its k/v rows load with q.
-    const int nsl = attn_splits_base(op, P.binding);
-    const bool fold = !kMMA && (op.flags & 1024) && c == (nsl > 0 ? nsl : 1) - 1;
-    float* kv_new = st + 4 * G + 8;  // [2][dh] new k, v
-    if (fold && !(kQK && (op.flags & 1))) {  // (q/k-norm mode: normalised from the raw projection below)
-        const long long row = static_cast<long long>(bq) * op.i[8] + (static_cast<long long>(g) * op.i[3] + s) * dh;
-        const uint16_t* kn = reinterpret_cast<const uint16_t*>(op.p[1]) + row;
-        const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + row;
-        for (int d = ctid; d < dh; d += kConsumers) {
+    if (kv1) {
+        kv_new[ctid] = kn0;
+        kv_new[dh + ctid] = vn0;
+    }
+    if (fold_kv)
+        for (int d = ctid + kConsumers; d < dh; d += kConsumers) {  // dh > kConsumers (not used by the models)
             kv_new[d] = bf2f(__ldcg(kn + d));
             kv_new[dh + d] = bf2f(__ldcg(vn + d));
         }
-    }
     if (ctid < G) {
         st[4 * ctid] = -INFINITY;
         st[4 * ctid + 1] = 0.f;
