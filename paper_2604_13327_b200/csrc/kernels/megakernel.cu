@@ -1607,6 +1607,24 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     const uint16_t* vn = reinterpret_cast<const uint16_t*>(op.p[2]) + krow;
     const bool kv1 = fold_kv && ctid < dh;  // dh <= kConsumers: one new k / v element per thread
     const float kn0 = kv1 ? bf2f(__ldcg(kn + ctid)) : 0.f, vn0 = kv1 ? bf2f(__ldcg(vn + ctid)) : 0.f;
+    // q/k-norm mode (flags bit 0): the norm weights, RoPE frequencies and the raw new k / v of
+    // this thread's dimension, loaded with q as well (used below)
+    const bool qkm = kQK && (op.flags & 1) != 0;
+    const bool knew = qkm && (((op.flags & 2) && c == 0) || fold);  // this task appends the new k / v
+    const bool nw = (op.flags & 64) == 0;
+    float wq0 = 0.f, wk0 = 0.f, fr0 = 0.f, kr0 = 0.f, vr0 = 0.f;
+    const float* kraw = reinterpret_cast<const float*>(op.p[8]) + rb + static_cast<long long>(g) * dh;
+    if (qkm && ctid < dh) {
+        if (nw) {
+            wq0 = __ldg(reinterpret_cast<const float*>(op.p[(op.flags & 2) ? 9 : 5]) + ctid);
+            wk0 = __ldg(reinterpret_cast<const float*>(op.p[6]) + ctid);
+        }
+        if (ctid < dh / 2) fr0 = __ldg(reinterpret_cast<const float*>(op.p[7]) + ctid);
+        if (knew) {
+            kr0 = __ldcg(kraw + ctid);
+            vr0 = __ldcg(kraw + static_cast<long long>(kvh) * dh + ctid);
+        }
+    }
     for (int i0 = ctid; i0 < G * dh; i0 += 2 * kConsumers) {  // both loads ahead of the stores
         const int i1 = i0 + kConsumers;
         const float a = __ldcg(q + i0), b = i1 < G * dh ? __ldcg(q + i1) : 0.f;
@@ -1628,37 +1646,26 @@ __device__ void body_attn_split(const StaticParams& P, const et_op& op, const Sl
     }
     if constexpr (kQK) {
         if (op.flags & 1) {  // q-norm + RoPE applied here (q is the raw projection)
-            // the q / k norm weights and the RoPE frequencies load with q (one L2 round
-            // trip; the wait's acquire left L1 cold)
+            // the q / k norm weights and the RoPE frequencies loaded with q above (one L2
+            // round trip; the wait's acquire left L1 cold)
             float* wqs = kv_new + 2 * dh;  // [dh] q-norm, [dh] k-norm, [dh/2] inverse frequencies
-            {
-                const bool nw = (op.flags & 64) == 0;
-                const float* wq = reinterpret_cast<const float*>(op.p[(op.flags & 2) ? 9 : 5]);
-                const float* wk = reinterpret_cast<const float*>(op.p[6]);
-                const float* fr = reinterpret_cast<const float*>(op.p[7]);
-                for (int d = ctid; d < dh; d += kConsumers) {
-                    if (nw) {
-                        wqs[d] = __ldg(wq + d);
-                        wqs[dh + d] = __ldg(wk + d);
-                    }
-                    if (d < dh / 2) wqs[2 * dh + d] = __ldg(fr + d);
+            if (ctid < dh) {
+                if (nw) {
+                    wqs[ctid] = wq0;
+                    wqs[dh + ctid] = wk0;
                 }
+                if (ctid < dh / 2) wqs[2 * dh + ctid] = fr0;
             }
             // fused merge: split 0 also normalises + rotates the new k and appends the
             // new k/v (bf16) to the cache row s before it arrives, so the merger reads
             // them like any cached row
             // no merge task (flags bit 10): the last split does it and keeps them for its fold
-            const bool knew = ((op.flags & 2) && c == 0) || fold;
             // [2][dh]: sc is scratch before the blocks use it; the tensor-core split keeps them
             // past its per-warp P scratch (attn_solo_finish reads them after the blocks)
             float* kv = fold ? kv_new : kMMA ? sc + kAttnSoloKv : sc;
-            if (knew) {
-                const float* kr = reinterpret_cast<const float*>(op.p[8]) + rb + static_cast<long long>(g) * dh;
-                const float* vr = kr + static_cast<long long>(kvh) * dh;
-                for (int d = ctid; d < dh; d += kConsumers) {
-                    kv[d] = __ldcg(kr + d);
-                    kv[dh + d] = __ldcg(vr + d);
-                }
+            if (knew && ctid < dh) {
+                kv[ctid] = kr0;
+                kv[dh + ctid] = vr0;
             }
             bar_sync(1, kConsumers);
             for (int h = warp; h < G + (knew ? 1 : 0); h += kConsumerWarps)

@@ -772,6 +772,8 @@ int et_bind_ops(et_runtime* rt, const et_op* ops, int32_t num_calls) {
     for (int32_t c = 0; c < num_calls; ++c) {
         if (ops[c].kind != ET_OP_ATTN_SPLIT && ops[c].kind != ET_OP_ATTN_MERGE) continue;
         const int dh = ops[c].i[0], G = ops[c].i[1], CH = ops[c].i[2];
+        if (dh > etk::kConsumers)  // the split prologue loads one dimension per consumer thread
+            return rt->fail(ET_ERR_INVALID, "attention head_dim must not exceed 256");
         if (G * dh > 4 * etk::kConsumers)  // the wide bodies hold 4 (head, dim) outputs per thread
             return rt->fail(ET_ERR_INVALID, "attention groups need q heads per kv head x head_dim <= 1024");
         if ((ops[c].flags & 256) && dh % 64 != 0)  // chunk j ^ (pos % 8) must stay inside the row
